@@ -1,0 +1,370 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 FHT hot path (BASELINE.json metric: input Gpixel/s for the full
+four-quadrant FHT; achieved HBM GB/s against the roofline).
+
+    python bench.py [--gpus N --steps K --warmup W] [--config 2|5|...] [--impl ours|reference]
+
+A step = one pass of the config's hot path over one batch of synthetic input already resident
+in HBM: C2 = full four-quadrant FHT + fhtshift (BASELINE configs[1], the default), C5 = the
+same on 16 x 2048^2, C3 = full FHT of 64 x 512^2 u8, C4 = angle-range FHT + fhtshift, C1 = one
+quadrant. Rank 0 prints ONE JSON line. Under torchrun each rank runs its own batch (weak
+scaling, no collective: images are independent).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import multiprocessing as mp
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "input Gpixel/s for full 4-quadrant FHT; achieved HBM GB/s vs roofline"
+L2_FLUSH_BYTES = 512 << 20
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy r+w)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# ----------------------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index, self.samples, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.samples.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": float(self.samples[0][1]) if self.samples[0][1].replace(".", "").isdigit() else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------------------- workloads
+def workload(cfg_id: int):
+    import synth
+    c = synth.CONFIGS[cfg_id]
+    imgs = synth.batch(cfg_id)
+    return c, imgs
+
+
+def out_bytes_per_step(cfg_id, c, imgs):
+    B, h, w = imgs.shape
+    Hp, Wp = 1 << (h - 1).bit_length(), 1 << (w - 1).bit_length()
+    if c["mode"] == "quadrant":
+        return Hp * (w + Hp) * 4, 0
+    if c["mode"] == "full":
+        hough = B * 4 * max(Hp, Wp) * (Hp + Wp) * 4
+        return hough, (hough if cfg_id in (2, 5) else 0)
+    return None, None
+
+
+def make_step(fht, cfg_id, c, t, ws, outs):
+    """Returns step() -> number of kernel launches it enqueued (all through the C ABI)."""
+    if c["mode"] == "quadrant":
+        def step():
+            outs["h"] = fht.quadrant(t, fht.QA, workspace=ws)
+            return outs["h"].launches
+        return step
+    if c["mode"] == "full":
+        do_shift = cfg_id in (2, 5)
+
+        def step():
+            outs["h"] = fht.full(t, workspace=ws, out=outs.get("h"))
+            n = outs["h"].launches
+            if do_shift:
+                outs["s"] = fht.fhtshift(outs["h"], out=outs.get("s"))
+                n += outs["s"].launches
+            return n
+        return step
+    plan = fht.angle_plan(c["h"], c["w"], c["theta_min"], c["theta_max"])
+    outs["plan"] = plan
+
+    def step():
+        outs["h"] = fht.angle_range(t, plan, workspace=ws, out=outs.get("h"))
+        outs["s"] = fht.fhtshift(outs["h"], out=outs.get("s"))
+        return outs["h"].launches + outs["s"].launches
+    return step
+
+
+# ----------------------------------------------------------------------------------------- oracle arm
+_ORACLE_IMGS = None
+
+
+def _oracle_unit(args):
+    cfg_id, b, q = args
+    import synth
+    from oracle import fht_oracle as O
+    img = _ORACLE_IMGS[b]
+    c = synth.CONFIGS[cfg_id]
+    if c["mode"] == "range":
+        p = O.angle_plan(c["h"], c["w"], c["theta_min"], c["theta_max"])
+        R = O.angle_range(img, p)
+        O.fhtshift_range(R, p)
+    elif c["mode"] == "quadrant":
+        O.hough_recursive(img, O.QA)
+    else:
+        Hp, Wp = O.full_padding(*img.shape)
+        fr = O.quadrant_frame(img, q, square_to=(Hp, Wp))
+        H = O.hough_of_frame_recursive(fr)
+        if cfg_id in (2, 5):
+            O.fhtshift_quadrant(H, fr.sigma)
+    return 0
+
+
+def oracle_sample(cfg_id: int, c, imgs, max_units: int | None = None):
+    """Time the oracle as it stands (tier-2 recursion, float64/int64) over a bounded sample of
+    the workload: whole (image, quadrant) units in a fork pool over the host cores."""
+    global _ORACLE_IMGS
+    _ORACLE_IMGS = imgs
+    if c["mode"] == "full":
+        units = [(cfg_id, b, q) for b in range(imgs.shape[0]) for q in range(4)]
+        per_unit_px = c["h"] * c["w"] / 4.0
+    else:
+        units = [(cfg_id, 0, 0)]
+        per_unit_px = c["h"] * c["w"]
+    if max_units:
+        units = units[:max_units]
+    cores = max(1, min(len(units), len(os.sched_getaffinity(0))))
+    with mp.get_context("fork").Pool(cores) as pool:
+        t0 = time.perf_counter()
+        pool.map(_oracle_unit, units, chunksize=1)
+        dt = time.perf_counter() - t0
+    px = per_unit_px * len(units)
+    return {"value": px / dt / 1e9, "unit": "Gpixel/s", "cores": cores, "kind": "oracle",
+            "sample": f"{len(units)} (image, quadrant) units of config {cfg_id} "
+                      f"({'full FHT' if c['mode'] == 'full' else c['mode']}"
+                      f"{' + fhtshift' if cfg_id in (2, 4, 5) else ''}), tier-2 numpy recursion f64/i64, "
+                      f"{dt:.2f} s wall"}
+
+
+def oracle_units_budget(cfg_id):
+    return {1: None, 2: None, 3: 32, 4: None, 5: 8}[cfg_id]
+
+
+# ----------------------------------------------------------------------------------------- main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--extra-configs", default="5,3,4,1",
+                    help="other configs also timed (reported under 'configs', not the headline)")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    import synth
+    c = synth.CONFIGS[args.config]
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        _, ref_imgs = workload(args.config)
+        times = []
+        for i in range(args.warmup + args.steps):
+            cb = oracle_sample(args.config, c, ref_imgs, oracle_units_budget(args.config))
+            if i >= args.warmup:
+                times.append(cb)
+        v = statistics.mean(x["value"] for x in times)
+        line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "Gpixel/s", "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64" if c["dtype"] == "f32" else "int64", "data": "synthetic",
+                "config": {"workload": c["name"], "batch": c["batch"], "h": c["h"], "w": c["w"]},
+                "cpu_baseline": dict(times[-1], value=v),
+                "e2e": {"value": v, "unit": "Gpixel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    if world > 1:
+        dist.init_process_group("nccl", init_method="env://")
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    import paper_1811_06378_b200 as fht
+
+    peak_gbs, peak_src = load_peaks()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def run_config(cfg_id, steps, warmup, with_e2e):
+        cc = synth.CONFIGS[cfg_id]
+        _, imgs = workload(cfg_id)
+        t = torch.from_numpy(imgs).to(dev)
+        B, h, w = imgs.shape
+        outs = {}
+        ws = None
+        step = make_step(fht, cfg_id, cc, t, ws, outs)
+        step()
+        torch.cuda.synchronize()
+        flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+        in_bytes = imgs.nbytes
+        need_flush = (in_bytes + sum(o.storage.numel() * 4 for k, o in outs.items() if hasattr(o, "storage"))) < (
+            300 << 20)
+        stream = torch.cuda.current_stream()
+        for _ in range(warmup):
+            step()
+        torch.cuda.synchronize()
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        launches = 0
+        barrier()
+        torch.cuda.synchronize()
+        with ClockSampler(local_rank) as clk:
+            t_wall = time.perf_counter()
+            for i in range(steps):
+                if need_flush:
+                    flush.zero_()
+                evs[i][0].record(stream)
+                launches += step()
+                evs[i][1].record(stream)
+            torch.cuda.synchronize()
+            barrier()
+            t_wall = time.perf_counter() - t_wall
+        per = [a.elapsed_time(b) for a, b in evs]
+        ms = statistics.mean(per)
+        if world > 1:
+            tt = torch.tensor([ms], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ms = float(tt.item())
+        px = B * h * w
+        hough_b = sum(o.storage.numel() * 4 for k, o in outs.items() if hasattr(o, "storage"))
+        res = {"workload": cc["name"], "ms_per_step": ms, "gpix_s": px * world / (ms * 1e-3) / 1e9,
+               "bytes_per_step": in_bytes + hough_b, "l2_flushed": need_flush, "launches": launches // steps,
+               "clocks": clk.summary(), "wall_s": t_wall}
+        res["achieved_gbs"] = res["bytes_per_step"] / (ms * 1e-3) / 1e9
+        if with_e2e:
+            res["e2e"] = e2e_config(cfg_id, cc, imgs, step_host(fht, cfg_id, cc, imgs, dev), steps)
+        return res
+
+    def step_host(fht_, cfg_id, cc, imgs, dev_):
+        pinned_in = torch.from_numpy(imgs).pin_memory()
+        outs = {}
+        holder = {}
+
+        def run():
+            t = pinned_in.to(dev_, non_blocking=True)
+            st = make_step(fht_, cfg_id, cc, t, None, outs)
+            st()
+            res = outs.get("s") or outs["h"]
+            if "pin" not in holder:
+                holder["pin"] = torch.empty(res.storage.shape, dtype=res.storage.dtype).pin_memory()
+                holder["pin_h"] = torch.empty(outs["h"].storage.shape, dtype=outs["h"].storage.dtype).pin_memory()
+            holder["pin"].copy_(res.storage, non_blocking=True)
+            d2h = res.storage.numel() * 4
+            if "s" in outs:
+                holder["pin_h"].copy_(outs["h"].storage, non_blocking=True)
+                d2h += outs["h"].storage.numel() * 4
+            return pinned_in.numel() * pinned_in.element_size(), d2h
+        return run
+
+    def e2e_config(cfg_id, cc, imgs, run, steps):
+        for _ in range(3):
+            run()
+        torch.cuda.synchronize()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record()
+        for _ in range(steps):
+            hb, db = run()
+        t1.record()
+        torch.cuda.synchronize()
+        ms = t0.elapsed_time(t1) / steps
+        px = imgs.shape[0] * imgs.shape[1] * imgs.shape[2]
+        return {"value": px * world / (ms * 1e-3) / 1e9, "unit": "Gpixel/s", "h2d_bytes_per_step": hb,
+                "d2h_bytes_per_step": db, "ms_per_step": ms}
+
+    head = run_config(args.config, args.steps, args.warmup, with_e2e=True)
+    extra = {}
+    if rank == 0 or world > 1:
+        for cid in [int(x) for x in args.extra_configs.split(",") if x and int(x) != args.config]:
+            try:
+                r = run_config(cid, max(5, args.steps // 2), 3, with_e2e=False)
+                extra[r["workload"]] = {k: r[k] for k in ("ms_per_step", "gpix_s", "achieved_gbs", "bytes_per_step",
+                                                          "l2_flushed", "launches")}
+                extra[r["workload"]]["frac_of_measured_hbm"] = r["achieved_gbs"] / peak_gbs
+            except Exception as e:  # noqa: BLE001 -- report, do not hide
+                extra[synth.CONFIGS[cid]["name"]] = {"error": repr(e)}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        cpu = oracle_sample(args.config, c, workload(args.config)[1], oracle_units_budget(args.config))
+    frac = head["achieved_gbs"] / peak_gbs
+    line = {
+        "metric": METRIC, "value": head["gpix_s"], "unit": "Gpixel/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": head["ms_per_step"], "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32" if c["dtype"] == "f32" else "int32", "data": "synthetic",
+        "config": {"workload": c["name"], "batch": c["batch"] * world, "h": c["h"], "w": c["w"],
+                   "mode": c["mode"] + (" + fhtshift" if args.config in (2, 4, 5) else ""),
+                   "parallelism": f"dp{world} (independent images per rank)",
+                   "l2": "flushed between steps (512 MiB write outside the per-step events)" if head["l2_flushed"]
+                   else "working set > L2", "timing": "CUDA events per step, mean; max over ranks"},
+        "roofline": {"bound": "hbm", "achieved": head["achieved_gbs"], "peak": peak_gbs, "unit": "GB/s",
+                     "frac": frac, "traffic": None, "kernel": "whole step (pass1 + pass2 + fhtshift launches)",
+                     "algorithmic_bytes_per_step": head["bytes_per_step"], "peak_source": peak_src},
+        "cpu_baseline": cpu,
+        "e2e": {k: head["e2e"][k] for k in ("value", "unit", "h2d_bytes_per_step", "d2h_bytes_per_step")},
+        "gpu_launches": head["launches"] * args.steps,
+        "clocks": head["clocks"],
+        "configs": extra,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

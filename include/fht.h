@@ -1,0 +1,150 @@
+/*
+ * fht.h -- C ABI of libfht.so: the Brady dyadic Fast Hough Transform on one B200 (sm_100a),
+ * as studied in M. Aliev, E.I. Ershov, D.P. Nikolaev, "On the use of FHT, its modification for
+ * practical applications and the structure of Hough image" (arXiv 1811.06378).
+ *
+ * Citations: P:n = PAPER.md line n (section in brackets); S:n = SPEC.md line n.
+ * Readings R1..R23 are listed in DESIGN.md ("Readings of the paper").
+ *
+ * Conventions common to every call
+ * --------------------------------
+ *  - Every buffer pointer in fht_image / fht_hough and every workspace pointer is a DEVICE
+ *    pointer allocated and owned by the caller. The library allocates no device memory, keeps
+ *    no global mutable state and retains no pointer after a call returns. All device work is
+ *    enqueued on `stream` (0 = legacy default stream); buffers must stay alive until it ends.
+ *  - Strides are in ELEMENTS. Pointers must be aligned to their element size (FHT_ERR_ALIGN
+ *    otherwise). Output descriptors from fht_hough_describe() have 16-byte row pitches; the
+ *    kernels pick 128-bit vector accesses where base pointers and pitches allow them.
+ *  - Argument errors are detected synchronously, before anything is enqueued, and reported as
+ *    a negative fht_status; nothing is thrown across the ABI. On success the compute calls
+ *    (fht_quadrant, fht_full, fht_angle_range, fhtshift) return the number (>= 1) of kernels
+ *    they enqueued; the host-only calls return FHT_OK (0). A launch failure returns
+ *    FHT_ERR_CUDA; device faults surface at the caller's next synchronisation.
+ *  - Element types: input u8, i32 or f32. Output is i32 for u8/i32 input (exact; the caller
+ *    owns i32 overflow), f32 for f32 input (IEEE round-to-nearest adds, R21 tolerance).
+ *  - Coordinates: x = column (right), y = row (down). A Hough cell is (s, x0): s = shift
+ *    row, x0 = column in the cyclic layout of width W ("mod(w + h)").
+ *  - Quadrants (R4): QA = (I, +), QB = (I, -), QC = (I^T, -), QD = (I^T, +) where
+ *    (image, sigma) means H[s][x0] = sum_y Ipad[y][(x0 + sigma * D_{Hp,s}(y)) mod W] and
+ *    D is the dyadic pattern of S:71 (R1). QC/QD use the transposed image by index
+ *    transposition -- no copy is made. Ipad is the image zero-extended to Hp = next_pow2(rows)
+ *    rows (R3) and W = cols + Hp columns ("(w + h) x h").
+ */
+#ifndef FHT_H
+#define FHT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* fht_stream_t; /* == cudaStream_t */
+
+typedef enum {
+  FHT_OK = 0,
+  FHT_ERR_ARG = -1,         /* bad scalar argument, NULL pointer, aliasing, bad angle range */
+  FHT_ERR_DTYPE = -2,       /* dtype not supported for this call / output dtype mismatch */
+  FHT_ERR_SHAPE = -3,       /* output descriptor shape does not match the transform */
+  FHT_ERR_ALIGN = -4,       /* pointer or row pitch not 16-byte aligned */
+  FHT_ERR_UNSUPPORTED = -5, /* valid request the GPU path does not implement (e.g. pad != Hp) */
+  FHT_ERR_WORKSPACE = -6,   /* workspace NULL or smaller than fht_workspace_bytes() */
+  FHT_ERR_STATE = -7,       /* fhtshift on an already shifted descriptor */
+  FHT_ERR_CUDA = -8         /* a CUDA launch or runtime call failed */
+} fht_status;
+
+typedef enum { FHT_U8 = 0, FHT_I32 = 1, FHT_F32 = 2 } fht_dtype;
+typedef enum { FHT_QA = 0, FHT_QB = 1, FHT_QC = 2, FHT_QD = 3 } fht_quadrant_id;
+typedef enum { FHT_MODE_QUADRANT = 0, FHT_MODE_FULL = 1, FHT_MODE_RANGE = 2 } fht_mode;
+/* QUADS: [batch][4][Pmax][W] unflipped quadrant images (BASELINE C2 "four quadrants").
+ * CONCAT: [batch][2(Hp+Wp)-3][W], P:89 order "QA flipped; QB; QC flipped; QD", a row shared by
+ * two neighbours written once by the earlier quadrant (R8). */
+typedef enum { FHT_LAYOUT_QUADS = 0, FHT_LAYOUT_CONCAT = 1 } fht_layout;
+
+/* Input image batch: element (b, y, x) at data[b*batch_stride + y*row_stride + x]. */
+typedef struct {
+  const void* data;
+  int32_t dtype; /* fht_dtype */
+  int32_t _pad0;
+  int64_t batch, h, w;
+  int64_t batch_stride, row_stride;
+} fht_image;
+
+/* §4 plan (R12-R17). theta = inclination from vertical, tan(theta) = dx/dy.
+ * Lines with slope k in [k_lo, k_hi] are sheared by k_lo and scaled by alpha = 1/(k_hi-k_lo)
+ * onto QA's slopes [0, 1] (scale law P:124, shear law P:132, composition P:144).
+ * Transformed row y (never materialised):
+ *   T(x', y) = I[y][colmap[x' - e_y]] if 0 <= x' - e_y < w_content, else 0   (unwrapped x')
+ *   e_y = floor(g*y + 0.5), g = alpha*(-k_lo);  colmap[u] = min(w-1, floor((u+0.5)/alpha)).
+ * Output: Hp rows x W cyclic columns, W = w_content + max(Hp, 1 + max_s spread_s) (R17). */
+typedef struct {
+  double theta_min_deg, theta_max_deg;
+  double k_lo, k_hi, alpha, g;
+  int64_t h, w, Hp;
+  int64_t w_content; /* w' = ceil(alpha*w) */
+  int64_t W;         /* W' */
+  int64_t e_min, e_max; /* min / max of e_y over y < h */
+} fht_angle_plan;
+
+/* Output (Hough image) descriptor. Fill it with fht_hough_describe(), then set `data`. */
+typedef struct {
+  void* data;
+  int32_t dtype;    /* I32 for integer input, F32 for float input */
+  int32_t mode;     /* fht_mode */
+  int32_t layout;   /* fht_layout (FULL mode only) */
+  int32_t shifted;  /* 1 = rows hold the fhtshift-ed image (§5). Setting it to 1 BEFORE an
+                       fht_* call makes that call write the shifted image directly (fused). */
+  int32_t quadrant; /* QUADRANT mode: which quadrant */
+  int32_t _pad0;
+  int64_t batch, nquad, rows, cols;       /* nquad = 4 for FULL/QUADS, else 1 */
+  int64_t batch_stride, quad_stride, row_stride;
+  int64_t h, w, Hp, Wp;                   /* source image dims; Hp/Wp = padded powers of two */
+  fht_angle_plan plan;                    /* valid iff mode == RANGE */
+} fht_hough;
+
+/* Fill `out` (except `data`) with the contiguous shape of the transform of `img`:
+ *   QUADRANT: rows = Hp, cols = W = w + Hp (QA/QB) or Wp rows, h + Wp cols (QC/QD);
+ *   FULL/QUADS: nquad 4, rows = max(Hp, Wp), cols = Hp + Wp (R9);
+ *   FULL/CONCAT: rows = 2(Hp+Wp)-3, cols = Hp + Wp;
+ *   RANGE: rows = plan->Hp, cols = plan->W.
+ * `plan` may be NULL unless mode == RANGE. Returns FHT_OK or a negative fht_status. */
+int fht_hough_describe(int mode, int layout, int quadrant, const fht_image* img,
+                       const fht_angle_plan* plan, fht_hough* out);
+
+/* Device workspace (bytes) the call needs for `img` (pass-1 scratch + tables). */
+size_t fht_workspace_bytes(int mode, const fht_image* img, const fht_angle_plan* plan);
+
+/* One quadrant. pad_cols: -1 or Hp (the paper's h x h extension);
+ * other pads return FHT_ERR_UNSUPPORTED on the GPU (the oracle handles any pad cyclically).
+ * `out` from fht_hough_describe(FHT_MODE_QUADRANT, 0, quadrant, ...). */
+int fht_quadrant(const fht_image* img, int quadrant, int64_t pad_cols, fht_hough* out, void* ws,
+                 size_t ws_bytes, fht_stream_t stream);
+
+/* Full four-quadrant transform. `layout` must equal out->layout. */
+int fht_full(const fht_image* img, int layout, fht_hough* out, void* ws, size_t ws_bytes,
+             fht_stream_t stream);
+
+/* Host-only: build the §4 plan. FHT_ERR_ARG if theta_min >= theta_max,
+ * |theta| >= 90 deg, or alpha*w < 1. Deterministic double arithmetic, no FMA (R16). */
+int fht_angle_plan_make(int64_t h, int64_t w, double theta_min_deg, double theta_max_deg,
+                        fht_angle_plan* out);
+
+/* Angle-range-restricted transform: QA of the virtually sheared+scaled image, the
+ * shear and scale fused into the first FHT iteration (pass-1 loader). f32/u8/i32 input. */
+int fht_angle_range(const fht_image* img, const fht_angle_plan* plan, fht_hough* out, void* ws,
+                    size_t ws_bytes, fht_stream_t stream);
+
+/* §5 fhtshift (R11): out[r][x] = in[r][(x - k_r) mod cols], k_r = ceil((n+s)/2) for
+ * sigma=+1 quadrants, ceil((n-s)/2) for sigma=-1, and ceil((W'-len_s)/2) - start_s in RANGE
+ * mode. `in` must be unshifted (FHT_ERR_STATE otherwise); `out` must have the same shape and
+ * not alias `in`; on success out->shifted = 1. Bit copy: exact for every dtype. */
+int fhtshift(const fht_hough* in, fht_hough* out, fht_stream_t stream);
+
+/* Human-readable name of a status code (static string). */
+const char* fht_status_string(int status);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FHT_H */

@@ -373,6 +373,22 @@ def angle_range(img: np.ndarray, plan: AnglePlan, tier: int = 2) -> np.ndarray:
     return hough_of_frame_recursive(fr) if tier == 2 else hough_of_frame_direct(fr)
 
 
+def range_cells_direct(img: np.ndarray, plan: AnglePlan, cells) -> np.ndarray:
+    """The §4 definition evaluated at listed (s, x0) cells without materialising T:
+    sum_y T[y][(x0 + D_s(y)) mod W'] with T as in `transformed_image`."""
+    a = _as_acc(np.asarray(img))
+    colmap = scale_colmap(plan.alpha, plan.w, plan.w_content)
+    e = shear_offsets(plan.g, plan.h)
+    ys = np.arange(plan.h)
+    out = np.zeros(len(cells), dtype=a.dtype)
+    D = pattern_offsets(plan.Hp)
+    for k, (s, x0) in enumerate(cells):
+        u = (int(x0) + D[int(s)][: plan.h] - e) % plan.W
+        ok = u < plan.w_content
+        out[k] = a[ys[ok], colmap[u[ok]]].sum()
+    return out
+
+
 def angle_of_row(s: int, plan: AnglePlan) -> float:
     """R19 metadata: row s of the range output holds lines of slope k_lo + s / (alpha (Hp - 1))."""
     k = plan.k_lo + s / (plan.alpha * (plan.Hp - 1)) if plan.Hp > 1 else plan.k_lo

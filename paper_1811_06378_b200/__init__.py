@@ -1,0 +1,164 @@
+"""paper_1811_06378_b200 -- B200-native Brady dyadic Fast Hough Transform (arXiv 1811.06378).
+
+Thin torch-facing wrapper over the C ABI of ``libfht.so`` (``include/fht.h``). torch provides
+device memory (``data_ptr``) and the current CUDA stream; every step of the transform runs in
+the sm_100a kernels behind the ABI. There is no CPU fallback: importing without the built
+library, or calling with a non-CUDA tensor, raises.
+
+    full(img, layout="quads", shifted=False)        -> HoughImage
+    quadrant(img, q, pad=None, shifted=False)       -> HoughImage
+    angle_plan(h, w, theta_min, theta_max)          -> FhtAnglePlan
+    angle_range(img, plan, shifted=False)           -> HoughImage
+    fhtshift(hough)                                 -> HoughImage
+
+`shifted=True` makes the transform write the fhtshift-ed image directly (fused store).
+"""
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _lib
+from ._lib import (FHT_F32, FHT_I32, FHT_LAYOUT_CONCAT, FHT_LAYOUT_QUADS, FHT_MODE_FULL, FHT_MODE_QUADRANT,
+                   FHT_MODE_RANGE, FHT_QA, FHT_QB, FHT_QC, FHT_QD, FHT_U8, FhtAnglePlan, FhtError, FhtHough,
+                   FhtImage)
+
+__all__ = ["full", "quadrant", "angle_plan", "angle_range", "fhtshift", "HoughImage", "FhtError",
+           "QA", "QB", "QC", "QD", "workspace_bytes", "LIB_PATH"]
+
+QA, QB, QC, QD = FHT_QA, FHT_QB, FHT_QC, FHT_QD
+LIB_PATH = _lib.LIB_PATH
+_DT_IN = {torch.uint8: FHT_U8, torch.int32: FHT_I32, torch.float32: FHT_F32}
+_DT_OUT = {FHT_I32: torch.int32, FHT_F32: torch.float32}
+_LAYOUTS = {"quads": FHT_LAYOUT_QUADS, "concat": FHT_LAYOUT_CONCAT}
+
+
+class HoughImage:
+    """A Hough image on the device: `storage` is the pitched tensor the kernels wrote,
+    `desc` its C descriptor; `view` is the logical [B][nquad][rows][cols] tensor view."""
+
+    def __init__(self, storage: torch.Tensor, desc: FhtHough):
+        self.storage = storage
+        self.desc = desc
+        self.launches = 0  # kernels enqueued by the call that last wrote this image
+
+    @property
+    def view(self) -> torch.Tensor:
+        d = self.desc
+        return self.storage.view(d.batch, d.nquad, d.rows, d.row_stride)[..., : d.cols]
+
+    @property
+    def shifted(self) -> bool:
+        return bool(self.desc.shifted)
+
+    @property
+    def plan(self):
+        return self.desc.plan if self.desc.mode == FHT_MODE_RANGE else None
+
+
+def _image(t: torch.Tensor) -> tuple[FhtImage, torch.Tensor]:
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError("image must be a CUDA tensor (no CPU path)")
+    if t.dtype not in _DT_IN:
+        raise TypeError(f"unsupported dtype {t.dtype}; use uint8, int32 or float32")
+    if t.dim() == 2:
+        t = t.unsqueeze(0)
+    if t.dim() != 3:
+        raise ValueError("image must be [h][w] or [B][h][w]")
+    if t.stride(2) != 1:
+        t = t.contiguous()
+    img = FhtImage()
+    img.data = t.data_ptr()
+    img.dtype = _DT_IN[t.dtype]
+    img.batch, img.h, img.w = t.shape
+    img.batch_stride = t.stride(0) if t.shape[0] > 1 else t.shape[1] * t.stride(1)
+    img.row_stride = t.stride(1)
+    return img, t
+
+
+def _alloc_out(mode: int, layout: int, q: int, img: FhtImage, plan, device) -> tuple[FhtHough, torch.Tensor]:
+    d = FhtHough()
+    _lib.check("fht_hough_describe",
+               _lib.lib.fht_hough_describe(mode, layout, q, ctypes.byref(img),
+                                           ctypes.byref(plan) if plan is not None else None, ctypes.byref(d)))
+    storage = torch.empty(d.batch * d.batch_stride, dtype=_DT_OUT[d.dtype], device=device)
+    d.data = storage.data_ptr()
+    return d, storage
+
+
+def workspace_bytes(mode: int, img: FhtImage, plan=None) -> int:
+    return int(_lib.lib.fht_workspace_bytes(mode, ctypes.byref(img), ctypes.byref(plan) if plan is not None else None))
+
+
+def _workspace(nbytes: int, device, workspace: torch.Tensor | None):
+    if workspace is not None:
+        if workspace.numel() * workspace.element_size() < nbytes:
+            raise ValueError("workspace too small")
+        return workspace
+    return torch.empty(max(nbytes, 16), dtype=torch.uint8, device=device)
+
+
+def _stream(t: torch.Tensor):
+    return ctypes.c_void_p(torch.cuda.current_stream(t.device).cuda_stream)
+
+
+def quadrant(t: torch.Tensor, q: int, pad: int | None = None, shifted: bool = False,
+             workspace: torch.Tensor | None = None) -> HoughImage:
+    img, t = _image(t)
+    d, storage = _alloc_out(FHT_MODE_QUADRANT, 0, q, img, None, t.device)
+    d.shifted = int(shifted)
+    ws_n = workspace_bytes(FHT_MODE_QUADRANT, img)
+    ws = _workspace(ws_n, t.device, workspace)
+    n = _lib.check("fht_quadrant", _lib.lib.fht_quadrant(ctypes.byref(img), q, -1 if pad is None else pad,
+                                                          ctypes.byref(d), ws.data_ptr(), ws_n, _stream(t)))
+    h = HoughImage(storage, d)
+    h.launches = n
+    return h
+
+
+def full(t: torch.Tensor, layout: str = "quads", shifted: bool = False,
+         workspace: torch.Tensor | None = None, out: HoughImage | None = None) -> HoughImage:
+    img, t = _image(t)
+    lay = _LAYOUTS[layout]
+    if out is None:
+        d, storage = _alloc_out(FHT_MODE_FULL, lay, 0, img, None, t.device)
+        out = HoughImage(storage, d)
+    out.desc.shifted = int(shifted)
+    ws_n = workspace_bytes(FHT_MODE_FULL, img)
+    ws = _workspace(ws_n, t.device, workspace)
+    out.launches = _lib.check("fht_full", _lib.lib.fht_full(ctypes.byref(img), lay, ctypes.byref(out.desc), ws.data_ptr(), ws_n,
+                                              _stream(t)))
+    return out
+
+
+def angle_plan(h: int, w: int, theta_min_deg: float, theta_max_deg: float) -> FhtAnglePlan:
+    p = FhtAnglePlan()
+    _lib.check("fht_angle_plan_make", _lib.lib.fht_angle_plan_make(h, w, float(theta_min_deg),
+                                                                    float(theta_max_deg), ctypes.byref(p)))
+    return p
+
+
+def angle_range(t: torch.Tensor, plan: FhtAnglePlan, shifted: bool = False,
+                workspace: torch.Tensor | None = None, out: HoughImage | None = None) -> HoughImage:
+    img, t = _image(t)
+    if out is None:
+        d, storage = _alloc_out(FHT_MODE_RANGE, 0, 0, img, plan, t.device)
+        out = HoughImage(storage, d)
+    out.desc.shifted = int(shifted)
+    ws_n = workspace_bytes(FHT_MODE_RANGE, img, plan)
+    ws = _workspace(ws_n, t.device, workspace)
+    out.launches = _lib.check("fht_angle_range", _lib.lib.fht_angle_range(ctypes.byref(img), ctypes.byref(plan),
+                                                            ctypes.byref(out.desc), ws.data_ptr(), ws_n, _stream(t)))
+    return out
+
+
+def fhtshift(h: HoughImage, out: HoughImage | None = None) -> HoughImage:
+    if out is None:
+        d = FhtHough.from_buffer_copy(h.desc)
+        storage = torch.empty_like(h.storage)
+        d.data = storage.data_ptr()
+        out = HoughImage(storage, d)
+    out.desc.shifted = 0
+    out.launches = _lib.check("fhtshift", _lib.lib.fhtshift(ctypes.byref(h.desc), ctypes.byref(out.desc), _stream(h.storage)))
+    return out

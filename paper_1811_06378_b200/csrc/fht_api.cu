@@ -1,0 +1,604 @@
+// fht_api.cu -- C ABI (include/fht.h) and host dispatch for libfht.so.
+//
+// Host side: argument validation, frame geometry, the pass split m + L = K, batch
+// chunking so one chunk's pass-1 scratch stays L2-resident, and the launches. No device
+// memory is allocated here; scratch and tables live in the caller's workspace.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+
+#include "../../include/fht.h"
+#include "fht_kernels.cuh"
+
+namespace {
+
+using namespace fht;
+
+constexpr size_t kScratchBudget = size_t(48) << 20;  // bytes of pass-1 scratch per chunk
+
+int64_t next_pow2(int64_t n) {
+  int64_t p = 1;
+  while (p < n) p <<= 1;
+  return p;
+}
+int ilog2(int64_t p) {
+  int k = 0;
+  while ((int64_t(1) << k) < p) ++k;
+  return k;
+}
+size_t dtype_size(int dt) { return dt == FHT_U8 ? 1 : 4; }
+int out_dtype(int in_dt) { return in_dt == FHT_F32 ? FHT_F32 : FHT_I32; }
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// Frame of one orientation (mostly-horizontal quadrants use the transposed image).
+struct Frame {
+  int transposed;
+  int Hp, K;        // FHT rows (power of two), K = log2 Hp
+  int wc;           // content width (columns that may hold pixels: image cols, or Wp in FULL)
+  int W;            // cyclic width wc + Hp
+  int rows_avail;   // FHT rows actually backed by the image
+  int cols_avail;   // FHT columns actually backed by the image
+  int m, L;         // pass split
+};
+
+void split_levels(Frame& f) {
+  f.m = (f.K + 1) / 2;
+  f.L = f.K - f.m;
+}
+
+Frame make_frame(int64_t h, int64_t w, int transposed, int full) {
+  Frame f{};
+  f.transposed = transposed;
+  const int64_t rows = transposed ? w : h, cols = transposed ? h : w;
+  f.Hp = (int)next_pow2(rows);
+  f.K = ilog2(f.Hp);
+  f.wc = full ? (int)next_pow2(cols) : (int)cols;  // R9: FULL pads both dims to powers of two
+  f.W = f.wc + f.Hp;
+  f.rows_avail = (int)rows;
+  f.cols_avail = (int)cols;
+  split_levels(f);
+  return f;
+}
+
+int check_image(const fht_image* img) {
+  if (!img || !img->data) return FHT_ERR_ARG;
+  if (img->dtype != FHT_U8 && img->dtype != FHT_I32 && img->dtype != FHT_F32) return FHT_ERR_DTYPE;
+  if (img->batch < 1 || img->h < 1 || img->w < 1) return FHT_ERR_ARG;
+  if (img->row_stride < img->w || (img->batch > 1 && img->batch_stride < img->h * img->row_stride))
+    return FHT_ERR_ARG;
+  if (img->h > (1 << 20) || img->w > (1 << 20)) return FHT_ERR_UNSUPPORTED;
+  const size_t es = dtype_size(img->dtype);
+  if ((reinterpret_cast<uintptr_t>(img->data) % es) != 0) return FHT_ERR_ALIGN;
+  return FHT_OK;
+}
+
+int check_frame_supported(const Frame& f) {
+  if (f.m > kMaxLog || f.L > kMaxLog) return FHT_ERR_UNSUPPORTED;  // Hp > 4096 needs 3 passes
+  if ((int64_t)f.W + 2 * f.Hp > (int64_t(1) << 30)) return FHT_ERR_UNSUPPORTED;
+  return FHT_OK;
+}
+
+int scratch_width(const Frame& f) {
+  const int ws = f.wc + (1 << f.m) - 1;
+  return (ws + 3) & ~3;  // 16-byte rows
+}
+
+// Pass-1 scratch bytes for one image and `nq` quadrant slots.
+size_t scratch_bytes_per_image(const Frame& f, int nq) {
+  return (size_t)nq * f.Hp * scratch_width(f) * 4;
+}
+
+int chunk_images(size_t per_image, int64_t batch) {
+  int64_t c = (int64_t)(kScratchBudget / (per_image ? per_image : 1));
+  if (c < 1) c = 1;
+  if (c > batch) c = batch;
+  return (int)c;
+}
+
+// ---------------------------------------------------------------- launch helpers
+template <typename Tin, int LOGR>
+cudaError_t launch_pass1_t(dim3 grid, const Pass1Args& a, cudaStream_t st) {
+  using A = typename AccOf<Tin>::type;
+  constexpr int R = 1 << LOGR;
+  const size_t smem = 2 * (size_t)R * tile_pitch(R) * sizeof(A);
+  static const cudaError_t attr =
+      cudaFuncSetAttribute(k_pass1<Tin, LOGR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (attr != cudaSuccess) return attr;
+  k_pass1<Tin, LOGR><<<grid, kThreads, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+template <typename Tin>
+cudaError_t launch_pass1(int logr, dim3 grid, const Pass1Args& a, cudaStream_t st) {
+  switch (logr) {
+    case 0: return launch_pass1_t<Tin, 0>(grid, a, st);
+    case 1: return launch_pass1_t<Tin, 1>(grid, a, st);
+    case 2: return launch_pass1_t<Tin, 2>(grid, a, st);
+    case 3: return launch_pass1_t<Tin, 3>(grid, a, st);
+    case 4: return launch_pass1_t<Tin, 4>(grid, a, st);
+    case 5: return launch_pass1_t<Tin, 5>(grid, a, st);
+    case 6: return launch_pass1_t<Tin, 6>(grid, a, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+template <typename A, int LOGR>
+cudaError_t launch_pass2_t(dim3 grid, const Pass2Args& a, cudaStream_t st) {
+  constexpr int R = 1 << LOGR;
+  const size_t smem = 2 * (size_t)R * tile_pitch(R) * sizeof(A);
+  static const cudaError_t attr =
+      cudaFuncSetAttribute(k_pass2<A, LOGR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (attr != cudaSuccess) return attr;
+  k_pass2<A, LOGR><<<grid, kThreads, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+template <typename A>
+cudaError_t launch_pass2(int logr, dim3 grid, const Pass2Args& a, cudaStream_t st) {
+  switch (logr) {
+    case 0: return launch_pass2_t<A, 0>(grid, a, st);
+    case 1: return launch_pass2_t<A, 1>(grid, a, st);
+    case 2: return launch_pass2_t<A, 2>(grid, a, st);
+    case 3: return launch_pass2_t<A, 3>(grid, a, st);
+    case 4: return launch_pass2_t<A, 4>(grid, a, st);
+    case 5: return launch_pass2_t<A, 5>(grid, a, st);
+    case 6: return launch_pass2_t<A, 6>(grid, a, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+// One orientation's quadrant slots (1 or 2), with output placement.
+struct Slot {
+  int sigma;
+  int64_t out_q_offset;  // element offset of the quadrant's row 0 inside one output image
+  int row_base, row_sign, skip_t;
+};
+
+struct RangeDev {
+  const int* e_tab;
+  const int* colmap;
+  const int* start_tab;
+  const int* len_tab;
+  int w_content, x_lo, x_hi;  // scratch signed x range (pass 1)
+  int out_lo, out_hi;         // signed x range covered by pass 2 tiles
+};
+
+// Run the two passes for one orientation over all images, chunked. Returns launches or error.
+int run_orientation(const fht_image* img, const Frame& f, const Slot* slots, int nq, const fht_hough* out,
+                    void* ws, size_t ws_bytes, cudaStream_t st, const RangeDev* rg, int shift_mode) {
+  const int Ws = rg ? ((rg->x_hi - rg->x_lo + 3) & ~3) : scratch_width(f);
+  const size_t per_img = (size_t)nq * f.Hp * Ws * 4;
+  const int chunk = rg ? 1 : chunk_images(per_img, img->batch);
+  if (ws_bytes < per_img * chunk || !ws) return FHT_ERR_WORKSPACE;
+  const int nstrips = 1 << f.L, ngroups = 1 << f.m;
+  int launches = 0;
+  for (int64_t b0 = 0; b0 < img->batch; b0 += chunk) {
+    const int nb = (int)((img->batch - b0) < chunk ? (img->batch - b0) : chunk);
+    Pass1Args p1{};
+    p1.img = img->data;
+    p1.img_bstride = img->batch_stride;
+    p1.img_rstride = img->row_stride;
+    p1.img_rows = f.rows_avail;
+    p1.img_cols = f.cols_avail;
+    p1.transposed = f.transposed;
+    p1.scratch = ws;
+    p1.scratch_zstride = (int64_t)f.Hp * Ws;
+    p1.L = f.L;
+    p1.Ws = Ws;
+    p1.nq = nq;
+    p1.img0 = (int)b0;
+    for (int q = 0; q < nq; ++q) {
+      p1.sigma[q] = slots[q].sigma;
+      p1.xlo[q] = rg ? rg->x_lo : (slots[q].sigma > 0 ? -((1 << f.m) - 1) : 0);
+    }
+    if (rg) {
+      p1.range = 1;
+      p1.e_tab = rg->e_tab;
+      p1.colmap = rg->colmap;
+      p1.w_content = rg->w_content;
+    }
+    const int ntile1 = (Ws + kTileX - 1) / kTileX;
+    dim3 g1(ntile1, nstrips, nb * nq);
+    cudaError_t e;
+    switch (img->dtype) {
+      case FHT_U8: e = launch_pass1<uint8_t>(f.m, g1, p1, st); break;
+      case FHT_I32: e = launch_pass1<int32_t>(f.m, g1, p1, st); break;
+      default: e = launch_pass1<float>(f.m, g1, p1, st); break;
+    }
+    if (e != cudaSuccess) return FHT_ERR_CUDA;
+    ++launches;
+
+    Pass2Args p2{};
+    p2.scratch = ws;
+    p2.scratch_zstride = p1.scratch_zstride;
+    p2.Ws = Ws;
+    p2.m = f.m;
+    p2.L = f.L;
+    p2.out = out->data;
+    p2.out_img_stride = out->batch_stride;
+    p2.out_row_stride = out->row_stride;
+    p2.W = rg ? (int)out->cols : f.W;
+    p2.wc = f.wc;
+    p2.Hp = f.Hp;
+    p2.nq = nq;
+    p2.img0 = (int)b0;
+    p2.shift = shift_mode;
+    int span = p2.W;
+    for (int q = 0; q < nq; ++q) {
+      p2.sigma[q] = slots[q].sigma;
+      p2.xlo[q] = p1.xlo[q];
+      p2.out_q_offset[q] = slots[q].out_q_offset;
+      p2.row_base[q] = slots[q].row_base;
+      p2.row_sign[q] = slots[q].row_sign;
+      p2.skip_t[q] = slots[q].skip_t;
+      p2.xbeg[q] = rg ? rg->out_lo : (slots[q].sigma > 0 ? -f.Hp : 0);
+    }
+    if (rg) {
+      p2.range = 1;
+      p2.start_tab = rg->start_tab;
+      p2.len_tab = rg->len_tab;
+      span = rg->out_hi - rg->out_lo;
+    }
+    const int ntile2 = (span + kTileX - 1) / kTileX;
+    dim3 g2(ntile2, ngroups, nb * nq);
+    e = img->dtype == FHT_F32 ? launch_pass2<float>(f.L, g2, p2, st) : launch_pass2<int>(f.L, g2, p2, st);
+    if (e != cudaSuccess) return FHT_ERR_CUDA;
+    ++launches;
+  }
+  return launches;
+}
+
+int validate_out(const fht_hough* out, const fht_hough& want) {
+  if (!out || !out->data) return FHT_ERR_ARG;
+  if (out->dtype != want.dtype) return FHT_ERR_DTYPE;
+  if (out->mode != want.mode || out->batch != want.batch || out->nquad != want.nquad ||
+      out->rows != want.rows || out->cols != want.cols)
+    return FHT_ERR_SHAPE;
+  if (want.mode == FHT_MODE_FULL && out->layout != want.layout) return FHT_ERR_SHAPE;
+  if (out->row_stride < out->cols) return FHT_ERR_SHAPE;
+  if (out->nquad > 1 && out->quad_stride < out->rows * out->row_stride) return FHT_ERR_SHAPE;
+  if (out->batch > 1 && out->batch_stride < out->nquad * (out->nquad > 1 ? out->quad_stride : out->rows * out->row_stride))
+    return FHT_ERR_SHAPE;
+  if ((reinterpret_cast<uintptr_t>(out->data) & 3u) != 0) return FHT_ERR_ALIGN;
+  return FHT_OK;
+}
+
+bool overlaps(const void* a, size_t an, const void* b, size_t bn) {
+  const char* pa = static_cast<const char*>(a);
+  const char* pb = static_cast<const char*>(b);
+  return pa < pb + bn && pb < pa + an;
+}
+size_t image_extent_bytes(const fht_image* img) {
+  return ((size_t)(img->batch - 1) * img->batch_stride + (size_t)(img->h - 1) * img->row_stride + img->w) *
+         dtype_size(img->dtype);
+}
+size_t hough_extent_bytes(const fht_hough* h) {
+  const int64_t qs = h->nquad > 1 ? h->quad_stride : 0;
+  return ((size_t)(h->batch - 1) * h->batch_stride + (size_t)(h->nquad - 1) * qs + (size_t)(h->rows - 1) * h->row_stride +
+          h->cols) * 4;
+}
+
+// Plan geometry helpers (R13, R16, R17): identical double formulas to the device tables.
+int plan_e(double g, int64_t y) {
+  volatile double p = g * (double)y;  // volatile: forbid contraction into an FMA
+  return (int)std::floor(p + 0.5);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* fht_status_string(int s) {
+  if (s >= 0) return "ok";
+  switch (s) {
+    case FHT_ERR_ARG: return "invalid argument";
+    case FHT_ERR_DTYPE: return "unsupported dtype";
+    case FHT_ERR_SHAPE: return "output shape mismatch";
+    case FHT_ERR_ALIGN: return "pointer or pitch not 16-byte aligned";
+    case FHT_ERR_UNSUPPORTED: return "unsupported on the GPU path";
+    case FHT_ERR_WORKSPACE: return "workspace missing or too small";
+    case FHT_ERR_STATE: return "descriptor already shifted";
+    case FHT_ERR_CUDA: return "CUDA error";
+  }
+  return "unknown status";
+}
+
+int fht_angle_plan_make(int64_t h, int64_t w, double tmin, double tmax, fht_angle_plan* out) {
+  if (!out || h < 1 || w < 1) return FHT_ERR_ARG;
+  if (!(tmin > -90.0 && tmin < tmax && tmax < 90.0)) return FHT_ERR_ARG;
+  const double deg = M_PI / 180.0;
+  const double k_lo = std::tan(tmin * deg), k_hi = std::tan(tmax * deg);
+  const double alpha = 1.0 / (k_hi - k_lo);
+  if (!(alpha * (double)w >= 1.0)) return FHT_ERR_ARG;
+  const int64_t Hp = next_pow2(h);
+  if (Hp > 4096 || h > 4096) return FHT_ERR_UNSUPPORTED;
+  const int64_t w_content = (int64_t)std::ceil(alpha * (double)w - 1e-9);
+  const double g = alpha * (-k_lo);
+  // e_y and the largest per-row spread of e_y - D_s(y) over y < h (R17)
+  const int K = ilog2(Hp);
+  int* e = new int[h];
+  int* D = new int[h];
+  int e_min = 1 << 30, e_max = -(1 << 30);
+  for (int64_t y = 0; y < h; ++y) {
+    e[y] = plan_e(g, y);
+    e_min = e[y] < e_min ? e[y] : e_min;
+    e_max = e[y] > e_max ? e[y] : e_max;
+  }
+  int64_t spread_max = 0;
+  for (int64_t s = 0; s < Hp; ++s) {
+    // D_s(y) by lowest-set-bit recurrence: bit p of y carries weight ceil((s >> (K-1-p))/2)
+    int mn = 1 << 30, mx = -(1 << 30);
+    for (int64_t y = 0; y < h; ++y) {
+      if (y == 0) D[0] = 0;
+      else {
+        const int64_t low = y & (-y);
+        const int p = ilog2(low);
+        D[y] = D[y & (y - 1)] + (int)(((s >> (K - 1 - p)) + 1) >> 1);
+      }
+      const int v = e[y] - D[y];
+      mn = v < mn ? v : mn;
+      mx = v > mx ? v : mx;
+    }
+    if (mx - mn > spread_max) spread_max = mx - mn;
+  }
+  delete[] e;
+  delete[] D;
+  fht_angle_plan p{};
+  p.theta_min_deg = tmin;
+  p.theta_max_deg = tmax;
+  p.k_lo = k_lo;
+  p.k_hi = k_hi;
+  p.alpha = alpha;
+  p.g = g;
+  p.h = h;
+  p.w = w;
+  p.Hp = Hp;
+  p.w_content = w_content;
+  p.W = w_content + (Hp > spread_max + 1 ? Hp : spread_max + 1);
+  p.e_min = e_min;
+  p.e_max = e_max;
+  *out = p;
+  return FHT_OK;
+}
+
+int fht_hough_describe(int mode, int layout, int quadrant, const fht_image* img, const fht_angle_plan* plan,
+                       fht_hough* out) {
+  if (!img || !out) return FHT_ERR_ARG;
+  if (img->dtype != FHT_U8 && img->dtype != FHT_I32 && img->dtype != FHT_F32) return FHT_ERR_DTYPE;
+  if (img->batch < 1 || img->h < 1 || img->w < 1) return FHT_ERR_ARG;
+  fht_hough d{};
+  d.dtype = out_dtype(img->dtype);
+  d.mode = mode;
+  d.layout = layout;
+  d.batch = img->batch;
+  d.h = img->h;
+  d.w = img->w;
+  d.Hp = next_pow2(img->h);
+  d.Wp = next_pow2(img->w);
+  d.quadrant = quadrant;
+  if (mode == FHT_MODE_QUADRANT) {
+    if (quadrant < 0 || quadrant > 3) return FHT_ERR_ARG;
+    const bool tr = quadrant >= 2;
+    d.nquad = 1;
+    d.rows = tr ? d.Wp : d.Hp;
+    d.cols = tr ? img->h + d.Wp : img->w + d.Hp;
+  } else if (mode == FHT_MODE_FULL) {
+    if (layout == FHT_LAYOUT_QUADS) {
+      d.nquad = 4;
+      d.rows = d.Hp > d.Wp ? d.Hp : d.Wp;
+    } else if (layout == FHT_LAYOUT_CONCAT) {
+      d.nquad = 1;
+      d.rows = 2 * (d.Hp + d.Wp) - 3;
+    } else {
+      return FHT_ERR_ARG;
+    }
+    d.cols = d.Hp + d.Wp;
+  } else if (mode == FHT_MODE_RANGE) {
+    if (!plan || plan->h != img->h || plan->w != img->w) return FHT_ERR_ARG;
+    d.nquad = 1;
+    d.rows = plan->Hp;
+    d.cols = plan->W;
+    d.plan = *plan;
+  } else {
+    return FHT_ERR_ARG;
+  }
+  d.row_stride = (d.cols + 3) & ~int64_t(3);
+  d.quad_stride = d.rows * d.row_stride;
+  d.batch_stride = d.nquad * d.quad_stride;
+  *out = d;
+  return FHT_OK;
+}
+
+size_t fht_workspace_bytes(int mode, const fht_image* img, const fht_angle_plan* plan) {
+  if (!img || img->batch < 1 || img->h < 1 || img->w < 1) return 0;
+  if (mode == FHT_MODE_RANGE) {
+    if (!plan) return 0;
+    const int m = (ilog2(plan->Hp) + 1) / 2;
+    const int64_t x_lo = plan->e_min - ((1 << m) - 1), x_hi = plan->e_max + plan->w_content;
+    const int64_t Ws = (x_hi - x_lo + 3) & ~int64_t(3);
+    const size_t tables = (size_t)(plan->h + plan->w_content + 2 * plan->Hp + 64) * 4;
+    return (size_t)plan->Hp * Ws * 4 + ((tables + 255) & ~size_t(255));
+  }
+  size_t need = 0;
+  for (int tr = 0; tr < 2; ++tr) {
+    const Frame f = make_frame(img->h, img->w, tr, mode == FHT_MODE_FULL);
+    const int nq = mode == FHT_MODE_FULL ? 2 : 1;
+    const size_t per = scratch_bytes_per_image(f, nq);
+    const size_t tot = per * chunk_images(per, img->batch);
+    need = tot > need ? tot : need;
+  }
+  return need;
+}
+
+int fht_quadrant(const fht_image* img, int quadrant, int64_t pad_cols, fht_hough* out, void* ws, size_t ws_bytes,
+                 fht_stream_t stream) {
+  int s = check_image(img);
+  if (s) return s;
+  if (quadrant < 0 || quadrant > 3) return FHT_ERR_ARG;
+  fht_hough want;
+  s = fht_hough_describe(FHT_MODE_QUADRANT, 0, quadrant, img, nullptr, &want);
+  if (s) return s;
+  const Frame f = make_frame(img->h, img->w, quadrant >= 2, 0);
+  if (pad_cols != -1 && pad_cols != f.Hp) return FHT_ERR_UNSUPPORTED;
+  if ((s = validate_out(out, want))) return s;
+  if (out->quadrant != quadrant) return FHT_ERR_ARG;
+  if ((s = check_frame_supported(f))) return s;
+  if (overlaps(img->data, image_extent_bytes(img), out->data, hough_extent_bytes(out))) return FHT_ERR_ARG;
+  if (ws && overlaps(ws, ws_bytes, out->data, hough_extent_bytes(out))) return FHT_ERR_ARG;
+  Slot sl{};
+  sl.sigma = (quadrant == FHT_QA || quadrant == FHT_QD) ? 1 : -1;
+  sl.out_q_offset = 0;
+  sl.row_base = 0;
+  sl.row_sign = 1;
+  sl.skip_t = -1;
+  return run_orientation(img, f, &sl, 1, out, ws, ws_bytes, (cudaStream_t)stream, nullptr, out->shifted ? 1 : 0);
+}
+
+int fht_full(const fht_image* img, int layout, fht_hough* out, void* ws, size_t ws_bytes, fht_stream_t stream) {
+  int s = check_image(img);
+  if (s) return s;
+  fht_hough want;
+  if ((s = fht_hough_describe(FHT_MODE_FULL, layout, 0, img, nullptr, &want))) return s;
+  if ((s = validate_out(out, want))) return s;
+  if (overlaps(img->data, image_extent_bytes(img), out->data, hough_extent_bytes(out))) return FHT_ERR_ARG;
+  if (ws && overlaps(ws, ws_bytes, out->data, hough_extent_bytes(out))) return FHT_ERR_ARG;
+  const int Hp = (int)want.Hp, Wp = (int)want.Wp;
+  int launches = 0;
+  for (int tr = 0; tr < 2; ++tr) {
+    const Frame f = make_frame(img->h, img->w, tr, 1);
+    if ((s = check_frame_supported(f))) return s;
+    Slot sl[2];
+    // orientation 0: QA (+), QB (-); orientation 1: QC (-), QD (+)   (R4)
+    const int qid[2] = {tr ? FHT_QC : FHT_QA, tr ? FHT_QD : FHT_QB};
+    for (int k = 0; k < 2; ++k) {
+      const int q = qid[k];
+      sl[k].sigma = (q == FHT_QA || q == FHT_QD) ? 1 : -1;
+      if (layout == FHT_LAYOUT_QUADS) {
+        sl[k].out_q_offset = (int64_t)q * out->quad_stride;
+        sl[k].row_base = 0;
+        sl[k].row_sign = 1;
+        sl[k].skip_t = -1;
+      } else {  // CONCAT (R7, R8)
+        sl[k].out_q_offset = 0;
+        switch (q) {
+          case FHT_QA: sl[k].row_base = Hp - 1; sl[k].row_sign = -1; sl[k].skip_t = -1; break;
+          case FHT_QB: sl[k].row_base = Hp - 1; sl[k].row_sign = 1; sl[k].skip_t = 0; break;
+          case FHT_QC: sl[k].row_base = 2 * Hp - 2 + Wp - 1; sl[k].row_sign = -1; sl[k].skip_t = Wp - 1; break;
+          default: sl[k].row_base = 2 * Hp + Wp - 3; sl[k].row_sign = 1; sl[k].skip_t = 0; break;
+        }
+      }
+    }
+    const int r = run_orientation(img, f, sl, 2, out, ws, ws_bytes, (cudaStream_t)stream, nullptr,
+                                  out->shifted ? 1 : 0);
+    if (r < 0) return r;
+    launches += r;
+  }
+  return launches;
+}
+
+int fht_angle_range(const fht_image* img, const fht_angle_plan* plan, fht_hough* out, void* ws, size_t ws_bytes,
+                    fht_stream_t stream) {
+  int s = check_image(img);
+  if (s) return s;
+  if (!plan || plan->h != img->h || plan->w != img->w) return FHT_ERR_ARG;
+  fht_hough want;
+  if ((s = fht_hough_describe(FHT_MODE_RANGE, 0, 0, img, plan, &want))) return s;
+  if ((s = validate_out(out, want))) return s;
+  if (overlaps(img->data, image_extent_bytes(img), out->data, hough_extent_bytes(out))) return FHT_ERR_ARG;
+  const size_t need = fht_workspace_bytes(FHT_MODE_RANGE, img, plan);
+  if (!ws || ws_bytes < need) return FHT_ERR_WORKSPACE;
+  if (overlaps(ws, ws_bytes, out->data, hough_extent_bytes(out))) return FHT_ERR_ARG;
+  Frame f{};
+  f.transposed = 0;
+  f.Hp = (int)plan->Hp;
+  f.K = ilog2(f.Hp);
+  f.wc = (int)plan->w_content;
+  f.W = (int)plan->W;
+  f.rows_avail = (int)img->h;
+  f.cols_avail = (int)img->w;
+  split_levels(f);
+  if ((s = check_frame_supported(f))) return s;
+  // workspace: [scratch][e_tab h][colmap w'][start Hp][len Hp]
+  const int x_lo = (int)plan->e_min - ((1 << f.m) - 1), x_hi = (int)(plan->e_max + plan->w_content);
+  const int Ws = (x_hi - x_lo + 3) & ~3;
+  const size_t scratch = (size_t)f.Hp * Ws * 4;
+  int* tab = reinterpret_cast<int*>(static_cast<char*>(ws) + scratch);
+  RangeDev rg{};
+  rg.e_tab = tab;
+  rg.colmap = tab + img->h;
+  rg.start_tab = tab + img->h + plan->w_content;
+  rg.len_tab = rg.start_tab + f.Hp;
+  rg.w_content = (int)plan->w_content;
+  rg.x_lo = x_lo;
+  rg.x_hi = x_hi;
+  // pass-2 signed columns: [min_s start_s, max_s start_s + W'); start_s in [e_min-(Hp-1), e_max]
+  rg.out_lo = (int)plan->e_min - (f.Hp - 1);
+  rg.out_hi = (int)plan->e_max + (int)plan->W;
+  RangeTableArgs ta{};
+  ta.g = plan->g;
+  ta.alpha = plan->alpha;
+  ta.h = (int)img->h;
+  ta.w = (int)img->w;
+  ta.w_content = (int)plan->w_content;
+  ta.Hp = f.Hp;
+  ta.K = f.K;
+  ta.e_tab = const_cast<int*>(rg.e_tab);
+  ta.colmap = const_cast<int*>(rg.colmap);
+  ta.start_tab = const_cast<int*>(rg.start_tab);
+  ta.len_tab = const_cast<int*>(rg.len_tab);
+  const int nb_tab = f.Hp + (int)((std::max<int64_t>(img->h, plan->w_content) + kThreads - 1) / kThreads);
+  k_range_tables<<<nb_tab, kThreads, 0, (cudaStream_t)stream>>>(ta);
+  if (cudaGetLastError() != cudaSuccess) return FHT_ERR_CUDA;
+  Slot sl{};
+  sl.sigma = 1;
+  sl.row_sign = 1;
+  sl.skip_t = -1;
+  const int r = run_orientation(img, f, &sl, 1, out, ws, scratch, (cudaStream_t)stream, &rg, out->shifted ? 2 : 0);
+  return r < 0 ? r : r + 1;
+}
+
+int fhtshift(const fht_hough* in, fht_hough* out, fht_stream_t stream) {
+  if (!in || !out || !in->data || !out->data) return FHT_ERR_ARG;
+  if (in->shifted) return FHT_ERR_STATE;
+  if (in->dtype != out->dtype || (in->dtype != FHT_I32 && in->dtype != FHT_F32)) return FHT_ERR_DTYPE;
+  if (in->mode != out->mode || in->layout != out->layout || in->batch != out->batch || in->nquad != out->nquad ||
+      in->rows != out->rows || in->cols != out->cols || in->Hp != out->Hp || in->Wp != out->Wp ||
+      in->quadrant != out->quadrant)
+    return FHT_ERR_SHAPE;
+  if (overlaps(in->data, hough_extent_bytes(in), out->data, hough_extent_bytes(out))) return FHT_ERR_ARG;
+  if (in->rows < 1 || in->cols < 1 || in->batch < 1) return FHT_ERR_ARG;
+  ShiftArgs a{};
+  a.in = in->data;
+  a.out = out->data;
+  a.in_img_stride = in->batch_stride;
+  a.in_q_stride = in->quad_stride;
+  a.in_row_stride = in->row_stride;
+  a.out_img_stride = out->batch_stride;
+  a.out_q_stride = out->quad_stride;
+  a.out_row_stride = out->row_stride;
+  a.rows = (int)in->rows;
+  a.W = (int)in->cols;
+  a.nquad = (int)in->nquad;
+  a.mode = in->mode;
+  a.layout = in->layout;
+  a.quadrant = in->quadrant;
+  if (in->mode == FHT_MODE_QUADRANT) {
+    a.Hp = a.Wp = (int)in->rows;  // the quadrant's own row count
+  } else if (in->mode == FHT_MODE_FULL) {
+    a.Hp = (int)in->Hp;
+    a.Wp = (int)in->Wp;
+  } else {
+    a.g = in->plan.g;
+    a.h = (int)in->plan.h;
+    a.K = ilog2(in->plan.Hp);
+    a.w_content = (int)in->plan.w_content;
+  }
+  dim3 grid((unsigned)in->rows, (unsigned)(in->batch * in->nquad));
+  if (in->dtype == FHT_F32) k_fhtshift<float><<<grid, kThreads, 0, (cudaStream_t)stream>>>(a);
+  else k_fhtshift<int><<<grid, kThreads, 0, (cudaStream_t)stream>>>(a);
+  if (cudaGetLastError() != cudaSuccess) return FHT_ERR_CUDA;
+  out->shifted = 1;
+  return 1;
+}
+
+}  // extern "C"

@@ -1,0 +1,374 @@
+// fht_kernels.cuh -- sm_100a kernels of the FHT hot path.
+//
+//   k_pass1   : SURVEY a3 -- levels 1..m of a 2^m-row strip, loaded once from the image
+//               (row or transposed loads = quadrant handling by index transposition, a1),
+//               optional §4 shear+scale loader (a6). Writes F_m to scratch.
+//   k_pass2   : SURVEY a4 -- levels m+1..K of one group j through the pre-shear identity,
+//               black-zone tiles written as zeros without loads, store addressing for the
+//               QUADS / CONCAT layouts (a5) and an optional fused fhtshift (§5).
+//   k_fhtshift: SURVEY a7 -- standalone per-row cyclic rotation.
+//   k_range_tables : §4 per-row shear offsets e_y, scale map colmap[u] and per-row support.
+#pragma once
+#include "fht_common.cuh"
+
+namespace fht {
+
+constexpr int kThreads = 256;
+constexpr int kTileX = 128;  // output columns per tile (both passes)
+
+// ------------------------------------------------------------------------------------------
+// In-tile butterfly (north_star; Fig. 6). Rows 0..R-1 of `src` hold R input
+// rows; local column c holds signed x = X + c (sigma=+1) or X + TX-1-c (sigma=-1), so the
+// shifted partner is always at c + ceil(t/2) ("halo" columns [TX, TX+R-1) on the right).
+// After level k the block of 2^k rows starting at row r0 holds shifts t = 0..2^k-1:
+//   dst[r0 + t][c] = src[r0 + (t>>1)][c] + src[r0 + 2^(k-1) + (t>>1)][c + ceil(t/2)].
+// Returns the buffer holding the final R rows (shift u in row u).
+// ------------------------------------------------------------------------------------------
+template <int LOGR, typename A>
+__device__ __forceinline__ A* tile_levels(A* src, A* dst, int pitch, int TX) {
+  constexpr int R = 1 << LOGR;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+#pragma unroll 1
+  for (int k = 1; k <= LOGR; ++k) {
+    const int half = 1 << (k - 1);
+    const int valid = TX + R - (1 << k);  // columns still needed by the levels above
+    for (int row = warp; row < R; row += nw) {
+      const int t = row & ((1 << k) - 1);
+      const int a = (row - t) + (t >> 1);
+      const A* pa = src + a * pitch;
+      const A* pb = src + (a + half) * pitch + ((t + 1) >> 1);
+      A* pd = dst + row * pitch;
+      for (int c = lane; c < valid; c += 32) pd[c] = pa[c] + pb[c];
+    }
+    __syncthreads();
+    A* tmp = src;
+    src = dst;
+    dst = tmp;
+  }
+  return src;
+}
+
+__host__ __device__ constexpr int tile_pitch(int R) { return (kTileX + R - 1) | 1; }
+
+// ------------------------------------------------------------------------------------------
+// Pass 1
+// ------------------------------------------------------------------------------------------
+struct Pass1Args {
+  const void* img;
+  int64_t img_bstride, img_rstride;  // elements
+  int img_rows, img_cols;            // FRAME coordinates: FHT rows / cols that hold pixels
+  int transposed;                    // FHT row y = image column, FHT col x = image row
+  void* scratch;                     // [z][2^m][2^L][Ws]
+  int64_t scratch_zstride;
+  int L;                             // log2(#strips)
+  int Ws;                            // scratch row length
+  int xlo[2];                        // signed x of scratch column 0, per quadrant slot
+  int sigma[2];
+  int nq;                            // quadrants per image in this launch (1 or 2)
+  int img0;                          // first image of the chunk
+  // §4 range loader (sigma = +1 only)
+  int range;
+  const int* e_tab;                  // [rows] shear offsets e_y
+  const int* colmap;                 // [w_content]
+  int w_content;
+};
+
+template <typename Tin>
+__device__ __forceinline__ typename AccOf<Tin>::type load_px(const Tin* p) {
+  return static_cast<typename AccOf<Tin>::type>(*p);
+}
+
+template <typename Tin, int LOGR>
+__global__ void __launch_bounds__(kThreads) k_pass1(const Pass1Args a) {
+  using A = typename AccOf<Tin>::type;
+  constexpr int R = 1 << LOGR;
+  constexpr int TX = kTileX;
+  constexpr int WT = TX + R - 1;
+  constexpr int pitch = tile_pitch(R);
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  A* b0 = reinterpret_cast<A*>(smem_raw);
+  A* b1 = b0 + R * pitch;
+
+  const int z = blockIdx.z;
+  const int qi = z % a.nq;
+  const int img = a.img0 + z / a.nq;
+  const int sigma = a.sigma[qi];
+  const int strip = blockIdx.y;
+  const int X = a.xlo[qi] + blockIdx.x * TX;
+  const Tin* src = static_cast<const Tin*>(a.img) + (int64_t)img * a.img_bstride;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+
+  if (!a.transposed) {
+    for (int r = warp; r < R; r += nw) {
+      const int y = strip * R + r;
+      const bool row_ok = y < a.img_rows;
+      const Tin* prow = src + (int64_t)y * a.img_rstride;
+      int e = 0;
+      if (a.range && row_ok) e = a.e_tab[y];
+      for (int c = lane; c < WT; c += 32) {
+        const int x = sigma > 0 ? X + c : X + TX - 1 - c;
+        A v = A(0);
+        if (row_ok) {
+          if (!a.range) {
+            if (x >= 0 && x < a.img_cols) v = load_px(prow + x);
+          } else {  // T(x, y) = I[y][colmap[x - e_y]] (unwrapped; R13, R14)
+            const int u = x - e;
+            if (u >= 0 && u < a.w_content) v = load_px(prow + a.colmap[u]);
+          }
+        }
+        b0[r * pitch + c] = v;
+      }
+    }
+  } else {
+    // FHT row y = image column y, FHT column x = image row x: lanes run along image columns
+    // (coalesced), smem pitch is odd so the column-wise smem writes are conflict-free.
+    for (int c = warp; c < WT; c += nw) {
+      const int x = sigma > 0 ? X + c : X + TX - 1 - c;
+      const bool ok = x >= 0 && x < a.img_cols;
+      const Tin* prow = src + (int64_t)x * a.img_rstride;
+      for (int r = lane; r < R; r += 32) {
+        const int y = strip * R + r;
+        A v = A(0);
+        if (ok && y < a.img_rows) v = load_px(prow + y);
+        b0[r * pitch + c] = v;
+      }
+    }
+  }
+  __syncthreads();
+  A* res = tile_levels<LOGR, A>(b0, b1, pitch, TX);
+
+  A* dst = static_cast<A*>(a.scratch) + (int64_t)z * a.scratch_zstride;
+  const int nstrips = 1 << a.L;
+  for (int t = warp; t < R; t += nw) {
+    A* drow = dst + ((int64_t)t * nstrips + strip) * a.Ws;
+    for (int c = lane; c < TX; c += 32) {
+      const int x = sigma > 0 ? X + c : X + TX - 1 - c;
+      const int col = x - a.xlo[qi];
+      if (col >= 0 && col < a.Ws) drow[col] = res[t * pitch + c];
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// Pass 2
+// ------------------------------------------------------------------------------------------
+struct Pass2Args {
+  const void* scratch;
+  int64_t scratch_zstride;
+  int Ws;
+  int xlo[2];
+  int sigma[2];
+  int m, L;
+  void* out;
+  int64_t out_img_stride, out_row_stride;
+  int64_t out_q_offset[2];  // element offset of the quadrant's row-0 base inside an image
+  int row_base[2], row_sign[2], skip_t[2];  // output row = base + sign*t; t == skip not stored
+  int W, wc, Hp;
+  int xbeg[2];              // signed x of the first output column computed
+  int nq, img0;
+  int shift;                // fused fhtshift: 1 = quadrant rule, 2 = range rule
+  int range;
+  const int* start_tab;     // range: per-row unwrapped support start
+  const int* len_tab;       // range: per-row support length
+};
+
+template <typename A, int LOGR>
+__global__ void __launch_bounds__(kThreads) k_pass2(const Pass2Args a) {
+  constexpr int R = 1 << LOGR;
+  constexpr int TX = kTileX;
+  constexpr int WT = TX + R - 1;
+  constexpr int pitch = tile_pitch(R);
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  A* b0 = reinterpret_cast<A*>(smem_raw);
+  A* b1 = b0 + R * pitch;
+
+  const int z = blockIdx.z;
+  const int qi = z % a.nq;
+  const int img = a.img0 + z / a.nq;
+  const int sigma = a.sigma[qi];
+  const int j = blockIdx.y;
+  const int X = a.xbeg[qi] + blockIdx.x * TX;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int t0 = j << a.L;
+  const int tmax = t0 + R - 1;
+
+  A* outp = static_cast<A*>(a.out) + (int64_t)img * a.out_img_stride + a.out_q_offset[qi];
+
+  bool zero_tile = false;
+  if (!a.range) {  // black zone: sigma=+1 cells x < -t, sigma=-1 cells x >= wc + t
+    zero_tile = sigma > 0 ? (X + TX - 1 < -tmax) : (X >= a.wc + tmax);
+  }
+  A* res = nullptr;
+  if (!zero_tile) {
+    const A* src = static_cast<const A*>(a.scratch) + (int64_t)z * a.scratch_zstride +
+                   (int64_t)(j << a.L) * a.Ws;
+    for (int i = warp; i < R; i += nw) {
+      const A* srow = src + (int64_t)i * a.Ws;
+      const int off = sigma * j * i - a.xlo[qi];  // pre-shear by sigma*j*i
+      for (int c = lane; c < WT; c += 32) {
+        const int x = sigma > 0 ? X + c : X + TX - 1 - c;
+        const int col = x + off;
+        b0[i * pitch + c] = (col >= 0 && col < a.Ws) ? srow[col] : A(0);
+      }
+    }
+    __syncthreads();
+    res = tile_levels<LOGR, A>(b0, b1, pitch, TX);
+  }
+
+  for (int u = warp; u < R; u += nw) {
+    const int t = t0 + u;
+    if (t == a.skip_t[qi]) continue;
+    A* orow = outp + (int64_t)(a.row_base[qi] + a.row_sign[qi] * t) * a.out_row_stride;
+    int lo, hi, k = 0;
+    if (!a.range) {
+      lo = a.xbeg[qi];
+      hi = lo + a.W;
+      if (a.shift) k = sigma > 0 ? ceil_half(a.Hp + t) : ceil_half(a.Hp - t);
+    } else {
+      lo = a.start_tab[t];
+      hi = lo + a.W;
+      if (a.shift) k = ceil_half(a.W - a.len_tab[t]) - lo;
+    }
+    for (int c = lane; c < TX; c += 32) {
+      const int x = sigma > 0 ? X + c : X + TX - 1 - c;
+      if (x < lo || x >= hi) continue;
+      int x0 = x % a.W;
+      if (x0 < 0) x0 += a.W;
+      if (k) {
+        x0 = (x0 + k) % a.W;
+        if (x0 < 0) x0 += a.W;
+      }
+      orow[x0] = zero_tile ? A(0) : res[u * pitch + c];
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// §4 tables: e_y (rows), colmap (w_content), per-row support start/len (Hp rows).
+// Double arithmetic with explicit round-to-nearest intrinsics (no FMA contraction, R16).
+// ------------------------------------------------------------------------------------------
+struct RangeTableArgs {
+  double g, alpha;
+  int h, w, w_content, Hp, K;
+  int* e_tab;     // [h]
+  int* colmap;    // [w_content]
+  int* start_tab; // [Hp]
+  int* len_tab;   // [Hp]
+};
+
+__device__ __forceinline__ int shear_e(double g, int y) {
+  return (int)floor(__dadd_rn(__dmul_rn(g, (double)y), 0.5));
+}
+
+__global__ void k_range_tables(const RangeTableArgs a) {
+  const int b = blockIdx.x;
+  if (b < a.Hp) {  // one block per output row s: reduce e_y - D_s(y) over y < h
+    const int s = b;
+    int mn = INT32_MAX, mx = INT32_MIN;
+    for (int y = threadIdx.x; y < a.h; y += blockDim.x) {
+      const int v = shear_e(a.g, y) - dyadic_offset(a.K, s, y);
+      mn = min(mn, v);
+      mx = max(mx, v);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    __shared__ int smn[32], smx[32];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) { smn[warp] = mn; smx[warp] = mx; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int i = 1; i < (int)(blockDim.x >> 5); ++i) { mn = min(mn, smn[i]); mx = max(mx, smx[i]); }
+      a.start_tab[s] = mn;
+      a.len_tab[s] = mx - mn + a.w_content;
+    }
+    return;
+  }
+  // remaining blocks: e_y and colmap
+  const int idx = (b - a.Hp) * blockDim.x + threadIdx.x;
+  if (idx < a.h) a.e_tab[idx] = shear_e(a.g, idx);
+  if (idx < a.w_content) {
+    const int c = (int)floor(__ddiv_rn((double)idx + 0.5, a.alpha));
+    a.colmap[idx] = min(a.w - 1, c);
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// Standalone fhtshift (R11): out[r][x] = in[r][(x - k_r) mod W].
+// ------------------------------------------------------------------------------------------
+struct ShiftArgs {
+  const void* in;
+  void* out;
+  int64_t in_img_stride, in_q_stride, in_row_stride;
+  int64_t out_img_stride, out_q_stride, out_row_stride;
+  int rows, W, nquad;
+  int mode, layout;   // fht_mode / fht_layout
+  int quadrant;       // QUADRANT mode
+  int Hp, Wp;         // quadrant row counts (QA/QB: Hp, QC/QD: Wp)
+  // range
+  double g;
+  int h, K, w_content;
+};
+
+__device__ __forceinline__ int quadrant_sigma(int q) { return (q == 0 || q == 3) ? 1 : -1; }
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_fhtshift(const ShiftArgs a) {
+  const int r = blockIdx.x;
+  const int zq = blockIdx.y;  // image * nquad + quadrant slot
+  const int img = zq / a.nquad, qs = zq % a.nquad;
+  __shared__ int k_sh;
+  if (a.mode == 2) {  // RANGE: k = ceil((W - len)/2) - start, start/len by reduction over y < h
+    int mn = INT32_MAX, mx = INT32_MIN;
+    for (int y = threadIdx.x; y < a.h; y += blockDim.x) {
+      const int v = shear_e(a.g, y) - dyadic_offset(a.K, r, y);
+      mn = min(mn, v);
+      mx = max(mx, v);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    __shared__ int smn[32], smx[32];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) { smn[warp] = mn; smx[warp] = mx; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int i = 1; i < (int)(blockDim.x >> 5); ++i) { mn = min(mn, smn[i]); mx = max(mx, smx[i]); }
+      const int len = mx - mn + a.w_content;
+      int k = (ceil_half(a.W - len) - mn) % a.W;
+      if (k < 0) k += a.W;
+      k_sh = k;
+    }
+  } else if (threadIdx.x == 0) {
+    int q, s;
+    if (a.mode == 1 && a.layout == 1) {  // CONCAT: attribute the row (R8)
+      const int Hp = a.Hp, Wp = a.Wp;
+      if (r < Hp) { q = 0; s = Hp - 1 - r; }
+      else if (r < 2 * Hp - 1) { q = 1; s = r - (Hp - 1); }
+      else if (r < 2 * Hp - 2 + Wp) { q = 2; s = Wp - 1 - (r - (2 * Hp - 2)); }
+      else { q = 3; s = r - (2 * Hp + Wp - 3); }
+    } else {
+      q = a.mode == 0 ? a.quadrant : qs;
+      s = r;
+    }
+    const int n = (q < 2) ? a.Hp : a.Wp;
+    int k = 0;
+    if (s < n) k = (quadrant_sigma(q) > 0 ? ceil_half(n + s) : ceil_half(n - s)) % a.W;
+    k_sh = k;
+  }
+  __syncthreads();
+  const int k = k_sh;
+  const T* src = static_cast<const T*>(a.in) + (int64_t)img * a.in_img_stride + (int64_t)qs * a.in_q_stride +
+                 (int64_t)r * a.in_row_stride;
+  T* dst = static_cast<T*>(a.out) + (int64_t)img * a.out_img_stride + (int64_t)qs * a.out_q_stride +
+           (int64_t)r * a.out_row_stride;
+  for (int x = threadIdx.x; x < a.W; x += blockDim.x) {
+    int sx = x - k;
+    if (sx < 0) sx += a.W;
+    dst[x] = src[sx];
+  }
+}
+
+}  // namespace fht

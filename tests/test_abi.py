@@ -1,0 +1,125 @@
+"""CPU tests of the C ABI boundary: the library loads, exports every symbol include/fht.h
+declares, and the host-only calls (describe, workspace sizing, plan, argument checks) behave
+as documented. No compute call runs here (no GPU)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _lib():
+    from paper_1811_06378_b200 import _lib as L
+    return L
+
+
+def test_header_symbols_exported():
+    L = _lib()
+    hdr = open(os.path.join(ROOT, "include", "fht.h")).read()
+    decl = set(re.findall(r"^(?:int|size_t|const char\*)\s+(\w+)\s*\(", hdr, flags=re.M))
+    assert decl == set(L.EXPORTED), decl
+    for name in decl:
+        assert hasattr(L.lib, name)
+
+
+def test_struct_sizes_match_header():
+    L = _lib()
+    assert ctypes.sizeof(L.FhtImage) == 56
+    assert ctypes.sizeof(L.FhtAnglePlan) == 6 * 8 + 7 * 8
+    assert ctypes.sizeof(L.FhtHough) == 8 + 6 * 4 + 11 * 8 + ctypes.sizeof(L.FhtAnglePlan)
+
+
+def _img(L, h, w, b=1, dt=2, data=4096):
+    img = L.FhtImage()
+    img.data, img.dtype, img.batch, img.h, img.w = data, dt, b, h, w
+    img.row_stride, img.batch_stride = w, h * w
+    return img
+
+
+@pytest.mark.parametrize("h,w", [(1024, 1024), (512, 512), (3, 5), (100, 37)])
+def test_describe_shapes(h, w):
+    L = _lib()
+    img = _img(L, h, w)
+    Hp, Wp = 1 << (h - 1).bit_length(), 1 << (w - 1).bit_length()
+    d = L.FhtHough()
+    assert L.lib.fht_hough_describe(L.FHT_MODE_FULL, L.FHT_LAYOUT_QUADS, 0, ctypes.byref(img), None, ctypes.byref(d)) == 0
+    assert (d.nquad, d.rows, d.cols) == (4, max(Hp, Wp), Hp + Wp)
+    assert L.lib.fht_hough_describe(L.FHT_MODE_FULL, L.FHT_LAYOUT_CONCAT, 0, ctypes.byref(img), None, ctypes.byref(d)) == 0
+    assert (d.nquad, d.rows, d.cols) == (1, 2 * (Hp + Wp) - 3, Hp + Wp)
+    assert L.lib.fht_hough_describe(L.FHT_MODE_QUADRANT, 0, 0, ctypes.byref(img), None, ctypes.byref(d)) == 0
+    assert (d.rows, d.cols) == (Hp, w + Hp)
+    assert L.lib.fht_hough_describe(L.FHT_MODE_QUADRANT, 0, 2, ctypes.byref(img), None, ctypes.byref(d)) == 0
+    assert (d.rows, d.cols) == (Wp, h + Wp)
+    assert d.row_stride % 4 == 0 and d.row_stride >= d.cols
+
+
+def test_plan_matches_oracle_rule():
+    from oracle import fht_oracle as O
+    L = _lib()
+    for h, w, a, b in [(4096, 4096, -15, 15), (64, 48, 5, 40), (33, 17, -45, 0), (16, 16, 0, 45), (32, 32, -80, 80)]:
+        p = L.FhtAnglePlan()
+        assert L.lib.fht_angle_plan_make(h, w, a, b, ctypes.byref(p)) == 0
+        o = O.angle_plan(h, w, a, b)
+        assert (p.k_lo, p.k_hi, p.alpha, p.g) == (o.k_lo, o.k_hi, o.alpha, o.g)
+        assert (p.Hp, p.w_content, p.W) == (o.Hp, o.w_content, o.W)
+        e = O.shear_offsets(o.g, h)
+        assert (p.e_min, p.e_max) == (e.min(), e.max())
+
+
+def test_plan_errors():
+    L = _lib()
+    p = L.FhtAnglePlan()
+    assert L.lib.fht_angle_plan_make(16, 16, 10, 10, ctypes.byref(p)) == -1
+    assert L.lib.fht_angle_plan_make(16, 16, -90, 10, ctypes.byref(p)) == -1
+    assert L.lib.fht_angle_plan_make(16, 16, 20, 10, ctypes.byref(p)) == -1
+    assert L.lib.fht_angle_plan_make(1, 1, -89.9, 89.9, ctypes.byref(p)) == -1      # alpha * w < 1
+    assert L.lib.fht_angle_plan_make(0, 16, -10, 10, ctypes.byref(p)) == -1
+
+
+def test_argument_errors_are_synchronous():
+    """Checks that return before anything is enqueued (no GPU needed)."""
+    L = _lib()
+    img = _img(L, 16, 16)
+    d = L.FhtHough()
+    assert L.lib.fht_hough_describe(1, 0, 0, ctypes.byref(img), None, ctypes.byref(d)) == 0
+    d.data = 1 << 20
+    ws_n = L.lib.fht_workspace_bytes(1, ctypes.byref(img), None)
+    assert ws_n > 0
+    assert L.lib.fht_full(None, 0, ctypes.byref(d), 1 << 24, ws_n, None) == -1         # NULL image
+    bad = _img(L, 16, 16, dt=7)
+    assert L.lib.fht_full(ctypes.byref(bad), 0, ctypes.byref(d), 1 << 24, ws_n, None) == -2
+    zero = _img(L, 0, 16)
+    assert L.lib.fht_full(ctypes.byref(zero), 0, ctypes.byref(d), 1 << 24, ws_n, None) == -1
+    d2 = L.FhtHough.from_buffer_copy(d)
+    d2.rows += 1
+    assert L.lib.fht_full(ctypes.byref(img), 0, ctypes.byref(d2), 1 << 24, ws_n, None) == -3
+    assert L.lib.fht_full(ctypes.byref(img), 1, ctypes.byref(d), 1 << 24, ws_n, None) == -3   # layout mismatch
+    assert L.lib.fht_full(ctypes.byref(img), 0, ctypes.byref(d), None, ws_n, None) == -6
+    assert L.lib.fht_full(ctypes.byref(img), 0, ctypes.byref(d), 1 << 24, 16, None) == -6
+    alias = _img(L, 16, 16, data=d.data)
+    assert L.lib.fht_full(ctypes.byref(alias), 0, ctypes.byref(d), 1 << 24, ws_n, None) == -1
+    odd = _img(L, 16, 16, data=4098)
+    assert L.lib.fht_full(ctypes.byref(odd), 0, ctypes.byref(d), 1 << 24, ws_n, None) == -4
+    dq = L.FhtHough()
+    assert L.lib.fht_hough_describe(0, 0, 0, ctypes.byref(img), None, ctypes.byref(dq)) == 0
+    dq.data = 1 << 20
+    assert L.lib.fht_quadrant(ctypes.byref(img), 0, 5, ctypes.byref(dq), 1 << 24, ws_n, None) == -5
+    ds = L.FhtHough.from_buffer_copy(d)
+    ds.shifted = 1
+    d3 = L.FhtHough.from_buffer_copy(d)
+    d3.data = 1 << 28
+    assert L.lib.fhtshift(ctypes.byref(ds), ctypes.byref(d3), None) == -7
+    assert L.lib.fhtshift(ctypes.byref(d), ctypes.byref(d), None) == -1                   # aliasing
+    big = _img(L, 8192, 8192)
+    db = L.FhtHough()
+    assert L.lib.fht_hough_describe(1, 0, 0, ctypes.byref(big), None, ctypes.byref(db)) == 0
+    db.data = 1 << 40
+    assert L.lib.fht_full(ctypes.byref(big), 0, ctypes.byref(db), 1 << 44, 1 << 40, None) == -5
+
+
+def test_status_strings():
+    L = _lib()
+    for s in range(-8, 1):
+        assert L.lib.fht_status_string(s)

@@ -1,0 +1,244 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle on the same seeded inputs.
+
+Bar: integer input -> bit-exact int32; float32 input -> |gpu - o64| <=
+ATOL + RTOL |o64| with RTOL = 1e-5, ATOL = 1e-3 (north_star; R21). fhtshift is a bit copy
+and is compared exactly against the oracle's rotation of the GPU's own unshifted output.
+"""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+RTOL, ATOL = 1e-5, 1e-3
+
+
+@pytest.fixture(scope="module")
+def fht():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1811_06378_b200 as F
+    return F
+
+
+@pytest.fixture(scope="module")
+def O():
+    from oracle import fht_oracle
+    return fht_oracle
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def check(got, want, integer):
+    got = np.asarray(got)
+    if integer:
+        assert got.dtype == np.int32
+        assert np.array_equal(got.astype(np.int64), want), f"max |diff| {np.abs(got.astype(np.int64) - want).max()}"
+    else:
+        assert got.dtype == np.float32
+        err = np.abs(got.astype(np.float64) - want)
+        bad = err > ATOL + RTOL * np.abs(want)
+        assert not bad.any(), f"{bad.sum()} cells out of tolerance, max err {err.max()}"
+
+
+SHAPES = [(1, 1), (2, 2), (3, 5), (5, 3), (7, 9), (16, 16), (33, 17), (64, 64), (100, 37), (129, 200), (256, 256)]
+
+
+@pytest.mark.parametrize("shape", SHAPES, ids=str)
+@pytest.mark.parametrize("dt", ["u8", "i32", "f32"])
+def test_quadrants_small(fht, O, shape, dt):
+    from synth import random_image
+    img = random_image(shape, dt, seed=shape[0] * 1000 + shape[1])
+    t = dev(img)
+    for q in range(4):
+        h = fht.quadrant(t, q)
+        torch.cuda.synchronize()
+        want = O.hough_recursive(img, q)
+        check(h.view[0, 0].cpu().numpy(), want, dt != "f32")
+        if dt == "f32":  # internal pin: same add tree as the float32 recursion -> bit-identical
+            w32 = O.hough_recursive(img, q, dtype=np.float32)
+            assert np.array_equal(h.view[0, 0].cpu().numpy(), w32)
+
+
+@pytest.mark.parametrize("shape", [(8, 8), (16, 16), (3, 5), (16, 4), (5, 16), (48, 40), (64, 128), (200, 129)], ids=str)
+@pytest.mark.parametrize("dt", ["u8", "f32"])
+def test_full_layouts_and_shift(fht, O, shape, dt):
+    from synth import random_image
+    img = random_image(shape, dt, seed=sum(shape))
+    t = dev(img)
+    Hp, Wp = O.full_padding(*shape)
+    quads = O.full_quadrants(img)
+    hq = fht.full(t, "quads")
+    hc = fht.full(t, "concat")
+    sq = fht.fhtshift(hq)
+    sc = fht.fhtshift(hc)
+    fq = fht.full(t, "quads", shifted=True)
+    fc = fht.full(t, "concat", shifted=True)
+    torch.cuda.synchronize()
+    gq = hq.view[0].cpu().numpy()
+    for q in range(4):
+        n = quads[q].shape[0]
+        check(gq[q, :n], quads[q], dt != "f32")
+        want_s = O.fhtshift_quadrant(gq[q, :n], O.QUADRANT_FRAME[q][1])
+        assert np.array_equal(sq.view[0, q, :n].cpu().numpy(), want_s)
+        assert np.array_equal(fq.view[0, q, :n].cpu().numpy(), want_s)
+    gc = hc.view[0, 0].cpu().numpy()
+    check(gc, O.full_concat(quads, Hp, Wp), dt != "f32")
+    want_cs = O.fhtshift_concat(gc, Hp, Wp)
+    assert np.array_equal(sc.view[0, 0].cpu().numpy(), want_cs)
+    assert np.array_equal(fc.view[0, 0].cpu().numpy(), want_cs)
+
+
+RANGES = [(-15, 15), (5, 40), (-30, -2), (0, 45), (-45, 0), (-80, 80), (1, 2)]
+
+
+@pytest.mark.parametrize("shape", [(16, 16), (33, 17), (64, 48), (128, 128)], ids=str)
+@pytest.mark.parametrize("dt", ["u8", "f32"])
+def test_angle_range_small(fht, O, shape, dt):
+    from synth import random_image
+    img = random_image(shape, dt, seed=shape[0] + 3 * shape[1])
+    t = dev(img)
+    for tmin, tmax in RANGES:
+        p = fht.angle_plan(*shape, tmin, tmax)
+        op = O.angle_plan(*shape, tmin, tmax, k_lo=p.k_lo, k_hi=p.k_hi)   # R16: same scalars
+        assert (op.W, op.w_content) == (p.W, p.w_content)
+        r = fht.angle_range(t, p)
+        rs = fht.fhtshift(r)
+        fr = fht.angle_range(t, p, shifted=True)
+        torch.cuda.synchronize()
+        got = r.view[0, 0].cpu().numpy()
+        check(got, O.angle_range(img, op), dt != "f32")
+        want_s = O.fhtshift_range(got, op)
+        assert np.array_equal(rs.view[0, 0].cpu().numpy(), want_s)
+        assert np.array_equal(fr.view[0, 0].cpu().numpy(), want_s)
+
+
+def test_strided_batch_input(fht, O):
+    """Non-contiguous rows (a column slice of a wider tensor) and a batch of 3."""
+    from synth import random_image
+    big = np.stack([random_image((40, 60), "f32", seed=s) for s in range(3)])
+    t = dev(big)[:, :, 5:45]
+    assert t.stride(1) == 60
+    h = fht.full(t)
+    torch.cuda.synchronize()
+    for b in range(3):
+        quads = O.full_quadrants(big[b, :, 5:45])
+        for q in range(4):
+            check(h.view[b, q, : quads[q].shape[0]].cpu().numpy(), quads[q], False)
+
+
+def test_deterministic(fht):
+    from synth import random_image
+    t = dev(random_image((300, 257), "f32", seed=1))
+    a = fht.full(t).view.cpu()
+    b = fht.full(t).view.cpu()
+    assert torch.equal(a, b)
+
+
+# ------------------------------------------------------------------ the five BASELINE configs
+def _sample_cells(Hp, W, n, rng, extra=()):
+    s = np.concatenate([rng.integers(0, Hp, n), [0, Hp - 1, 0, Hp - 1]])
+    x = np.concatenate([rng.integers(0, W, n), [0, 0, W - 1, W - 1]])
+    cells = list(zip(s.tolist(), x.tolist())) + list(extra)
+    return cells
+
+
+def test_config1_quadrant_u8(fht, O):
+    import synth
+    img = synth.batch(1)[0]
+    h = fht.quadrant(dev(img), fht.QA)
+    torch.cuda.synchronize()
+    got = h.view[0, 0].cpu().numpy()
+    assert got.shape == (256, 512)
+    check(got, O.hough_direct(img, O.QA), True)           # tier 1, every cell
+    check(got, O.hough_recursive(img, O.QA), True)
+
+
+def test_config2_full_f32_shift(fht, O):
+    import synth
+    img = synth.batch(2)[0]
+    t = dev(img)
+    h = fht.full(t)
+    s = fht.fhtshift(h)
+    torch.cuda.synchronize()
+    got = h.view[0].cpu().numpy()
+    quads = O.full_quadrants(img)
+    for q in range(4):
+        check(got[q], quads[q], False)
+        assert np.array_equal(s.view[0, q].cpu().numpy(), O.fhtshift_quadrant(got[q], O.QUADRANT_FRAME[q][1]))
+
+
+def test_config3_batch_u8(fht, O):
+    import synth
+    imgs = synth.batch(3)
+    h = fht.full(dev(imgs))
+    torch.cuda.synchronize()
+    got = h.view.cpu().numpy()
+    rng = np.random.default_rng(3)
+    for b in range(imgs.shape[0]):
+        if b in (0, 31, 63):
+            quads = O.full_quadrants(imgs[b])
+            for q in range(4):
+                check(got[b, q], quads[q], True)
+        else:
+            for q in range(4):
+                fr = O.quadrant_frame(imgs[b], q, square_to=(512, 512))
+                cells = _sample_cells(fr.Hp, fr.W, 64, rng)
+                want = O.hough_cells_direct(fr, cells)
+                assert np.array_equal(np.array([got[b, q, s, x] for s, x in cells], dtype=np.int64), want)
+            # row conservation on every row of every quadrant
+            assert (got[b].astype(np.int64).sum(axis=2) == int(imgs[b].sum())).all()
+
+
+def test_config4_range_f32(fht, O):
+    import synth
+    img = synth.batch(4)[0]
+    p = fht.angle_plan(4096, 4096, -15.0, 15.0)
+    op = O.angle_plan(4096, 4096, -15.0, 15.0, k_lo=p.k_lo, k_hi=p.k_hi)
+    assert (p.W, p.w_content) == (11740, 7644)
+    r = fht.angle_range(dev(img), p)
+    s = fht.fhtshift(r)
+    torch.cuda.synchronize()
+    got = r.view[0, 0].cpu().numpy()
+    rng = np.random.default_rng(4)
+    start, length = O.range_support(op)
+    extra = [(sr, int((start[sr] + dx) % op.W)) for sr in (0, 1, 2047, 4095) for dx in (-1, 0, 1, int(length[sr]) - 1)]
+    cells = _sample_cells(op.Hp, op.W, 2048, rng, extra)
+    want = O.range_cells_direct(img, op, cells)
+    check(np.array([got[a, b] for a, b in cells], dtype=np.float32), want, False)
+    # full rows for a few shifts, all columns
+    T_total = float(np.sum(img.astype(np.float64)[np.arange(4096)[:, None],
+                                                 O.scale_colmap(op.alpha, 4096, op.w_content)[None, :]]))
+    sums = got.astype(np.float64).sum(axis=1)
+    assert np.all(np.abs(sums - T_total) <= 1e-4 * T_total)          # row conservation
+    gs = s.view[0, 0].cpu().numpy()
+    k = O.fhtshift_amounts_range(op)
+    for row in (0, 17, 2048, 4095):
+        assert np.array_equal(gs[row], np.roll(got[row], int(k[row])))
+
+
+def test_config5_batch_f32(fht, O):
+    import synth
+    imgs = synth.batch(5)
+    h = fht.full(dev(imgs))
+    s = fht.fhtshift(h)
+    torch.cuda.synchronize()
+    got = h.view.cpu().numpy()
+    rng = np.random.default_rng(5)
+    quads = O.full_quadrants(imgs[0])
+    for q in range(4):
+        check(got[0, q], quads[q], False)
+    for b in range(1, imgs.shape[0]):
+        for q in range(4):
+            fr = O.quadrant_frame(imgs[b], q, square_to=(2048, 2048))
+            cells = _sample_cells(fr.Hp, fr.W, 48, rng)
+            want = O.hough_cells_direct(fr, cells)
+            check(np.array([got[b, q, a, c] for a, c in cells], dtype=np.float32), want, False)
+    gs = s.view.cpu().numpy()
+    for b in (0, 15):
+        for q in range(4):
+            k = O.fhtshift_amounts_quadrant(2048, 4096, O.QUADRANT_FRAME[q][1])
+            for row in (0, 1, 1000, 2047):
+                assert np.array_equal(gs[b, q, row], np.roll(got[b, q, row], int(k[row])))

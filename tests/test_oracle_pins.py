@@ -355,3 +355,22 @@ def test_float32_recursion_close_to_f64():
     a = O.hough_recursive(img, O.QA)
     b = O.hough_recursive(img, O.QA, dtype=np.float32)
     assert np.all(np.abs(a - b) <= 1e-3 + 1e-5 * np.abs(a))
+
+
+def test_range_cells_direct_equals_materialised():
+    img = random_image((24, 20), "i32", seed=8)
+    for tmin, tmax in [(-15, 15), (5, 40), (-60, 10)]:
+        p = O.angle_plan(24, 20, tmin, tmax)
+        R = O.angle_range(img, p)
+        cells = [(s, x) for s in range(p.Hp) for x in range(0, p.W, 3)]
+        got = O.range_cells_direct(img, p, cells)
+        assert (got == np.array([R[s, x] for s, x in cells])).all()
+
+
+def test_cells_direct_equals_full():
+    img = random_image((20, 13), "i32", seed=9)
+    for q in range(4):
+        fr = O.quadrant_frame(img, q)
+        H = O.hough_of_frame_direct(fr)
+        cells = [(s, x) for s in range(fr.Hp) for x in range(fr.W)]
+        assert (O.hough_cells_direct(fr, cells) == H.ravel()).all()
