@@ -100,30 +100,31 @@ def out_bytes_per_step(cfg_id, c, imgs):
 
 
 def make_step(fht, cfg_id, c, t, ws, outs):
-    """Returns step() -> number of kernel launches it enqueued (all through the C ABI)."""
+    """Returns step() -> number of kernel launches it enqueued (all through the C ABI).
+    C2/C5/C4 write the Hough image AND its fhtshift in the same pass (pair=True)."""
     if c["mode"] == "quadrant":
         def step():
-            outs["h"] = fht.quadrant(t, fht.QA, workspace=ws)
+            outs["h"] = fht.quadrant(t, fht.QA, workspace=ws, out=outs.get("h"))
             return outs["h"].launches
         return step
     if c["mode"] == "full":
         do_shift = cfg_id in (2, 5)
 
         def step():
-            outs["h"] = fht.full(t, workspace=ws, out=outs.get("h"))
-            n = outs["h"].launches
             if do_shift:
-                outs["s"] = fht.fhtshift(outs["h"], out=outs.get("s"))
-                n += outs["s"].launches
-            return n
+                outs["h"], outs["s"] = fht.full(t, pair=True, workspace=ws, out=outs.get("h"),
+                                                out_shifted=outs.get("s"))
+            else:
+                outs["h"] = fht.full(t, workspace=ws, out=outs.get("h"))
+            return outs["h"].launches
         return step
     plan = fht.angle_plan(c["h"], c["w"], c["theta_min"], c["theta_max"])
     outs["plan"] = plan
 
     def step():
-        outs["h"] = fht.angle_range(t, plan, workspace=ws, out=outs.get("h"))
-        outs["s"] = fht.fhtshift(outs["h"], out=outs.get("s"))
-        return outs["h"].launches + outs["s"].launches
+        outs["h"], outs["s"] = fht.angle_range(t, plan, pair=True, workspace=ws, out=outs.get("h"),
+                                               out_shifted=outs.get("s"))
+        return outs["h"].launches
     return step
 
 

@@ -93,8 +93,7 @@ typedef struct {
   int32_t dtype;    /* I32 for integer input, F32 for float input */
   int32_t mode;     /* fht_mode */
   int32_t layout;   /* fht_layout (FULL mode only) */
-  int32_t shifted;  /* 1 = rows hold the fhtshift-ed image (§5). Setting it to 1 BEFORE an
-                       fht_* call makes that call write the shifted image directly (fused). */
+  int32_t shifted;  /* 1 = rows hold the fhtshift-ed image (§5); set by the library */
   int32_t quadrant; /* QUADRANT mode: which quadrant */
   int32_t _pad0;
   int64_t batch, nquad, rows, cols;       /* nquad = 4 for FULL/QUADS, else 1 */
@@ -115,15 +114,22 @@ int fht_hough_describe(int mode, int layout, int quadrant, const fht_image* img,
 /* Device workspace (bytes) the call needs for `img` (pass-1 scratch + tables). */
 size_t fht_workspace_bytes(int mode, const fht_image* img, const fht_angle_plan* plan);
 
+/* Output pair of the transform calls below. `out` receives the Hough image H; `out_shifted`
+ * receives fhtshift(H) (§5), written by the same pass-2 kernel from the same
+ * registers (no re-read of H). Either may be NULL, not both; both must be described by
+ * fht_hough_describe() for the same transform, with `data` set, 16-byte aligned base and row
+ * pitch, and must not overlap each other, the image or the workspace. On success
+ * out->shifted = 0 and out_shifted->shifted = 1. */
+
 /* One quadrant. pad_cols: -1 or Hp (the paper's h x h extension);
  * other pads return FHT_ERR_UNSUPPORTED on the GPU (the oracle handles any pad cyclically).
- * `out` from fht_hough_describe(FHT_MODE_QUADRANT, 0, quadrant, ...). */
-int fht_quadrant(const fht_image* img, int quadrant, int64_t pad_cols, fht_hough* out, void* ws,
-                 size_t ws_bytes, fht_stream_t stream);
+ * Outputs from fht_hough_describe(FHT_MODE_QUADRANT, 0, quadrant, ...). */
+int fht_quadrant(const fht_image* img, int quadrant, int64_t pad_cols, fht_hough* out,
+                 fht_hough* out_shifted, void* ws, size_t ws_bytes, fht_stream_t stream);
 
-/* Full four-quadrant transform. `layout` must equal out->layout. */
-int fht_full(const fht_image* img, int layout, fht_hough* out, void* ws, size_t ws_bytes,
-             fht_stream_t stream);
+/* Full four-quadrant transform. `layout` must equal the outputs' layout. */
+int fht_full(const fht_image* img, int layout, fht_hough* out, fht_hough* out_shifted, void* ws,
+             size_t ws_bytes, fht_stream_t stream);
 
 /* Host-only: build the §4 plan. FHT_ERR_ARG if theta_min >= theta_max,
  * |theta| >= 90 deg, or alpha*w < 1. Deterministic double arithmetic, no FMA (R16). */
@@ -132,8 +138,8 @@ int fht_angle_plan_make(int64_t h, int64_t w, double theta_min_deg, double theta
 
 /* Angle-range-restricted transform: QA of the virtually sheared+scaled image, the
  * shear and scale fused into the first FHT iteration (pass-1 loader). f32/u8/i32 input. */
-int fht_angle_range(const fht_image* img, const fht_angle_plan* plan, fht_hough* out, void* ws,
-                    size_t ws_bytes, fht_stream_t stream);
+int fht_angle_range(const fht_image* img, const fht_angle_plan* plan, fht_hough* out,
+                    fht_hough* out_shifted, void* ws, size_t ws_bytes, fht_stream_t stream);
 
 /* §5 fhtshift (R11): out[r][x] = in[r][(x - k_r) mod cols], k_r = ceil((n+s)/2) for
  * sigma=+1 quadrants, ceil((n-s)/2) for sigma=-1, and ceil((W'-len_s)/2) - start_s in RANGE

@@ -5,13 +5,14 @@ device memory (``data_ptr``) and the current CUDA stream; every step of the tran
 the sm_100a kernels behind the ABI. There is no CPU fallback: importing without the built
 library, or calling with a non-CUDA tensor, raises.
 
-    full(img, layout="quads", shifted=False)        -> HoughImage   (P:89-113)
-    quadrant(img, q, pad=None, shifted=False)       -> HoughImage   (P:52-67)
+    full(img, layout="quads", shifted=False, pair=False)   -> HoughImage | (H, S)  (P:89-113)
+    quadrant(img, q, pad=None, shifted=False, pair=False)  -> HoughImage | (H, S)  (P:52-67)
     angle_plan(h, w, theta_min, theta_max)          -> FhtAnglePlan (P:124, P:132, P:144)
-    angle_range(img, plan, shifted=False)           -> HoughImage   (P:146-152)
+    angle_range(img, plan, shifted=False, pair=False)      -> HoughImage | (H, S)  (P:146-152)
     fhtshift(hough)                                 -> HoughImage   (P:154-172)
 
-`shifted=True` makes the transform write the fhtshift-ed image directly (fused store).
+`shifted=True` makes the transform write the fhtshift-ed image directly (fused store);
+`pair=True` returns (H, fhtshift(H)) written by the same kernels in one pass.
 """
 from __future__ import annotations
 
@@ -103,33 +104,62 @@ def _stream(t: torch.Tensor):
     return ctypes.c_void_p(torch.cuda.current_stream(t.device).cuda_stream)
 
 
-def quadrant(t: torch.Tensor, q: int, pad: int | None = None, shifted: bool = False,
-             workspace: torch.Tensor | None = None) -> HoughImage:
+def _descs(kind, img, plan, q, layout, device, shifted, pair, out, out_shifted):
+    """The (plain, shifted) output pair a transform call writes; None where not requested."""
+    want_plain = pair or not shifted
+    want_shift = pair or shifted
+    res = []
+    for want, given in ((want_plain, out), (want_shift, out_shifted)):
+        if not want:
+            res.append(None)
+            continue
+        if given is None:
+            d, storage = _alloc_out(kind, layout, q, img, plan, device)
+            given = HoughImage(storage, d)
+        res.append(given)
+    return res
+
+
+def _ptr(h):
+    return ctypes.byref(h.desc) if h is not None else None
+
+
+def _finish(res, n, shifted, pair):
+    for h in res:
+        if h is not None:
+            h.launches = n
+    if pair:
+        return res[0], res[1]
+    return res[1] if shifted else res[0]
+
+
+def quadrant(t: torch.Tensor, q: int, pad: int | None = None, shifted: bool = False, pair: bool = False,
+             workspace: torch.Tensor | None = None, out: HoughImage | None = None,
+             out_shifted: HoughImage | None = None):
+    """One quadrant (P:52-67). shifted=True returns fhtshift(H) written directly by the transform;
+    pair=True returns (H, fhtshift(H)) from one pass."""
     img, t = _image(t)
-    d, storage = _alloc_out(FHT_MODE_QUADRANT, 0, q, img, None, t.device)
-    d.shifted = int(shifted)
+    res = _descs(FHT_MODE_QUADRANT, img, None, q, 0, t.device, shifted, pair, out, out_shifted)
     ws_n = workspace_bytes(FHT_MODE_QUADRANT, img)
     ws = _workspace(ws_n, t.device, workspace)
     n = _lib.check("fht_quadrant", _lib.lib.fht_quadrant(ctypes.byref(img), q, -1 if pad is None else pad,
-                                                          ctypes.byref(d), ws.data_ptr(), ws_n, _stream(t)))
-    h = HoughImage(storage, d)
-    h.launches = n
-    return h
+                                                          _ptr(res[0]), _ptr(res[1]), ws.data_ptr(), ws_n,
+                                                          _stream(t)))
+    return _finish(res, n, shifted, pair)
 
 
-def full(t: torch.Tensor, layout: str = "quads", shifted: bool = False,
-         workspace: torch.Tensor | None = None, out: HoughImage | None = None) -> HoughImage:
+def full(t: torch.Tensor, layout: str = "quads", shifted: bool = False, pair: bool = False,
+         workspace: torch.Tensor | None = None, out: HoughImage | None = None,
+         out_shifted: HoughImage | None = None):
+    """Full four-quadrant transform. See quadrant() for shifted / pair."""
     img, t = _image(t)
     lay = _LAYOUTS[layout]
-    if out is None:
-        d, storage = _alloc_out(FHT_MODE_FULL, lay, 0, img, None, t.device)
-        out = HoughImage(storage, d)
-    out.desc.shifted = int(shifted)
+    res = _descs(FHT_MODE_FULL, img, None, 0, lay, t.device, shifted, pair, out, out_shifted)
     ws_n = workspace_bytes(FHT_MODE_FULL, img)
     ws = _workspace(ws_n, t.device, workspace)
-    out.launches = _lib.check("fht_full", _lib.lib.fht_full(ctypes.byref(img), lay, ctypes.byref(out.desc), ws.data_ptr(), ws_n,
-                                              _stream(t)))
-    return out
+    n = _lib.check("fht_full", _lib.lib.fht_full(ctypes.byref(img), lay, _ptr(res[0]), _ptr(res[1]),
+                                                  ws.data_ptr(), ws_n, _stream(t)))
+    return _finish(res, n, shifted, pair)
 
 
 def angle_plan(h: int, w: int, theta_min_deg: float, theta_max_deg: float) -> FhtAnglePlan:
@@ -139,18 +169,18 @@ def angle_plan(h: int, w: int, theta_min_deg: float, theta_max_deg: float) -> Fh
     return p
 
 
-def angle_range(t: torch.Tensor, plan: FhtAnglePlan, shifted: bool = False,
-                workspace: torch.Tensor | None = None, out: HoughImage | None = None) -> HoughImage:
+def angle_range(t: torch.Tensor, plan: FhtAnglePlan, shifted: bool = False, pair: bool = False,
+                workspace: torch.Tensor | None = None, out: HoughImage | None = None,
+                out_shifted: HoughImage | None = None):
+    """Angle-range-restricted transform. See quadrant() for shifted / pair."""
     img, t = _image(t)
-    if out is None:
-        d, storage = _alloc_out(FHT_MODE_RANGE, 0, 0, img, plan, t.device)
-        out = HoughImage(storage, d)
-    out.desc.shifted = int(shifted)
+    res = _descs(FHT_MODE_RANGE, img, plan, 0, 0, t.device, shifted, pair, out, out_shifted)
     ws_n = workspace_bytes(FHT_MODE_RANGE, img, plan)
     ws = _workspace(ws_n, t.device, workspace)
-    out.launches = _lib.check("fht_angle_range", _lib.lib.fht_angle_range(ctypes.byref(img), ctypes.byref(plan),
-                                                            ctypes.byref(out.desc), ws.data_ptr(), ws_n, _stream(t)))
-    return out
+    n = _lib.check("fht_angle_range", _lib.lib.fht_angle_range(ctypes.byref(img), ctypes.byref(plan),
+                                                                _ptr(res[0]), _ptr(res[1]), ws.data_ptr(),
+                                                                ws_n, _stream(t)))
+    return _finish(res, n, shifted, pair)
 
 
 def fhtshift(h: HoughImage, out: HoughImage | None = None) -> HoughImage:

@@ -72,10 +72,10 @@ def _load():
     lib.fht_hough_describe.argtypes = [i32, i32, i32, P(FhtImage), P(FhtAnglePlan), P(FhtHough)]
     lib.fht_workspace_bytes.argtypes = [i32, P(FhtImage), P(FhtAnglePlan)]
     lib.fht_workspace_bytes.restype = sz
-    lib.fht_quadrant.argtypes = [P(FhtImage), i32, i64, P(FhtHough), vp, sz, vp]
-    lib.fht_full.argtypes = [P(FhtImage), i32, P(FhtHough), vp, sz, vp]
+    lib.fht_quadrant.argtypes = [P(FhtImage), i32, i64, P(FhtHough), P(FhtHough), vp, sz, vp]
+    lib.fht_full.argtypes = [P(FhtImage), i32, P(FhtHough), P(FhtHough), vp, sz, vp]
     lib.fht_angle_plan_make.argtypes = [i64, i64, dbl, dbl, P(FhtAnglePlan)]
-    lib.fht_angle_range.argtypes = [P(FhtImage), P(FhtAnglePlan), P(FhtHough), vp, sz, vp]
+    lib.fht_angle_range.argtypes = [P(FhtImage), P(FhtAnglePlan), P(FhtHough), P(FhtHough), vp, sz, vp]
     lib.fhtshift.argtypes = [P(FhtHough), P(FhtHough), vp]
     lib.fht_status_string.argtypes = [i32]
     lib.fht_status_string.restype = ctypes.c_char_p

@@ -1,20 +1,30 @@
-// fht_api.cu -- C ABI (include/fht.h) and host dispatch (SURVEY B1/B2) for libfht.so.
+// fht_api.cu -- C ABI (include/fht.h) and host dispatch for libfht.so.
 //
 // Host side: argument validation, frame geometry, the pass split m + L = K, batch
-// chunking so one chunk's pass-1 scratch stays L2-resident, and the launches. No device
-// memory is allocated here; scratch and tables live in the caller's workspace.
+// chunking so one chunk's pass-1 scratch stays L2-resident, TMA tensor maps, and the launches.
+// No device memory is allocated here; scratch and tables live in the caller's workspace.
+//
+// Two kernel generations share this dispatch:
+//   v2 (fht_tile.cuh) -- register-resident warp butterflies + TMA stores; every frame with
+//                        K >= 2 and at least 8 columns in both passes (all BASELINE configs).
+//   v1 (fht_kernels.cuh) -- level-by-level shared-memory butterflies; only the degenerate
+//                        frames v2 does not tile (Hp <= 2 or fewer than 8 columns).
+#include <cudaTypedefs.h>
+
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "../../include/fht.h"
 #include "fht_kernels.cuh"
+#include "fht_tile.cuh"
 
 namespace {
 
 using namespace fht;
 
-constexpr size_t kScratchBudget = size_t(48) << 20;  // bytes of pass-1 scratch per chunk
+constexpr size_t kScratchBudget = size_t(48) << 20;  // touched pass-1 scratch bytes per chunk
 
 int64_t next_pow2(int64_t n) {
   int64_t p = 1;
@@ -78,24 +88,116 @@ int check_frame_supported(const Frame& f) {
   return FHT_OK;
 }
 
-int scratch_width(const Frame& f) {
+// ---------------------------------------------------------------- pass geometry (v1 and v2)
+// Pass-1 range of F_m for a slot: sigma=+1 [-(2^m-1), wc), sigma=-1 [0, wc + 2^m - 1); range mode
+// uses the plan's shear extent.
+struct RangeDev {
+  const int* e_tab;
+  const int* colmap;
+  const int* start_tab;
+  const int* len_tab;
+  int w_content, x_lo, x_hi;  // scratch signed x range (pass 1)
+  int out_lo, out_hi;         // signed x range covered by pass 2 tiles
+};
+
+void pass1_range(const Frame& f, int sigma, const RangeDev* rg, int& lo, int& hi) {
+  if (rg) { lo = rg->x_lo; hi = rg->x_hi; return; }
+  const int hm = (1 << f.m) - 1;
+  lo = sigma > 0 ? -hm : 0;
+  hi = sigma > 0 ? f.wc : f.wc + hm;
+}
+
+bool use_v2(const Frame& f, const RangeDev* rg) {
+  if (f.K < 2 || f.m > 6 || f.L < 1 || f.L > 6) return false;
+  int lo, hi;
+  pass1_range(f, +1, rg, lo, hi);
+  if (hi - lo < 8) return false;
+  pass1_range(f, -1, rg, lo, hi);
+  if (hi - lo < 8) return false;
+  const int span2 = rg ? rg->out_hi - rg->out_lo : f.W;
+  return f.W >= 12 && span2 >= 12;
+}
+
+// v2 pass-1 columns [lo, hi) rounded up to a multiple of 4 (16-byte aligned TMA rows); the
+// extra columns hold zeros (no pixel reaches them), so pass 2 may read them freely.
+void v2_pass1_range(const Frame& f, int sigma, const RangeDev* rg, int& lo, int& hi) {
+  pass1_range(f, sigma, rg, lo, hi);
+  hi = lo + ((hi - lo + 3) & ~3);
+}
+int64_t v2_scratch_pitch(const Frame& f, const RangeDev* rg) {
+  int lo, hi, w = 0;
+  for (int s = -1; s <= 1; s += 2) {
+    v2_pass1_range(f, s, rg, lo, hi);
+    w = (hi - lo) > w ? (hi - lo) : w;
+  }
+  return w;
+}
+
+// v1 scratch
+int v1_scratch_width(const Frame& f) {
   const int ws = f.wc + (1 << f.m) - 1;
-  return (ws + 3) & ~3;  // 16-byte rows
+  return (ws + 3) & ~3;
 }
 
-// Pass-1 scratch bytes for one image and `nq` quadrant slots.
-size_t scratch_bytes_per_image(const Frame& f, int nq) {
-  return (size_t)nq * f.Hp * scratch_width(f) * 4;
-}
-
-int chunk_images(size_t per_image, int64_t batch) {
-  int64_t c = (int64_t)(kScratchBudget / (per_image ? per_image : 1));
+int chunk_images(size_t per_image_touched, int64_t batch) {
+  int64_t c = (int64_t)(kScratchBudget / (per_image_touched ? per_image_touched : 1));
   if (c < 1) c = 1;
   if (c > batch) c = batch;
   return (int)c;
 }
 
-// ---------------------------------------------------------------- launch helpers
+// Scratch bytes (address extent) and chunk for one orientation with nq slots.
+struct ScratchPlan {
+  int v2;
+  int64_t pitch;       // elements
+  int chunk;
+  size_t bytes;
+};
+ScratchPlan scratch_plan(const Frame& f, int nq, int64_t batch, const RangeDev* rg) {
+  ScratchPlan sp{};
+  sp.v2 = use_v2(f, rg);
+  if (sp.v2) {
+    sp.pitch = v2_scratch_pitch(f, rg);
+    const size_t touched = (size_t)nq * f.Hp * (size_t)sp.pitch * 4;
+    sp.chunk = rg ? 1 : chunk_images(touched, batch);
+    sp.bytes = (size_t)sp.chunk * nq * f.Hp * (size_t)sp.pitch * 4;
+  } else {
+    sp.pitch = rg ? ((rg->x_hi - rg->x_lo + 3) & ~3) : v1_scratch_width(f);
+    const size_t per = (size_t)nq * f.Hp * (size_t)sp.pitch * 4;
+    sp.chunk = rg ? 1 : chunk_images(per, batch);
+    sp.bytes = per * sp.chunk;
+  }
+  return sp;
+}
+
+// ---------------------------------------------------------------- TMA tensor maps
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = []() -> PFN_cuTensorMapEncodeTiled_v12000 {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
+}
+
+// 2-D row-major tensor [rows][cols] with a 1 x box_cols box (one output row per store).
+bool make_row_map(CUtensorMap* m, const void* base, bool f32, uint64_t cols, uint64_t rows, uint64_t pitch_elems,
+                  uint32_t box_cols) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {pitch_elems * 4};
+  cuuint32_t box[2] = {box_cols, 1};
+  cuuint32_t es[2] = {1, 1};
+  return fn(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_INT32, 2, const_cast<void*>(base), dims,
+            strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// ---------------------------------------------------------------- v1 launch helpers
 template <typename Tin, int LOGR>
 cudaError_t launch_pass1_t(dim3 grid, const Pass1Args& a, cudaStream_t st) {
   using A = typename AccOf<Tin>::type;
@@ -147,33 +249,202 @@ cudaError_t launch_pass2(int logr, dim3 grid, const Pass2Args& a, cudaStream_t s
   return cudaErrorInvalidValue;
 }
 
-// One orientation's quadrant slots (1 or 2), with output placement.
+// ---------------------------------------------------------------- v2 launch helpers
+template <typename Tin, int R>
+cudaError_t launch_p1_t(dim3 grid, const CUtensorMap& tm, const v2::P1Params& a, cudaStream_t st) {
+  const size_t smem = v2::tile_smem_bytes(R, 1);
+  static const cudaError_t attr =
+      cudaFuncSetAttribute(v2::k_p1<Tin, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (attr != cudaSuccess) return attr;
+  v2::k_p1<Tin, R><<<grid, v2::Split<R>::nw * 32, smem, st>>>(tm, a);
+  return cudaGetLastError();
+}
+template <typename Tin>
+cudaError_t launch_p1(int r, dim3 grid, const CUtensorMap& tm, const v2::P1Params& a, cudaStream_t st) {
+  switch (r) {
+    case 1: return launch_p1_t<Tin, 1>(grid, tm, a, st);
+    case 2: return launch_p1_t<Tin, 2>(grid, tm, a, st);
+    case 3: return launch_p1_t<Tin, 3>(grid, tm, a, st);
+    case 4: return launch_p1_t<Tin, 4>(grid, tm, a, st);
+    case 5: return launch_p1_t<Tin, 5>(grid, tm, a, st);
+    case 6: return launch_p1_t<Tin, 6>(grid, tm, a, st);
+  }
+  return cudaErrorInvalidValue;
+}
+template <typename A, int R>
+cudaError_t launch_p2_t(dim3 grid, const CUtensorMap& t0, const CUtensorMap& t1, const v2::P2Params& a,
+                        cudaStream_t st) {
+  const size_t smem = v2::tile_smem_bytes(R, a.ndest);
+  static const cudaError_t attr = cudaFuncSetAttribute(v2::k_p2<A, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                       (int)v2::tile_smem_bytes(R, 2));
+  if (attr != cudaSuccess) return attr;
+  v2::k_p2<A, R><<<grid, v2::Split<R>::nw * 32, smem, st>>>(t0, t1, a);
+  return cudaGetLastError();
+}
+template <typename A>
+cudaError_t launch_p2(int r, dim3 grid, const CUtensorMap& t0, const CUtensorMap& t1, const v2::P2Params& a,
+                      cudaStream_t st) {
+  switch (r) {
+    case 1: return launch_p2_t<A, 1>(grid, t0, t1, a, st);
+    case 2: return launch_p2_t<A, 2>(grid, t0, t1, a, st);
+    case 3: return launch_p2_t<A, 3>(grid, t0, t1, a, st);
+    case 4: return launch_p2_t<A, 4>(grid, t0, t1, a, st);
+    case 5: return launch_p2_t<A, 5>(grid, t0, t1, a, st);
+    case 6: return launch_p2_t<A, 6>(grid, t0, t1, a, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+// One quadrant slot of an orientation: sign, source orientation and output row placement.
 struct Slot {
   int sigma;
-  int64_t out_q_offset;  // element offset of the quadrant's row 0 inside one output image
+  int64_t qrow;          // output row (in the [batch*rows_per_img][W] view) of the quadrant's row 0
   int row_base, row_sign, skip_t;
 };
 
-struct RangeDev {
-  const int* e_tab;
-  const int* colmap;
-  const int* start_tab;
-  const int* len_tab;
-  int w_content, x_lo, x_hi;  // scratch signed x range (pass 1)
-  int out_lo, out_hi;         // signed x range covered by pass 2 tiles
+// Output destinations: [0] = Hough image, [1] = its fhtshift (either may be NULL).
+struct Outs {
+  const fht_hough* d[2];
 };
 
 // Run the two passes for one orientation over all images, chunked. Returns launches or error.
-int run_orientation(const fht_image* img, const Frame& f, const Slot* slots, int nq, const fht_hough* out,
-                    void* ws, size_t ws_bytes, cudaStream_t st, const RangeDev* rg, int shift_mode) {
-  const int Ws = rg ? ((rg->x_hi - rg->x_lo + 3) & ~3) : scratch_width(f);
-  const size_t per_img = (size_t)nq * f.Hp * Ws * 4;
-  const int chunk = rg ? 1 : chunk_images(per_img, img->batch);
-  if (ws_bytes < per_img * chunk || !ws) return FHT_ERR_WORKSPACE;
-  const int nstrips = 1 << f.L, ngroups = 1 << f.m;
+int run_orientation(const fht_image* img, const Frame& f, const Slot* slots, int nq, const Outs& outs, void* ws,
+                    size_t ws_bytes, cudaStream_t st, const RangeDev* rg) {
+  const ScratchPlan sp = scratch_plan(f, nq, img->batch, rg);
+  if (!ws || ws_bytes < sp.bytes) return FHT_ERR_WORKSPACE;
   int launches = 0;
-  for (int64_t b0 = 0; b0 < img->batch; b0 += chunk) {
-    const int nb = (int)((img->batch - b0) < chunk ? (img->batch - b0) : chunk);
+  const fht_hough* any = outs.d[0] ? outs.d[0] : outs.d[1];
+
+  if (sp.v2) {
+    const int nstrips = 1 << f.L, ngroups = 1 << f.m;
+    v2::P1Params p1{};
+    p1.img = img->data;
+    p1.img_bstride = img->batch_stride;
+    p1.img_rstride = img->row_stride;
+    p1.rows_avail = f.rows_avail;
+    p1.cols_avail = f.cols_avail;
+    p1.transposed = f.transposed;
+    p1.nq = nq;
+    p1.L = f.L;
+    p1.scratch_img_rows = (int64_t)nq * f.Hp;
+    p1.scratch = ws;
+    p1.scr_pitch = sp.pitch;
+    {
+      const char* e = std::getenv("FHT_DEBUG_NO_TMA");
+      p1.no_tma = (e && e[0] == '1') ? 1 : 0;
+    }
+    int span1 = 1 << 30;
+    for (int q = 0; q < nq; ++q) {
+      v2::P1Slot& s = p1.slot[q];
+      s.sigma = slots[q].sigma;
+      v2_pass1_range(f, s.sigma, rg, s.xlo, s.xhi);
+      s.srow0 = (int64_t)q * f.Hp;
+      span1 = (s.xhi - s.xlo) < span1 ? (s.xhi - s.xlo) : span1;
+    }
+    p1.TX = span1 < v2::TX1 ? span1 : v2::TX1;
+    int ntile1 = 0;
+    for (int q = 0; q < nq; ++q) {
+      v2::P1Slot& s = p1.slot[q];
+      s.ntiles = (s.xhi - s.xlo + p1.TX - 1) / p1.TX;
+      ntile1 = s.ntiles > ntile1 ? s.ntiles : ntile1;
+    }
+    if (rg) {
+      p1.range = 1;
+      p1.e_tab = rg->e_tab;
+      p1.colmap = rg->colmap;
+      p1.w_content = rg->w_content;
+    }
+
+    // pass-2 geometry
+    v2::P2Params p2{};
+    p2.scratch = ws;
+    p2.scr_pitch = sp.pitch;
+    p2.scratch_img_rows = p1.scratch_img_rows;
+    p2.no_tma = p1.no_tma;
+    p2.nq = nq;
+    p2.W = (int)any->cols;
+    p2.Hp = f.Hp;
+    p2.wc = f.wc;
+    const int span2 = rg ? rg->out_hi - rg->out_lo : p2.W;
+    int box2 = v2::BOX2;
+    if (box2 > (p2.W & ~3)) box2 = p2.W & ~3;
+    if (box2 > (span2 & ~3)) box2 = span2 & ~3;
+    p2.TX = box2 - v2::WO2;
+    int ntile2 = 0;
+    for (int q = 0; q < nq; ++q) {
+      v2::P2Slot& s = p2.slot[q];
+      s.sigma = slots[q].sigma;
+      s.xlo1 = p1.slot[q].xlo;
+      s.xhi1 = p1.slot[q].xhi;
+      s.srow0 = p1.slot[q].srow0;
+      if (rg) {
+        s.xbeg = rg->out_lo;
+        s.xend = rg->out_hi;
+      } else {
+        s.xbeg = s.sigma > 0 ? -f.Hp : 0;
+        s.xend = s.xbeg + p2.W;
+      }
+      s.ntiles = (s.xend - s.xbeg + p2.TX - 1) / p2.TX;
+      ntile2 = s.ntiles > ntile2 ? s.ntiles : ntile2;
+      s.qrow = slots[q].qrow;
+      s.rbase = slots[q].row_base;
+      s.rsign = slots[q].row_sign;
+      s.skip = slots[q].skip_t;
+    }
+    if (rg) {
+      p2.range = 1;
+      p2.start_tab = rg->start_tab;
+      p2.len_tab = rg->len_tab;
+    }
+    CUtensorMap tm_out[2];
+    p2.ndest = 0;
+    for (int d = 0; d < 2; ++d) {
+      const fht_hough* o = outs.d[d];
+      if (!o) continue;
+      v2::P2Dest& D = p2.dest[p2.ndest];
+      D.shifted = d;
+      D.ptr = o->data;
+      D.pitch = o->row_stride;
+      D.rows_per_img = o->batch_stride / o->row_stride;
+      if (!make_row_map(&tm_out[p2.ndest], o->data, o->dtype == FHT_F32, (uint64_t)o->cols,
+                        (uint64_t)(o->batch * D.rows_per_img), (uint64_t)o->row_stride, (uint32_t)box2))
+        return FHT_ERR_CUDA;
+      ++p2.ndest;
+    }
+    if (p2.ndest == 1) tm_out[1] = tm_out[0];
+    const bool f32 = img->dtype == FHT_F32;
+    CUtensorMap tm_scr;
+    if (!make_row_map(&tm_scr, ws, f32, (uint64_t)sp.pitch, (uint64_t)sp.chunk * p1.scratch_img_rows,
+                      (uint64_t)sp.pitch, (uint32_t)p1.TX))
+      return FHT_ERR_CUDA;
+
+    for (int64_t b0 = 0; b0 < img->batch; b0 += sp.chunk) {
+      const int nb = (int)((img->batch - b0) < sp.chunk ? (img->batch - b0) : sp.chunk);
+      p1.img0 = (int)b0;
+      p2.img0 = (int)b0;
+      dim3 g1(ntile1, nstrips, nb * nq);
+      cudaError_t e;
+      switch (img->dtype) {
+        case FHT_U8: e = launch_p1<uint8_t>(f.m, g1, tm_scr, p1, st); break;
+        case FHT_I32: e = launch_p1<int32_t>(f.m, g1, tm_scr, p1, st); break;
+        default: e = launch_p1<float>(f.m, g1, tm_scr, p1, st); break;
+      }
+      if (e != cudaSuccess) return FHT_ERR_CUDA;
+      ++launches;
+      dim3 g2(ntile2, ngroups, nb * nq);
+      e = f32 ? launch_p2<float>(f.L, g2, tm_out[0], tm_out[1], p2, st)
+              : launch_p2<int>(f.L, g2, tm_out[0], tm_out[1], p2, st);
+      if (e != cudaSuccess) return FHT_ERR_CUDA;
+      ++launches;
+    }
+    return launches;
+  }
+
+  // ---------------- v1 (degenerate frames only)
+  const int Ws = (int)sp.pitch;
+  const int nstrips = 1 << f.L, ngroups = 1 << f.m;
+  for (int64_t b0 = 0; b0 < img->batch; b0 += sp.chunk) {
+    const int nb = (int)((img->batch - b0) < sp.chunk ? (img->batch - b0) : sp.chunk);
     Pass1Args p1{};
     p1.img = img->data;
     p1.img_bstride = img->batch_stride;
@@ -208,58 +479,65 @@ int run_orientation(const fht_image* img, const Frame& f, const Slot* slots, int
     if (e != cudaSuccess) return FHT_ERR_CUDA;
     ++launches;
 
-    Pass2Args p2{};
-    p2.scratch = ws;
-    p2.scratch_zstride = p1.scratch_zstride;
-    p2.Ws = Ws;
-    p2.m = f.m;
-    p2.L = f.L;
-    p2.out = out->data;
-    p2.out_img_stride = out->batch_stride;
-    p2.out_row_stride = out->row_stride;
-    p2.W = rg ? (int)out->cols : f.W;
-    p2.wc = f.wc;
-    p2.Hp = f.Hp;
-    p2.nq = nq;
-    p2.img0 = (int)b0;
-    p2.shift = shift_mode;
-    int span = p2.W;
-    for (int q = 0; q < nq; ++q) {
-      p2.sigma[q] = slots[q].sigma;
-      p2.xlo[q] = p1.xlo[q];
-      p2.out_q_offset[q] = slots[q].out_q_offset;
-      p2.row_base[q] = slots[q].row_base;
-      p2.row_sign[q] = slots[q].row_sign;
-      p2.skip_t[q] = slots[q].skip_t;
-      p2.xbeg[q] = rg ? rg->out_lo : (slots[q].sigma > 0 ? -f.Hp : 0);
+    for (int d = 0; d < 2; ++d) {
+      const fht_hough* out = outs.d[d];
+      if (!out) continue;
+      Pass2Args p2{};
+      p2.scratch = ws;
+      p2.scratch_zstride = p1.scratch_zstride;
+      p2.Ws = Ws;
+      p2.m = f.m;
+      p2.L = f.L;
+      p2.out = out->data;
+      p2.out_img_stride = out->batch_stride;
+      p2.out_row_stride = out->row_stride;
+      p2.W = (int)out->cols;
+      p2.wc = f.wc;
+      p2.Hp = f.Hp;
+      p2.nq = nq;
+      p2.img0 = (int)b0;
+      p2.shift = d ? (rg ? 2 : 1) : 0;
+      int span = p2.W;
+      for (int q = 0; q < nq; ++q) {
+        p2.sigma[q] = slots[q].sigma;
+        p2.xlo[q] = p1.xlo[q];
+        p2.out_q_offset[q] = slots[q].qrow * out->row_stride;
+        p2.row_base[q] = slots[q].row_base;
+        p2.row_sign[q] = slots[q].row_sign;
+        p2.skip_t[q] = slots[q].skip_t;
+        p2.xbeg[q] = rg ? rg->out_lo : (slots[q].sigma > 0 ? -f.Hp : 0);
+      }
+      if (rg) {
+        p2.range = 1;
+        p2.start_tab = rg->start_tab;
+        p2.len_tab = rg->len_tab;
+        span = rg->out_hi - rg->out_lo;
+      }
+      const int ntile2 = (span + kTileX - 1) / kTileX;
+      dim3 g2(ntile2, ngroups, nb * nq);
+      e = img->dtype == FHT_F32 ? launch_pass2<float>(f.L, g2, p2, st) : launch_pass2<int>(f.L, g2, p2, st);
+      if (e != cudaSuccess) return FHT_ERR_CUDA;
+      ++launches;
     }
-    if (rg) {
-      p2.range = 1;
-      p2.start_tab = rg->start_tab;
-      p2.len_tab = rg->len_tab;
-      span = rg->out_hi - rg->out_lo;
-    }
-    const int ntile2 = (span + kTileX - 1) / kTileX;
-    dim3 g2(ntile2, ngroups, nb * nq);
-    e = img->dtype == FHT_F32 ? launch_pass2<float>(f.L, g2, p2, st) : launch_pass2<int>(f.L, g2, p2, st);
-    if (e != cudaSuccess) return FHT_ERR_CUDA;
-    ++launches;
   }
   return launches;
 }
 
 int validate_out(const fht_hough* out, const fht_hough& want) {
-  if (!out || !out->data) return FHT_ERR_ARG;
+  if (!out->data) return FHT_ERR_ARG;
   if (out->dtype != want.dtype) return FHT_ERR_DTYPE;
   if (out->mode != want.mode || out->batch != want.batch || out->nquad != want.nquad ||
       out->rows != want.rows || out->cols != want.cols)
     return FHT_ERR_SHAPE;
   if (want.mode == FHT_MODE_FULL && out->layout != want.layout) return FHT_ERR_SHAPE;
   if (out->row_stride < out->cols) return FHT_ERR_SHAPE;
-  if (out->nquad > 1 && out->quad_stride < out->rows * out->row_stride) return FHT_ERR_SHAPE;
-  if (out->batch > 1 && out->batch_stride < out->nquad * (out->nquad > 1 ? out->quad_stride : out->rows * out->row_stride))
+  // uniform row pitch across quadrants and images: the kernels address a [rows_total][W] view
+  if (out->nquad > 1 && out->quad_stride != out->rows * out->row_stride) return FHT_ERR_SHAPE;
+  const int64_t per_img = out->nquad * out->rows * out->row_stride;
+  if (out->batch > 1 && (out->batch_stride < per_img || out->batch_stride % out->row_stride != 0))
     return FHT_ERR_SHAPE;
-  if ((reinterpret_cast<uintptr_t>(out->data) & 3u) != 0) return FHT_ERR_ALIGN;
+  if (out->batch == 1 && out->batch_stride % out->row_stride != 0) return FHT_ERR_SHAPE;
+  if (!aligned16(out->data) || (out->row_stride & 3) != 0) return FHT_ERR_ALIGN;  // TMA row stores
   return FHT_OK;
 }
 
@@ -278,10 +556,62 @@ size_t hough_extent_bytes(const fht_hough* h) {
           h->cols) * 4;
 }
 
+// Validate the (out, out_shifted) pair against the wanted shape; no aliasing between any of
+// image, outputs and workspace.
+int validate_outs(const fht_image* img, const fht_hough* out, const fht_hough* out_s, const fht_hough& want,
+                  const void* ws, size_t ws_bytes) {
+  if (!out && !out_s) return FHT_ERR_ARG;
+  const fht_hough* o[2] = {out, out_s};
+  for (int d = 0; d < 2; ++d) {
+    if (!o[d]) continue;
+    int s = validate_out(o[d], want);
+    if (s) return s;
+    if (overlaps(img->data, image_extent_bytes(img), o[d]->data, hough_extent_bytes(o[d]))) return FHT_ERR_ARG;
+    if (ws && overlaps(ws, ws_bytes, o[d]->data, hough_extent_bytes(o[d]))) return FHT_ERR_ARG;
+  }
+  if (out && out_s && overlaps(out->data, hough_extent_bytes(out), out_s->data, hough_extent_bytes(out_s)))
+    return FHT_ERR_ARG;
+  return FHT_OK;
+}
+
+void mark_outs(fht_hough* out, fht_hough* out_s) {
+  if (out) out->shifted = 0;
+  if (out_s) out_s->shifted = 1;
+}
+
 // Plan geometry helpers (R13, R16, R17): identical double formulas to the device tables.
 int plan_e(double g, int64_t y) {
   volatile double p = g * (double)y;  // volatile: forbid contraction into an FMA
   return (int)std::floor(p + 0.5);
+}
+
+Frame range_frame(const fht_image* img, const fht_angle_plan* plan) {
+  Frame f{};
+  f.transposed = 0;
+  f.Hp = (int)plan->Hp;
+  f.K = ilog2(f.Hp);
+  f.wc = (int)plan->w_content;
+  f.W = (int)plan->W;
+  f.rows_avail = (int)img->h;
+  f.cols_avail = (int)img->w;
+  split_levels(f);
+  return f;
+}
+
+RangeDev range_geometry(const Frame& f, const fht_angle_plan* plan) {
+  RangeDev rg{};
+  rg.w_content = (int)plan->w_content;
+  rg.x_lo = (int)plan->e_min - ((1 << f.m) - 1);
+  rg.x_hi = (int)(plan->e_max + plan->w_content);
+  // pass-2 signed columns: [min_s start_s, max_s start_s + W'); start_s in [e_min-(Hp-1), e_max]
+  rg.out_lo = (int)plan->e_min - (f.Hp - 1);
+  rg.out_hi = (int)plan->e_max + (int)plan->W;
+  return rg;
+}
+
+size_t range_tables_bytes(const fht_angle_plan* plan) {
+  const size_t tables = (size_t)(plan->h + plan->w_content + 2 * plan->Hp + 64) * 4;
+  return (tables + 255) & ~size_t(255);
 }
 
 }  // namespace
@@ -413,25 +743,23 @@ size_t fht_workspace_bytes(int mode, const fht_image* img, const fht_angle_plan*
   if (!img || img->batch < 1 || img->h < 1 || img->w < 1) return 0;
   if (mode == FHT_MODE_RANGE) {
     if (!plan) return 0;
-    const int m = (ilog2(plan->Hp) + 1) / 2;
-    const int64_t x_lo = plan->e_min - ((1 << m) - 1), x_hi = plan->e_max + plan->w_content;
-    const int64_t Ws = (x_hi - x_lo + 3) & ~int64_t(3);
-    const size_t tables = (size_t)(plan->h + plan->w_content + 2 * plan->Hp + 64) * 4;
-    return (size_t)plan->Hp * Ws * 4 + ((tables + 255) & ~size_t(255));
+    const Frame f = range_frame(img, plan);
+    const RangeDev rg = range_geometry(f, plan);
+    const ScratchPlan sp = scratch_plan(f, 1, 1, &rg);
+    return ((sp.bytes + 255) & ~size_t(255)) + range_tables_bytes(plan);
   }
   size_t need = 0;
   for (int tr = 0; tr < 2; ++tr) {
     const Frame f = make_frame(img->h, img->w, tr, mode == FHT_MODE_FULL);
     const int nq = mode == FHT_MODE_FULL ? 2 : 1;
-    const size_t per = scratch_bytes_per_image(f, nq);
-    const size_t tot = per * chunk_images(per, img->batch);
-    need = tot > need ? tot : need;
+    const ScratchPlan sp = scratch_plan(f, nq, img->batch, nullptr);
+    need = sp.bytes > need ? sp.bytes : need;
   }
   return need;
 }
 
-int fht_quadrant(const fht_image* img, int quadrant, int64_t pad_cols, fht_hough* out, void* ws, size_t ws_bytes,
-                 fht_stream_t stream) {
+int fht_quadrant(const fht_image* img, int quadrant, int64_t pad_cols, fht_hough* out, fht_hough* out_shifted,
+                 void* ws, size_t ws_bytes, fht_stream_t stream) {
   int s = check_image(img);
   if (s) return s;
   if (quadrant < 0 || quadrant > 3) return FHT_ERR_ARG;
@@ -440,30 +768,31 @@ int fht_quadrant(const fht_image* img, int quadrant, int64_t pad_cols, fht_hough
   if (s) return s;
   const Frame f = make_frame(img->h, img->w, quadrant >= 2, 0);
   if (pad_cols != -1 && pad_cols != f.Hp) return FHT_ERR_UNSUPPORTED;
-  if ((s = validate_out(out, want))) return s;
-  if (out->quadrant != quadrant) return FHT_ERR_ARG;
+  if ((s = validate_outs(img, out, out_shifted, want, ws, ws_bytes))) return s;
+  if ((out && out->quadrant != quadrant) || (out_shifted && out_shifted->quadrant != quadrant)) return FHT_ERR_ARG;
   if ((s = check_frame_supported(f))) return s;
-  if (overlaps(img->data, image_extent_bytes(img), out->data, hough_extent_bytes(out))) return FHT_ERR_ARG;
-  if (ws && overlaps(ws, ws_bytes, out->data, hough_extent_bytes(out))) return FHT_ERR_ARG;
   Slot sl{};
   sl.sigma = (quadrant == FHT_QA || quadrant == FHT_QD) ? 1 : -1;
-  sl.out_q_offset = 0;
+  sl.qrow = 0;
   sl.row_base = 0;
   sl.row_sign = 1;
   sl.skip_t = -1;
-  return run_orientation(img, f, &sl, 1, out, ws, ws_bytes, (cudaStream_t)stream, nullptr, out->shifted ? 1 : 0);
+  Outs o{{out, out_shifted}};
+  const int r = run_orientation(img, f, &sl, 1, o, ws, ws_bytes, (cudaStream_t)stream, nullptr);
+  if (r > 0) mark_outs(out, out_shifted);
+  return r;
 }
 
-int fht_full(const fht_image* img, int layout, fht_hough* out, void* ws, size_t ws_bytes, fht_stream_t stream) {
+int fht_full(const fht_image* img, int layout, fht_hough* out, fht_hough* out_shifted, void* ws, size_t ws_bytes,
+             fht_stream_t stream) {
   int s = check_image(img);
   if (s) return s;
   fht_hough want;
   if ((s = fht_hough_describe(FHT_MODE_FULL, layout, 0, img, nullptr, &want))) return s;
-  if ((s = validate_out(out, want))) return s;
-  if (overlaps(img->data, image_extent_bytes(img), out->data, hough_extent_bytes(out))) return FHT_ERR_ARG;
-  if (ws && overlaps(ws, ws_bytes, out->data, hough_extent_bytes(out))) return FHT_ERR_ARG;
+  if ((s = validate_outs(img, out, out_shifted, want, ws, ws_bytes))) return s;
   const int Hp = (int)want.Hp, Wp = (int)want.Wp;
   int launches = 0;
+  Outs o{{out, out_shifted}};
   for (int tr = 0; tr < 2; ++tr) {
     const Frame f = make_frame(img->h, img->w, tr, 1);
     if ((s = check_frame_supported(f))) return s;
@@ -474,12 +803,12 @@ int fht_full(const fht_image* img, int layout, fht_hough* out, void* ws, size_t 
       const int q = qid[k];
       sl[k].sigma = (q == FHT_QA || q == FHT_QD) ? 1 : -1;
       if (layout == FHT_LAYOUT_QUADS) {
-        sl[k].out_q_offset = (int64_t)q * out->quad_stride;
+        sl[k].qrow = (int64_t)q * want.rows;
         sl[k].row_base = 0;
         sl[k].row_sign = 1;
         sl[k].skip_t = -1;
       } else {  // CONCAT (R7, R8)
-        sl[k].out_q_offset = 0;
+        sl[k].qrow = 0;
         switch (q) {
           case FHT_QA: sl[k].row_base = Hp - 1; sl[k].row_sign = -1; sl[k].skip_t = -1; break;
           case FHT_QB: sl[k].row_base = Hp - 1; sl[k].row_sign = 1; sl[k].skip_t = 0; break;
@@ -488,52 +817,35 @@ int fht_full(const fht_image* img, int layout, fht_hough* out, void* ws, size_t 
         }
       }
     }
-    const int r = run_orientation(img, f, sl, 2, out, ws, ws_bytes, (cudaStream_t)stream, nullptr,
-                                  out->shifted ? 1 : 0);
+    const int r = run_orientation(img, f, sl, 2, o, ws, ws_bytes, (cudaStream_t)stream, nullptr);
     if (r < 0) return r;
     launches += r;
   }
+  mark_outs(out, out_shifted);
   return launches;
 }
 
-int fht_angle_range(const fht_image* img, const fht_angle_plan* plan, fht_hough* out, void* ws, size_t ws_bytes,
-                    fht_stream_t stream) {
+int fht_angle_range(const fht_image* img, const fht_angle_plan* plan, fht_hough* out, fht_hough* out_shifted,
+                    void* ws, size_t ws_bytes, fht_stream_t stream) {
   int s = check_image(img);
   if (s) return s;
   if (!plan || plan->h != img->h || plan->w != img->w) return FHT_ERR_ARG;
   fht_hough want;
   if ((s = fht_hough_describe(FHT_MODE_RANGE, 0, 0, img, plan, &want))) return s;
-  if ((s = validate_out(out, want))) return s;
-  if (overlaps(img->data, image_extent_bytes(img), out->data, hough_extent_bytes(out))) return FHT_ERR_ARG;
+  if ((s = validate_outs(img, out, out_shifted, want, ws, ws_bytes))) return s;
   const size_t need = fht_workspace_bytes(FHT_MODE_RANGE, img, plan);
   if (!ws || ws_bytes < need) return FHT_ERR_WORKSPACE;
-  if (overlaps(ws, ws_bytes, out->data, hough_extent_bytes(out))) return FHT_ERR_ARG;
-  Frame f{};
-  f.transposed = 0;
-  f.Hp = (int)plan->Hp;
-  f.K = ilog2(f.Hp);
-  f.wc = (int)plan->w_content;
-  f.W = (int)plan->W;
-  f.rows_avail = (int)img->h;
-  f.cols_avail = (int)img->w;
-  split_levels(f);
+  const Frame f = range_frame(img, plan);
   if ((s = check_frame_supported(f))) return s;
+  RangeDev rg = range_geometry(f, plan);
+  const ScratchPlan sp = scratch_plan(f, 1, 1, &rg);
   // workspace: [scratch][e_tab h][colmap w'][start Hp][len Hp]
-  const int x_lo = (int)plan->e_min - ((1 << f.m) - 1), x_hi = (int)(plan->e_max + plan->w_content);
-  const int Ws = (x_hi - x_lo + 3) & ~3;
-  const size_t scratch = (size_t)f.Hp * Ws * 4;
+  const size_t scratch = (sp.bytes + 255) & ~size_t(255);
   int* tab = reinterpret_cast<int*>(static_cast<char*>(ws) + scratch);
-  RangeDev rg{};
   rg.e_tab = tab;
   rg.colmap = tab + img->h;
   rg.start_tab = tab + img->h + plan->w_content;
   rg.len_tab = rg.start_tab + f.Hp;
-  rg.w_content = (int)plan->w_content;
-  rg.x_lo = x_lo;
-  rg.x_hi = x_hi;
-  // pass-2 signed columns: [min_s start_s, max_s start_s + W'); start_s in [e_min-(Hp-1), e_max]
-  rg.out_lo = (int)plan->e_min - (f.Hp - 1);
-  rg.out_hi = (int)plan->e_max + (int)plan->W;
   RangeTableArgs ta{};
   ta.g = plan->g;
   ta.alpha = plan->alpha;
@@ -553,8 +865,11 @@ int fht_angle_range(const fht_image* img, const fht_angle_plan* plan, fht_hough*
   sl.sigma = 1;
   sl.row_sign = 1;
   sl.skip_t = -1;
-  const int r = run_orientation(img, f, &sl, 1, out, ws, scratch, (cudaStream_t)stream, &rg, out->shifted ? 2 : 0);
-  return r < 0 ? r : r + 1;
+  Outs o{{out, out_shifted}};
+  const int r = run_orientation(img, f, &sl, 1, o, ws, scratch, (cudaStream_t)stream, &rg);
+  if (r < 0) return r;
+  mark_outs(out, out_shifted);
+  return r + 1;
 }
 
 int fhtshift(const fht_hough* in, fht_hough* out, fht_stream_t stream) {

@@ -242,3 +242,63 @@ def test_config5_batch_f32(fht, O):
             k = O.fhtshift_amounts_quadrant(2048, 4096, O.QUADRANT_FRAME[q][1])
             for row in (0, 1, 1000, 2047):
                 assert np.array_equal(gs[b, q, row], np.roll(got[b, q, row], int(k[row])))
+
+
+# ------------------------------------------------------------------ v2 tiling coverage
+# Shapes chosen so the v2 kernels see: every pass split r = 1..6 (K = 2..12), tiles narrower
+# than the 216-column maximum, several tiles with a ragged (clamped, overlapping) last tile,
+# the sigma=+1 wrap at x = 0, transposed loads, and non-square frames.
+V2_SHAPES = [(3, 500), (4, 300), (8, 61), (20, 1000), (70, 333), (300, 129), (513, 40), (1000, 37),
+             (129, 1500), (2049, 9)]
+
+
+@pytest.mark.parametrize("shape", V2_SHAPES, ids=str)
+@pytest.mark.parametrize("dt", ["u8", "f32"])
+def test_v2_quadrant_tiling(fht, O, shape, dt):
+    from synth import random_image
+    img = random_image(shape, dt, seed=7 * shape[0] + shape[1])
+    t = dev(img)
+    for q in range(4):
+        h, s = fht.quadrant(t, q, pair=True)
+        torch.cuda.synchronize()
+        got = h.view[0, 0].cpu().numpy()
+        want = O.hough_recursive(img, q)
+        check(got, want, dt != "f32")
+        sigma = O.QUADRANT_FRAME[q][1]
+        assert np.array_equal(s.view[0, 0].cpu().numpy(), O.fhtshift_quadrant(got, sigma))
+
+
+@pytest.mark.parametrize("shape", [(300, 700), (257, 255), (1024, 64)], ids=str)
+@pytest.mark.parametrize("dt", ["u8", "i32", "f32"])
+def test_v2_full_pair(fht, O, shape, dt):
+    """Full transform written as (H, fhtshift(H)) by one pass, QUADS and CONCAT layouts."""
+    from synth import random_image
+    img = random_image(shape, dt, seed=shape[0] + 11 * shape[1])
+    t = dev(img)
+    Hp, Wp = O.full_padding(*shape)
+    quads = O.full_quadrants(img)
+    hq, sq = fht.full(t, "quads", pair=True)
+    hc, sc = fht.full(t, "concat", pair=True)
+    torch.cuda.synchronize()
+    gq = hq.view[0].cpu().numpy()
+    for q in range(4):
+        n = quads[q].shape[0]
+        check(gq[q, :n], quads[q], dt != "f32")
+        assert np.array_equal(sq.view[0, q, :n].cpu().numpy(), O.fhtshift_quadrant(gq[q, :n], O.QUADRANT_FRAME[q][1]))
+    gc = hc.view[0, 0].cpu().numpy()
+    check(gc, O.full_concat(quads, Hp, Wp), dt != "f32")
+    assert np.array_equal(sc.view[0, 0].cpu().numpy(), O.fhtshift_concat(gc, Hp, Wp))
+
+
+def test_v2_batch_chunks(fht, O):
+    """A batch large enough to need several pass-1 scratch chunks (48 MiB budget)."""
+    from synth import random_image
+    imgs = np.stack([random_image((1024, 1024), "f32", seed=100 + b) for b in range(7)])
+    h = fht.full(dev(imgs))
+    torch.cuda.synchronize()
+    assert h.launches > 4
+    got = h.view.cpu().numpy()
+    for b in (0, 4, 6):
+        quads = O.full_quadrants(imgs[b])
+        for q in range(4):
+            check(got[b, q], quads[q], False)
