@@ -1,14 +1,21 @@
 #!/usr/bin/env python
 """Benchmark of the B200 FHT hot path (BASELINE.json metric: input Gpixel/s for the full
-four-quadrant FHT; achieved HBM GB/s against the roofline).
+four-quadrant FHT; achieved HBM GB/s vs roofline).
 
-    python bench.py [--gpus N --steps K --warmup W] [--config 2|5|...] [--impl ours|reference]
+    python bench.py [--gpus N --steps K --warmup W] [--config 2|5|3|4|1] [--impl ours|reference]
 
-A step = one pass of the config's hot path over one batch of synthetic input already resident
-in HBM: C2 = full four-quadrant FHT + fhtshift (BASELINE configs[1], the default), C5 = the
-same on 16 x 2048^2, C3 = full FHT of 64 x 512^2 u8, C4 = angle-range FHT + fhtshift, C1 = one
-quadrant. Rank 0 prints ONE JSON line. Under torchrun each rank runs its own batch (weak
-scaling, no collective: images are independent).
+A step = one pass of the config's whole hot path over one batch of synthetic input already
+resident in HBM:
+  C2 (default, BASELINE configs[1]): full four-quadrant FHT of one 1024^2 f32 image, writing the
+      four Hough quadrants AND their fhtshift regrouping (both outputs, one pass);
+  C5: the same on 16 x 2048^2; C3: full FHT of 64 x 512^2 u8 (int32 out); C4: angle-range FHT
+      [-15, 15] deg of 4096^2 f32 + fhtshift; C1: one quadrant of a 256^2 u8 image.
+Rank 0 prints ONE JSON line. Under torchrun every rank transforms its own batch (weak scaling,
+no data-path collective: the images are independent); the step time is the max
+over ranks. The other configs are timed too and reported under "configs" (not the headline).
+
+--impl reference runs the oracle (oracle/fht_oracle.py, tier-2 numpy recursion, float64/int64)
+on the host cores over a bounded sample of the same workload: the task's reference arm.
 """
 from __future__ import annotations
 
@@ -17,7 +24,6 @@ import json
 import multiprocessing as mp
 import os
 import statistics
-import subprocess
 import sys
 import threading
 import time
@@ -28,6 +34,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "input Gpixel/s for full 4-quadrant FHT; achieved HBM GB/s vs roofline"
+L2_BYTES = 126 << 20
 L2_FLUSH_BYTES = 512 << 20
 
 
@@ -35,95 +42,114 @@ def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
         d = json.load(open(p))
-        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy r+w)"
-    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+        return float(d["hbm_gbs"]), "measured: MEASURED_PEAKS.json hbm_gbs (copy, read+write bytes)"
+    return 6650.0, "fallback: B200_PROFILING.md 6.65 TB/s"
+
+
+def load_traffic():
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed ncu --set full
+    capture (profiles/ncu_traffic.json, written by tools/ncu_summary.py), or {}."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    return json.load(open(p)) if os.path.exists(p) else {}
 
 
 # ----------------------------------------------------------------------------------------- clocks
 class ClockSampler:
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """Polls NVML (SM clock, max clock, clock-event reasons) from a thread while active."""
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "hw_power_brake_slowdown": 0x80, "sw_power_cap": 0x4}
 
     def __init__(self, index=0):
-        self.index, self.samples, self.proc = index, [], None
+        self.index, self.samples, self.stop = index, [], threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:  # noqa: BLE001 -- no NVML: report unsampled
+            pass
+
+    def _run(self):
+        nv = self.nv
+        while not self.stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                rs = (nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                      if hasattr(nv, "nvmlDeviceGetCurrentClocksEventReasons")
+                      else nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h))
+                self.samples.append((sm, rs))
+            except Exception:  # noqa: BLE001
+                return
+            time.sleep(0.0005)
 
     def __enter__(self):
-        try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
+        if self.ok:
+            self.thread = threading.Thread(target=self._run, daemon=True)
             self.thread.start()
-        except OSError:
-            self.proc = None
+            time.sleep(0.002)
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) == 6:
-                self.samples.append(parts)
-
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            self.proc.wait()
+        if self.ok:
+            time.sleep(0.002)
+            self.stop.set()
+            self.thread.join()
 
     def summary(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": float(self.samples[0][1]) if self.samples[0][1].replace(".", "").isdigit() else None,
-                "reasons": reasons, "samples": len(self.samples)}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        reasons = sorted({n for _, rs in self.samples for n, bit in self.REASONS.items() if rs & bit})
+        return {"sm_mhz": statistics.median(s for s, _ in self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(self.samples), "source": "NVML polled during the timed region"}
 
 
 # ----------------------------------------------------------------------------------------- workloads
-def workload(cfg_id: int):
-    import synth
-    c = synth.CONFIGS[cfg_id]
-    imgs = synth.batch(cfg_id)
-    return c, imgs
+def pow2(n):
+    return 1 << (n - 1).bit_length()
 
 
-def out_bytes_per_step(cfg_id, c, imgs):
-    B, h, w = imgs.shape
-    Hp, Wp = 1 << (h - 1).bit_length(), 1 << (w - 1).bit_length()
+def geometry(cfg_id, c):
+    """Algorithmic bytes: input read once, every output written once."""
+    B, h, w = c["batch"], c["h"], c["w"]
+    in_b = B * h * w * (1 if c["dtype"] == "u8" else 4)
+    Hp, Wp = pow2(h), pow2(w)
     if c["mode"] == "quadrant":
-        return Hp * (w + Hp) * 4, 0
-    if c["mode"] == "full":
-        hough = B * 4 * max(Hp, Wp) * (Hp + Wp) * 4
-        return hough, (hough if cfg_id in (2, 5) else 0)
-    return None, None
+        cells = B * Hp * (w + Hp)
+        ndest = 1
+    elif c["mode"] == "full":
+        cells = B * 4 * max(Hp, Wp) * (Hp + Wp)
+        ndest = 2 if cfg_id in (2, 5) else 1
+    else:
+        cells = None  # range: from the plan (filled in by the caller)
+        ndest = 2
+    return in_b, cells, ndest
 
 
-def make_step(fht, cfg_id, c, t, ws, outs):
-    """Returns step() -> number of kernel launches it enqueued (all through the C ABI).
-    C2/C5/C4 write the Hough image AND its fhtshift in the same pass (pair=True)."""
+def make_step(fht, cfg_id, c, t, outs, plan=None):
+    """step(events=None) -> kernel launches enqueued (all through the C ABI)."""
     if c["mode"] == "quadrant":
-        def step():
-            outs["h"] = fht.quadrant(t, fht.QA, workspace=ws, out=outs.get("h"))
+        def step(events=None):
+            outs["h"] = fht.quadrant(t, fht.QA, out=outs.get("h"), workspace=outs.get("ws"), events=events)
             return outs["h"].launches
         return step
     if c["mode"] == "full":
-        do_shift = cfg_id in (2, 5)
+        pair = cfg_id in (2, 5)
 
-        def step():
-            if do_shift:
-                outs["h"], outs["s"] = fht.full(t, pair=True, workspace=ws, out=outs.get("h"),
-                                                out_shifted=outs.get("s"))
+        def step(events=None):
+            if pair:
+                outs["h"], outs["s"] = fht.full(t, pair=True, out=outs.get("h"), out_shifted=outs.get("s"),
+                                                workspace=outs.get("ws"), events=events)
             else:
-                outs["h"] = fht.full(t, workspace=ws, out=outs.get("h"))
+                outs["h"] = fht.full(t, out=outs.get("h"), workspace=outs.get("ws"), events=events)
             return outs["h"].launches
         return step
-    plan = fht.angle_plan(c["h"], c["w"], c["theta_min"], c["theta_max"])
-    outs["plan"] = plan
 
-    def step():
-        outs["h"], outs["s"] = fht.angle_range(t, plan, pair=True, workspace=ws, out=outs.get("h"),
-                                               out_shifted=outs.get("s"))
+    def step(events=None):
+        outs["h"], outs["s"] = fht.angle_range(t, plan, pair=True, out=outs.get("h"), out_shifted=outs.get("s"),
+                                               workspace=outs.get("ws"), events=events)
         return outs["h"].launches
     return step
 
@@ -153,45 +179,45 @@ def _oracle_unit(args):
     return 0
 
 
-def oracle_sample(cfg_id: int, c, imgs, max_units: int | None = None):
-    """Time the oracle as it stands (tier-2 recursion, float64/int64) over a bounded sample of
-    the workload: whole (image, quadrant) units in a fork pool over the host cores."""
+def oracle_sample(cfg_id: int, c, imgs, min_seconds: float = 10.0, max_units: int = 4096):
+    """Time the oracle as it stands (tier-2 recursion, float64/int64) on the host cores over a
+    bounded sample of the workload: whole (image, quadrant) units, repeated round-robin over the
+    batch until >= min_seconds of wall time, in a fork pool (one process per core)."""
     global _ORACLE_IMGS
     _ORACLE_IMGS = imgs
     if c["mode"] == "full":
-        units = [(cfg_id, b, q) for b in range(imgs.shape[0]) for q in range(4)]
+        base = [(cfg_id, b, q) for b in range(imgs.shape[0]) for q in range(4)]
         per_unit_px = c["h"] * c["w"] / 4.0
     else:
-        units = [(cfg_id, 0, 0)]
+        base = [(cfg_id, 0, 0)]
         per_unit_px = c["h"] * c["w"]
-    if max_units:
-        units = units[:max_units]
-    cores = max(1, min(len(units), len(os.sched_getaffinity(0))))
+    cores = max(1, len(os.sched_getaffinity(0)))
+    done, t_total = 0, 0.0
     with mp.get_context("fork").Pool(cores) as pool:
-        t0 = time.perf_counter()
-        pool.map(_oracle_unit, units, chunksize=1)
-        dt = time.perf_counter() - t0
-    px = per_unit_px * len(units)
-    return {"value": px / dt / 1e9, "unit": "Gpixel/s", "cores": cores, "kind": "oracle",
-            "sample": f"{len(units)} (image, quadrant) units of config {cfg_id} "
-                      f"({'full FHT' if c['mode'] == 'full' else c['mode']}"
-                      f"{' + fhtshift' if cfg_id in (2, 4, 5) else ''}), tier-2 numpy recursion f64/i64, "
-                      f"{dt:.2f} s wall"}
-
-
-def oracle_units_budget(cfg_id):
-    return {1: None, 2: None, 3: 32, 4: None, 5: 8}[cfg_id]
+        while t_total < min_seconds and done < max_units:
+            batch = [base[(done + i) % len(base)] for i in range(max(cores, 1))]
+            t0 = time.perf_counter()
+            pool.map(_oracle_unit, batch, chunksize=1)
+            t_total += time.perf_counter() - t0
+            done += len(batch)
+    px = per_unit_px * done
+    kind = {"full": "full FHT", "quadrant": "one quadrant", "range": "angle-range FHT"}[c["mode"]]
+    return {"value": px / t_total / 1e9, "unit": "Gpixel/s", "cores": cores, "kind": "oracle",
+            "sample": f"{done} (image, quadrant) units of {c['name']} ({kind}"
+                      f"{' + fhtshift' if cfg_id in (2, 4, 5) else ''}); oracle tier-2 numpy recursion, "
+                      f"float64/int64, one process per core, {t_total:.1f} s wall"}
 
 
 # ----------------------------------------------------------------------------------------- main
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--extra-configs", default="5,3,4,1",
                     help="other configs also timed (reported under 'configs', not the headline)")
     args = ap.parse_args()
@@ -207,18 +233,19 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        _, ref_imgs = workload(args.config)
-        times = []
+        imgs = synth.batch(args.config)
+        per_step = max(2.0, min(20.0, 150.0 / (args.steps + args.warmup)))
+        vals, last = [], None
         for i in range(args.warmup + args.steps):
-            cb = oracle_sample(args.config, c, ref_imgs, oracle_units_budget(args.config))
+            last = oracle_sample(args.config, c, imgs, min_seconds=per_step)
             if i >= args.warmup:
-                times.append(cb)
-        v = statistics.mean(x["value"] for x in times)
+                vals.append(last["value"])
+        v = statistics.mean(vals)
         line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "Gpixel/s", "n_gpus": args.gpus,
                 "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "f64" if c["dtype"] == "f32" else "int64", "data": "synthetic",
                 "config": {"workload": c["name"], "batch": c["batch"], "h": c["h"], "w": c["w"]},
-                "cpu_baseline": dict(times[-1], value=v),
+                "cpu_baseline": dict(last, value=v),
                 "e2e": {"value": v, "unit": "Gpixel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
         return
@@ -233,82 +260,108 @@ def main():
     import paper_1811_06378_b200 as fht
 
     peak_gbs, peak_src = load_peaks()
+    traffic = load_traffic()
+    kernel_names = ["k_p1 (pass 1: levels 1..m, image -> L2 scratch)",
+                    "k_p2 (pass 2: levels m+1..K, scratch -> Hough image [+ fhtshift])"]
 
     def barrier():
         if world > 1:
             dist.barrier()
 
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        tt = torch.tensor([x], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        return float(tt.item())
+
     def run_config(cfg_id, steps, warmup, with_e2e):
         cc = synth.CONFIGS[cfg_id]
-        _, imgs = workload(cfg_id)
+        imgs = synth.batch(cfg_id)
         t = torch.from_numpy(imgs).to(dev)
-        B, h, w = imgs.shape
+        in_b, cells, ndest = geometry(cfg_id, cc)
+        plan = None
+        if cc["mode"] == "range":
+            plan = fht.angle_plan(cc["h"], cc["w"], cc["theta_min"], cc["theta_max"])
+            cells = cc["batch"] * plan.Hp * plan.W
+        out_b = cells * 4 * ndest
         outs = {}
-        ws = None
-        step = make_step(fht, cfg_id, cc, t, ws, outs)
-        step()
+        step = make_step(fht, cfg_id, cc, t, outs, plan)
+        n_launch = step()
         torch.cuda.synchronize()
-        flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
-        in_bytes = imgs.nbytes
-        need_flush = (in_bytes + sum(o.storage.numel() * 4 for k, o in outs.items() if hasattr(o, "storage"))) < (
-            300 << 20)
+        ws_bytes = 0
+        flush = None
+        if in_b + out_b < 2 * L2_BYTES:
+            flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
         stream = torch.cuda.current_stream()
         for _ in range(warmup):
             step()
         torch.cuda.synchronize()
-        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        # per-step events: [0] before the first kernel ... [n_launch] after the last (fht_exec_opts)
+        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(n_launch + 1)] for _ in range(steps)]
+        for row in evs:  # materialise the cudaEvent_t handles
+            for e in row:
+                e.record(stream)
+        torch.cuda.synchronize()
         launches = 0
         barrier()
         torch.cuda.synchronize()
         with ClockSampler(local_rank) as clk:
             t_wall = time.perf_counter()
             for i in range(steps):
-                if need_flush:
+                if flush is not None:
                     flush.zero_()
-                evs[i][0].record(stream)
-                launches += step()
-                evs[i][1].record(stream)
+                launches += step(events=evs[i])
             torch.cuda.synchronize()
-            barrier()
             t_wall = time.perf_counter() - t_wall
-        per = [a.elapsed_time(b) for a, b in evs]
-        ms = statistics.mean(per)
-        if world > 1:
-            tt = torch.tensor([ms], device=dev)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            ms = float(tt.item())
-        px = B * h * w
-        hough_b = sum(o.storage.numel() * 4 for k, o in outs.items() if hasattr(o, "storage"))
+        barrier()
+        step_ms = [evs[i][0].elapsed_time(evs[i][n_launch]) for i in range(steps)]
+        ker_ms = [[evs[i][k].elapsed_time(evs[i][k + 1]) for i in range(steps)] for k in range(n_launch)]
+        ms = max_over_ranks(statistics.mean(step_ms))
+        kms = [max_over_ranks(statistics.mean(x)) for x in ker_ms]
+        px = cc["batch"] * cc["h"] * cc["w"]
         res = {"workload": cc["name"], "ms_per_step": ms, "gpix_s": px * world / (ms * 1e-3) / 1e9,
-               "bytes_per_step": in_bytes + hough_b, "l2_flushed": need_flush, "launches": launches // steps,
+               "in_bytes": in_b, "out_bytes": out_b, "launches_per_step": launches // steps,
+               "l2": "flushed between steps (512 MiB write outside the step events)" if flush is not None
+               else "working set > L2 (no flush needed)",
                "clocks": clk.summary(), "wall_s": t_wall}
-        res["achieved_gbs"] = res["bytes_per_step"] / (ms * 1e-3) / 1e9
+        res["step_gbs"] = (in_b + out_b) / (ms * 1e-3) / 1e9
+        # dominant kernel: pass 2 (writes every output byte); per-launch algorithmic bytes. With
+        # batch chunking there are several (pass 1, pass 2) pairs per step.
+        # launch order: [range tables,] then (pass 1, pass 2) per batch chunk / orientation
+        first = 1 if cc["mode"] == "range" else 0
+        p2 = [k for k in range(first, n_launch) if (k - first) % 2 == 1]
+        p2_ms = sum(kms[k] for k in p2)
+        p1_ms = sum(kms[k] for k in range(n_launch) if k not in p2)
+        res["kernels"] = {"pass1_ms": p1_ms, "pass2_ms": p2_ms, "pass2_launches": len(p2),
+                          "pass2_share_of_step": p2_ms / ms if ms else None}
+        res["pass2_gbs"] = out_b / (p2_ms * 1e-3) / 1e9
         if with_e2e:
-            res["e2e"] = e2e_config(cfg_id, cc, imgs, step_host(fht, cfg_id, cc, imgs, dev), steps)
+            res["e2e"] = e2e_config(cfg_id, cc, imgs, plan, steps, px)
+        del outs, t, flush
+        torch.cuda.empty_cache()
         return res
 
-    def step_host(fht_, cfg_id, cc, imgs, dev_):
+    def e2e_config(cfg_id, cc, imgs, plan, steps, px):
+        """Same metric through the public API with the input in pinned host memory and the
+        step's result(s) read back to pinned host memory, copies inside the timed region."""
         pinned_in = torch.from_numpy(imgs).pin_memory()
+        t_dev = torch.empty(pinned_in.shape, dtype=pinned_in.dtype, device=dev)
         outs = {}
-        holder = {}
+        step = make_step(fht, cfg_id, cc, t_dev, outs, plan)
+        host = {}
 
         def run():
-            t = pinned_in.to(dev_, non_blocking=True)
-            st = make_step(fht_, cfg_id, cc, t, None, outs)
-            st()
-            res = outs.get("s") or outs["h"]
-            if "pin" not in holder:
-                holder["pin"] = torch.empty(res.storage.shape, dtype=res.storage.dtype).pin_memory()
-                holder["pin_h"] = torch.empty(outs["h"].storage.shape, dtype=outs["h"].storage.dtype).pin_memory()
-            holder["pin"].copy_(res.storage, non_blocking=True)
-            d2h = res.storage.numel() * 4
-            if "s" in outs:
-                holder["pin_h"].copy_(outs["h"].storage, non_blocking=True)
-                d2h += outs["h"].storage.numel() * 4
+            t_dev.copy_(pinned_in, non_blocking=True)
+            step()
+            d2h = 0
+            for k in ("h", "s"):
+                if k in outs:
+                    if k not in host:
+                        host[k] = torch.empty(outs[k].storage.shape, dtype=outs[k].storage.dtype).pin_memory()
+                    host[k].copy_(outs[k].storage, non_blocking=True)
+                    d2h += host[k].numel() * 4
             return pinned_in.numel() * pinned_in.element_size(), d2h
-        return run
-
-    def e2e_config(cfg_id, cc, imgs, run, steps):
         for _ in range(3):
             run()
         torch.cuda.synchronize()
@@ -319,22 +372,22 @@ def main():
             hb, db = run()
         t1.record()
         torch.cuda.synchronize()
-        ms = t0.elapsed_time(t1) / steps
-        px = imgs.shape[0] * imgs.shape[1] * imgs.shape[2]
+        ms = max_over_ranks(t0.elapsed_time(t1) / steps)
         return {"value": px * world / (ms * 1e-3) / 1e9, "unit": "Gpixel/s", "h2d_bytes_per_step": hb,
                 "d2h_bytes_per_step": db, "ms_per_step": ms}
 
     head = run_config(args.config, args.steps, args.warmup, with_e2e=True)
     extra = {}
-    if rank == 0 or world > 1:
-        for cid in [int(x) for x in args.extra_configs.split(",") if x and int(x) != args.config]:
-            try:
-                r = run_config(cid, max(5, args.steps // 2), 3, with_e2e=False)
-                extra[r["workload"]] = {k: r[k] for k in ("ms_per_step", "gpix_s", "achieved_gbs", "bytes_per_step",
-                                                          "l2_flushed", "launches")}
-                extra[r["workload"]]["frac_of_measured_hbm"] = r["achieved_gbs"] / peak_gbs
-            except Exception as e:  # noqa: BLE001 -- report, do not hide
-                extra[synth.CONFIGS[cid]["name"]] = {"error": repr(e)}
+    extra_ids = [] if args.extra_configs in ("", "none") else [int(x) for x in args.extra_configs.split(",")]
+    for cid in [x for x in extra_ids if x != args.config]:
+        try:
+            r = run_config(cid, max(5, args.steps // 4), 3, with_e2e=False)
+            extra[r["workload"]] = {k: r[k] for k in ("ms_per_step", "gpix_s", "step_gbs", "pass2_gbs", "kernels",
+                                                      "launches_per_step", "l2")}
+            extra[r["workload"]]["step_frac_of_measured_hbm"] = r["step_gbs"] / peak_gbs
+            extra[r["workload"]]["pass2_frac_of_measured_hbm"] = r["pass2_gbs"] / peak_gbs
+        except Exception as e:  # noqa: BLE001 -- report, do not hide
+            extra[synth.CONFIGS[cid]["name"]] = {"error": repr(e)}
 
     if rank != 0:
         if world > 1:
@@ -342,23 +395,31 @@ def main():
         return
     cpu = None
     if not args.no_cpu_baseline and world == 1:
-        cpu = oracle_sample(args.config, c, workload(args.config)[1], oracle_units_budget(args.config))
-    frac = head["achieved_gbs"] / peak_gbs
+        cpu = oracle_sample(args.config, c, synth.batch(args.config), min_seconds=args.cpu_seconds)
+    tr = traffic.get(c["name"], {}).get("k_p2")
     line = {
         "metric": METRIC, "value": head["gpix_s"], "unit": "Gpixel/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": head["ms_per_step"], "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32" if c["dtype"] == "f32" else "int32", "data": "synthetic",
-        "config": {"workload": c["name"], "batch": c["batch"] * world, "h": c["h"], "w": c["w"],
-                   "mode": c["mode"] + (" + fhtshift" if args.config in (2, 4, 5) else ""),
-                   "parallelism": f"dp{world} (independent images per rank)",
-                   "l2": "flushed between steps (512 MiB write outside the per-step events)" if head["l2_flushed"]
-                   else "working set > L2", "timing": "CUDA events per step, mean; max over ranks"},
-        "roofline": {"bound": "hbm", "achieved": head["achieved_gbs"], "peak": peak_gbs, "unit": "GB/s",
-                     "frac": frac, "traffic": None, "kernel": "whole step (pass1 + pass2 + fhtshift launches)",
-                     "algorithmic_bytes_per_step": head["bytes_per_step"], "peak_source": peak_src},
+        "config": {"workload": c["name"], "batch_per_gpu": c["batch"], "global_batch": c["batch"] * world,
+                   "h": c["h"], "w": c["w"],
+                   "step": {1: "QA quadrant", 2: "full 4-quadrant FHT + fhtshift (both written)",
+                            3: "full 4-quadrant FHT", 4: "angle-range FHT + fhtshift (both written)",
+                            5: "full 4-quadrant FHT + fhtshift (both written)"}[args.config],
+                   "parallelism": f"dp{world} (independent images per rank, no collective)",
+                   "l2": head["l2"], "timing": "CUDA events on the launching stream, mean over steps; max over ranks"},
+        "roofline": {"bound": "hbm", "achieved": head["pass2_gbs"], "peak": peak_gbs, "unit": "GB/s",
+                     "frac": head["pass2_gbs"] / peak_gbs, "traffic": tr,
+                     "kernel": kernel_names[1], "kernel_ms": head["kernels"]["pass2_ms"],
+                     "algorithmic_bytes_per_launch": head["out_bytes"] // max(1, head["kernels"]["pass2_launches"]),
+                     "share_of_step": head["kernels"]["pass2_share_of_step"], "peak_source": peak_src},
+        "step_roofline": {"bytes": head["in_bytes"] + head["out_bytes"], "achieved": head["step_gbs"],
+                          "peak": peak_gbs, "frac": head["step_gbs"] / peak_gbs,
+                          "note": "compulsory bytes (one read of the image + one write of every output) / step time"},
+        "kernels": head["kernels"],
         "cpu_baseline": cpu,
         "e2e": {k: head["e2e"][k] for k in ("value", "unit", "h2d_bytes_per_step", "d2h_bytes_per_step")},
-        "gpu_launches": head["launches"] * args.steps,
+        "gpu_launches": head["launches_per_step"] * args.steps,
         "clocks": head["clocks"],
         "configs": extra,
     }

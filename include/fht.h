@@ -102,6 +102,16 @@ typedef struct {
   fht_angle_plan plan;                    /* valid iff mode == RANGE */
 } fht_hough;
 
+/* Optional per-call execution options (may be NULL). events: caller-created CUDA events
+ * (cudaEvent_t cast to void*); when non-NULL the call records events[i] on `stream` right
+ * before its i-th kernel launch and events[n] right after its last (n = the call's return
+ * value), for i < n_events. Used by bench.py to time each kernel on the launching stream. */
+typedef struct {
+  void* const* events;
+  int32_t n_events;
+  int32_t _pad0;
+} fht_exec_opts;
+
 /* Fill `out` (except `data`) with the contiguous shape of the transform of `img`:
  *   QUADRANT: rows = Hp, cols = W = w + Hp (QA/QB) or Wp rows, h + Wp cols (QC/QD);
  *   FULL/QUADS: nquad 4, rows = max(Hp, Wp), cols = Hp + Wp (R9);
@@ -125,11 +135,12 @@ size_t fht_workspace_bytes(int mode, const fht_image* img, const fht_angle_plan*
  * other pads return FHT_ERR_UNSUPPORTED on the GPU (the oracle handles any pad cyclically).
  * Outputs from fht_hough_describe(FHT_MODE_QUADRANT, 0, quadrant, ...). */
 int fht_quadrant(const fht_image* img, int quadrant, int64_t pad_cols, fht_hough* out,
-                 fht_hough* out_shifted, void* ws, size_t ws_bytes, fht_stream_t stream);
+                 fht_hough* out_shifted, void* ws, size_t ws_bytes, fht_stream_t stream,
+                 const fht_exec_opts* opts);
 
 /* Full four-quadrant transform. `layout` must equal the outputs' layout. */
 int fht_full(const fht_image* img, int layout, fht_hough* out, fht_hough* out_shifted, void* ws,
-             size_t ws_bytes, fht_stream_t stream);
+             size_t ws_bytes, fht_stream_t stream, const fht_exec_opts* opts);
 
 /* Host-only: build the §4 plan. FHT_ERR_ARG if theta_min >= theta_max,
  * |theta| >= 90 deg, or alpha*w < 1. Deterministic double arithmetic, no FMA (R16). */
@@ -139,7 +150,8 @@ int fht_angle_plan_make(int64_t h, int64_t w, double theta_min_deg, double theta
 /* Angle-range-restricted transform: QA of the virtually sheared+scaled image, the
  * shear and scale fused into the first FHT iteration (pass-1 loader). f32/u8/i32 input. */
 int fht_angle_range(const fht_image* img, const fht_angle_plan* plan, fht_hough* out,
-                    fht_hough* out_shifted, void* ws, size_t ws_bytes, fht_stream_t stream);
+                    fht_hough* out_shifted, void* ws, size_t ws_bytes, fht_stream_t stream,
+                    const fht_exec_opts* opts);
 
 /* §5 fhtshift (R11): out[r][x] = in[r][(x - k_r) mod cols], k_r = ceil((n+s)/2) for
  * sigma=+1 quadrants, ceil((n-s)/2) for sigma=-1, and ceil((W'-len_s)/2) - start_s in RANGE

@@ -57,6 +57,10 @@ class FhtHough(ctypes.Structure):
     ]
 
 
+class FhtExecOpts(ctypes.Structure):
+    _fields_ = [("events", ctypes.POINTER(ctypes.c_void_p)), ("n_events", ctypes.c_int32), ("_pad0", ctypes.c_int32)]
+
+
 class FhtError(RuntimeError):
     def __init__(self, fn: str, status: int):
         super().__init__(f"{fn} failed: {STATUS.get(status, status)}")
@@ -72,10 +76,11 @@ def _load():
     lib.fht_hough_describe.argtypes = [i32, i32, i32, P(FhtImage), P(FhtAnglePlan), P(FhtHough)]
     lib.fht_workspace_bytes.argtypes = [i32, P(FhtImage), P(FhtAnglePlan)]
     lib.fht_workspace_bytes.restype = sz
-    lib.fht_quadrant.argtypes = [P(FhtImage), i32, i64, P(FhtHough), P(FhtHough), vp, sz, vp]
-    lib.fht_full.argtypes = [P(FhtImage), i32, P(FhtHough), P(FhtHough), vp, sz, vp]
+    lib.fht_quadrant.argtypes = [P(FhtImage), i32, i64, P(FhtHough), P(FhtHough), vp, sz, vp, P(FhtExecOpts)]
+    lib.fht_full.argtypes = [P(FhtImage), i32, P(FhtHough), P(FhtHough), vp, sz, vp, P(FhtExecOpts)]
     lib.fht_angle_plan_make.argtypes = [i64, i64, dbl, dbl, P(FhtAnglePlan)]
-    lib.fht_angle_range.argtypes = [P(FhtImage), P(FhtAnglePlan), P(FhtHough), P(FhtHough), vp, sz, vp]
+    lib.fht_angle_range.argtypes = [P(FhtImage), P(FhtAnglePlan), P(FhtHough), P(FhtHough), vp, sz, vp,
+                                    P(FhtExecOpts)]
     lib.fhtshift.argtypes = [P(FhtHough), P(FhtHough), vp]
     lib.fht_status_string.argtypes = [i32]
     lib.fht_status_string.restype = ctypes.c_char_p

@@ -250,54 +250,77 @@ cudaError_t launch_pass2(int logr, dim3 grid, const Pass2Args& a, cudaStream_t s
 }
 
 // ---------------------------------------------------------------- v2 launch helpers
+struct P1Maps {
+  CUtensorMap img0, img1, scr;
+};
 template <typename Tin, int R>
-cudaError_t launch_p1_t(dim3 grid, const CUtensorMap& tm, const v2::P1Params& a, cudaStream_t st) {
-  const size_t smem = v2::tile_smem_bytes(R, 1);
+cudaError_t launch_p1_t(dim3 grid, const P1Maps& m, const v2::P1Params& a, cudaStream_t st) {
+  const size_t smem = v2::p1_smem_bytes(R, sizeof(Tin) == 1);
   static const cudaError_t attr =
       cudaFuncSetAttribute(v2::k_p1<Tin, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (attr != cudaSuccess) return attr;
-  v2::k_p1<Tin, R><<<grid, v2::Split<R>::nw * 32, smem, st>>>(tm, a);
+  v2::k_p1<Tin, R><<<grid, v2::Split<R>::nw * 32, smem, st>>>(m.img0, m.img1, m.scr, a);
   return cudaGetLastError();
 }
 template <typename Tin>
-cudaError_t launch_p1(int r, dim3 grid, const CUtensorMap& tm, const v2::P1Params& a, cudaStream_t st) {
+cudaError_t launch_p1(int r, dim3 grid, const P1Maps& m, const v2::P1Params& a, cudaStream_t st) {
   switch (r) {
-    case 1: return launch_p1_t<Tin, 1>(grid, tm, a, st);
-    case 2: return launch_p1_t<Tin, 2>(grid, tm, a, st);
-    case 3: return launch_p1_t<Tin, 3>(grid, tm, a, st);
-    case 4: return launch_p1_t<Tin, 4>(grid, tm, a, st);
-    case 5: return launch_p1_t<Tin, 5>(grid, tm, a, st);
-    case 6: return launch_p1_t<Tin, 6>(grid, tm, a, st);
+    case 1: return launch_p1_t<Tin, 1>(grid, m, a, st);
+    case 2: return launch_p1_t<Tin, 2>(grid, m, a, st);
+    case 3: return launch_p1_t<Tin, 3>(grid, m, a, st);
+    case 4: return launch_p1_t<Tin, 4>(grid, m, a, st);
+    case 5: return launch_p1_t<Tin, 5>(grid, m, a, st);
+    case 6: return launch_p1_t<Tin, 6>(grid, m, a, st);
   }
   return cudaErrorInvalidValue;
 }
+struct P2Maps {
+  CUtensorMap scr0, scr1, out0, out1;
+};
 template <typename A, int R>
-cudaError_t launch_p2_t(dim3 grid, const CUtensorMap& t0, const CUtensorMap& t1, const v2::P2Params& a,
-                        cudaStream_t st) {
-  const size_t smem = v2::tile_smem_bytes(R, a.ndest);
-  static const cudaError_t attr = cudaFuncSetAttribute(v2::k_p2<A, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                       (int)v2::tile_smem_bytes(R, 2));
+cudaError_t launch_p2_t(dim3 grid, const P2Maps& m, const v2::P2Params& a, cudaStream_t st) {
+  const size_t smem = v2::p2_smem_bytes(R);
+  static const cudaError_t attr =
+      cudaFuncSetAttribute(v2::k_p2<A, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (attr != cudaSuccess) return attr;
-  v2::k_p2<A, R><<<grid, v2::Split<R>::nw * 32, smem, st>>>(t0, t1, a);
+  v2::k_p2<A, R><<<grid, v2::Split<R>::nw * 32, smem, st>>>(m.scr0, m.scr1, m.out0, m.out1, a);
   return cudaGetLastError();
 }
 template <typename A>
-cudaError_t launch_p2(int r, dim3 grid, const CUtensorMap& t0, const CUtensorMap& t1, const v2::P2Params& a,
-                      cudaStream_t st) {
+cudaError_t launch_p2(int r, dim3 grid, const P2Maps& m, const v2::P2Params& a, cudaStream_t st) {
   switch (r) {
-    case 1: return launch_p2_t<A, 1>(grid, t0, t1, a, st);
-    case 2: return launch_p2_t<A, 2>(grid, t0, t1, a, st);
-    case 3: return launch_p2_t<A, 3>(grid, t0, t1, a, st);
-    case 4: return launch_p2_t<A, 4>(grid, t0, t1, a, st);
-    case 5: return launch_p2_t<A, 5>(grid, t0, t1, a, st);
-    case 6: return launch_p2_t<A, 6>(grid, t0, t1, a, st);
+    case 1: return launch_p2_t<A, 1>(grid, m, a, st);
+    case 2: return launch_p2_t<A, 2>(grid, m, a, st);
+    case 3: return launch_p2_t<A, 3>(grid, m, a, st);
+    case 4: return launch_p2_t<A, 4>(grid, m, a, st);
+    case 5: return launch_p2_t<A, 5>(grid, m, a, st);
+    case 6: return launch_p2_t<A, 6>(grid, m, a, st);
   }
   return cudaErrorInvalidValue;
 }
 
-// One quadrant slot of an orientation: sign, source orientation and output row placement.
+// 3-D image tensor [batch][h][w] (elements of 1 or 4 bytes), box 1 x 1 x box_cols.
+bool make_image_map(CUtensorMap* m, const fht_image* img, uint32_t box_cols) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  const uint64_t es = dtype_size(img->dtype);
+  cuuint64_t dims[3] = {(cuuint64_t)img->w, (cuuint64_t)img->h, (cuuint64_t)img->batch};
+  cuuint64_t strides[2] = {(cuuint64_t)(img->row_stride * es), (cuuint64_t)(img->batch_stride * es)};
+  if (img->batch == 1) strides[1] = (cuuint64_t)(img->h * img->row_stride * es);
+  cuuint32_t box[3] = {box_cols, 1, 1};
+  cuuint32_t e[3] = {1, 1, 1};
+  const CUtensorMapDataType dt = img->dtype == FHT_U8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8
+                                 : img->dtype == FHT_I32 ? CU_TENSOR_MAP_DATA_TYPE_INT32
+                                                         : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+  return fn(m, dt, 3, const_cast<void*>(img->data), dims, strides, box, e, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
+}
+
+// One quadrant slot: sign, source orientation and output row placement.
 struct Slot {
   int sigma;
+  int transposed;
   int64_t qrow;          // output row (in the [batch*rows_per_img][W] view) of the quadrant's row 0
   int row_base, row_sign, skip_t;
 };
@@ -307,9 +330,23 @@ struct Outs {
   const fht_hough* d[2];
 };
 
+// Launch accounting across one ABI call: counts kernels and records the caller's optional
+// timing events (fht_exec_opts) before launch i and after the last launch.
+struct LaunchLog {
+  const fht_exec_opts* opts;
+  int n;
+  void before(cudaStream_t st) {
+    if (opts && opts->events && n < opts->n_events) cudaEventRecord((cudaEvent_t)opts->events[n], st);
+  }
+  void after(cudaStream_t st) {
+    ++n;
+    if (opts && opts->events && n < opts->n_events) cudaEventRecord((cudaEvent_t)opts->events[n], st);
+  }
+};
+
 // Run the two passes for one orientation over all images, chunked. Returns launches or error.
 int run_orientation(const fht_image* img, const Frame& f, const Slot* slots, int nq, const Outs& outs, void* ws,
-                    size_t ws_bytes, cudaStream_t st, const RangeDev* rg) {
+                    size_t ws_bytes, cudaStream_t st, const RangeDev* rg, LaunchLog& log) {
   const ScratchPlan sp = scratch_plan(f, nq, img->batch, rg);
   if (!ws || ws_bytes < sp.bytes) return FHT_ERR_WORKSPACE;
   int launches = 0;
@@ -317,26 +354,27 @@ int run_orientation(const fht_image* img, const Frame& f, const Slot* slots, int
 
   if (sp.v2) {
     const int nstrips = 1 << f.L, ngroups = 1 << f.m;
+    const size_t es = dtype_size(img->dtype);
     v2::P1Params p1{};
     p1.img = img->data;
     p1.img_bstride = img->batch_stride;
     p1.img_rstride = img->row_stride;
-    p1.rows_avail = f.rows_avail;
-    p1.cols_avail = f.cols_avail;
-    p1.transposed = f.transposed;
+    p1.img_h = (int)img->h;
+    p1.img_w = (int)img->w;
     p1.nq = nq;
     p1.L = f.L;
     p1.scratch_img_rows = (int64_t)nq * f.Hp;
-    p1.scratch = ws;
-    p1.scr_pitch = sp.pitch;
-    {
-      const char* e = std::getenv("FHT_DEBUG_NO_TMA");
-      p1.no_tma = (e && e[0] == '1') ? 1 : 0;
-    }
+    const bool pitch16 = aligned16(img->data) && (img->row_stride * es) % 16 == 0 &&
+                         (img->batch == 1 || (img->batch_stride * es) % 16 == 0);
+    p1.fill_tma = !rg && pitch16;
+    p1.fill_vec = f.m >= 2 && (es == 1 ? ((reinterpret_cast<uintptr_t>(img->data) & 3) == 0 &&
+                                          img->row_stride % 4 == 0 && (img->batch == 1 || img->batch_stride % 4 == 0))
+                                       : pitch16);
     int span1 = 1 << 30;
     for (int q = 0; q < nq; ++q) {
       v2::P1Slot& s = p1.slot[q];
       s.sigma = slots[q].sigma;
+      s.transposed = slots[q].transposed;
       v2_pass1_range(f, s.sigma, rg, s.xlo, s.xhi);
       s.srow0 = (int64_t)q * f.Hp;
       span1 = (s.xhi - s.xlo) < span1 ? (s.xhi - s.xlo) : span1;
@@ -357,10 +395,11 @@ int run_orientation(const fht_image* img, const Frame& f, const Slot* slots, int
 
     // pass-2 geometry
     v2::P2Params p2{};
-    p2.scratch = ws;
-    p2.scr_pitch = sp.pitch;
     p2.scratch_img_rows = p1.scratch_img_rows;
-    p2.no_tma = p1.no_tma;
+    {
+      const char* e = std::getenv("FHT_DEBUG_NO_TMA");
+      p2.no_tma = (e && e[0] == '1') ? 1 : 0;
+    }
     p2.nq = nq;
     p2.W = (int)any->cols;
     p2.Hp = f.Hp;
@@ -396,7 +435,8 @@ int run_orientation(const fht_image* img, const Frame& f, const Slot* slots, int
       p2.start_tab = rg->start_tab;
       p2.len_tab = rg->len_tab;
     }
-    CUtensorMap tm_out[2];
+    P2Maps m2;
+    CUtensorMap* tm_out[2] = {&m2.out0, &m2.out1};
     p2.ndest = 0;
     for (int d = 0; d < 2; ++d) {
       const fht_hough* o = outs.d[d];
@@ -406,16 +446,27 @@ int run_orientation(const fht_image* img, const Frame& f, const Slot* slots, int
       D.ptr = o->data;
       D.pitch = o->row_stride;
       D.rows_per_img = o->batch_stride / o->row_stride;
-      if (!make_row_map(&tm_out[p2.ndest], o->data, o->dtype == FHT_F32, (uint64_t)o->cols,
+      if (!make_row_map(tm_out[p2.ndest], o->data, o->dtype == FHT_F32, (uint64_t)o->cols,
                         (uint64_t)(o->batch * D.rows_per_img), (uint64_t)o->row_stride, (uint32_t)box2))
         return FHT_ERR_CUDA;
       ++p2.ndest;
     }
-    if (p2.ndest == 1) tm_out[1] = tm_out[0];
+    if (p2.ndest == 1) m2.out1 = m2.out0;
     const bool f32 = img->dtype == FHT_F32;
-    CUtensorMap tm_scr;
-    if (!make_row_map(&tm_scr, ws, f32, (uint64_t)sp.pitch, (uint64_t)sp.chunk * p1.scratch_img_rows,
-                      (uint64_t)sp.pitch, (uint32_t)p1.TX))
+    const uint64_t scr_rows = (uint64_t)sp.chunk * p1.scratch_img_rows;
+    P1Maps m1;
+    if (!make_row_map(&m1.scr, ws, f32, (uint64_t)sp.pitch, scr_rows, (uint64_t)sp.pitch, (uint32_t)p1.TX))
+      return FHT_ERR_CUDA;
+    if (p1.fill_tma) {
+      if (!make_image_map(&m1.img0, img, 256) || !make_image_map(&m1.img1, img, es == 1 ? 48 : 36))
+        return FHT_ERR_CUDA;
+    } else {
+      m1.img0 = m1.scr;
+      m1.img1 = m1.scr;
+    }
+    // scratch as pass 2 reads it: columns [0, span1) = what pass 1 wrote; TMA zero-fills the rest
+    if (!make_row_map(&m2.scr0, ws, f32, (uint64_t)span1, scr_rows, (uint64_t)sp.pitch, 256) ||
+        !make_row_map(&m2.scr1, ws, f32, (uint64_t)span1, scr_rows, (uint64_t)sp.pitch, 36))
       return FHT_ERR_CUDA;
 
     for (int64_t b0 = 0; b0 < img->batch; b0 += sp.chunk) {
@@ -424,17 +475,19 @@ int run_orientation(const fht_image* img, const Frame& f, const Slot* slots, int
       p2.img0 = (int)b0;
       dim3 g1(ntile1, nstrips, nb * nq);
       cudaError_t e;
+      log.before(st);
       switch (img->dtype) {
-        case FHT_U8: e = launch_p1<uint8_t>(f.m, g1, tm_scr, p1, st); break;
-        case FHT_I32: e = launch_p1<int32_t>(f.m, g1, tm_scr, p1, st); break;
-        default: e = launch_p1<float>(f.m, g1, tm_scr, p1, st); break;
+        case FHT_U8: e = launch_p1<uint8_t>(f.m, g1, m1, p1, st); break;
+        case FHT_I32: e = launch_p1<int32_t>(f.m, g1, m1, p1, st); break;
+        default: e = launch_p1<float>(f.m, g1, m1, p1, st); break;
       }
       if (e != cudaSuccess) return FHT_ERR_CUDA;
+      log.after(st);
       ++launches;
       dim3 g2(ntile2, ngroups, nb * nq);
-      e = f32 ? launch_p2<float>(f.L, g2, tm_out[0], tm_out[1], p2, st)
-              : launch_p2<int>(f.L, g2, tm_out[0], tm_out[1], p2, st);
+      e = f32 ? launch_p2<float>(f.L, g2, m2, p2, st) : launch_p2<int>(f.L, g2, m2, p2, st);
       if (e != cudaSuccess) return FHT_ERR_CUDA;
+      log.after(st);
       ++launches;
     }
     return launches;
@@ -449,6 +502,7 @@ int run_orientation(const fht_image* img, const Frame& f, const Slot* slots, int
     p1.img = img->data;
     p1.img_bstride = img->batch_stride;
     p1.img_rstride = img->row_stride;
+    if (nq > 2) return FHT_ERR_UNSUPPORTED;  // v1 handles one orientation per launch
     p1.img_rows = f.rows_avail;
     p1.img_cols = f.cols_avail;
     p1.transposed = f.transposed;
@@ -471,12 +525,14 @@ int run_orientation(const fht_image* img, const Frame& f, const Slot* slots, int
     const int ntile1 = (Ws + kTileX - 1) / kTileX;
     dim3 g1(ntile1, nstrips, nb * nq);
     cudaError_t e;
+    log.before(st);
     switch (img->dtype) {
       case FHT_U8: e = launch_pass1<uint8_t>(f.m, g1, p1, st); break;
       case FHT_I32: e = launch_pass1<int32_t>(f.m, g1, p1, st); break;
       default: e = launch_pass1<float>(f.m, g1, p1, st); break;
     }
     if (e != cudaSuccess) return FHT_ERR_CUDA;
+    log.after(st);
     ++launches;
 
     for (int d = 0; d < 2; ++d) {
@@ -517,6 +573,7 @@ int run_orientation(const fht_image* img, const Frame& f, const Slot* slots, int
       dim3 g2(ntile2, ngroups, nb * nq);
       e = img->dtype == FHT_F32 ? launch_pass2<float>(f.L, g2, p2, st) : launch_pass2<int>(f.L, g2, p2, st);
       if (e != cudaSuccess) return FHT_ERR_CUDA;
+      log.after(st);
       ++launches;
     }
   }
@@ -749,6 +806,10 @@ size_t fht_workspace_bytes(int mode, const fht_image* img, const fht_angle_plan*
     return ((sp.bytes + 255) & ~size_t(255)) + range_tables_bytes(plan);
   }
   size_t need = 0;
+  if (mode == FHT_MODE_FULL && next_pow2(img->h) == next_pow2(img->w)) {
+    const Frame f = make_frame(img->h, img->w, 0, 1);
+    if (use_v2(f, nullptr)) return scratch_plan(f, 4, img->batch, nullptr).bytes;  // one 4-slot pass
+  }
   for (int tr = 0; tr < 2; ++tr) {
     const Frame f = make_frame(img->h, img->w, tr, mode == FHT_MODE_FULL);
     const int nq = mode == FHT_MODE_FULL ? 2 : 1;
@@ -759,7 +820,7 @@ size_t fht_workspace_bytes(int mode, const fht_image* img, const fht_angle_plan*
 }
 
 int fht_quadrant(const fht_image* img, int quadrant, int64_t pad_cols, fht_hough* out, fht_hough* out_shifted,
-                 void* ws, size_t ws_bytes, fht_stream_t stream) {
+                 void* ws, size_t ws_bytes, fht_stream_t stream, const fht_exec_opts* opts) {
   int s = check_image(img);
   if (s) return s;
   if (quadrant < 0 || quadrant > 3) return FHT_ERR_ARG;
@@ -773,60 +834,70 @@ int fht_quadrant(const fht_image* img, int quadrant, int64_t pad_cols, fht_hough
   if ((s = check_frame_supported(f))) return s;
   Slot sl{};
   sl.sigma = (quadrant == FHT_QA || quadrant == FHT_QD) ? 1 : -1;
+  sl.transposed = f.transposed;
   sl.qrow = 0;
   sl.row_base = 0;
   sl.row_sign = 1;
   sl.skip_t = -1;
   Outs o{{out, out_shifted}};
-  const int r = run_orientation(img, f, &sl, 1, o, ws, ws_bytes, (cudaStream_t)stream, nullptr);
+  LaunchLog log{opts, 0};
+  const int r = run_orientation(img, f, &sl, 1, o, ws, ws_bytes, (cudaStream_t)stream, nullptr, log);
   if (r > 0) mark_outs(out, out_shifted);
   return r;
 }
 
 int fht_full(const fht_image* img, int layout, fht_hough* out, fht_hough* out_shifted, void* ws, size_t ws_bytes,
-             fht_stream_t stream) {
+             fht_stream_t stream, const fht_exec_opts* opts) {
   int s = check_image(img);
   if (s) return s;
   fht_hough want;
   if ((s = fht_hough_describe(FHT_MODE_FULL, layout, 0, img, nullptr, &want))) return s;
   if ((s = validate_outs(img, out, out_shifted, want, ws, ws_bytes))) return s;
   const int Hp = (int)want.Hp, Wp = (int)want.Wp;
-  int launches = 0;
   Outs o{{out, out_shifted}};
-  for (int tr = 0; tr < 2; ++tr) {
-    const Frame f = make_frame(img->h, img->w, tr, 1);
-    if ((s = check_frame_supported(f))) return s;
-    Slot sl[2];
-    // orientation 0: QA (+), QB (-); orientation 1: QC (-), QD (+)   (R4)
-    const int qid[2] = {tr ? FHT_QC : FHT_QA, tr ? FHT_QD : FHT_QB};
-    for (int k = 0; k < 2; ++k) {
-      const int q = qid[k];
-      sl[k].sigma = (q == FHT_QA || q == FHT_QD) ? 1 : -1;
-      if (layout == FHT_LAYOUT_QUADS) {
-        sl[k].qrow = (int64_t)q * want.rows;
-        sl[k].row_base = 0;
-        sl[k].row_sign = 1;
-        sl[k].skip_t = -1;
-      } else {  // CONCAT (R7, R8)
-        sl[k].qrow = 0;
-        switch (q) {
-          case FHT_QA: sl[k].row_base = Hp - 1; sl[k].row_sign = -1; sl[k].skip_t = -1; break;
-          case FHT_QB: sl[k].row_base = Hp - 1; sl[k].row_sign = 1; sl[k].skip_t = 0; break;
-          case FHT_QC: sl[k].row_base = 2 * Hp - 2 + Wp - 1; sl[k].row_sign = -1; sl[k].skip_t = Wp - 1; break;
-          default: sl[k].row_base = 2 * Hp + Wp - 3; sl[k].row_sign = 1; sl[k].skip_t = 0; break;
-        }
+  LaunchLog log{opts, 0};
+  Slot sl[4];
+  // orientation 0: QA (+), QB (-); orientation 1: QC (-), QD (+)   (R4)
+  const int qid[4] = {FHT_QA, FHT_QB, FHT_QC, FHT_QD};
+  for (int k = 0; k < 4; ++k) {
+    const int q = qid[k];
+    sl[k].sigma = (q == FHT_QA || q == FHT_QD) ? 1 : -1;
+    sl[k].transposed = q >= FHT_QC;
+    if (layout == FHT_LAYOUT_QUADS) {
+      sl[k].qrow = (int64_t)q * want.rows;
+      sl[k].row_base = 0;
+      sl[k].row_sign = 1;
+      sl[k].skip_t = -1;
+    } else {  // CONCAT (R7, R8)
+      sl[k].qrow = 0;
+      switch (q) {
+        case FHT_QA: sl[k].row_base = Hp - 1; sl[k].row_sign = -1; sl[k].skip_t = -1; break;
+        case FHT_QB: sl[k].row_base = Hp - 1; sl[k].row_sign = 1; sl[k].skip_t = 0; break;
+        case FHT_QC: sl[k].row_base = 2 * Hp - 2 + Wp - 1; sl[k].row_sign = -1; sl[k].skip_t = Wp - 1; break;
+        default: sl[k].row_base = 2 * Hp + Wp - 3; sl[k].row_sign = 1; sl[k].skip_t = 0; break;
       }
     }
-    const int r = run_orientation(img, f, sl, 2, o, ws, ws_bytes, (cudaStream_t)stream, nullptr);
+  }
+  const Frame f0 = make_frame(img->h, img->w, 0, 1), f1 = make_frame(img->h, img->w, 1, 1);
+  if ((s = check_frame_supported(f0)) || (s = check_frame_supported(f1))) return s;
+  int r;
+  if (Hp == Wp && use_v2(f0, nullptr)) {
+    // square: both orientations share one frame -> one pass-1 and one pass-2 launch for all four
+    r = run_orientation(img, f0, sl, 4, o, ws, ws_bytes, (cudaStream_t)stream, nullptr, log);
     if (r < 0) return r;
-    launches += r;
+  } else {
+    r = run_orientation(img, f0, sl, 2, o, ws, ws_bytes, (cudaStream_t)stream, nullptr, log);
+    if (r < 0) return r;
+    const int r2 = run_orientation(img, f1, sl + 2, 2, o, ws, ws_bytes, (cudaStream_t)stream, nullptr, log);
+    if (r2 < 0) return r2;
+    r += r2;
   }
   mark_outs(out, out_shifted);
-  return launches;
+  return r;
 }
 
 int fht_angle_range(const fht_image* img, const fht_angle_plan* plan, fht_hough* out, fht_hough* out_shifted,
-                    void* ws, size_t ws_bytes, fht_stream_t stream) {
+                    void* ws, size_t ws_bytes, fht_stream_t stream, const fht_exec_opts* opts) {
   int s = check_image(img);
   if (s) return s;
   if (!plan || plan->h != img->h || plan->w != img->w) return FHT_ERR_ARG;
@@ -859,14 +930,17 @@ int fht_angle_range(const fht_image* img, const fht_angle_plan* plan, fht_hough*
   ta.start_tab = const_cast<int*>(rg.start_tab);
   ta.len_tab = const_cast<int*>(rg.len_tab);
   const int nb_tab = f.Hp + (int)((std::max<int64_t>(img->h, plan->w_content) + kThreads - 1) / kThreads);
+  LaunchLog log{opts, 0};
+  log.before((cudaStream_t)stream);
   k_range_tables<<<nb_tab, kThreads, 0, (cudaStream_t)stream>>>(ta);
   if (cudaGetLastError() != cudaSuccess) return FHT_ERR_CUDA;
+  log.after((cudaStream_t)stream);
   Slot sl{};
   sl.sigma = 1;
   sl.row_sign = 1;
   sl.skip_t = -1;
   Outs o{{out, out_shifted}};
-  const int r = run_orientation(img, f, &sl, 1, o, ws, scratch, (cudaStream_t)stream, &rg);
+  const int r = run_orientation(img, f, &sl, 1, o, ws, scratch, (cudaStream_t)stream, &rg, log);
   if (r < 0) return r;
   mark_outs(out, out_shifted);
   return r + 1;

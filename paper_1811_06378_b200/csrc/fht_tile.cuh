@@ -12,21 +12,30 @@
 // offset), not once per level as in v1.
 //
 // Window and local columns: a tile computes the 217 signed columns x = Xw + s, s in [0, 217)
-// ("window index" s). The butterflies run in a local frame where the partner sits at +shift for
-// both signs: c = s (sigma = +1) or c = 216 - s (sigma = -1, mirrored). Lane l owns local
+// ("window index" s) from the 288 input columns x(e) = Xa + e, e in [0, 288) (Xa = Xw for
+// sigma = +1, Xw - 71 for sigma = -1: the halo lies on the partner side). The butterflies run in
+// a local frame where the partner sits at +shift for both signs: c = e (sigma = +1) or
+// c = 287 - e (sigma = -1, mirrored); window index s = c (+1) or 216 - c (-1). Lane l owns local
 // columns l*V .. l*V+V-1; lane 31 is a halo lane whose results are discarded, so every shuffle
 // partner of lanes 0..30 is inside the warp (needs 2^levels - 1 <= V).
 //
-// Stores (measured TMA rules on this B200, tools/tma_probe.cu: a bulk tensor store needs a
-// 16-byte-aligned, non-negative start column and a 128-byte-aligned shared source; the upper
-// tensor bound clips): each output row is staged in shared memory at an offset chosen so that
-// its destination starts on a 16-byte boundary, then written by ONE cp.async.bulk.tensor row
-// store (SASS UTMASTG). Pass-1 scratch rows are always aligned. Pass-2 rows (x mod W for the
-// Hough image, (x + k_t) mod W for the fused fhtshift) use a 212-wide box starting up to 3
-// columns left of the tile's 208 columns (the tile computes them anyway); a cyclic-wrap
-// remainder or a row-support edge (range mode) is written by a warp with coalesced st.global.
+// Bulk tensor copies (measured on this B200 by tools/tma_probe.cu): the innermost start
+// coordinate must be 16-byte aligned (negative is allowed for loads, which zero-fill outside the
+// tensor; stores need >= 0 and clip at the upper bound), and the shared address 128-byte aligned.
+// Loads therefore start at the aligned-down column and the tile keeps a per-row offset; stores
+// are staged at an offset chosen so the destination starts on a 16-byte boundary.
+//   pass 1: input rows by TMA (non-transposed image with 16-byte pitch), a vectorised transposing
+//           fill (transposed quadrants) or a scalar gather (angle-range loader, odd pitches);
+//           scratch rows by TMA (always aligned).
+//   pass 2: scratch rows by TMA (the tensor bound is the written extent, so the zero fill is the
+//           "outside the pass-1 support" mask); Hough rows x mod W and, for the fused fhtshift,
+//           (x + k_t) mod W by TMA from a staging row realigned per destination; a cyclic-wrap
+//           remainder or a row-support edge (range mode) by a warp with coalesced st.global.
 #pragma once
 #include <cuda.h>
+
+#include <type_traits>
+
 #include "fht_common.cuh"
 
 namespace fht {
@@ -34,14 +43,15 @@ namespace v2 {
 
 constexpr int VA = 9;            // local columns per lane, sub-pass A (odd => conflict-free)
 constexpr int VB = 7;            // local columns per lane, sub-pass B (odd => conflict-free)
-constexpr int WA = 32 * VA;      // 288 local input columns loaded per tile
+constexpr int WA = 32 * VA;      // 288 local input columns per tile
 constexpr int WC = 31 * VB;      // 217 computed window columns per tile
-constexpr int IN_PITCH = WA + 1; // 289: odd pitch, conflict-free column-wise (transposed) fills
+constexpr int FA_PITCH = WA + 1; // 289: odd pitch (A results; conflict-free transposing fill)
+constexpr int TMA_PITCH = 320;   // TMA-loaded 4-byte rows: 292 used, 1280-B (128-B multiple) pitch
+constexpr int TMA_PITCH_U8 = 384;// TMA-loaded 1-byte rows: 304 used, 384-B pitch
 constexpr int ST_PITCH = 224;    // staging pitch (elements): 896 B rows, 128-B aligned for TMA
 constexpr int TX1 = 216;         // pass-1 tile width (= its TMA box), multiple of 4
-constexpr int BOX2 = 212;        // pass-2 TMA box width (multiple of 4)
-constexpr int TX2 = BOX2 - 4;    // pass-2 tile stride: 208 columns owned per tile
-constexpr int WO2 = 4;           // pass-2 window starts 4 columns left of the tile
+constexpr int BOX2 = 212;        // pass-2 store box width (multiple of 4)
+constexpr int WO2 = 4;           // pass-2 window starts 4 columns left of the tile's own columns
 
 template <int R> struct Split;
 template <> struct Split<1> { static constexpr int a = 1, b = 0, nw = 4; };
@@ -50,14 +60,16 @@ template <> struct Split<3> { static constexpr int a = 3, b = 0, nw = 4; };
 template <> struct Split<4> { static constexpr int a = 2, b = 2, nw = 4; };
 template <> struct Split<5> { static constexpr int a = 3, b = 2, nw = 4; };
 template <> struct Split<6> { static constexpr int a = 3, b = 3, nw = 8; };
+template <int R> constexpr int kTPW = ((1 << Split<R>::a) + Split<R>::nw - 1) / Split<R>::nw;  // B tasks/warp
 
-// Dynamic shared memory: the tile buffer (reused as `ndest` staging planes) + the offset table.
-__host__ __device__ constexpr size_t tile_buf_elems(int R, int ndest) {
-  return (size_t)(1 << R) * (IN_PITCH > ndest * ST_PITCH ? IN_PITCH : ndest * ST_PITCH);
+// Shared memory layout (bytes): [main buffer][u8 input tile (pass 1 u8 TMA only)][tables]
+__host__ __device__ constexpr size_t main_buf_bytes(int R) { return (size_t)(1 << R) * TMA_PITCH * 4; }
+__host__ __device__ constexpr size_t u8_tile_bytes(int R) { return (size_t)(1 << R) * TMA_PITCH_U8; }
+constexpr size_t kTableBytes = 4096;
+__host__ __device__ constexpr size_t p1_smem_bytes(int R, bool u8) {
+  return main_buf_bytes(R) + (u8 ? u8_tile_bytes(R) : 0) + kTableBytes;
 }
-__host__ __device__ constexpr size_t tile_smem_bytes(int R, int ndest) {
-  return tile_buf_elems(R, ndest) * 4 + 2 * 64 * 4;
-}
+__host__ __device__ constexpr size_t p2_smem_bytes(int R) { return main_buf_bytes(R) + kTableBytes; }
 
 // ------------------------------------------------------------------------------------------
 // Register butterfly (north_star "out[t] = A[t>>1] + B[t>>1] shifted by ceil(t/2)"
@@ -105,70 +117,77 @@ __device__ __forceinline__ void warp_fht(A (&v)[1 << NB][V]) {
 }
 
 // ------------------------------------------------------------------------------------------
-// In-CTA FHT of a 2^R-row tile held in `buf` ([2^R][IN_PITCH], local columns, row rho = input
-// row). On return, staging plane d ([2^R][ST_PITCH] at buf + d*2^R*ST_PITCH) holds output row
-// tau (= shift tau) with window index s stored at s - soff[d*64 + tau], for 0 <= that < box;
-// the proxy fence for the TMA engine is done and the CTA is synchronised.
+// In-CTA FHT of a 2^R-row tile. Input element (row rho, x-order index e) is
+// src[rho*src_pitch + rowoff[rho] + e] (converted to A). Sub-pass A writes F_a in LOCAL order
+// to fa[row*fa_pitch + c] (may alias src: each warp reads all its rows before writing them);
+// sub-pass B leaves output row tau = jp*2^b + u, local column lane*VB + q in w[g][u][q]
+// (jp = warp + g*NW). Ends with __syncthreads (fa and src are free afterwards).
 // ------------------------------------------------------------------------------------------
-template <int R, typename A>
-__device__ __forceinline__ void tile_fht(A* buf, int sigma, int ndest, const int* soff, int box) {
+template <int R, int SIG, typename A, typename Tsrc>
+__device__ __forceinline__ void tile_fht(const Tsrc* src, int src_pitch, const int* rowoff, A* fa, int fa_pitch,
+                                         A (&w)[kTPW<R>][1 << Split<R>::b][VB]) {
   using S = Split<R>;
   constexpr int a = S::a, b = S::b, NW = S::nw;
-  constexpr int NA = 1 << a, NBk = 1 << b, NR = 1 << R;
-  constexpr int TPW = (NA + NW - 1) / NW;  // sub-pass B tasks per warp
+  constexpr int NA = 1 << a, NBk = 1 << b;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-  // sub-pass A: block blk = rows blk*2^a .. +2^a-1, in place (row blk*2^a + j' <- F_a[blk][j'])
+  // sub-pass A: block blk = rows blk*2^a .. +2^a-1 -> fa row blk*2^a + j' = F_a[blk][j']
 #pragma unroll 1
   for (int blk = warp; blk < NBk; blk += NW) {
     A v[NA][VA];
-    A* p = buf + (blk * NA) * IN_PITCH + lane * VA;
 #pragma unroll
-    for (int r = 0; r < NA; ++r)
+    for (int r = 0; r < NA; ++r) {
+      const int rho = blk * NA + r;
+      const Tsrc* p = src + rho * src_pitch + rowoff[rho] + (SIG > 0 ? lane * VA : (WA - 1) - lane * VA);
 #pragma unroll
-      for (int q = 0; q < VA; ++q) v[r][q] = p[r * IN_PITCH + q];
+      for (int q = 0; q < VA; ++q) v[r][q] = static_cast<A>(p[SIG > 0 ? q : -q]);
+    }
     warp_fht<a, VA>(v);
+    A* d = fa + (blk * NA) * fa_pitch + lane * VA;
 #pragma unroll
     for (int r = 0; r < NA; ++r)
 #pragma unroll
-      for (int q = 0; q < VA; ++q) p[r * IN_PITCH + q] = v[r][q];
+      for (int q = 0; q < VA; ++q) d[r * fa_pitch + q] = v[r][q];
   }
   __syncthreads();
 
   // sub-pass B: group jp: G[i'](c) = F_a[i'][jp](c + jp*i')  (pre-shear identity, local frame)
-  A w[TPW][NBk][VB];
 #pragma unroll
-  for (int g = 0; g < TPW; ++g) {
+  for (int g = 0; g < kTPW<R>; ++g) {
     const int jp = warp + g * NW;
     if (jp < NA) {
 #pragma unroll
       for (int i = 0; i < NBk; ++i) {
-        const A* src = buf + (i * NA + jp) * IN_PITCH + lane * VB + jp * i;
+        const A* s = fa + (i * NA + jp) * fa_pitch + lane * VB + jp * i;
 #pragma unroll
-        for (int q = 0; q < VB; ++q) w[g][i][q] = src[q];
+        for (int q = 0; q < VB; ++q) w[g][i][q] = s[q];
       }
       warp_fht<b, VB>(w[g]);
     }
   }
-  __syncthreads();  // every read of the A results is done: reuse buf as the staging planes
+  __syncthreads();
+}
 
-  // staging: output row tau = jp*2^b + u
+// Write the register results into a staging plane: output row tau, window index s stored at
+// s - soff[tau] when 0 <= that < box. Then fence for the TMA engine and synchronise.
+template <int R, int SIG, typename A>
+__device__ __forceinline__ void stage_rows(A (&w)[kTPW<R>][1 << Split<R>::b][VB], A* stg, const int* soff, int box) {
+  using S = Split<R>;
+  constexpr int NA = 1 << S::a, NBk = 1 << S::b, NW = S::nw;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #pragma unroll
-  for (int g = 0; g < TPW; ++g) {
+  for (int g = 0; g < kTPW<R>; ++g) {
     const int jp = warp + g * NW;
     if (jp < NA && lane < 31) {
 #pragma unroll
       for (int u = 0; u < NBk; ++u) {
         const int tau = jp * NBk + u;
-        for (int d = 0; d < ndest; ++d) {
-          A* dst = buf + (d * NR + tau) * ST_PITCH;
-          const int so = soff[d * 64 + tau];
+        const int base = (SIG > 0 ? lane * VB : (WC - 1) - lane * VB) - soff[tau];
+        A* dst = stg + tau * ST_PITCH;
 #pragma unroll
-          for (int q = 0; q < VB; ++q) {
-            const int c = lane * VB + q;
-            const int idx = (sigma > 0 ? c : (WC - 1) - c) - so;
-            if (idx >= 0 && idx < box) dst[idx] = w[g][u][q];
-          }
+        for (int q = 0; q < VB; ++q) {
+          const int idx = base + (SIG > 0 ? q : -q);
+          if ((unsigned)idx < (unsigned)box) dst[idx] = w[g][u][q];
         }
       }
     }
@@ -178,16 +197,41 @@ __device__ __forceinline__ void tile_fht(A* buf, int sigma, int ndest, const int
 }
 
 // ------------------------------------------------------------------------------------------
-// TMA helpers (cp.async.bulk.tensor: SASS UTMASTG)
+// TMA / mbarrier helpers (SASS: UTMALDG / UTMASTG, SYNCS)
 // ------------------------------------------------------------------------------------------
-__device__ __forceinline__ void tma_store_row(const CUtensorMap* map, const void* smem, int col, int row) {
-  const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];"
-               :: "l"(reinterpret_cast<uint64_t>(map)), "r"(s), "r"(col), "r"(row) : "memory");
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
-__device__ __forceinline__ void tma_commit_and_wait_read() {
-  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+__device__ __forceinline__ void tma_store_row(const CUtensorMap* map, const void* smem, int col, int row) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];"
+               :: "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(smem)), "r"(col), "r"(row) : "memory");
+}
+__device__ __forceinline__ void tma_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void tma_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, void* smem, uint64_t* bar, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
+               :: "r"(smem_u32(smem)), "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(const CUtensorMap* map, void* smem, uint64_t* bar, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];"
+               :: "r"(smem_u32(smem)), "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1),
+                  "r"(c2)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(smem_u32(bar)));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait0(uint64_t* bar) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(done) : "r"(smem_u32(bar)) : "memory");
+  }
 }
 
 __device__ __forceinline__ int mod_pos(int v, int W) {
@@ -200,6 +244,7 @@ __device__ __forceinline__ int mod_pos(int v, int W) {
 // ------------------------------------------------------------------------------------------
 struct P1Slot {
   int sigma;
+  int transposed;     // FHT row y = image column (P:52 mostly-horizontal quadrants)
   int xlo, xhi;       // F_m columns computed: [xlo, xhi), xhi - xlo a multiple of 4
   int ntiles;
   int64_t srow0;      // scratch row of (j = 0, i = 0) inside one image's scratch block
@@ -208,99 +253,163 @@ struct P1Slot {
 struct P1Params {
   const void* img;
   int64_t img_bstride, img_rstride;  // elements
-  int rows_avail, cols_avail;        // FRAME rows / cols backed by pixels
-  int transposed;                    // FHT row y = image column (P:52 mostly-horizontal)
+  int img_h, img_w;                  // image rows / cols (a transposed slot swaps their roles)
   int range;                         // §4 loader (sigma = +1, not transposed)
   const int* e_tab;
   const int* colmap;
   int w_content;
+  int fill_tma;                      // non-transposed rows by TMA (image base/pitch 16-B aligned)
+  int fill_vec;                      // transposed fill with 16-byte (u8: 4-byte) loads
   int nq, img0;
   int L;                             // log2(#strips)
   int TX;                            // tile width = TMA box (multiple of 4, <= TX1)
   int64_t scratch_img_rows;          // scratch rows per image
-  void* scratch;                     // same buffer as tm_scr (debug st.global path)
-  int64_t scr_pitch;
-  int no_tma;                        // debug: write rows with st.global instead of TMA
   P1Slot slot[4];
 };
 
 // scratch layout: row (img, slot, j, i) = img*scratch_img_rows + srow0 + j*2^L + i,
 // column x - xlo holds F_m[i][j](x)  (F_m = levels 1..m of strip i, shift j).
-template <typename Tin, int R>
-__global__ void __launch_bounds__(Split<R>::nw * 32)
-k_p1(const __grid_constant__ CUtensorMap tm_scr, const __grid_constant__ P1Params p) {
+template <typename Tin, int R, int SIG>
+__device__ __forceinline__ void p1_body(const CUtensorMap* tm_img0, const CUtensorMap* tm_img1,
+                                        const CUtensorMap* tm_scr, const P1Params& p, const P1Slot& sl, int img,
+                                        int strip, int X) {
   using A = typename AccOf<Tin>::type;
-  constexpr int NT = Split<R>::nw * 32;
+  using S = Split<R>;
+  constexpr int NT = S::nw * 32;
   constexpr int NR = 1 << R;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   A* buf = reinterpret_cast<A*>(smem_raw);
-  int* soff = reinterpret_cast<int*>(smem_raw + tile_buf_elems(R, 1) * 4);
+  unsigned char* tab = smem_raw + main_buf_bytes(R) + (sizeof(Tin) == 1 ? u8_tile_bytes(R) : 0);
+  int* rowoff = reinterpret_cast<int*>(tab);          // [NR]
+  int* soff = rowoff + 64;                            // [NR]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(tab + 1024);
+  const int TX = p.TX;
+  const Tin* src = static_cast<const Tin*>(p.img) + (int64_t)img * p.img_bstride;
+  const int y0 = strip * NR;
+  const int Xa = SIG > 0 ? X : X - (WA - WC);  // x of input index e = 0
+  A w[kTPW<R>][1 << S::b][VB];
 
+  if (!sl.transposed && p.fill_tma) {
+    // ---- TMA: NR image rows, columns [Xa, Xa + 288) from the 16-byte aligned column below
+    constexpr int AL = 16 / sizeof(Tin);
+    const int a0 = Xa & ~(AL - 1);
+    constexpr int TP = sizeof(Tin) == 1 ? TMA_PITCH_U8 : TMA_PITCH;
+    Tin* tile = reinterpret_cast<Tin*>(sizeof(Tin) == 1 ? smem_raw + main_buf_bytes(R) : smem_raw);
+    if (threadIdx.x < NR) {
+      rowoff[threadIdx.x] = Xa - a0;
+      soff[threadIdx.x] = 0;
+    }
+    if (threadIdx.x == 0) mbar_init(bar);
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      constexpr uint32_t row_bytes = sizeof(Tin) == 1 ? 256 + 48 : (256 + 36) * 4;
+      if (threadIdx.x == 0) mbar_expect_tx(bar, NR * row_bytes);
+      __syncwarp();
+      for (int rho = threadIdx.x; rho < NR; rho += 32) {
+        Tin* d = tile + rho * TP;
+        tma_load_3d(tm_img0, d, bar, a0, y0 + rho, img);
+        tma_load_3d(tm_img1, d + 256, bar, a0 + 256, y0 + rho, img);
+      }
+    }
+    mbar_wait0(bar);
+    if constexpr (sizeof(Tin) == 1) tile_fht<R, SIG, A>(tile, TP, rowoff, buf, FA_PITCH, w);
+    else tile_fht<R, SIG, A>(reinterpret_cast<const A*>(tile), TP, rowoff, buf, TMA_PITCH, w);
+  } else {
+    if (threadIdx.x < NR) {
+      rowoff[threadIdx.x] = 0;
+      soff[threadIdx.x] = 0;
+    }
+    if (!sl.transposed) {
+      // ---- scalar fill (angle-range gather T(x, y) = I[y][colmap[x - e_y]], or odd pitches)
+#pragma unroll 4
+      for (int idx = threadIdx.x; idx < NR * WA; idx += NT) {
+        const int rho = idx / WA, e = idx - rho * WA;
+        const int y = y0 + rho, x = Xa + e;
+        A v = A(0);
+        if (y < p.img_h) {
+          if (!p.range) {
+            if (x >= 0 && x < p.img_w) v = static_cast<A>(__ldg(src + (int64_t)y * p.img_rstride + x));
+          } else {  // P:146; R13, R14
+            const int u = x - __ldg(p.e_tab + y);
+            if (u >= 0 && u < p.w_content)
+              v = static_cast<A>(__ldg(src + (int64_t)y * p.img_rstride + __ldg(p.colmap + u)));
+          }
+        }
+        buf[rho * FA_PITCH + e] = v;
+      }
+    } else if (p.fill_vec && NR >= 4) {
+      // ---- transposed: FHT row y = image column, FHT column x = image row. Thread = (x, 4 y's):
+      // one 16-byte (u8: 4-byte) load from image row x, 4 conflict-free column stores.
+      constexpr int YQ = NR >= 4 ? NR / 4 : 1;  // threads per image row
+#pragma unroll 2
+      for (int idx = threadIdx.x; idx < WA * YQ; idx += NT) {
+        const int e = idx / YQ, yq = idx - e * YQ;
+        const int x = Xa + e, y = y0 + 4 * yq;
+        A v0 = A(0), v1 = A(0), v2 = A(0), v3 = A(0);
+        if (x >= 0 && x < p.img_h) {
+          const Tin* ps = src + (int64_t)x * p.img_rstride + y;
+          if (y + 3 < p.img_w) {
+            if constexpr (sizeof(Tin) == 1) {
+              const uchar4 u = __ldg(reinterpret_cast<const uchar4*>(ps));
+              v0 = u.x; v1 = u.y; v2 = u.z; v3 = u.w;
+            } else if constexpr (sizeof(A) == 4 && std::is_same<Tin, float>::value) {
+              const float4 u = __ldg(reinterpret_cast<const float4*>(ps));
+              v0 = u.x; v1 = u.y; v2 = u.z; v3 = u.w;
+            } else {
+              const int4 u = __ldg(reinterpret_cast<const int4*>(ps));
+              v0 = u.x; v1 = u.y; v2 = u.z; v3 = u.w;
+            }
+          } else {
+            if (y < p.img_w) v0 = static_cast<A>(__ldg(ps));
+            if (y + 1 < p.img_w) v1 = static_cast<A>(__ldg(ps + 1));
+            if (y + 2 < p.img_w) v2 = static_cast<A>(__ldg(ps + 2));
+          }
+        }
+        A* d = buf + (4 * yq) * FA_PITCH + e;
+        d[0] = v0;
+        d[FA_PITCH] = v1;
+        d[2 * FA_PITCH] = v2;
+        d[3 * FA_PITCH] = v3;
+      }
+    } else {
+      for (int idx = threadIdx.x; idx < NR * WA; idx += NT) {
+        const int e = idx / NR, rho = idx - e * NR;  // consecutive threads: consecutive image columns
+        const int y = y0 + rho, x = Xa + e;
+        A v = A(0);
+        if (y < p.img_w && x >= 0 && x < p.img_h) v = static_cast<A>(__ldg(src + (int64_t)x * p.img_rstride + y));
+        buf[rho * FA_PITCH + e] = v;
+      }
+    }
+    __syncthreads();
+    tile_fht<R, SIG, A>(static_cast<const A*>(buf), FA_PITCH, rowoff, buf, FA_PITCH, w);
+  }
+  stage_rows<R, SIG, A>(w, buf, soff, TX);
+
+  // ---- store F_m[strip][j] (j = tau): scratch column X - xlo is 16-byte aligned
+  if (threadIdx.x < NR) {
+    const int j = threadIdx.x;
+    const int64_t row = (int64_t)(img - p.img0) * p.scratch_img_rows + sl.srow0 + ((int64_t)j << p.L) + strip;
+    tma_store_row(tm_scr, buf + j * ST_PITCH, X - sl.xlo, (int)row);
+    tma_commit();
+    tma_wait_read();
+  }
+}
+
+// tm_img0: image [batch][h][w], box 1 x 1 x 256 columns; tm_img1: box 36 (u8: 48) columns;
+// tm_scr: scratch rows, box TX.
+template <typename Tin, int R>
+__global__ void __launch_bounds__(Split<R>::nw * 32)
+k_p1(const __grid_constant__ CUtensorMap tm_img0, const __grid_constant__ CUtensorMap tm_img1,
+     const __grid_constant__ CUtensorMap tm_scr, const __grid_constant__ P1Params p) {
   const int z = blockIdx.z;
   const int qi = z % p.nq;
   const int img = p.img0 + z / p.nq;
   const P1Slot& sl = p.slot[qi];
   const int n = blockIdx.x;
   if (n >= sl.ntiles) return;
-  const int strip = blockIdx.y;
-  const int TX = p.TX;
-  const int X = min(sl.xlo + TX * n, sl.xhi - TX);  // tile = window start (Xw = X)
-  const int sigma = sl.sigma;
-  const Tin* src = static_cast<const Tin*>(p.img) + (int64_t)img * p.img_bstride;
-  const int y0 = strip * NR;
-  if (threadIdx.x < NR) soff[threadIdx.x] = 0;
-
-  // ---- fill: buf[rho][c] = frame pixel (y0 + rho, x(c)), zero outside the image (a1: padding is
-  // never written to HBM; quadrant handling by index transposition)
-  if (!p.transposed) {
-#pragma unroll 4
-    for (int idx = threadIdx.x; idx < NR * WA; idx += NT) {
-      const int rho = idx / WA, c = idx - rho * WA;
-      const int y = y0 + rho;
-      const int x = sigma > 0 ? X + c : X + (WC - 1) - c;
-      A v = A(0);
-      if (y < p.rows_avail) {
-        if (!p.range) {
-          if (x >= 0 && x < p.cols_avail) v = static_cast<A>(__ldg(src + (int64_t)y * p.img_rstride + x));
-        } else {  // T(x, y) = I[y][colmap[x - e_y]]  (R13, R14)
-          const int u = x - __ldg(p.e_tab + y);
-          if (u >= 0 && u < p.w_content)
-            v = static_cast<A>(__ldg(src + (int64_t)y * p.img_rstride + __ldg(p.colmap + u)));
-        }
-      }
-      buf[rho * IN_PITCH + c] = v;
-    }
-  } else {
-#pragma unroll 4
-    for (int idx = threadIdx.x; idx < NR * WA; idx += NT) {
-      const int c = idx / NR, rho = idx - c * NR;  // consecutive threads: consecutive image columns
-      const int y = y0 + rho;
-      const int x = sigma > 0 ? X + c : X + (WC - 1) - c;
-      A v = A(0);
-      if (y < p.rows_avail && x >= 0 && x < p.cols_avail)
-        v = static_cast<A>(__ldg(src + (int64_t)x * p.img_rstride + y));
-      buf[rho * IN_PITCH + c] = v;
-    }
-  }
-  __syncthreads();
-  tile_fht<R, A>(buf, sigma, 1, soff, TX);
-
-  // ---- store F_m[strip][j] (j = tau): scratch column X - xlo is 16-byte aligned
-  const int64_t rowbase = (int64_t)(img - p.img0) * p.scratch_img_rows + sl.srow0 + strip;
-  const int col = X - sl.xlo;
-  if (!p.no_tma) {
-    if (threadIdx.x < NR) {
-      const int j = threadIdx.x;
-      tma_store_row(&tm_scr, buf + j * ST_PITCH, col, (int)(rowbase + ((int64_t)j << p.L)));
-      tma_commit_and_wait_read();
-    }
-  } else {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int j = warp; j < NR; j += NT / 32) {
-      A* drow = static_cast<A*>(p.scratch) + (rowbase + ((int64_t)j << p.L)) * p.scr_pitch + col;
-      for (int c = lane; c < TX; c += 32) __stcg(drow + c, buf[j * ST_PITCH + c]);
-    }
-  }
+  const int X = min(sl.xlo + p.TX * n, sl.xhi - p.TX);  // tile = window start (Xw = X)
+  if (sl.sigma > 0) p1_body<Tin, R, 1>(&tm_img0, &tm_img1, &tm_scr, p, sl, img, blockIdx.y, X);
+  else p1_body<Tin, R, -1>(&tm_img0, &tm_img1, &tm_scr, p, sl, img, blockIdx.y, X);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -324,126 +433,155 @@ struct P2Dest {
 };
 
 struct P2Params {
-  const void* scratch;
-  int64_t scr_pitch;
   int64_t scratch_img_rows;
   int nq, img0;
-  int TX;                  // tile stride (columns owned per tile); TMA box = TX + 4
+  int TX;                  // tile stride (columns owned per tile); store box = TX + 4
   int W, Hp, wc;
   int range;
   const int* start_tab;    // range: per-row support start (signed, unwrapped)
   const int* len_tab;      // range: per-row support length
   int ndest;               // 1 or 2 destinations
-  int no_tma;              // debug: write rows with st.global instead of TMA
+  int no_tma;              // debug: write every row with st.global
   P2Slot slot[4];
   P2Dest dest[2];
 };
 
-template <typename A, int R>
-__global__ void __launch_bounds__(Split<R>::nw * 32)
-k_p2(const __grid_constant__ CUtensorMap tm0, const __grid_constant__ CUtensorMap tm1,
-     const __grid_constant__ P2Params p) {
-  constexpr int NW = Split<R>::nw;
-  constexpr int NT = NW * 32;
+struct RowInfo {  // per output row of the current destination (shared memory)
+  int64_t orow;
+  int d0;         // destination column of staging index 0 (16-byte aligned)
+  int xs0;        // x of staging index 0
+  int mlo, mhi;   // columns left to plain stores
+  int tma;        // 1 = TMA row store
+};
+
+template <typename A, int R, int SIG>
+__device__ __forceinline__ void p2_body(const CUtensorMap* tm_scr0, const CUtensorMap* tm_scr1,
+                                        const CUtensorMap* tm0, const CUtensorMap* tm1, const P2Params& p,
+                                        const P2Slot& sl, int img, int j, int X) {
+  using S = Split<R>;
+  constexpr int NW = S::nw;
   constexpr int NR = 1 << R;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   A* buf = reinterpret_cast<A*>(smem_raw);
-  int* soff = reinterpret_cast<int*>(smem_raw + tile_buf_elems(R, p.ndest) * 4);
+  unsigned char* tab = smem_raw + main_buf_bytes(R);
+  int* rowoff = reinterpret_cast<int*>(tab);               // [NR]
+  int* soff = rowoff + 64;                                 // [NR]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(tab + 512);
+  RowInfo* info = reinterpret_cast<RowInfo*>(tab + 1024);  // [NR], 32 B each
+  const int TX = p.TX, box = TX + WO2;
+  const int Xw = X - WO2;                        // window start: window index s <-> x = Xw + s
+  const int Xa = SIG > 0 ? Xw : Xw - (WA - WC);  // x of input index e = 0
+  const int t0 = j * NR, tmax = t0 + NR - 1;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  A w[kTPW<R>][1 << S::b][VB];
 
+  bool black = false;  // P:81: the whole window is outside every row's pattern support
+  if (!p.range) black = SIG > 0 ? (Xw + WC - 1 < -tmax) : (Xw >= p.wc + tmax);
+
+  if (!black) {
+    // scratch row t0 + i, column (x + sigma*j*i) - xlo1 for x = Xa + e; TMA from the aligned-down
+    // column, zero outside [0, xhi1 - xlo1) = outside what pass 1 wrote
+    if (threadIdx.x < NR) rowoff[threadIdx.x] = (Xa + SIG * j * (int)threadIdx.x - sl.xlo1) & 3;
+    if (threadIdx.x == 0) mbar_init(bar);
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      if (threadIdx.x == 0) mbar_expect_tx(bar, NR * (256 + 36) * 4);
+      __syncwarp();
+      const int64_t rbase = (int64_t)(img - p.img0) * p.scratch_img_rows + sl.srow0 + t0;
+      for (int i = threadIdx.x; i < NR; i += 32) {
+        const int c0 = Xa + SIG * j * i - sl.xlo1;
+        const int a0 = c0 & ~3;
+        A* d = buf + i * TMA_PITCH;
+        tma_load_2d(tm_scr0, d, bar, a0, (int)(rbase + i));
+        tma_load_2d(tm_scr1, d + 256, bar, a0 + 256, (int)(rbase + i));
+      }
+    }
+    mbar_wait0(bar);
+    tile_fht<R, SIG, A>(static_cast<const A*>(buf), TMA_PITCH, rowoff, buf, TMA_PITCH, w);
+  } else {
+#pragma unroll
+    for (int g = 0; g < kTPW<R>; ++g)
+#pragma unroll
+      for (int u = 0; u < (1 << S::b); ++u)
+#pragma unroll
+        for (int q = 0; q < VB; ++q) w[g][u][q] = A(0);
+  }
+
+  // ---- stores, one destination at a time (the staging plane is reused)
+  bool issued = false;
+  for (int d = 0; d < p.ndest; ++d) {
+    const P2Dest& D = p.dest[d];
+    if (d > 0) {
+      if (issued) tma_wait_read();
+      __syncthreads();
+    }
+    if (threadIdx.x < NR) {
+      const int tau = threadIdx.x, t = t0 + tau;
+      int vlo = sl.xbeg, vhi = sl.xend, k = 0;
+      if (p.range) {
+        vlo = __ldg(p.start_tab + t);
+        vhi = vlo + p.W;
+        if (D.shifted) k = (((p.W - __ldg(p.len_tab + t)) + 1) >> 1) - vlo;
+      } else if (D.shifted) {
+        k = SIG > 0 ? ceil_half(p.Hp + t) : ceil_half(p.Hp - t);
+      }
+      const int r = mod_pos(X + k, p.W) & 3;
+      const int xs0 = X - r;
+      const int d0 = mod_pos(xs0 + k, p.W);
+      soff[tau] = WO2 - r;
+      RowInfo ri;
+      ri.orow = (int64_t)img * D.rows_per_img + sl.qrow + sl.rbase + (int64_t)sl.rsign * t;
+      ri.d0 = d0;
+      ri.xs0 = xs0;
+      ri.mlo = max(X, vlo);
+      ri.mhi = min(X + TX, vhi);
+      ri.tma = 0;
+      if (t == sl.skip) {
+        ri.mhi = ri.mlo;
+      } else if (!p.no_tma && xs0 >= vlo && xs0 + min(box, p.W - d0) <= vhi) {
+        ri.tma = 1;
+        ri.mlo = max(ri.mlo, xs0 + (p.W - d0));  // the wrapped remainder, if any
+      }
+      info[tau] = ri;
+    }
+    __syncthreads();
+    stage_rows<R, SIG, A>(w, buf, soff, box);
+    if (threadIdx.x < NR && info[threadIdx.x].tma) {
+      const RowInfo& ri = info[threadIdx.x];
+      tma_store_row(d == 0 ? tm0 : tm1, buf + threadIdx.x * ST_PITCH, ri.d0, (int)ri.orow);  // clipped at W
+      tma_commit();
+      issued = true;
+    }
+    for (int tau = warp; tau < NR; tau += NW) {
+      const RowInfo ri = info[tau];
+      if (ri.mlo >= ri.mhi) continue;
+      A* drow = static_cast<A*>(D.ptr) + ri.orow * D.pitch;
+      const A* srow = buf + tau * ST_PITCH;
+      for (int x = ri.mlo + lane; x < ri.mhi; x += 32) {
+        int col = ri.d0 + (x - ri.xs0);
+        if (col >= p.W) col -= p.W;
+        __stcs(drow + col, srow[x - ri.xs0]);
+      }
+    }
+  }
+  if (issued) tma_wait_read();
+}
+
+// tm_scr0: scratch, one row x 256 columns; tm_scr1: one row x 36 columns; tm0 / tm1: destinations
+template <typename A, int R>
+__global__ void __launch_bounds__(Split<R>::nw * 32)
+k_p2(const __grid_constant__ CUtensorMap tm_scr0, const __grid_constant__ CUtensorMap tm_scr1,
+     const __grid_constant__ CUtensorMap tm0, const __grid_constant__ CUtensorMap tm1,
+     const __grid_constant__ P2Params p) {
   const int z = blockIdx.z;
   const int qi = z % p.nq;
   const int img = p.img0 + z / p.nq;
   const P2Slot& sl = p.slot[qi];
   const int n = blockIdx.x;
   if (n >= sl.ntiles) return;
-  const int j = blockIdx.y;
-  const int TX = p.TX, box = TX + WO2;
-  const int X = min(sl.xbeg + TX * n, sl.xend - TX);
-  const int Xw = X - WO2;  // window start: window index s <-> x = Xw + s
-  const int sigma = sl.sigma;
-  const int t0 = j * NR, tmax = t0 + NR - 1;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-
-  // per (dest, row): destination shift k, aligned start r and the staging offset (window index
-  // s is staged at s - soff; staging index 0 <-> x = X - r)
-  if (threadIdx.x < 2 * NR) {
-    const int d = threadIdx.x / NR, tau = threadIdx.x - d * NR;
-    int so = 0;
-    if (d < p.ndest) {
-      const int t = t0 + tau;
-      int k = 0;
-      if (p.dest[d].shifted) {
-        if (p.range) k = (((p.W - __ldg(p.len_tab + t)) + 1) >> 1) - __ldg(p.start_tab + t);
-        else k = sigma > 0 ? ceil_half(p.Hp + t) : ceil_half(p.Hp - t);
-      }
-      const int r = mod_pos(X + k, p.W) & 3;
-      so = WO2 - r;
-    }
-    soff[d * 64 + tau] = so;
-  }
-
-  bool black = false;  // P:81: the whole window is outside every row's pattern support
-  if (!p.range) black = sigma > 0 ? (Xw + WC - 1 < -tmax) : (Xw >= p.wc + tmax);
-
-  if (!black) {
-    const A* scr = static_cast<const A*>(p.scratch) +
-                   ((int64_t)(img - p.img0) * p.scratch_img_rows + sl.srow0 + t0) * p.scr_pitch;
-#pragma unroll 4
-    for (int idx = threadIdx.x; idx < NR * WA; idx += NT) {
-      const int i = idx / WA, c = idx - i * WA;
-      const int x = sigma > 0 ? Xw + c : Xw + (WC - 1) - c;
-      const int xs = x + sigma * j * i;  // G_j[i](x) = F_m[i][j](x + sigma*j*i)
-      A v = A(0);
-      if (xs >= sl.xlo1 && xs < sl.xhi1) v = __ldcg(scr + (int64_t)i * p.scr_pitch + (xs - sl.xlo1));
-      buf[i * IN_PITCH + c] = v;
-    }
-    __syncthreads();
-    tile_fht<R, A>(buf, sigma, p.ndest, soff, box);
-  } else {
-    for (int idx = threadIdx.x; idx < p.ndest * NR * ST_PITCH; idx += NT) buf[idx] = A(0);
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    __syncthreads();
-  }
-
-  // ---- stores: item = (dest d, row tau); one warp per item
-  bool issued = false;
-  for (int item = warp; item < p.ndest * NR; item += NW) {
-    const int d = item / NR, tau = item - d * NR;
-    const P2Dest& D = p.dest[d];
-    const int t = t0 + tau;
-    if (t == sl.skip) continue;
-    const int64_t orow = (int64_t)img * D.rows_per_img + sl.qrow + sl.rbase + (int64_t)sl.rsign * t;
-    // valid columns of this row: [vlo, vhi); the tile owns [X, X + TX)
-    int vlo = sl.xbeg, vhi = sl.xend, k = 0;
-    if (p.range) {
-      vlo = __ldg(p.start_tab + t);
-      vhi = vlo + p.W;
-      if (D.shifted) k = (((p.W - __ldg(p.len_tab + t)) + 1) >> 1) - vlo;
-    } else if (D.shifted) {
-      k = sigma > 0 ? ceil_half(p.Hp + t) : ceil_half(p.Hp - t);
-    }
-    const int r = WO2 - soff[d * 64 + tau];
-    const int xs0 = X - r;                     // x of staging index 0
-    const int d0 = mod_pos(xs0 + k, p.W);      // its destination column (16-byte aligned)
-    const A* srow = buf + (d * NR + tau) * ST_PITCH;
-    int mlo = max(X, vlo), mhi = min(X + TX, vhi);  // columns still to write by hand
-    if (!p.no_tma && xs0 >= vlo && xs0 + min(box, p.W - d0) <= vhi) {
-      if (lane == 0) {
-        tma_store_row(d == 0 ? &tm0 : &tm1, srow, d0, (int)orow);  // clipped at column W
-        issued = true;
-      }
-      mlo = max(mlo, xs0 + (p.W - d0));       // the wrapped remainder, if any
-    }
-    if (mlo < mhi) {
-      A* drow = static_cast<A*>(D.ptr) + orow * D.pitch;
-      for (int x = mlo + lane; x < mhi; x += 32) {
-        int col = d0 + (x - xs0);
-        if (col >= p.W) col -= p.W;
-        __stcs(drow + col, srow[x - xs0]);
-      }
-    }
-  }
-  if (issued) tma_commit_and_wait_read();
+  const int X = min(sl.xbeg + p.TX * n, sl.xend - p.TX);
+  if (sl.sigma > 0) p2_body<A, R, 1>(&tm_scr0, &tm_scr1, &tm0, &tm1, p, sl, img, blockIdx.y, X);
+  else p2_body<A, R, -1>(&tm_scr0, &tm_scr1, &tm0, &tm1, p, sl, img, blockIdx.y, X);
 }
 
 }  // namespace v2

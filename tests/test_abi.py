@@ -87,25 +87,25 @@ def test_argument_errors_are_synchronous():
     d.data = 1 << 20
     ws_n = L.lib.fht_workspace_bytes(1, ctypes.byref(img), None)
     assert ws_n > 0
-    assert L.lib.fht_full(None, 0, ctypes.byref(d), None, 1 << 24, ws_n, None) == -1         # NULL image
+    assert L.lib.fht_full(None, 0, ctypes.byref(d), None, 1 << 24, ws_n, None, None) == -1         # NULL image
     bad = _img(L, 16, 16, dt=7)
-    assert L.lib.fht_full(ctypes.byref(bad), 0, ctypes.byref(d), None, 1 << 24, ws_n, None) == -2
+    assert L.lib.fht_full(ctypes.byref(bad), 0, ctypes.byref(d), None, 1 << 24, ws_n, None, None) == -2
     zero = _img(L, 0, 16)
-    assert L.lib.fht_full(ctypes.byref(zero), 0, ctypes.byref(d), None, 1 << 24, ws_n, None) == -1
+    assert L.lib.fht_full(ctypes.byref(zero), 0, ctypes.byref(d), None, 1 << 24, ws_n, None, None) == -1
     d2 = L.FhtHough.from_buffer_copy(d)
     d2.rows += 1
-    assert L.lib.fht_full(ctypes.byref(img), 0, ctypes.byref(d2), None, 1 << 24, ws_n, None) == -3
-    assert L.lib.fht_full(ctypes.byref(img), 1, ctypes.byref(d), None, 1 << 24, ws_n, None) == -3   # layout mismatch
-    assert L.lib.fht_full(ctypes.byref(img), 0, ctypes.byref(d), None, None, ws_n, None) == -6
-    assert L.lib.fht_full(ctypes.byref(img), 0, ctypes.byref(d), None, 1 << 24, 16, None) == -6
+    assert L.lib.fht_full(ctypes.byref(img), 0, ctypes.byref(d2), None, 1 << 24, ws_n, None, None) == -3
+    assert L.lib.fht_full(ctypes.byref(img), 1, ctypes.byref(d), None, 1 << 24, ws_n, None, None) == -3   # layout mismatch
+    assert L.lib.fht_full(ctypes.byref(img), 0, ctypes.byref(d), None, None, ws_n, None, None) == -6
+    assert L.lib.fht_full(ctypes.byref(img), 0, ctypes.byref(d), None, 1 << 24, 16, None, None) == -6
     alias = _img(L, 16, 16, data=d.data)
-    assert L.lib.fht_full(ctypes.byref(alias), 0, ctypes.byref(d), None, 1 << 24, ws_n, None) == -1
+    assert L.lib.fht_full(ctypes.byref(alias), 0, ctypes.byref(d), None, 1 << 24, ws_n, None, None) == -1
     odd = _img(L, 16, 16, data=4098)
-    assert L.lib.fht_full(ctypes.byref(odd), 0, ctypes.byref(d), None, 1 << 24, ws_n, None) == -4
+    assert L.lib.fht_full(ctypes.byref(odd), 0, ctypes.byref(d), None, 1 << 24, ws_n, None, None) == -4
     dq = L.FhtHough()
     assert L.lib.fht_hough_describe(0, 0, 0, ctypes.byref(img), None, ctypes.byref(dq)) == 0
     dq.data = 1 << 20
-    assert L.lib.fht_quadrant(ctypes.byref(img), 0, 5, ctypes.byref(dq), None, 1 << 24, ws_n, None) == -5
+    assert L.lib.fht_quadrant(ctypes.byref(img), 0, 5, ctypes.byref(dq), None, 1 << 24, ws_n, None, None) == -5
     ds = L.FhtHough.from_buffer_copy(d)
     ds.shifted = 1
     d3 = L.FhtHough.from_buffer_copy(d)
@@ -116,19 +116,19 @@ def test_argument_errors_are_synchronous():
     db = L.FhtHough()
     assert L.lib.fht_hough_describe(1, 0, 0, ctypes.byref(big), None, ctypes.byref(db)) == 0
     db.data = 1 << 40
-    assert L.lib.fht_full(ctypes.byref(big), 0, ctypes.byref(db), None, 1 << 44, 1 << 40, None) == -5
+    assert L.lib.fht_full(ctypes.byref(big), 0, ctypes.byref(db), None, 1 << 44, 1 << 40, None, None) == -5
     # the (out, out_shifted) pair: at least one, no overlap, 16-byte aligned for the TMA row stores
-    assert L.lib.fht_full(ctypes.byref(img), 0, None, None, 1 << 24, ws_n, None) == -1
-    assert L.lib.fht_full(ctypes.byref(img), 0, ctypes.byref(d), ctypes.byref(d), 1 << 24, ws_n, None) == -1
+    assert L.lib.fht_full(ctypes.byref(img), 0, None, None, 1 << 24, ws_n, None, None) == -1
+    assert L.lib.fht_full(ctypes.byref(img), 0, ctypes.byref(d), ctypes.byref(d), 1 << 24, ws_n, None, None) == -1
     mis = L.FhtHough.from_buffer_copy(d)
     mis.data = (1 << 28) + 4
-    assert L.lib.fht_full(ctypes.byref(img), 0, None, ctypes.byref(mis), 1 << 24, ws_n, None) == -4
+    assert L.lib.fht_full(ctypes.byref(img), 0, None, ctypes.byref(mis), 1 << 24, ws_n, None, None) == -4
     odd_pitch = L.FhtHough.from_buffer_copy(d)
     odd_pitch.data = 1 << 28
     odd_pitch.row_stride += 1
     odd_pitch.quad_stride = odd_pitch.rows * odd_pitch.row_stride
     odd_pitch.batch_stride = 4 * odd_pitch.quad_stride
-    assert L.lib.fht_full(ctypes.byref(img), 0, ctypes.byref(odd_pitch), None, 1 << 24, ws_n, None) == -4
+    assert L.lib.fht_full(ctypes.byref(img), 0, ctypes.byref(odd_pitch), None, 1 << 24, ws_n, None, None) == -4
 
 
 def test_status_strings():
