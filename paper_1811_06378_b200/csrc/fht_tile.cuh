@@ -60,6 +60,7 @@ template <> struct Split<3> { static constexpr int a = 3, b = 0, nw = 4; };
 template <> struct Split<4> { static constexpr int a = 2, b = 2, nw = 4; };
 template <> struct Split<5> { static constexpr int a = 3, b = 2, nw = 4; };
 template <> struct Split<6> { static constexpr int a = 3, b = 3, nw = 8; };
+template <int R> constexpr int kMinBlocks = Split<R>::nw == 4 ? 5 : 2;  // occupancy target (regs <= 102 / 128)
 template <int R> constexpr int kTPW = ((1 << Split<R>::a) + Split<R>::nw - 1) / Split<R>::nw;  // B tasks/warp
 
 // Shared memory layout (bytes): [main buffer][u8 input tile (pass 1 u8 TMA only)][tables]
@@ -339,37 +340,44 @@ __device__ __forceinline__ void p1_body(const CUtensorMap* tm_img0, const CUtens
       }
     } else if (p.fill_vec && NR >= 4) {
       // ---- transposed: FHT row y = image column, FHT column x = image row. Thread = (x, 4 y's):
-      // one 16-byte (u8: 4-byte) load from image row x, 4 conflict-free column stores.
+      // one 16-byte (u8: 4-byte) load from image row x, 4 conflict-free column stores. All of a
+      // thread's loads are issued before its first store (memory-level parallelism).
       constexpr int YQ = NR >= 4 ? NR / 4 : 1;  // threads per image row
-#pragma unroll 2
-      for (int idx = threadIdx.x; idx < WA * YQ; idx += NT) {
+      constexpr int IT = (WA * YQ + NT - 1) / NT;
+      using V4 = typename std::conditional<sizeof(Tin) == 1, uchar4,
+                 typename std::conditional<std::is_same<Tin, float>::value, float4, int4>::type>::type;
+      V4 vals[IT];
+#pragma unroll
+      for (int it = 0; it < IT; ++it) {
+        const int idx = threadIdx.x + it * NT;
         const int e = idx / YQ, yq = idx - e * YQ;
         const int x = Xa + e, y = y0 + 4 * yq;
-        A v0 = A(0), v1 = A(0), v2 = A(0), v3 = A(0);
-        if (x >= 0 && x < p.img_h) {
+        vals[it] = V4{};
+        if (idx < WA * YQ && x >= 0 && x < p.img_h) {
           const Tin* ps = src + (int64_t)x * p.img_rstride + y;
           if (y + 3 < p.img_w) {
-            if constexpr (sizeof(Tin) == 1) {
-              const uchar4 u = __ldg(reinterpret_cast<const uchar4*>(ps));
-              v0 = u.x; v1 = u.y; v2 = u.z; v3 = u.w;
-            } else if constexpr (sizeof(A) == 4 && std::is_same<Tin, float>::value) {
-              const float4 u = __ldg(reinterpret_cast<const float4*>(ps));
-              v0 = u.x; v1 = u.y; v2 = u.z; v3 = u.w;
-            } else {
-              const int4 u = __ldg(reinterpret_cast<const int4*>(ps));
-              v0 = u.x; v1 = u.y; v2 = u.z; v3 = u.w;
-            }
+            vals[it] = __ldg(reinterpret_cast<const V4*>(ps));
           } else {
-            if (y < p.img_w) v0 = static_cast<A>(__ldg(ps));
-            if (y + 1 < p.img_w) v1 = static_cast<A>(__ldg(ps + 1));
-            if (y + 2 < p.img_w) v2 = static_cast<A>(__ldg(ps + 2));
+            Tin t[4] = {Tin(0), Tin(0), Tin(0), Tin(0)};
+            for (int k = 0; k < 3; ++k)
+              if (y + k < p.img_w) t[k] = __ldg(ps + k);
+            vals[it].x = t[0];
+            vals[it].y = t[1];
+            vals[it].z = t[2];
           }
         }
-        A* d = buf + (4 * yq) * FA_PITCH + e;
-        d[0] = v0;
-        d[FA_PITCH] = v1;
-        d[2 * FA_PITCH] = v2;
-        d[3 * FA_PITCH] = v3;
+      }
+#pragma unroll
+      for (int it = 0; it < IT; ++it) {
+        const int idx = threadIdx.x + it * NT;
+        if (idx < WA * YQ) {
+          const int e = idx / YQ, yq = idx - e * YQ;
+          A* d = buf + (4 * yq) * FA_PITCH + e;
+          d[0] = static_cast<A>(vals[it].x);
+          d[FA_PITCH] = static_cast<A>(vals[it].y);
+          d[2 * FA_PITCH] = static_cast<A>(vals[it].z);
+          d[3 * FA_PITCH] = static_cast<A>(vals[it].w);
+        }
       }
     } else {
       for (int idx = threadIdx.x; idx < NR * WA; idx += NT) {
@@ -398,7 +406,7 @@ __device__ __forceinline__ void p1_body(const CUtensorMap* tm_img0, const CUtens
 // tm_img0: image [batch][h][w], box 1 x 1 x 256 columns; tm_img1: box 36 (u8: 48) columns;
 // tm_scr: scratch rows, box TX.
 template <typename Tin, int R>
-__global__ void __launch_bounds__(Split<R>::nw * 32)
+__global__ void __launch_bounds__(Split<R>::nw * 32, kMinBlocks<R>)
 k_p1(const __grid_constant__ CUtensorMap tm_img0, const __grid_constant__ CUtensorMap tm_img1,
      const __grid_constant__ CUtensorMap tm_scr, const __grid_constant__ P1Params p) {
   const int z = blockIdx.z;
@@ -498,13 +506,6 @@ __device__ __forceinline__ void p2_body(const CUtensorMap* tm_scr0, const CUtens
     }
     mbar_wait0(bar);
     tile_fht<R, SIG, A>(static_cast<const A*>(buf), TMA_PITCH, rowoff, buf, TMA_PITCH, w);
-  } else {
-#pragma unroll
-    for (int g = 0; g < kTPW<R>; ++g)
-#pragma unroll
-      for (int u = 0; u < (1 << S::b); ++u)
-#pragma unroll
-        for (int q = 0; q < VB; ++q) w[g][u][q] = A(0);
   }
 
   // ---- stores, one destination at a time (the staging plane is reused)
@@ -545,7 +546,13 @@ __device__ __forceinline__ void p2_body(const CUtensorMap* tm_scr0, const CUtens
       info[tau] = ri;
     }
     __syncthreads();
-    stage_rows<R, SIG, A>(w, buf, soff, box);
+    if (!black) {
+      stage_rows<R, SIG, A>(w, buf, soff, box);
+    } else {  // every output of a black tile is 0 (no pattern touches a pixel)
+      for (int idx = threadIdx.x; idx < NR * ST_PITCH; idx += S::nw * 32) buf[idx] = A(0);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncthreads();
+    }
     if (threadIdx.x < NR && info[threadIdx.x].tma) {
       const RowInfo& ri = info[threadIdx.x];
       tma_store_row(d == 0 ? tm0 : tm1, buf + threadIdx.x * ST_PITCH, ri.d0, (int)ri.orow);  // clipped at W
@@ -569,7 +576,7 @@ __device__ __forceinline__ void p2_body(const CUtensorMap* tm_scr0, const CUtens
 
 // tm_scr0: scratch, one row x 256 columns; tm_scr1: one row x 36 columns; tm0 / tm1: destinations
 template <typename A, int R>
-__global__ void __launch_bounds__(Split<R>::nw * 32)
+__global__ void __launch_bounds__(Split<R>::nw * 32, kMinBlocks<R>)
 k_p2(const __grid_constant__ CUtensorMap tm_scr0, const __grid_constant__ CUtensorMap tm_scr1,
      const __grid_constant__ CUtensorMap tm0, const __grid_constant__ CUtensorMap tm1,
      const __grid_constant__ P2Params p) {
