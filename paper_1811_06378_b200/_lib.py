@@ -10,7 +10,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfht.so")
+# FHT_LIB overrides the library path (A/B timing of alternative builds, tools/abbench.py)
+LIB_PATH = os.environ.get("FHT_LIB") or os.path.join(_HERE, "libfht.so")
 
 FHT_U8, FHT_I32, FHT_F32 = 0, 1, 2
 FHT_QA, FHT_QB, FHT_QC, FHT_QD = 0, 1, 2, 3

@@ -473,7 +473,8 @@ int run_orientation(const fht_image* img, const Frame& f, const Slot* slots, int
       const int nb = (int)((img->batch - b0) < sp.chunk ? (img->batch - b0) : sp.chunk);
       p1.img0 = (int)b0;
       p2.img0 = (int)b0;
-      dim3 g1(ntile1, nstrips, nb * nq);
+      p1.ntiles = ntile1;
+      dim3 g1((unsigned)(ntile1 * nstrips * nb * nq));
       cudaError_t e;
       log.before(st);
       switch (img->dtype) {
@@ -484,7 +485,9 @@ int run_orientation(const fht_image* img, const Frame& f, const Slot* slots, int
       if (e != cudaSuccess) return FHT_ERR_CUDA;
       log.after(st);
       ++launches;
-      dim3 g2(ntile2, ngroups, nb * nq);
+      p2.ntiles = ntile2;
+      p2.m = f.m;
+      dim3 g2((unsigned)(ntile2 * ngroups * nb * nq));
       e = f32 ? launch_p2<float>(f.L, g2, m2, p2, st) : launch_p2<int>(f.L, g2, m2, p2, st);
       if (e != cudaSuccess) return FHT_ERR_CUDA;
       log.after(st);

@@ -186,7 +186,7 @@ __device__ __forceinline__ void stage_rows(A (&w)[kTPW<R>][1 << Split<R>::b][VB]
         const int base = (SIG > 0 ? lane * VB : (WC - 1) - lane * VB) - soff[tau];
         A* dst = stg + tau * ST_PITCH;
 #pragma unroll
-        for (int q = 0; q < VB; ++q) {
+        for (int q = 0; q < VB; ++q) {  // predicated stores: no divergent fast path (measured slower)
           const int idx = base + (SIG > 0 ? q : -q);
           if ((unsigned)idx < (unsigned)box) dst[idx] = w[g][u][q];
         }
@@ -262,6 +262,7 @@ struct P1Params {
   int fill_tma;                      // non-transposed rows by TMA (image base/pitch 16-B aligned)
   int fill_vec;                      // transposed fill with 16-byte (u8: 4-byte) loads
   int nq, img0;
+  int ntiles;                        // tiles per strip (max over slots)
   int L;                             // log2(#strips)
   int TX;                            // tile width = TMA box (multiple of 4, <= TX1)
   int64_t scratch_img_rows;          // scratch rows per image
@@ -270,7 +271,42 @@ struct P1Params {
 
 // scratch layout: row (img, slot, j, i) = img*scratch_img_rows + srow0 + j*2^L + i,
 // column x - xlo holds F_m[i][j](x)  (F_m = levels 1..m of strip i, shift j).
-template <typename Tin, int R, int SIG>
+//
+// The butterfly part is instantiated per sign (SIG); the fills are sign-independent (they only
+// need the input origin Xa) and exist once per kernel, which keeps the kernel's code footprint
+// inside the instruction cache.
+template <typename Tin, int R, int SIG, typename Tsrc>
+__device__ __noinline__ void p1_tail(const CUtensorMap* tm_scr, const P1Params& p, const P1Slot& sl, int img,
+                                     int strip, int X, const Tsrc* tsrc, int tpitch, int fa_pitch) {
+  using A = typename AccOf<Tin>::type;
+  using S = Split<R>;
+  constexpr int NR = 1 << R;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  A* buf = reinterpret_cast<A*>(smem_raw);
+  unsigned char* tab = smem_raw + main_buf_bytes(R) + (sizeof(Tin) == 1 ? u8_tile_bytes(R) : 0);
+  const int* rowoff = reinterpret_cast<const int*>(tab);
+  const int* soff = rowoff + 64;
+  A w[kTPW<R>][1 << S::b][VB];
+  tile_fht<R, SIG, A>(tsrc, tpitch, rowoff, buf, fa_pitch, w);
+  stage_rows<R, SIG, A>(w, buf, soff, p.TX);
+  // ---- store F_m[strip][j] (j = tau): scratch column X - xlo is 16-byte aligned
+  if (threadIdx.x < NR) {
+    const int j = threadIdx.x;
+    const int64_t row = (int64_t)(img - p.img0) * p.scratch_img_rows + sl.srow0 + ((int64_t)j << p.L) + strip;
+    tma_store_row(tm_scr, buf + j * ST_PITCH, X - sl.xlo, (int)row);
+    tma_commit();
+    tma_wait_read();
+  }
+}
+
+template <typename Tin, int R, typename Tsrc>
+__device__ __forceinline__ void p1_tail_sig(int sigma, const CUtensorMap* tm_scr, const P1Params& p, const P1Slot& sl,
+                                            int img, int strip, int X, const Tsrc* tsrc, int tpitch, int fa_pitch) {
+  if (sigma > 0) p1_tail<Tin, R, 1>(tm_scr, p, sl, img, strip, X, tsrc, tpitch, fa_pitch);
+  else p1_tail<Tin, R, -1>(tm_scr, p, sl, img, strip, X, tsrc, tpitch, fa_pitch);
+}
+
+template <typename Tin, int R>
 __device__ __forceinline__ void p1_body(const CUtensorMap* tm_img0, const CUtensorMap* tm_img1,
                                         const CUtensorMap* tm_scr, const P1Params& p, const P1Slot& sl, int img,
                                         int strip, int X) {
@@ -284,11 +320,9 @@ __device__ __forceinline__ void p1_body(const CUtensorMap* tm_img0, const CUtens
   int* rowoff = reinterpret_cast<int*>(tab);          // [NR]
   int* soff = rowoff + 64;                            // [NR]
   uint64_t* bar = reinterpret_cast<uint64_t*>(tab + 1024);
-  const int TX = p.TX;
   const Tin* src = static_cast<const Tin*>(p.img) + (int64_t)img * p.img_bstride;
   const int y0 = strip * NR;
-  const int Xa = SIG > 0 ? X : X - (WA - WC);  // x of input index e = 0
-  A w[kTPW<R>][1 << S::b][VB];
+  const int Xa = sl.sigma > 0 ? X : X - (WA - WC);  // x of input index e = 0
 
   if (!sl.transposed && p.fill_tma) {
     // ---- TMA: NR image rows, columns [Xa, Xa + 288) from the 16-byte aligned column below
@@ -313,94 +347,86 @@ __device__ __forceinline__ void p1_body(const CUtensorMap* tm_img0, const CUtens
       }
     }
     mbar_wait0(bar);
-    if constexpr (sizeof(Tin) == 1) tile_fht<R, SIG, A>(tile, TP, rowoff, buf, FA_PITCH, w);
-    else tile_fht<R, SIG, A>(reinterpret_cast<const A*>(tile), TP, rowoff, buf, TMA_PITCH, w);
-  } else {
-    if (threadIdx.x < NR) {
-      rowoff[threadIdx.x] = 0;
-      soff[threadIdx.x] = 0;
-    }
-    if (!sl.transposed) {
-      // ---- scalar fill (angle-range gather T(x, y) = I[y][colmap[x - e_y]], or odd pitches)
-#pragma unroll 4
-      for (int idx = threadIdx.x; idx < NR * WA; idx += NT) {
-        const int rho = idx / WA, e = idx - rho * WA;
-        const int y = y0 + rho, x = Xa + e;
-        A v = A(0);
-        if (y < p.img_h) {
-          if (!p.range) {
-            if (x >= 0 && x < p.img_w) v = static_cast<A>(__ldg(src + (int64_t)y * p.img_rstride + x));
-          } else {  // P:146; R13, R14
-            const int u = x - __ldg(p.e_tab + y);
-            if (u >= 0 && u < p.w_content)
-              v = static_cast<A>(__ldg(src + (int64_t)y * p.img_rstride + __ldg(p.colmap + u)));
-          }
-        }
-        buf[rho * FA_PITCH + e] = v;
-      }
-    } else if (p.fill_vec && NR >= 4) {
-      // ---- transposed: FHT row y = image column, FHT column x = image row. Thread = (x, 4 y's):
-      // one 16-byte (u8: 4-byte) load from image row x, 4 conflict-free column stores. All of a
-      // thread's loads are issued before its first store (memory-level parallelism).
-      constexpr int YQ = NR >= 4 ? NR / 4 : 1;  // threads per image row
-      constexpr int IT = (WA * YQ + NT - 1) / NT;
-      using V4 = typename std::conditional<sizeof(Tin) == 1, uchar4,
-                 typename std::conditional<std::is_same<Tin, float>::value, float4, int4>::type>::type;
-      V4 vals[IT];
-#pragma unroll
-      for (int it = 0; it < IT; ++it) {
-        const int idx = threadIdx.x + it * NT;
-        const int e = idx / YQ, yq = idx - e * YQ;
-        const int x = Xa + e, y = y0 + 4 * yq;
-        vals[it] = V4{};
-        if (idx < WA * YQ && x >= 0 && x < p.img_h) {
-          const Tin* ps = src + (int64_t)x * p.img_rstride + y;
-          if (y + 3 < p.img_w) {
-            vals[it] = __ldg(reinterpret_cast<const V4*>(ps));
-          } else {
-            Tin t[4] = {Tin(0), Tin(0), Tin(0), Tin(0)};
-            for (int k = 0; k < 3; ++k)
-              if (y + k < p.img_w) t[k] = __ldg(ps + k);
-            vals[it].x = t[0];
-            vals[it].y = t[1];
-            vals[it].z = t[2];
-          }
-        }
-      }
-#pragma unroll
-      for (int it = 0; it < IT; ++it) {
-        const int idx = threadIdx.x + it * NT;
-        if (idx < WA * YQ) {
-          const int e = idx / YQ, yq = idx - e * YQ;
-          A* d = buf + (4 * yq) * FA_PITCH + e;
-          d[0] = static_cast<A>(vals[it].x);
-          d[FA_PITCH] = static_cast<A>(vals[it].y);
-          d[2 * FA_PITCH] = static_cast<A>(vals[it].z);
-          d[3 * FA_PITCH] = static_cast<A>(vals[it].w);
-        }
-      }
-    } else {
-      for (int idx = threadIdx.x; idx < NR * WA; idx += NT) {
-        const int e = idx / NR, rho = idx - e * NR;  // consecutive threads: consecutive image columns
-        const int y = y0 + rho, x = Xa + e;
-        A v = A(0);
-        if (y < p.img_w && x >= 0 && x < p.img_h) v = static_cast<A>(__ldg(src + (int64_t)x * p.img_rstride + y));
-        buf[rho * FA_PITCH + e] = v;
-      }
-    }
-    __syncthreads();
-    tile_fht<R, SIG, A>(static_cast<const A*>(buf), FA_PITCH, rowoff, buf, FA_PITCH, w);
+    if constexpr (sizeof(Tin) == 1)
+      p1_tail_sig<Tin, R>(sl.sigma, tm_scr, p, sl, img, strip, X, static_cast<const Tin*>(tile), TP, FA_PITCH);
+    else
+      p1_tail_sig<Tin, R>(sl.sigma, tm_scr, p, sl, img, strip, X, reinterpret_cast<const A*>(tile), TP, TMA_PITCH);
+    return;
   }
-  stage_rows<R, SIG, A>(w, buf, soff, TX);
-
-  // ---- store F_m[strip][j] (j = tau): scratch column X - xlo is 16-byte aligned
   if (threadIdx.x < NR) {
-    const int j = threadIdx.x;
-    const int64_t row = (int64_t)(img - p.img0) * p.scratch_img_rows + sl.srow0 + ((int64_t)j << p.L) + strip;
-    tma_store_row(tm_scr, buf + j * ST_PITCH, X - sl.xlo, (int)row);
-    tma_commit();
-    tma_wait_read();
+    rowoff[threadIdx.x] = 0;
+    soff[threadIdx.x] = 0;
   }
+  if (!sl.transposed) {
+    // ---- scalar fill (angle-range gather T(x, y) = I[y][colmap[x - e_y]], or odd pitches)
+#pragma unroll 4
+    for (int idx = threadIdx.x; idx < NR * WA; idx += NT) {
+      const int rho = idx / WA, e = idx - rho * WA;
+      const int y = y0 + rho, x = Xa + e;
+      A v = A(0);
+      if (y < p.img_h) {
+        if (!p.range) {
+          if (x >= 0 && x < p.img_w) v = static_cast<A>(__ldg(src + (int64_t)y * p.img_rstride + x));
+        } else {  // P:146; R13, R14
+          const int u = x - __ldg(p.e_tab + y);
+          if (u >= 0 && u < p.w_content)
+            v = static_cast<A>(__ldg(src + (int64_t)y * p.img_rstride + __ldg(p.colmap + u)));
+        }
+      }
+      buf[rho * FA_PITCH + e] = v;
+    }
+  } else if (p.fill_vec && NR >= 4) {
+    // ---- transposed: FHT row y = image column, FHT column x = image row. Thread = (x, 4 y's):
+    // one 16-byte (u8: 4-byte) load from image row x, 4 conflict-free column stores. All of a
+    // thread's loads are issued before its first store (memory-level parallelism).
+    constexpr int YQ = NR >= 4 ? NR / 4 : 1;  // threads per image row
+    constexpr int IT = (WA * YQ + NT - 1) / NT;
+    using V4 = typename std::conditional<sizeof(Tin) == 1, uchar4,
+               typename std::conditional<std::is_same<Tin, float>::value, float4, int4>::type>::type;
+    V4 vals[IT];
+#pragma unroll
+    for (int it = 0; it < IT; ++it) {
+      const int idx = threadIdx.x + it * NT;
+      const int e = idx / YQ, yq = idx - e * YQ;
+      const int x = Xa + e, y = y0 + 4 * yq;
+      vals[it] = V4{};
+      if (idx < WA * YQ && x >= 0 && x < p.img_h) {
+        const Tin* ps = src + (int64_t)x * p.img_rstride + y;
+        if (y + 3 < p.img_w) {
+          vals[it] = __ldg(reinterpret_cast<const V4*>(ps));
+        } else {
+          Tin t[4] = {Tin(0), Tin(0), Tin(0), Tin(0)};
+          for (int k = 0; k < 3; ++k)
+            if (y + k < p.img_w) t[k] = __ldg(ps + k);
+          vals[it].x = t[0];
+          vals[it].y = t[1];
+          vals[it].z = t[2];
+        }
+      }
+    }
+#pragma unroll
+    for (int it = 0; it < IT; ++it) {
+      const int idx = threadIdx.x + it * NT;
+      if (idx < WA * YQ) {
+        const int e = idx / YQ, yq = idx - e * YQ;
+        A* d = buf + (4 * yq) * FA_PITCH + e;
+        d[0] = static_cast<A>(vals[it].x);
+        d[FA_PITCH] = static_cast<A>(vals[it].y);
+        d[2 * FA_PITCH] = static_cast<A>(vals[it].z);
+        d[3 * FA_PITCH] = static_cast<A>(vals[it].w);
+      }
+    }
+  } else {
+    for (int idx = threadIdx.x; idx < NR * WA; idx += NT) {
+      const int e = idx / NR, rho = idx - e * NR;  // consecutive threads: consecutive image columns
+      const int y = y0 + rho, x = Xa + e;
+      A v = A(0);
+      if (y < p.img_w && x >= 0 && x < p.img_h) v = static_cast<A>(__ldg(src + (int64_t)x * p.img_rstride + y));
+      buf[rho * FA_PITCH + e] = v;
+    }
+  }
+  __syncthreads();
+  p1_tail_sig<Tin, R>(sl.sigma, tm_scr, p, sl, img, strip, X, static_cast<const A*>(buf), FA_PITCH, FA_PITCH);
 }
 
 // tm_img0: image [batch][h][w], box 1 x 1 x 256 columns; tm_img1: box 36 (u8: 48) columns;
@@ -409,15 +435,19 @@ template <typename Tin, int R>
 __global__ void __launch_bounds__(Split<R>::nw * 32, kMinBlocks<R>)
 k_p1(const __grid_constant__ CUtensorMap tm_img0, const __grid_constant__ CUtensorMap tm_img1,
      const __grid_constant__ CUtensorMap tm_scr, const __grid_constant__ P1Params p) {
-  const int z = blockIdx.z;
-  const int qi = z % p.nq;
-  const int img = p.img0 + z / p.nq;
+  // flat grid, quadrant slot fastest: with 148 SMs (a multiple of 4) the round-robin CTA
+  // placement gives every SM CTAs of one slot, i.e. one sign and one fill path (I-cache locality)
+  int id = blockIdx.x;
+  const int qi = id % p.nq;
+  id /= p.nq;
+  const int n = id % p.ntiles;
+  id /= p.ntiles;
+  const int strip = id & ((1 << p.L) - 1);
+  const int img = p.img0 + (id >> p.L);
   const P1Slot& sl = p.slot[qi];
-  const int n = blockIdx.x;
   if (n >= sl.ntiles) return;
   const int X = min(sl.xlo + p.TX * n, sl.xhi - p.TX);  // tile = window start (Xw = X)
-  if (sl.sigma > 0) p1_body<Tin, R, 1>(&tm_img0, &tm_img1, &tm_scr, p, sl, img, blockIdx.y, X);
-  else p1_body<Tin, R, -1>(&tm_img0, &tm_img1, &tm_scr, p, sl, img, blockIdx.y, X);
+  p1_body<Tin, R>(&tm_img0, &tm_img1, &tm_scr, p, sl, img, strip, X);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -443,6 +473,8 @@ struct P2Dest {
 struct P2Params {
   int64_t scratch_img_rows;
   int nq, img0;
+  int ntiles;              // tiles per group (max over slots)
+  int m;                   // log2(#groups)
   int TX;                  // tile stride (columns owned per tile); store box = TX + 4
   int W, Hp, wc;
   int range;
@@ -580,15 +612,20 @@ __global__ void __launch_bounds__(Split<R>::nw * 32, kMinBlocks<R>)
 k_p2(const __grid_constant__ CUtensorMap tm_scr0, const __grid_constant__ CUtensorMap tm_scr1,
      const __grid_constant__ CUtensorMap tm0, const __grid_constant__ CUtensorMap tm1,
      const __grid_constant__ P2Params p) {
-  const int z = blockIdx.z;
-  const int qi = z % p.nq;
-  const int img = p.img0 + z / p.nq;
+  // flat grid, tile fastest: CTAs running together read overlapping scratch rows (L2 reuse of
+  // the 72-column halo and of the sheared rows of one group)
+  int id = blockIdx.x;
+  const int n = id % p.ntiles;
+  id /= p.ntiles;
+  const int j = id & ((1 << p.m) - 1);
+  id >>= p.m;
+  const int qi = id % p.nq;
+  const int img = p.img0 + id / p.nq;
   const P2Slot& sl = p.slot[qi];
-  const int n = blockIdx.x;
   if (n >= sl.ntiles) return;
   const int X = min(sl.xbeg + p.TX * n, sl.xend - p.TX);
-  if (sl.sigma > 0) p2_body<A, R, 1>(&tm_scr0, &tm_scr1, &tm0, &tm1, p, sl, img, blockIdx.y, X);
-  else p2_body<A, R, -1>(&tm_scr0, &tm_scr1, &tm0, &tm1, p, sl, img, blockIdx.y, X);
+  if (sl.sigma > 0) p2_body<A, R, 1>(&tm_scr0, &tm_scr1, &tm0, &tm1, p, sl, img, j, X);
+  else p2_body<A, R, -1>(&tm_scr0, &tm_scr1, &tm0, &tm1, p, sl, img, j, X);
 }
 
 }  // namespace v2

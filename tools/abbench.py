@@ -1,0 +1,93 @@
+#!/usr/bin/env python
+"""A/B timing of alternative libfht builds on the same GPU in one process each, interleaved.
+
+    python tools/abbench.py LIB1.so LIB2.so ... [--configs 2,5] [--rounds 3]
+
+Every round runs each library's step for each config in a fresh subprocess (FHT_LIB=...), so
+the builds see the same box, clocks and thermal state; prints per-kernel means.
+"""
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+CHILD = r'''
+import json, os, statistics, sys
+sys.path.insert(0, os.environ["ROOT"])
+import torch, synth
+import paper_1811_06378_b200 as fht
+cid = int(sys.argv[1])
+c = synth.CONFIGS[cid]
+imgs = synth.batch(cid)
+t = torch.from_numpy(imgs).cuda()
+outs = {}
+plan = fht.angle_plan(c["h"], c["w"], c["theta_min"], c["theta_max"]) if c["mode"] == "range" else None
+def step(ev=None):
+    if c["mode"] == "full":
+        if cid in (2, 5):
+            outs["h"], outs["s"] = fht.full(t, pair=True, out=outs.get("h"), out_shifted=outs.get("s"), events=ev)
+        else:
+            outs["h"] = fht.full(t, out=outs.get("h"), events=ev)
+    elif c["mode"] == "range":
+        outs["h"], outs["s"] = fht.angle_range(t, plan, pair=True, out=outs.get("h"), out_shifted=outs.get("s"), events=ev)
+    else:
+        outs["h"] = fht.quadrant(t, 0, out=outs.get("h"), events=ev)
+    return outs["h"].launches
+n = step()
+flush = torch.empty(128 << 20, dtype=torch.float32, device="cuda")
+for _ in range(5): step()
+torch.cuda.synchronize()
+steps = 30 if cid in (1, 2) else 8
+evs = [[torch.cuda.Event(enable_timing=True) for _ in range(n + 1)] for _ in range(steps)]
+for r in evs:
+    for e in r: e.record()
+torch.cuda.synchronize()
+for i in range(steps):
+    flush.zero_()
+    step(evs[i])
+torch.cuda.synchronize()
+tot = statistics.mean(evs[i][0].elapsed_time(evs[i][n]) for i in range(steps))
+ks = [statistics.mean(evs[i][k].elapsed_time(evs[i][k + 1]) for i in range(steps)) for k in range(n)]
+first = 1 if c["mode"] == "range" else 0
+p1 = sum(ks[k] for k in range(first, n) if (k - first) % 2 == 0)
+p2 = sum(ks[k] for k in range(first, n) if (k - first) % 2 == 1)
+print(json.dumps({"step_us": tot * 1e3, "p1_us": p1 * 1e3, "p2_us": p2 * 1e3}))
+'''
+
+
+def main():
+    args = sys.argv[1:]
+    cfgs = [2, 5]
+    rounds = 3
+    if "--configs" in args:
+        i = args.index("--configs")
+        cfgs = [int(x) for x in args[i + 1].split(",")]
+        del args[i:i + 2]
+    if "--rounds" in args:
+        i = args.index("--rounds")
+        rounds = int(args[i + 1])
+        del args[i:i + 2]
+    libs = args
+    res = {}
+    for r in range(rounds):
+        for lib in libs:
+            for cid in cfgs:
+                env = dict(os.environ, FHT_LIB=os.path.abspath(lib), ROOT=ROOT)
+                out = subprocess.run([sys.executable, "-c", CHILD, str(cid)], env=env, capture_output=True, text=True)
+                try:
+                    d = json.loads(out.stdout.strip().splitlines()[-1])
+                except Exception:
+                    print("FAIL", lib, cid, out.stderr[-500:])
+                    continue
+                res.setdefault((lib, cid), []).append(d)
+    for (lib, cid), ds in sorted(res.items()):
+        m = {k: sum(d[k] for d in ds) / len(ds) for k in ds[0]}
+        mn = {k: min(d[k] for d in ds) for k in ds[0]}
+        print(f"C{cid} {os.path.basename(lib):28s} step {m['step_us']:9.1f} us (min {mn['step_us']:9.1f})  "
+              f"p1 {m['p1_us']:9.1f}  p2 {m['p2_us']:9.1f}")
+
+
+if __name__ == "__main__":
+    main()
