@@ -268,16 +268,15 @@ def main():
         if world > 1:
             dist.barrier()
 
+    from paper_1811_06378_b200.sharding import max_over_ranks as _mor, rank_images
+
     def max_over_ranks(x):
-        if world == 1:
-            return x
-        tt = torch.tensor([x], device=dev, dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        return float(tt.item())
+        return _mor(x, device=dev)
 
     def run_config(cfg_id, steps, warmup, with_e2e):
         cc = synth.CONFIGS[cfg_id]
-        imgs = synth.batch(cfg_id)
+        mine = rank_images(cc["batch"], rank, world)  # weak scaling: this rank's own images
+        imgs = synth.batch(cfg_id, first=mine.start)
         t = torch.from_numpy(imgs).to(dev)
         in_b, cells, ndest = geometry(cfg_id, cc)
         plan = None

@@ -52,14 +52,14 @@ def _dda(x0: float, y0: float, x1: float, y1: float):
     return xs, ys
 
 
-def image_c1() -> np.ndarray:
+def image_c1(index: int = 0) -> np.ndarray:
     """C1: 256x256 uint8, i.i.d. uniform [0,255]."""
-    return rng_for(1).integers(0, 256, size=(256, 256), dtype=np.uint8)
+    return rng_for(1, index).integers(0, 256, size=(256, 256), dtype=np.uint8)
 
 
-def image_c2(P: int = 1024) -> np.ndarray:
+def image_c2(P: int = 1024, index: int = 0) -> np.ndarray:
     """C2: N(0, 0.1) noise plus 50 rasterised lines of intensity 1.0, endpoints uniform on the border."""
-    g = rng_for(2)
+    g = rng_for(2, index)
     img = g.normal(0.0, 0.1, size=(P, P))
     for _ in range(50):
         ta, tb = g.uniform(0, 4 * (P - 1), size=2)
@@ -84,9 +84,9 @@ def image_c3(index: int, P: int = 512) -> np.ndarray:
     return img
 
 
-def image_c4(P: int = 4096) -> np.ndarray:
+def image_c4(P: int = 4096, index: int = 0) -> np.ndarray:
     """C4: uniform [0,1) float32."""
-    return rng_for(4).random((P, P), dtype=np.float32)
+    return rng_for(4, index).random((P, P), dtype=np.float32)
 
 
 def image_c5(index: int, P: int = 2048) -> np.ndarray:
@@ -119,21 +119,17 @@ def image_c5(index: int, P: int = 2048) -> np.ndarray:
     return (img / img.max()).astype(np.float32)
 
 
-def batch(config_id: int, count: int | None = None) -> np.ndarray:
-    """[B][h][w] array for a config (optionally only the first `count` images)."""
+def batch(config_id: int, count: int | None = None, first: int = 0) -> np.ndarray:
+    """[B][h][w] array for a config: images first .. first+B-1 (B = the config's batch, or `count`).
+    `first` selects another rank's images under weak scaling (paper_1811_06378_b200.sharding)."""
     cfg = CONFIGS[config_id]
     n = cfg["batch"] if count is None else min(count, cfg["batch"])
-    if config_id == 1:
-        return image_c1()[None]
-    if config_id == 2:
-        return image_c2()[None]
-    if config_id == 3:
-        return np.stack([image_c3(i) for i in range(n)])
-    if config_id == 4:
-        return image_c4()[None]
-    if config_id == 5:
-        return np.stack([image_c5(i) for i in range(n)])
-    raise ValueError(config_id)
+    idx = range(first, first + n)
+    gen = {1: lambda i: image_c1(i), 2: lambda i: image_c2(index=i), 3: image_c3, 4: lambda i: image_c4(index=i),
+           5: image_c5}
+    if config_id not in gen:
+        raise ValueError(config_id)
+    return np.stack([gen[config_id](i) for i in idx])
 
 
 def random_image(shape, dtype: str, seed: int, density: float | None = None) -> np.ndarray:
