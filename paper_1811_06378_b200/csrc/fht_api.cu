@@ -183,14 +183,14 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-// 2-D row-major tensor [rows][cols] with a 1 x box_cols box (one output row per store).
+// 2-D row-major tensor [rows][cols] with a box_rows x box_cols box (default: one row per copy).
 bool make_row_map(CUtensorMap* m, const void* base, bool f32, uint64_t cols, uint64_t rows, uint64_t pitch_elems,
-                  uint32_t box_cols) {
+                  uint32_t box_cols, uint32_t box_rows = 1) {
   auto fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[2] = {cols, rows};
   cuuint64_t strides[1] = {pitch_elems * 4};
-  cuuint32_t box[2] = {box_cols, 1};
+  cuuint32_t box[2] = {box_cols, box_rows};
   cuuint32_t es[2] = {1, 1};
   return fn(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_INT32, 2, const_cast<void*>(base), dims,
             strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -275,7 +275,7 @@ cudaError_t launch_p1(int r, dim3 grid, const P1Maps& m, const v2::P1Params& a, 
   return cudaErrorInvalidValue;
 }
 struct P2Maps {
-  CUtensorMap scr0, scr1, out0, out1;
+  CUtensorMap scr0, scr1, out0, out1, out0_box;
 };
 template <typename A, int R>
 cudaError_t launch_p2_t(dim3 grid, const P2Maps& m, const v2::P2Params& a, cudaStream_t st) {
@@ -283,7 +283,7 @@ cudaError_t launch_p2_t(dim3 grid, const P2Maps& m, const v2::P2Params& a, cudaS
   static const cudaError_t attr =
       cudaFuncSetAttribute(v2::k_p2<A, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (attr != cudaSuccess) return attr;
-  v2::k_p2<A, R><<<grid, v2::Split<R>::nw * 32, smem, st>>>(m.scr0, m.scr1, m.out0, m.out1, a);
+  v2::k_p2<A, R><<<grid, v2::Split<R>::nw * 32, smem, st>>>(m.scr0, m.scr1, m.out0, m.out1, m.out0_box, a);
   return cudaGetLastError();
 }
 template <typename A>
@@ -449,14 +449,28 @@ int run_orientation(const fht_image* img, const Frame& f, const Slot* slots, int
       if (!make_row_map(tm_out[p2.ndest], o->data, o->dtype == FHT_F32, (uint64_t)o->cols,
                         (uint64_t)(o->batch * D.rows_per_img), (uint64_t)o->row_stride, (uint32_t)box2))
         return FHT_ERR_CUDA;
+      if (p2.ndest == 0 && !make_row_map(&m2.out0_box, o->data, o->dtype == FHT_F32, (uint64_t)o->cols,
+                                         (uint64_t)(o->batch * D.rows_per_img), (uint64_t)o->row_stride,
+                                         (uint32_t)box2, (uint32_t)(1 << f.L)))
+        return FHT_ERR_CUDA;
       ++p2.ndest;
     }
     if (p2.ndest == 1) m2.out1 = m2.out0;
+    if (!outs.d[0]) m2.out0_box = m2.out0;
     const bool f32 = img->dtype == FHT_F32;
     const uint64_t scr_rows = (uint64_t)sp.chunk * p1.scratch_img_rows;
     P1Maps m1;
-    if (!make_row_map(&m1.scr, ws, f32, (uint64_t)sp.pitch, scr_rows, (uint64_t)sp.pitch, (uint32_t)p1.TX))
-      return FHT_ERR_CUDA;
+    {  // pass-1 stores: scratch as [z*2^m + j][strip][column], one box {TX, 1, 2^m} per tile
+      auto fn = encode_fn();
+      cuuint64_t dims[3] = {(cuuint64_t)sp.pitch, (cuuint64_t)nstrips, (cuuint64_t)(scr_rows / nstrips)};
+      cuuint64_t strides[2] = {(cuuint64_t)(sp.pitch * 4), (cuuint64_t)(sp.pitch * 4 * nstrips)};
+      cuuint32_t box[3] = {(cuuint32_t)p1.TX, 1, (cuuint32_t)(1 << f.m)};
+      cuuint32_t e[3] = {1, 1, 1};
+      if (!fn || fn(&m1.scr, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_INT32, 3, ws, dims, strides,
+                    box, e, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return FHT_ERR_CUDA;
+    }
     if (p1.fill_tma) {
       if (!make_image_map(&m1.img0, img, 256) || !make_image_map(&m1.img1, img, es == 1 ? 48 : 36))
         return FHT_ERR_CUDA;

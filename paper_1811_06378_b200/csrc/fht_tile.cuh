@@ -35,8 +35,20 @@
 #include <cuda.h>
 
 #include <type_traits>
+#include <utility>
 
 #include "fht_common.cuh"
+
+// Compile-time variants for A/B timing (tools/build_variant.sh); defaults are the measured best.
+#ifndef FHT_STAGE_ASM
+#define FHT_STAGE_ASM 1   // staging: explicitly predicated st.shared (1) or C++ if (0)
+#endif
+#ifndef FHT_LOAD_LANES
+#define FHT_LOAD_LANES 1  // pass-2 TMA row loads issued by 32 lanes (1) or one thread (0)
+#endif
+#ifndef FHT_P2_DENSE
+#define FHT_P2_DENSE 1    // pass-2 plain destination of interior tiles as one 2-D box (1)
+#endif
 
 namespace fht {
 namespace v2 {
@@ -66,11 +78,15 @@ template <int R> constexpr int kTPW = ((1 << Split<R>::a) + Split<R>::nw - 1) / 
 // Shared memory layout (bytes): [main buffer][u8 input tile (pass 1 u8 TMA only)][tables]
 __host__ __device__ constexpr size_t main_buf_bytes(int R) { return (size_t)(1 << R) * TMA_PITCH * 4; }
 __host__ __device__ constexpr size_t u8_tile_bytes(int R) { return (size_t)(1 << R) * TMA_PITCH_U8; }
-constexpr size_t kTableBytes = 4096;
+// tables: [rowoff 64 ints][soff 2x64 ints][mbarrier] = 1 KB, then (pass 2) RowInfo [2][2^R], 16 B each.
+// Kept small: 5 CTAs of 2^R = 32 rows must fit in 228 KB (measured: 4 CTAs/SM cost 10%).
+constexpr size_t kTableBytes = 1024;
 __host__ __device__ constexpr size_t p1_smem_bytes(int R, bool u8) {
   return main_buf_bytes(R) + (u8 ? u8_tile_bytes(R) : 0) + kTableBytes;
 }
-__host__ __device__ constexpr size_t p2_smem_bytes(int R) { return main_buf_bytes(R) + kTableBytes; }
+__host__ __device__ constexpr size_t p2_smem_bytes(int R) {
+  return main_buf_bytes(R) + kTableBytes + 2 * (size_t)(1 << R) * 16;
+}
 
 // ------------------------------------------------------------------------------------------
 // Register butterfly (north_star "out[t] = A[t>>1] + B[t>>1] shifted by ceil(t/2)"
@@ -169,10 +185,23 @@ __device__ __forceinline__ void tile_fht(const Tsrc* src, int src_pitch, const i
   __syncthreads();
 }
 
-// Write the register results into a staging plane: output row tau, window index s stored at
-// s - soff[tau] when 0 <= that < box. Then fence for the TMA engine and synchronise.
+template <int Q, typename A>
+__device__ __forceinline__ void st_pred(uint32_t a, int idx, int box, A v) {
+  const uint32_t bits = *reinterpret_cast<const uint32_t*>(&v);
+  asm volatile("{ .reg .pred p; setp.lt.u32 p, %1, %2; @p st.shared.b32 [%0+%3], %4; }"
+               :: "r"(a), "r"(idx), "r"(box), "n"(Q * 4), "r"(bits) : "memory");
+}
+template <int SIG, typename A, int... Q>
+__device__ __forceinline__ void st_pred_row(uint32_t a, int lo, int box, const A (&v)[VB], std::integer_sequence<int, Q...>) {
+  (st_pred<Q>(a, lo + Q, box, v[SIG > 0 ? Q : VB - 1 - Q]), ...);
+}
+
+// Write the register results into a staging plane of row pitch `pitch`: output row tau, window
+// index s stored at s - soff[tau] when 0 <= that < box. Explicitly predicated st.shared (one
+// ISETP + one STS per element, no branches). Then fence for the TMA engine and synchronise.
 template <int R, int SIG, typename A>
-__device__ __forceinline__ void stage_rows(A (&w)[kTPW<R>][1 << Split<R>::b][VB], A* stg, const int* soff, int box) {
+__device__ __forceinline__ void stage_rows(A (&w)[kTPW<R>][1 << Split<R>::b][VB], A* stg, const int* soff, int box,
+                                           int pitch) {
   using S = Split<R>;
   constexpr int NA = 1 << S::a, NBk = 1 << S::b, NW = S::nw;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -183,13 +212,18 @@ __device__ __forceinline__ void stage_rows(A (&w)[kTPW<R>][1 << Split<R>::b][VB]
 #pragma unroll
       for (int u = 0; u < NBk; ++u) {
         const int tau = jp * NBk + u;
-        const int base = (SIG > 0 ? lane * VB : (WC - 1) - lane * VB) - soff[tau];
-        A* dst = stg + tau * ST_PITCH;
+        // lowest window index of the lane's 7 columns, and its staging index
+        const int lo = (SIG > 0 ? lane * VB : (WC - VB) - lane * VB) - soff[tau];
+#if FHT_STAGE_ASM
+        const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(stg + tau * pitch + lo));
+        // element q of the lane sits at staging index lo + q
+        st_pred_row<SIG>(a, lo, box, w[g][u], std::make_integer_sequence<int, VB>{});
+#else
+        A* dst = stg + tau * pitch;
 #pragma unroll
-        for (int q = 0; q < VB; ++q) {  // predicated stores: no divergent fast path (measured slower)
-          const int idx = base + (SIG > 0 ? q : -q);
-          if ((unsigned)idx < (unsigned)box) dst[idx] = w[g][u][q];
-        }
+        for (int q = 0; q < VB; ++q)
+          if ((unsigned)(lo + q) < (unsigned)box) dst[lo + q] = w[g][u][SIG > 0 ? q : VB - 1 - q];
+#endif
       }
     }
   }
@@ -206,6 +240,10 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 __device__ __forceinline__ void tma_store_row(const CUtensorMap* map, const void* smem, int col, int row) {
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];"
                :: "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(smem)), "r"(col), "r"(row) : "memory");
+}
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* smem, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];"
+               :: "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(smem)), "r"(c0), "r"(c1), "r"(c2) : "memory");
 }
 __device__ __forceinline__ void tma_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void tma_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
@@ -288,12 +326,12 @@ __device__ __noinline__ void p1_tail(const CUtensorMap* tm_scr, const P1Params& 
   const int* soff = rowoff + 64;
   A w[kTPW<R>][1 << S::b][VB];
   tile_fht<R, SIG, A>(tsrc, tpitch, rowoff, buf, fa_pitch, w);
-  stage_rows<R, SIG, A>(w, buf, soff, p.TX);
-  // ---- store F_m[strip][j] (j = tau): scratch column X - xlo is 16-byte aligned
-  if (threadIdx.x < NR) {
-    const int j = threadIdx.x;
-    const int64_t row = (int64_t)(img - p.img0) * p.scratch_img_rows + sl.srow0 + ((int64_t)j << p.L) + strip;
-    tma_store_row(tm_scr, buf + j * ST_PITCH, X - sl.xlo, (int)row);
+  stage_rows<R, SIG, A>(w, buf, soff, p.TX, p.TX);  // dense [NR][TX]: the box layout
+  // ---- store F_m[strip][j] for all j in ONE box {TX, 1, NR} of the 3-D scratch view
+  // [z*2^m + j][strip][column] (z = image-in-chunk * nq + slot); column X - xlo is 16-B aligned
+  if (threadIdx.x == 0) {
+    const int z = (img - p.img0) * p.nq + (int)(sl.srow0 >> (R + p.L));
+    tma_store_3d(tm_scr, buf, X - sl.xlo, strip, z << R);
     tma_commit();
     tma_wait_read();
   }
@@ -319,7 +357,7 @@ __device__ __forceinline__ void p1_body(const CUtensorMap* tm_img0, const CUtens
   unsigned char* tab = smem_raw + main_buf_bytes(R) + (sizeof(Tin) == 1 ? u8_tile_bytes(R) : 0);
   int* rowoff = reinterpret_cast<int*>(tab);          // [NR]
   int* soff = rowoff + 64;                            // [NR]
-  uint64_t* bar = reinterpret_cast<uint64_t*>(tab + 1024);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(tab + 768);
   const Tin* src = static_cast<const Tin*>(p.img) + (int64_t)img * p.img_bstride;
   const int y0 = strip * NR;
   const int Xa = sl.sigma > 0 ? X : X - (WA - WC);  // x of input index e = 0
@@ -430,7 +468,7 @@ __device__ __forceinline__ void p1_body(const CUtensorMap* tm_img0, const CUtens
 }
 
 // tm_img0: image [batch][h][w], box 1 x 1 x 256 columns; tm_img1: box 36 (u8: 48) columns;
-// tm_scr: scratch rows, box TX.
+// tm_scr: scratch as [z*2^m + j][strip][column], box {TX, 1, 2^m}.
 template <typename Tin, int R>
 __global__ void __launch_bounds__(Split<R>::nw * 32, kMinBlocks<R>)
 k_p1(const __grid_constant__ CUtensorMap tm_img0, const __grid_constant__ CUtensorMap tm_img1,
@@ -486,28 +524,28 @@ struct P2Params {
   P2Dest dest[2];
 };
 
-struct RowInfo {  // per output row of the current destination (shared memory)
-  int64_t orow;
-  int d0;         // destination column of staging index 0 (16-byte aligned)
-  int xs0;        // x of staging index 0
-  int mlo, mhi;   // columns left to plain stores
-  int tma;        // 1 = TMA row store
+struct RowInfo {  // per (destination, output row), shared memory, 16 B
+  int orow;       // row in the destination's [rows_total][W] view
+  int d0;         // destination column of staging index 0 (16-byte aligned); bit 30 = TMA row store
+  int mlo, mhi;   // columns [mlo, mhi) left to plain stores
 };
+constexpr int kTmaBit = 1 << 30;
 
 template <typename A, int R, int SIG>
 __device__ __forceinline__ void p2_body(const CUtensorMap* tm_scr0, const CUtensorMap* tm_scr1,
-                                        const CUtensorMap* tm0, const CUtensorMap* tm1, const P2Params& p,
-                                        const P2Slot& sl, int img, int j, int X) {
+                                        const CUtensorMap* tm0, const CUtensorMap* tm1, const CUtensorMap* tm0_box,
+                                        const P2Params& p, const P2Slot& sl, int img, int j, int X) {
   using S = Split<R>;
   constexpr int NW = S::nw;
+  constexpr int NT = NW * 32;
   constexpr int NR = 1 << R;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   A* buf = reinterpret_cast<A*>(smem_raw);
   unsigned char* tab = smem_raw + main_buf_bytes(R);
-  int* rowoff = reinterpret_cast<int*>(tab);               // [NR]
-  int* soff = rowoff + 64;                                 // [NR]
-  uint64_t* bar = reinterpret_cast<uint64_t*>(tab + 512);
-  RowInfo* info = reinterpret_cast<RowInfo*>(tab + 1024);  // [NR], 32 B each
+  int* rowoff = reinterpret_cast<int*>(tab);                  // [64]
+  int* soff = rowoff + 64;                                    // [2][64]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(tab + 768);
+  RowInfo* info = reinterpret_cast<RowInfo*>(tab + 1024);     // [2][NR], 16 B each
   const int TX = p.TX, box = TX + WO2;
   const int Xw = X - WO2;                        // window start: window index s <-> x = Xw + s
   const int Xa = SIG > 0 ? Xw : Xw - (WA - WC);  // x of input index e = 0
@@ -518,19 +556,57 @@ __device__ __forceinline__ void p2_body(const CUtensorMap* tm_scr0, const CUtens
   bool black = false;  // the whole window is outside every row's pattern support
   if (!p.range) black = SIG > 0 ? (Xw + WC - 1 < -tmax) : (Xw >= p.wc + tmax);
 
+  // ---- store plan per (destination, row): shift k, 16-byte aligned start, TMA or plain stores
+  for (int it = threadIdx.x; it < p.ndest * NR; it += NT) {
+    const int d = it / NR, tau = it - d * NR, t = t0 + tau;
+    const P2Dest& D = p.dest[d];
+    int vlo = sl.xbeg, vhi = sl.xend, k = 0;
+    if (p.range) {
+      vlo = __ldg(p.start_tab + t);
+      vhi = vlo + p.W;
+      if (D.shifted) k = (((p.W - __ldg(p.len_tab + t)) + 1) >> 1) - vlo;
+    } else if (D.shifted) {
+      k = SIG > 0 ? ceil_half(p.Hp + t) : ceil_half(p.Hp - t);
+    }
+    const int r = mod_pos(X + k, p.W) & 3;
+    const int xs0 = X - r;
+    const int d0 = mod_pos(xs0 + k, p.W);
+    RowInfo ri;
+    ri.orow = (int)((int64_t)img * D.rows_per_img + sl.qrow + sl.rbase + (int64_t)sl.rsign * t);
+    ri.d0 = d0;
+    ri.mlo = max(X, vlo);
+    ri.mhi = min(X + TX, vhi);
+    if (t == sl.skip) {
+      ri.mhi = ri.mlo;
+    } else if (!p.no_tma && xs0 >= vlo && xs0 + min(box, p.W - d0) <= vhi) {
+      ri.d0 |= kTmaBit;
+      ri.mlo = max(ri.mlo, xs0 + (p.W - d0));  // the wrapped remainder, if any
+    }
+    info[d * NR + tau] = ri;
+    soff[d * 64 + tau] = WO2 - r;
+  }
   if (!black) {
-    // scratch row t0 + i, column (x + sigma*j*i) - xlo1 for x = Xa + e; TMA from the aligned-down
-    // column, zero outside [0, xhi1 - xlo1) = outside what pass 1 wrote
     if (threadIdx.x < NR) rowoff[threadIdx.x] = (Xa + SIG * j * (int)threadIdx.x - sl.xlo1) & 3;
     if (threadIdx.x == 0) mbar_init(bar);
-    __syncthreads();
+  }
+  __syncthreads();
+
+  if (!black) {
+    // scratch row t0 + i, column (x + sigma*j*i) - xlo1 for x = Xa + e: TMA from the aligned-down
+    // column, zero outside [0, xhi1 - xlo1) = outside what pass 1 wrote. One lane, uniform loop.
+#if FHT_LOAD_LANES
     if (threadIdx.x < 32) {
       if (threadIdx.x == 0) mbar_expect_tx(bar, NR * (256 + 36) * 4);
       __syncwarp();
       const int64_t rbase = (int64_t)(img - p.img0) * p.scratch_img_rows + sl.srow0 + t0;
       for (int i = threadIdx.x; i < NR; i += 32) {
-        const int c0 = Xa + SIG * j * i - sl.xlo1;
-        const int a0 = c0 & ~3;
+#else
+    if (threadIdx.x == 0) {
+      mbar_expect_tx(bar, NR * (256 + 36) * 4);
+      const int64_t rbase = (int64_t)(img - p.img0) * p.scratch_img_rows + sl.srow0 + t0;
+      for (int i = 0; i < NR; ++i) {
+#endif
+        const int a0 = (Xa + SIG * j * i - sl.xlo1) & ~3;
         A* d = buf + i * TMA_PITCH;
         tma_load_2d(tm_scr0, d, bar, a0, (int)(rbase + i));
         tma_load_2d(tm_scr1, d + 256, bar, a0 + 256, (int)(rbase + i));
@@ -544,62 +620,48 @@ __device__ __forceinline__ void p2_body(const CUtensorMap* tm_scr0, const CUtens
   bool issued = false;
   for (int d = 0; d < p.ndest; ++d) {
     const P2Dest& D = p.dest[d];
+    const RowInfo* inf = info + d * NR;
+    const int* so = soff + d * 64;
     if (d > 0) {
       if (issued) tma_wait_read();
       __syncthreads();
     }
-    if (threadIdx.x < NR) {
-      const int tau = threadIdx.x, t = t0 + tau;
-      int vlo = sl.xbeg, vhi = sl.xend, k = 0;
-      if (p.range) {
-        vlo = __ldg(p.start_tab + t);
-        vhi = vlo + p.W;
-        if (D.shifted) k = (((p.W - __ldg(p.len_tab + t)) + 1) >> 1) - vlo;
-      } else if (D.shifted) {
-        k = SIG > 0 ? ceil_half(p.Hp + t) : ceil_half(p.Hp - t);
-      }
-      const int r = mod_pos(X + k, p.W) & 3;
-      const int xs0 = X - r;
-      const int d0 = mod_pos(xs0 + k, p.W);
-      soff[tau] = WO2 - r;
-      RowInfo ri;
-      ri.orow = (int64_t)img * D.rows_per_img + sl.qrow + sl.rbase + (int64_t)sl.rsign * t;
-      ri.d0 = d0;
-      ri.xs0 = xs0;
-      ri.mlo = max(X, vlo);
-      ri.mhi = min(X + TX, vhi);
-      ri.tma = 0;
-      if (t == sl.skip) {
-        ri.mhi = ri.mlo;
-      } else if (!p.no_tma && xs0 >= vlo && xs0 + min(box, p.W - d0) <= vhi) {
-        ri.tma = 1;
-        ri.mlo = max(ri.mlo, xs0 + (p.W - d0));  // the wrapped remainder, if any
-      }
-      info[tau] = ri;
-    }
-    __syncthreads();
+    // plain destination of an interior QUADS tile: every row has the same aligned start and no
+    // remainder, rows ascend -> ONE 2-D box {box, NR} from a dense [NR][box] staging plane
+    const bool dense = FHT_P2_DENSE && !p.range && !D.shifted && sl.rsign == 1 && (sl.skip < t0 || sl.skip > tmax) &&
+                       (inf[0].d0 & kTmaBit) && inf[0].mlo >= inf[0].mhi;
+    const int pitch = dense ? box : ST_PITCH;
     if (!black) {
-      stage_rows<R, SIG, A>(w, buf, soff, box);
+      stage_rows<R, SIG, A>(w, buf, so, box, pitch);
     } else {  // every output of a black tile is 0 (no pattern touches a pixel)
-      for (int idx = threadIdx.x; idx < NR * ST_PITCH; idx += S::nw * 32) buf[idx] = A(0);
+      for (int idx = threadIdx.x; idx < NR * pitch; idx += NT) buf[idx] = A(0);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncthreads();
     }
-    if (threadIdx.x < NR && info[threadIdx.x].tma) {
-      const RowInfo& ri = info[threadIdx.x];
-      tma_store_row(d == 0 ? tm0 : tm1, buf + threadIdx.x * ST_PITCH, ri.d0, (int)ri.orow);  // clipped at W
-      tma_commit();
-      issued = true;
-    }
-    for (int tau = warp; tau < NR; tau += NW) {
-      const RowInfo ri = info[tau];
-      if (ri.mlo >= ri.mhi) continue;
-      A* drow = static_cast<A*>(D.ptr) + ri.orow * D.pitch;
-      const A* srow = buf + tau * ST_PITCH;
-      for (int x = ri.mlo + lane; x < ri.mhi; x += 32) {
-        int col = ri.d0 + (x - ri.xs0);
-        if (col >= p.W) col -= p.W;
-        __stcs(drow + col, srow[x - ri.xs0]);
+    if (dense) {
+      if (threadIdx.x == 0) {
+        tma_store_row(tm0_box, buf, inf[0].d0 & ~kTmaBit, inf[0].orow);  // box {box, NR}
+        tma_commit();
+        issued = true;
+      }
+    } else {
+      if (threadIdx.x < NR && (inf[threadIdx.x].d0 & kTmaBit)) {  // one row store per thread
+        const RowInfo ri = inf[threadIdx.x];
+        tma_store_row(d == 0 ? tm0 : tm1, buf + threadIdx.x * ST_PITCH, ri.d0 & ~kTmaBit, ri.orow);  // clipped at W
+        tma_commit();
+        issued = true;
+      }
+      for (int tau = warp; tau < NR; tau += NW) {
+        const RowInfo ri = inf[tau];
+        if (ri.mlo >= ri.mhi) continue;
+        A* drow = static_cast<A*>(D.ptr) + (int64_t)ri.orow * D.pitch;
+        const A* srow = buf + tau * ST_PITCH;
+        const int xs0 = X - (WO2 - so[tau]), d0 = ri.d0 & ~kTmaBit;
+        for (int x = ri.mlo + lane; x < ri.mhi; x += 32) {
+          int col = d0 + (x - xs0);
+          if (col >= p.W) col -= p.W;
+          __stcs(drow + col, srow[x - xs0]);
+        }
       }
     }
   }
@@ -607,11 +669,12 @@ __device__ __forceinline__ void p2_body(const CUtensorMap* tm_scr0, const CUtens
 }
 
 // tm_scr0: scratch, one row x 256 columns; tm_scr1: one row x 36 columns; tm0 / tm1: destinations
+// (one-row boxes); tm0_box: destination 0 with box {TX + 4, 2^R} (dense interior tiles)
 template <typename A, int R>
 __global__ void __launch_bounds__(Split<R>::nw * 32, kMinBlocks<R>)
 k_p2(const __grid_constant__ CUtensorMap tm_scr0, const __grid_constant__ CUtensorMap tm_scr1,
      const __grid_constant__ CUtensorMap tm0, const __grid_constant__ CUtensorMap tm1,
-     const __grid_constant__ P2Params p) {
+     const __grid_constant__ CUtensorMap tm0_box, const __grid_constant__ P2Params p) {
   // flat grid, tile fastest: CTAs running together read overlapping scratch rows (L2 reuse of
   // the 72-column halo and of the sheared rows of one group)
   int id = blockIdx.x;
@@ -624,8 +687,8 @@ k_p2(const __grid_constant__ CUtensorMap tm_scr0, const __grid_constant__ CUtens
   const P2Slot& sl = p.slot[qi];
   if (n >= sl.ntiles) return;
   const int X = min(sl.xbeg + p.TX * n, sl.xend - p.TX);
-  if (sl.sigma > 0) p2_body<A, R, 1>(&tm_scr0, &tm_scr1, &tm0, &tm1, p, sl, img, j, X);
-  else p2_body<A, R, -1>(&tm_scr0, &tm_scr1, &tm0, &tm1, p, sl, img, j, X);
+  if (sl.sigma > 0) p2_body<A, R, 1>(&tm_scr0, &tm_scr1, &tm0, &tm1, &tm0_box, p, sl, img, j, X);
+  else p2_body<A, R, -1>(&tm_scr0, &tm_scr1, &tm0, &tm1, &tm0_box, p, sl, img, j, X);
 }
 
 }  // namespace v2

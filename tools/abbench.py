@@ -75,7 +75,12 @@ def main():
         for lib in libs:
             for cid in cfgs:
                 env = dict(os.environ, FHT_LIB=os.path.abspath(lib), ROOT=ROOT)
-                out = subprocess.run([sys.executable, "-c", CHILD, str(cid)], env=env, capture_output=True, text=True)
+                try:
+                    out = subprocess.run([sys.executable, "-c", CHILD, str(cid)], env=env, capture_output=True,
+                                         text=True, timeout=180)
+                except subprocess.TimeoutExpired:
+                    print("TIMEOUT", lib, cid)
+                    continue
                 try:
                     d = json.loads(out.stdout.strip().splitlines()[-1])
                 except Exception:
