@@ -423,7 +423,15 @@ int run_orientation(const fht_image* img, const Frame& f, const Slot* slots, int
         s.xbeg = s.sigma > 0 ? -f.Hp : 0;
         s.xend = s.xbeg + p2.W;
       }
-      s.ntiles = (s.xend - s.xbeg + p2.TX - 1) / p2.TX;
+      // sigma = +1 rows wrap at x = 0 (x < 0 is stored at x + W): no tile straddles it
+      s.xmid = (!rg && s.sigma > 0 && s.xbeg < 0 && s.xend > 0) ? 0 : s.xbeg;
+      auto part_tiles = [&](int lo, int hi) {
+        if (hi <= lo) return 0;
+        const int boxw = p2.TX + v2::WO2;
+        return hi - lo <= boxw ? 1 : 1 + (hi - lo - boxw + p2.TX - 1) / p2.TX;
+      };
+      s.ntiles_a = part_tiles(s.xbeg, s.xmid);
+      s.ntiles = s.ntiles_a + part_tiles(s.xmid, s.xend);
       ntile2 = s.ntiles > ntile2 ? s.ntiles : ntile2;
       s.qrow = slots[q].qrow;
       s.rbase = slots[q].row_base;

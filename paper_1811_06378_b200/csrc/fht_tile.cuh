@@ -43,9 +43,6 @@
 #ifndef FHT_STAGE_ASM
 #define FHT_STAGE_ASM 1   // staging: explicitly predicated st.shared (1) or C++ if (0)
 #endif
-#ifndef FHT_LOAD_LANES
-#define FHT_LOAD_LANES 1  // pass-2 TMA row loads issued by 32 lanes (1) or one thread (0)
-#endif
 #ifndef FHT_P2_DENSE
 #define FHT_P2_DENSE 1    // pass-2 plain destination of interior tiles as one 2-D box (1)
 #endif
@@ -240,6 +237,13 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 __device__ __forceinline__ void tma_store_row(const CUtensorMap* map, const void* smem, int col, int row) {
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];"
                :: "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(smem)), "r"(col), "r"(row) : "memory");
+}
+// Hough rows are never re-read: evict-first keeps the L2 for the pass-1 scratch
+__device__ __forceinline__ void tma_store_row_stream(const CUtensorMap* map, const void* smem, int col, int row) {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%2, %3}], [%1], %4;"
+               :: "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(smem)), "r"(col), "r"(row), "l"(pol) : "memory");
 }
 __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* smem, int c0, int c1, int c2) {
   asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];"
@@ -496,6 +500,8 @@ struct P2Slot {
   int xlo1, xhi1;    // pass-1 columns: F_m[i][j](x') stored for x' in [xlo1, xhi1)
   int64_t srow0;
   int xbeg, xend;    // output signed column range covered by tiles (width W, or range span)
+  int xmid;          // tiles never straddle xmid (the cyclic wrap x = 0 of sigma = +1 rows)
+  int ntiles_a;      // tiles in [xbeg, xmid); the rest tile [xmid, xend)
   int ntiles;
   int64_t qrow;      // output row (in the [rows_total][W] view) of quadrant row 0, per image
   int rbase, rsign, skip;  // output row = qrow + rbase + rsign*t; t == skip not stored
@@ -534,7 +540,7 @@ constexpr int kTmaBit = 1 << 30;
 template <typename A, int R, int SIG>
 __device__ __forceinline__ void p2_body(const CUtensorMap* tm_scr0, const CUtensorMap* tm_scr1,
                                         const CUtensorMap* tm0, const CUtensorMap* tm1, const CUtensorMap* tm0_box,
-                                        const P2Params& p, const P2Slot& sl, int img, int j, int X) {
+                                        const P2Params& p, const P2Slot& sl, int img, int j, int X, int own) {
   using S = Split<R>;
   constexpr int NW = S::nw;
   constexpr int NT = NW * 32;
@@ -556,6 +562,21 @@ __device__ __forceinline__ void p2_body(const CUtensorMap* tm_scr0, const CUtens
   bool black = false;  // the whole window is outside every row's pattern support
   if (!p.range) black = SIG > 0 ? (Xw + WC - 1 < -tmax) : (Xw >= p.wc + tmax);
 
+  // ---- scratch rows t0 + i, column (x + sigma*j*i) - xlo1 for x = Xa + e: TMA from the
+  // aligned-down column, zero outside [0, xhi1 - xlo1) = outside what pass 1 wrote. Issued first,
+  // by one thread, so the loads are in flight while the CTA plans its stores.
+  if (!black && threadIdx.x == 0) {
+    mbar_init(bar);
+    mbar_expect_tx(bar, NR * (256 + 36) * 4);
+    const int64_t rbase = (int64_t)(img - p.img0) * p.scratch_img_rows + sl.srow0 + t0;
+    for (int i = 0; i < NR; ++i) {
+      const int a0 = (Xa + SIG * j * i - sl.xlo1) & ~3;
+      A* d = buf + i * TMA_PITCH;
+      tma_load_2d(tm_scr0, d, bar, a0, (int)(rbase + i));
+      tma_load_2d(tm_scr1, d + 256, bar, a0 + 256, (int)(rbase + i));
+    }
+  }
+
   // ---- store plan per (destination, row): shift k, 16-byte aligned start, TMA or plain stores
   for (int it = threadIdx.x; it < p.ndest * NR; it += NT) {
     const int d = it / NR, tau = it - d * NR, t = t0 + tau;
@@ -575,43 +596,20 @@ __device__ __forceinline__ void p2_body(const CUtensorMap* tm_scr0, const CUtens
     ri.orow = (int)((int64_t)img * D.rows_per_img + sl.qrow + sl.rbase + (int64_t)sl.rsign * t);
     ri.d0 = d0;
     ri.mlo = max(X, vlo);
-    ri.mhi = min(X + TX, vhi);
+    ri.mhi = min(X + own, vhi);
     if (t == sl.skip) {
       ri.mhi = ri.mlo;
     } else if (!p.no_tma && xs0 >= vlo && xs0 + min(box, p.W - d0) <= vhi) {
       ri.d0 |= kTmaBit;
-      ri.mlo = max(ri.mlo, xs0 + (p.W - d0));  // the wrapped remainder, if any
+      ri.mlo = max(ri.mlo, xs0 + min(box, p.W - d0));  // what the box does not cover (wrap, tile end)
     }
     info[d * NR + tau] = ri;
     soff[d * 64 + tau] = WO2 - r;
   }
-  if (!black) {
-    if (threadIdx.x < NR) rowoff[threadIdx.x] = (Xa + SIG * j * (int)threadIdx.x - sl.xlo1) & 3;
-    if (threadIdx.x == 0) mbar_init(bar);
-  }
+  if (!black && threadIdx.x < NR) rowoff[threadIdx.x] = (Xa + SIG * j * (int)threadIdx.x - sl.xlo1) & 3;
   __syncthreads();
 
   if (!black) {
-    // scratch row t0 + i, column (x + sigma*j*i) - xlo1 for x = Xa + e: TMA from the aligned-down
-    // column, zero outside [0, xhi1 - xlo1) = outside what pass 1 wrote. One lane, uniform loop.
-#if FHT_LOAD_LANES
-    if (threadIdx.x < 32) {
-      if (threadIdx.x == 0) mbar_expect_tx(bar, NR * (256 + 36) * 4);
-      __syncwarp();
-      const int64_t rbase = (int64_t)(img - p.img0) * p.scratch_img_rows + sl.srow0 + t0;
-      for (int i = threadIdx.x; i < NR; i += 32) {
-#else
-    if (threadIdx.x == 0) {
-      mbar_expect_tx(bar, NR * (256 + 36) * 4);
-      const int64_t rbase = (int64_t)(img - p.img0) * p.scratch_img_rows + sl.srow0 + t0;
-      for (int i = 0; i < NR; ++i) {
-#endif
-        const int a0 = (Xa + SIG * j * i - sl.xlo1) & ~3;
-        A* d = buf + i * TMA_PITCH;
-        tma_load_2d(tm_scr0, d, bar, a0, (int)(rbase + i));
-        tma_load_2d(tm_scr1, d + 256, bar, a0 + 256, (int)(rbase + i));
-      }
-    }
     mbar_wait0(bar);
     tile_fht<R, SIG, A>(static_cast<const A*>(buf), TMA_PITCH, rowoff, buf, TMA_PITCH, w);
   }
@@ -632,7 +630,7 @@ __device__ __forceinline__ void p2_body(const CUtensorMap* tm_scr0, const CUtens
                        (inf[0].d0 & kTmaBit) && inf[0].mlo >= inf[0].mhi;
     const int pitch = dense ? box : ST_PITCH;
     if (!black) {
-      stage_rows<R, SIG, A>(w, buf, so, box, pitch);
+      stage_rows<R, SIG, A>(w, buf, so, pitch, pitch);  // every computed column that fits the row
     } else {  // every output of a black tile is 0 (no pattern touches a pixel)
       for (int idx = threadIdx.x; idx < NR * pitch; idx += NT) buf[idx] = A(0);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -640,14 +638,14 @@ __device__ __forceinline__ void p2_body(const CUtensorMap* tm_scr0, const CUtens
     }
     if (dense) {
       if (threadIdx.x == 0) {
-        tma_store_row(tm0_box, buf, inf[0].d0 & ~kTmaBit, inf[0].orow);  // box {box, NR}
+        tma_store_row_stream(tm0_box, buf, inf[0].d0 & ~kTmaBit, inf[0].orow);  // box {box, NR}
         tma_commit();
         issued = true;
       }
     } else {
       if (threadIdx.x < NR && (inf[threadIdx.x].d0 & kTmaBit)) {  // one row store per thread
         const RowInfo ri = inf[threadIdx.x];
-        tma_store_row(d == 0 ? tm0 : tm1, buf + threadIdx.x * ST_PITCH, ri.d0 & ~kTmaBit, ri.orow);  // clipped at W
+        tma_store_row_stream(d == 0 ? tm0 : tm1, buf + threadIdx.x * ST_PITCH, ri.d0 & ~kTmaBit, ri.orow);  // clipped at W
         tma_commit();
         issued = true;
       }
@@ -686,9 +684,15 @@ k_p2(const __grid_constant__ CUtensorMap tm_scr0, const __grid_constant__ CUtens
   const int img = p.img0 + id / p.nq;
   const P2Slot& sl = p.slot[qi];
   if (n >= sl.ntiles) return;
-  const int X = min(sl.xbeg + p.TX * n, sl.xend - p.TX);
-  if (sl.sigma > 0) p2_body<A, R, 1>(&tm_scr0, &tm_scr1, &tm0, &tm1, &tm0_box, p, sl, img, j, X);
-  else p2_body<A, R, -1>(&tm_scr0, &tm_scr1, &tm0, &tm1, &tm0_box, p, sl, img, j, X);
+  // tile n of part [lo, hi): X = lo + TX*k, owning TX columns; the last tile of a part sits at
+  // hi - (TX + 4) and owns the rest, so its 16-byte aligned store box ends inside the part
+  const bool pa = n < sl.ntiles_a;
+  const int lo = pa ? sl.xbeg : sl.xmid, hi = pa ? sl.xmid : sl.xend;
+  const int k = pa ? n : n - sl.ntiles_a, nk = pa ? sl.ntiles_a : sl.ntiles - sl.ntiles_a;
+  const int X = k + 1 < nk ? lo + p.TX * k : max(lo, hi - (p.TX + WO2));
+  const int own = k + 1 < nk ? p.TX : hi - X;
+  if (sl.sigma > 0) p2_body<A, R, 1>(&tm_scr0, &tm_scr1, &tm0, &tm1, &tm0_box, p, sl, img, j, X, own);
+  else p2_body<A, R, -1>(&tm_scr0, &tm_scr1, &tm0, &tm1, &tm0_box, p, sl, img, j, X, own);
 }
 
 }  // namespace v2
