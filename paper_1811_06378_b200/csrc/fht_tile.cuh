@@ -91,6 +91,55 @@ __host__ __device__ constexpr size_t p2_smem_bytes(int R) {
 // shift t of the 2^NB-row block. Partner columns beyond the lane come from lane+1 (shfl_down);
 // valid for lanes 0..30 when 2^NB - 1 <= V.
 // ------------------------------------------------------------------------------------------
+// ------------------------------------------------------------------------------------------
+// TMA / mbarrier helpers (SASS: UTMALDG / UTMASTG, SYNCS)
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void tma_store_row(const CUtensorMap* map, const void* smem, int col, int row) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];"
+               :: "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(smem)), "r"(col), "r"(row) : "memory");
+}
+// Hough rows are never re-read: evict-first keeps the L2 for the pass-1 scratch
+__device__ __forceinline__ void tma_store_row_stream(const CUtensorMap* map, const void* smem, int col, int row) {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%2, %3}], [%1], %4;"
+               :: "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(smem)), "r"(col), "r"(row), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* smem, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];"
+               :: "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(smem)), "r"(c0), "r"(c1), "r"(c2) : "memory");
+}
+__device__ __forceinline__ void tma_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void tma_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, void* smem, uint64_t* bar, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
+               :: "r"(smem_u32(smem)), "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(const CUtensorMap* map, void* smem, uint64_t* bar, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];"
+               :: "r"(smem_u32(smem)), "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1),
+                  "r"(c2)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(smem_u32(bar)));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait0(uint64_t* bar) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(done) : "r"(smem_u32(bar)) : "memory");
+  }
+}
+
 template <int NB, int V, int K, typename A>
 struct Level {
   static __device__ __forceinline__ void run(A (&v)[1 << NB][V]) {
@@ -139,7 +188,7 @@ __device__ __forceinline__ void warp_fht(A (&v)[1 << NB][V]) {
 // ------------------------------------------------------------------------------------------
 template <int R, int SIG, typename A, typename Tsrc>
 __device__ __forceinline__ void tile_fht(const Tsrc* src, int src_pitch, const int* rowoff, A* fa, int fa_pitch,
-                                         A (&w)[kTPW<R>][1 << Split<R>::b][VB]) {
+                                         A (&w)[kTPW<R>][1 << Split<R>::b][VB], uint64_t* blk_bars = nullptr) {
   using S = Split<R>;
   constexpr int a = S::a, b = S::b, NW = S::nw;
   constexpr int NA = 1 << a, NBk = 1 << b;
@@ -148,6 +197,7 @@ __device__ __forceinline__ void tile_fht(const Tsrc* src, int src_pitch, const i
   // sub-pass A: block blk = rows blk*2^a .. +2^a-1 -> fa row blk*2^a + j' = F_a[blk][j']
 #pragma unroll 1
   for (int blk = warp; blk < NBk; blk += NW) {
+    if (blk_bars) mbar_wait0(blk_bars + blk);  // this block's rows have landed (TMA)
     A v[NA][VA];
 #pragma unroll
     for (int r = 0; r < NA; ++r) {
@@ -231,52 +281,6 @@ __device__ __forceinline__ void stage_rows(A (&w)[kTPW<R>][1 << Split<R>::b][VB]
 // ------------------------------------------------------------------------------------------
 // TMA / mbarrier helpers (SASS: UTMALDG / UTMASTG, SYNCS)
 // ------------------------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void tma_store_row(const CUtensorMap* map, const void* smem, int col, int row) {
-  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];"
-               :: "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(smem)), "r"(col), "r"(row) : "memory");
-}
-// Hough rows are never re-read: evict-first keeps the L2 for the pass-1 scratch
-__device__ __forceinline__ void tma_store_row_stream(const CUtensorMap* map, const void* smem, int col, int row) {
-  uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%2, %3}], [%1], %4;"
-               :: "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(smem)), "r"(col), "r"(row), "l"(pol) : "memory");
-}
-__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* smem, int c0, int c1, int c2) {
-  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];"
-               :: "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(smem)), "r"(c0), "r"(c1), "r"(c2) : "memory");
-}
-__device__ __forceinline__ void tma_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void tma_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
-__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, void* smem, uint64_t* bar, int c0, int c1) {
-  asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
-               :: "r"(smem_u32(smem)), "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
-               : "memory");
-}
-__device__ __forceinline__ void tma_load_3d(const CUtensorMap* map, void* smem, uint64_t* bar, int c0, int c1, int c2) {
-  asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];"
-               :: "r"(smem_u32(smem)), "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1),
-                  "r"(c2)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(smem_u32(bar)));
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait0(uint64_t* bar) {
-  uint32_t done = 0;
-  while (!done) {
-    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
-                 : "=r"(done) : "r"(smem_u32(bar)) : "memory");
-  }
-}
-
 __device__ __forceinline__ int mod_pos(int v, int W) {
   int r = v % W;
   return r < 0 ? r + W : r;
@@ -550,7 +554,7 @@ __device__ __forceinline__ void p2_body(const CUtensorMap* tm_scr0, const CUtens
   unsigned char* tab = smem_raw + main_buf_bytes(R);
   int* rowoff = reinterpret_cast<int*>(tab);                  // [64]
   int* soff = rowoff + 64;                                    // [2][64]
-  uint64_t* bar = reinterpret_cast<uint64_t*>(tab + 768);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(tab + 768);     // [8] per-block mbarriers
   RowInfo* info = reinterpret_cast<RowInfo*>(tab + 1024);     // [2][NR], 16 B each
   const int TX = p.TX, box = TX + WO2;
   const int Xw = X - WO2;                        // window start: window index s <-> x = Xw + s
@@ -565,15 +569,18 @@ __device__ __forceinline__ void p2_body(const CUtensorMap* tm_scr0, const CUtens
   // ---- scratch rows t0 + i, column (x + sigma*j*i) - xlo1 for x = Xa + e: TMA from the
   // aligned-down column, zero outside [0, xhi1 - xlo1) = outside what pass 1 wrote. Issued first,
   // by one thread, so the loads are in flight while the CTA plans its stores.
+  constexpr int NA = 1 << S::a, NBk = 1 << S::b;  // sub-pass A blocks: one mbarrier each
   if (!black && threadIdx.x == 0) {
-    mbar_init(bar);
-    mbar_expect_tx(bar, NR * (256 + 36) * 4);
+    for (int b = 0; b < NBk; ++b) mbar_init(bar + b);
     const int64_t rbase = (int64_t)(img - p.img0) * p.scratch_img_rows + sl.srow0 + t0;
-    for (int i = 0; i < NR; ++i) {
-      const int a0 = (Xa + SIG * j * i - sl.xlo1) & ~3;
-      A* d = buf + i * TMA_PITCH;
-      tma_load_2d(tm_scr0, d, bar, a0, (int)(rbase + i));
-      tma_load_2d(tm_scr1, d + 256, bar, a0 + 256, (int)(rbase + i));
+    for (int b = 0; b < NBk; ++b) {
+      mbar_expect_tx(bar + b, NA * (256 + 36) * 4);
+      for (int i = b * NA; i < (b + 1) * NA; ++i) {
+        const int a0 = (Xa + SIG * j * i - sl.xlo1) & ~3;
+        A* d = buf + i * TMA_PITCH;
+        tma_load_2d(tm_scr0, d, bar + b, a0, (int)(rbase + i));
+        tma_load_2d(tm_scr1, d + 256, bar + b, a0 + 256, (int)(rbase + i));
+      }
     }
   }
 
@@ -609,10 +616,7 @@ __device__ __forceinline__ void p2_body(const CUtensorMap* tm_scr0, const CUtens
   if (!black && threadIdx.x < NR) rowoff[threadIdx.x] = (Xa + SIG * j * (int)threadIdx.x - sl.xlo1) & 3;
   __syncthreads();
 
-  if (!black) {
-    mbar_wait0(bar);
-    tile_fht<R, SIG, A>(static_cast<const A*>(buf), TMA_PITCH, rowoff, buf, TMA_PITCH, w);
-  }
+  if (!black) tile_fht<R, SIG, A>(static_cast<const A*>(buf), TMA_PITCH, rowoff, buf, TMA_PITCH, w, bar);
 
   // ---- stores, one destination at a time (the staging plane is reused)
   bool issued = false;
