@@ -15,6 +15,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <utility>
 
 #include "../../include/fht.h"
 #include "fht_kernels.cuh"
@@ -250,6 +251,23 @@ cudaError_t launch_pass2(int logr, dim3 grid, const Pass2Args& a, cudaStream_t s
 }
 
 // ---------------------------------------------------------------- v2 launch helpers
+// Launch with programmatic stream serialization (PDL): the kernel may be scheduled while its
+// predecessor in the stream drains; it calls griddepcontrol.wait before touching memory.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = FHT_PDL;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 struct P1Maps {
   CUtensorMap img0, img1, scr;
 };
@@ -259,8 +277,7 @@ cudaError_t launch_p1_t(dim3 grid, const P1Maps& m, const v2::P1Params& a, cudaS
   static const cudaError_t attr =
       cudaFuncSetAttribute(v2::k_p1<Tin, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (attr != cudaSuccess) return attr;
-  v2::k_p1<Tin, R><<<grid, v2::Split<R>::nw * 32, smem, st>>>(m.img0, m.img1, m.scr, a);
-  return cudaGetLastError();
+  return launch_pdl(v2::k_p1<Tin, R>, grid, dim3(v2::Split<R>::nw * 32), smem, st, m.img0, m.img1, m.scr, a);
 }
 template <typename Tin>
 cudaError_t launch_p1(int r, dim3 grid, const P1Maps& m, const v2::P1Params& a, cudaStream_t st) {
@@ -283,8 +300,8 @@ cudaError_t launch_p2_t(dim3 grid, const P2Maps& m, const v2::P2Params& a, cudaS
   static const cudaError_t attr =
       cudaFuncSetAttribute(v2::k_p2<A, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (attr != cudaSuccess) return attr;
-  v2::k_p2<A, R><<<grid, v2::Split<R>::nw * 32, smem, st>>>(m.scr0, m.scr1, m.out0, m.out1, m.out0_box, a);
-  return cudaGetLastError();
+  return launch_pdl(v2::k_p2<A, R>, grid, dim3(v2::Split<R>::nw * 32), smem, st, m.scr0, m.scr1, m.out0, m.out1,
+                    m.out0_box, a);
 }
 template <typename A>
 cudaError_t launch_p2(int r, dim3 grid, const P2Maps& m, const v2::P2Params& a, cudaStream_t st) {

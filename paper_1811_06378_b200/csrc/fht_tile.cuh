@@ -47,8 +47,26 @@
 #define FHT_P2_DENSE 1    // pass-2 plain destination of interior tiles as one 2-D box (1)
 #endif
 
+#ifndef FHT_PDL
+#define FHT_PDL 1         // programmatic dependent launch between the passes (griddepcontrol)
+#endif
+
 namespace fht {
 namespace v2 {
+
+// Programmatic dependent launch (PDL): a kernel launched with programmatic stream serialization
+// may start while its predecessor drains; griddepcontrol.wait blocks until the predecessor grid
+// has completed and its memory is visible, launch_dependents lets the successor be scheduled.
+__device__ __forceinline__ void pdl_wait() {
+#if FHT_PDL
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+__device__ __forceinline__ void pdl_trigger() {
+#if FHT_PDL
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
 
 constexpr int VA = 9;            // local columns per lane, sub-pass A (odd => conflict-free)
 constexpr int VB = 7;            // local columns per lane, sub-pass B (odd => conflict-free)
@@ -341,8 +359,9 @@ __device__ __noinline__ void p1_tail(const CUtensorMap* tm_scr, const P1Params& 
     const int z = (img - p.img0) * p.nq + (int)(sl.srow0 >> (R + p.L));
     tma_store_3d(tm_scr, buf, X - sl.xlo, strip, z << R);
     tma_commit();
-    tma_wait_read();
   }
+  pdl_trigger();
+  if (threadIdx.x == 0) tma_wait_read();
 }
 
 template <typename Tin, int R, typename Tsrc>
@@ -481,6 +500,7 @@ template <typename Tin, int R>
 __global__ void __launch_bounds__(Split<R>::nw * 32, kMinBlocks<R>)
 k_p1(const __grid_constant__ CUtensorMap tm_img0, const __grid_constant__ CUtensorMap tm_img1,
      const __grid_constant__ CUtensorMap tm_scr, const __grid_constant__ P1Params p) {
+  pdl_wait();  // the image may come from the previous kernel; the scratch may still be read by it
   // flat grid, quadrant slot fastest: with 148 SMs (a multiple of 4) the round-robin CTA
   // placement gives every SM CTAs of one slot, i.e. one sign and one fill path (I-cache locality)
   int id = blockIdx.x;
@@ -667,6 +687,7 @@ __device__ __forceinline__ void p2_body(const CUtensorMap* tm_scr0, const CUtens
       }
     }
   }
+  pdl_trigger();
   if (issued) tma_wait_read();
 }
 
@@ -677,6 +698,7 @@ __global__ void __launch_bounds__(Split<R>::nw * 32, kMinBlocks<R>)
 k_p2(const __grid_constant__ CUtensorMap tm_scr0, const __grid_constant__ CUtensorMap tm_scr1,
      const __grid_constant__ CUtensorMap tm0, const __grid_constant__ CUtensorMap tm1,
      const __grid_constant__ CUtensorMap tm0_box, const __grid_constant__ P2Params p) {
+  pdl_wait();  // pass 1 (the predecessor) has written the scratch
   // flat grid, tile fastest: CTAs running together read overlapping scratch rows (L2 reuse of
   // the 72-column halo and of the sheared rows of one group)
   int id = blockIdx.x;

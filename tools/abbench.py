@@ -49,11 +49,21 @@ for i in range(steps):
     step(evs[i])
 torch.cuda.synchronize()
 tot = statistics.mean(evs[i][0].elapsed_time(evs[i][n]) for i in range(steps))
+# whole-step time with NO events between the kernels (programmatic dependent launch can overlap)
+e0 = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+e1 = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+for i in range(steps):
+    flush.zero_()
+    e0[i].record()
+    step()
+    e1[i].record()
+torch.cuda.synchronize()
+whole = statistics.mean(e0[i].elapsed_time(e1[i]) for i in range(steps))
 ks = [statistics.mean(evs[i][k].elapsed_time(evs[i][k + 1]) for i in range(steps)) for k in range(n)]
 first = 1 if c["mode"] == "range" else 0
 p1 = sum(ks[k] for k in range(first, n) if (k - first) % 2 == 0)
 p2 = sum(ks[k] for k in range(first, n) if (k - first) % 2 == 1)
-print(json.dumps({"step_us": tot * 1e3, "p1_us": p1 * 1e3, "p2_us": p2 * 1e3}))
+print(json.dumps({"step_us": tot * 1e3, "p1_us": p1 * 1e3, "p2_us": p2 * 1e3, "whole_us": whole * 1e3}))
 '''
 
 
@@ -91,7 +101,7 @@ def main():
         m = {k: sum(d[k] for d in ds) / len(ds) for k in ds[0]}
         mn = {k: min(d[k] for d in ds) for k in ds[0]}
         print(f"C{cid} {os.path.basename(lib):28s} step {m['step_us']:9.1f} us (min {mn['step_us']:9.1f})  "
-              f"p1 {m['p1_us']:9.1f}  p2 {m['p2_us']:9.1f}")
+              f"p1 {m['p1_us']:9.1f}  p2 {m['p2_us']:9.1f}  | no inter-kernel events: {m['whole_us']:9.1f} us")
 
 
 if __name__ == "__main__":
