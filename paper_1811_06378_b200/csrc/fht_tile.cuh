@@ -616,9 +616,15 @@ __device__ __forceinline__ void p2_body(const CUtensorMap* tm_scr0, const CUtens
     } else if (D.shifted) {
       k = SIG > 0 ? ceil_half(p.Hp + t) : ceil_half(p.Hp - t);
     }
-    const int r = mod_pos(X + k, p.W) & 3;
+    // X in [xbeg, xend), k in [0, W): one conditional add/subtract replaces the modulo (range
+    // mode: k is arbitrary, keep the division)
+    int v = X + k;
+    if (p.range) v = mod_pos(v, p.W);
+    else { v += v < 0 ? p.W : 0; v -= v >= p.W ? p.W : 0; }
+    const int r = v & 3;
     const int xs0 = X - r;
-    const int d0 = mod_pos(xs0 + k, p.W);
+    int d0 = v - r;
+    d0 += d0 < 0 ? p.W : 0;
     RowInfo ri;
     ri.orow = (int)((int64_t)img * D.rows_per_img + sl.qrow + sl.rbase + (int64_t)sl.rsign * t);
     ri.d0 = d0;
