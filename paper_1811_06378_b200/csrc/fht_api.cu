@@ -984,10 +984,11 @@ int fht_angle_range(const fht_image* img, const fht_angle_plan* plan, fht_hough*
   ta.colmap = const_cast<int*>(rg.colmap);
   ta.start_tab = const_cast<int*>(rg.start_tab);
   ta.len_tab = const_cast<int*>(rg.len_tab);
-  const int nb_tab = f.Hp + (int)((std::max<int64_t>(img->h, plan->w_content) + kThreads - 1) / kThreads);
+  const int nb_tab = (f.Hp + kRangeRowsPerBlock - 1) / kRangeRowsPerBlock +
+                     (int)((std::max<int64_t>(img->h, plan->w_content) + kThreads - 1) / kThreads);
   LaunchLog log{opts, 0};
   log.before((cudaStream_t)stream);
-  k_range_tables<<<nb_tab, kThreads, 0, (cudaStream_t)stream>>>(ta);
+  k_range_tables<<<nb_tab, kThreads, (size_t)img->h * sizeof(int), (cudaStream_t)stream>>>(ta);
   if (cudaGetLastError() != cudaSuccess) return FHT_ERR_CUDA;
   log.after((cudaStream_t)stream);
   Slot sl{};

@@ -260,33 +260,58 @@ __device__ __forceinline__ int shear_e(double g, int y) {
   return (int)floor(__dadd_rn(__dmul_rn(g, (double)y), 0.5));
 }
 
+// Per output row s of the range frame: start_s = min_y (e_y - D_s(y)), len_s = max - min + w'
+// (R17). D_s(y) = sum over the set bits b of y of ceil((s >> (K-1-b)) / 2) (the closed form of
+// dyadic_offset) is additive over the bits. One warp per row: with y = 32k + lane the low 5 bits
+// are the lane (a per-lane constant) and the high bits are k (the same for the whole warp, from a
+// per-warp 128-entry table). The shear offsets e_y are computed once per block (shared memory).
+// Blocks [0, nsb) do kRangeRowsPerBlock rows with 8 warps; the remaining blocks write e_tab, colmap.
+constexpr int kRangeRowsPerBlock = 32;
 __global__ void k_range_tables(const RangeTableArgs a) {
-  const int b = blockIdx.x;
-  if (b < a.Hp) {  // one block per output row s: reduce e_y - D_s(y) over y < h
-    const int s = b;
-    int mn = INT32_MAX, mx = INT32_MIN;
-    for (int y = threadIdx.x; y < a.h; y += blockDim.x) {
-      const int v = shear_e(a.g, y) - dyadic_offset(a.K, s, y);
-      mn = min(mn, v);
-      mx = max(mx, v);
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-      mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-      mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    }
-    __shared__ int smn[32], smx[32];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (lane == 0) { smn[warp] = mn; smx[warp] = mx; }
+  extern __shared__ int e_s[];          // [h]
+  __shared__ int dh_s[8][128];          // per warp: D of the high bits, y >> 5
+  const int nsb = (a.Hp + kRangeRowsPerBlock - 1) / kRangeRowsPerBlock;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  if ((int)blockIdx.x < nsb) {
+    for (int y = threadIdx.x; y < a.h; y += blockDim.x) e_s[y] = shear_e(a.g, y);
     __syncthreads();
-    if (threadIdx.x == 0) {
-      for (int i = 1; i < (int)(blockDim.x >> 5); ++i) { mn = min(mn, smn[i]); mx = max(mx, smx[i]); }
-      a.start_tab[s] = mn;
-      a.len_tab[s] = mx - mn + a.w_content;
+    const int s_end = min(a.Hp, ((int)blockIdx.x + 1) * kRangeRowsPerBlock);
+    int* dh = dh_s[warp];
+    for (int s = blockIdx.x * kRangeRowsPerBlock + warp; s < s_end; s += nw) {
+      auto wbit = [&](int bit) { return bit < a.K ? ((s >> (a.K - 1 - bit)) + 1) >> 1 : 0; };
+      int dl = 0;  // bits 0..4 of y = lane
+      for (int b = 0; b < 5; ++b)
+        if ((lane >> b) & 1) dl += wbit(b);
+      for (int k = lane; k < 128; k += 32) {  // bits 5..11 of y = k
+        int d = 0;
+        for (int b = 0; b < 7; ++b)
+          if ((k >> b) & 1) d += wbit(5 + b);
+        dh[k] = d;
+      }
+      __syncwarp();
+      int mn = INT32_MAX, mx = INT32_MIN;
+      for (int k = 0; 32 * k < a.h; ++k) {
+        const int y = 32 * k + lane;
+        if (y < a.h) {
+          const int v = e_s[y] - dl - dh[k];
+          mn = min(mn, v);
+          mx = max(mx, v);
+        }
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      }
+      if (lane == 0) {
+        a.start_tab[s] = mn;
+        a.len_tab[s] = mx - mn + a.w_content;
+      }
+      __syncwarp();  // dh reused by the warp's next row
     }
     return;
   }
   // remaining blocks: e_y and colmap
-  const int idx = (b - a.Hp) * blockDim.x + threadIdx.x;
+  const int idx = ((int)blockIdx.x - nsb) * blockDim.x + threadIdx.x;
   if (idx < a.h) a.e_tab[idx] = shear_e(a.g, idx);
   if (idx < a.w_content) {
     const int c = (int)floor(__ddiv_rn((double)idx + 0.5, a.alpha));

@@ -423,22 +423,44 @@ __device__ __forceinline__ void p1_body(const CUtensorMap* tm_img0, const CUtens
     soff[threadIdx.x] = 0;
   }
   if (!sl.transposed) {
-    // ---- scalar fill (angle-range gather T(x, y) = I[y][colmap[x - e_y]], or odd pitches)
-#pragma unroll 4
-    for (int idx = threadIdx.x; idx < NR * WA; idx += NT) {
-      const int rho = idx / WA, e = idx - rho * WA;
-      const int y = y0 + rho, x = Xa + e;
-      A v = A(0);
-      if (y < p.img_h) {
-        if (!p.range) {
-          if (x >= 0 && x < p.img_w) v = static_cast<A>(__ldg(src + (int64_t)y * p.img_rstride + x));
-        } else {  // P:146; R13, R14
-          const int u = x - __ldg(p.e_tab + y);
-          if (u >= 0 && u < p.w_content)
-            v = static_cast<A>(__ldg(src + (int64_t)y * p.img_rstride + __ldg(p.colmap + u)));
+    // ---- scalar fill (angle-range gather T(x, y) = I[y][colmap[x - e_y]], or odd pitches), in
+    // batches of CH elements per thread: every gather of a batch is in flight before its stores
+    // (the colmap -> pixel chain is two dependent loads; 4 in flight per thread was latency-bound)
+    constexpr int ITS = (NR * WA + NT - 1) / NT;
+    constexpr int CH = ITS >= 12 ? 12 : ITS;
+#pragma unroll 1
+    for (int it0 = 0; it0 < ITS; it0 += CH) {
+      int cm[CH];
+      A v[CH];
+#pragma unroll
+      for (int c = 0; c < CH; ++c) {  // stage 1: colmap (range) or the column index itself
+        const int idx = threadIdx.x + (it0 + c) * NT;
+        const int rho = idx / WA, e = idx - rho * WA;
+        const int y = y0 + rho, x = Xa + e;
+        cm[c] = -1;
+        if (it0 + c < ITS && idx < NR * WA && y < p.img_h) {
+          if (!p.range) {
+            if (x >= 0 && x < p.img_w) cm[c] = x;
+          } else {  // P:146; R13, R14
+            const int u = x - __ldg(p.e_tab + y);
+            if (u >= 0 && u < p.w_content) cm[c] = __ldg(p.colmap + u);
+          }
         }
       }
-      buf[rho * FA_PITCH + e] = v;
+#pragma unroll
+      for (int c = 0; c < CH; ++c) {  // stage 2: the pixels
+        const int idx = threadIdx.x + (it0 + c) * NT;
+        const int rho = idx / WA;
+        v[c] = cm[c] >= 0 ? static_cast<A>(__ldg(src + (int64_t)(y0 + rho) * p.img_rstride + cm[c])) : A(0);
+      }
+#pragma unroll
+      for (int c = 0; c < CH; ++c) {  // stage 3: shared memory
+        const int idx = threadIdx.x + (it0 + c) * NT;
+        if (it0 + c < ITS && idx < NR * WA) {
+          const int rho = idx / WA, e = idx - rho * WA;
+          buf[rho * FA_PITCH + e] = v[c];
+        }
+      }
     }
   } else if (p.fill_vec && NR >= 4) {
     // ---- transposed: FHT row y = image column, FHT column x = image row. Thread = (x, 4 y's):
