@@ -128,8 +128,10 @@ def geometry(cfg_id, c):
     return in_b, cells, ndest
 
 
-def make_step(fht, cfg_id, c, t, outs, plan=None):
-    """step(events=None) -> kernel launches enqueued (all through the C ABI)."""
+def make_step(fht, cfg_id, c, t, outs, plan=None, aux=None):
+    """step(events=None) -> kernel launches enqueued (all through the C ABI). `aux`: the second
+    stream on which batched calls overlap pass 1 of the next chunk with pass 2 (not used while
+    per-kernel events are recorded)."""
     if c["mode"] == "quadrant":
         def step(events=None):
             outs["h"] = fht.quadrant(t, fht.QA, out=outs.get("h"), workspace=outs.get("ws"), events=events)
@@ -139,11 +141,12 @@ def make_step(fht, cfg_id, c, t, outs, plan=None):
         pair = cfg_id in (2, 5)
 
         def step(events=None):
+            a = None if events else aux
             if pair:
                 outs["h"], outs["s"] = fht.full(t, pair=True, out=outs.get("h"), out_shifted=outs.get("s"),
-                                                workspace=outs.get("ws"), events=events)
+                                                workspace=outs.get("ws"), events=events, aux_stream=a)
             else:
-                outs["h"] = fht.full(t, out=outs.get("h"), workspace=outs.get("ws"), events=events)
+                outs["h"] = fht.full(t, out=outs.get("h"), workspace=outs.get("ws"), events=events, aux_stream=a)
             return outs["h"].launches
         return step
 
@@ -285,8 +288,9 @@ def main():
             cells = cc["batch"] * plan.Hp * plan.W
         out_b = cells * 4 * ndest
         outs = {}
-        step = make_step(fht, cfg_id, cc, t, outs, plan)
-        n_launch = step()
+        aux = torch.cuda.Stream(device=dev)
+        step = make_step(fht, cfg_id, cc, t, outs, plan, aux)
+        n_launch = step(events=[])
         torch.cuda.synchronize()
         ws_bytes = 0
         flush = None

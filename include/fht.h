@@ -102,14 +102,21 @@ typedef struct {
   fht_angle_plan plan;                    /* valid iff mode == RANGE */
 } fht_hough;
 
-/* Optional per-call execution options (may be NULL). events: caller-created CUDA events
- * (cudaEvent_t cast to void*); when non-NULL the call records events[i] on `stream` right
- * before its i-th kernel launch and events[n] right after its last (n = the call's return
- * value), for i < n_events. Used by bench.py to time each kernel on the launching stream. */
+/* Optional per-call execution options (may be NULL).
+ *  events: caller-created CUDA events (cudaEvent_t cast to void*); when non-NULL the call records
+ *    events[i] on the launching stream right before its i-th kernel launch and events[n] right
+ *    after its last (n = the call's return value), for i < n_events. Used by bench.py to time
+ *    each kernel.
+ *  aux_stream: a second caller-owned stream (cudaStream_t, != stream) or NULL. When the batch is
+ *    processed in several scratch chunks, pass 1 of chunk k+1 runs on aux_stream concurrently
+ *    with pass 2 of chunk k on `stream` (two scratch buffers, ordered by events). The call is
+ *    still complete when `stream` reaches it; aux_stream is left with no pending work the caller
+ *    must wait for. fht_workspace_bytes() already includes the second buffer. */
 typedef struct {
   void* const* events;
   int32_t n_events;
   int32_t _pad0;
+  void* aux_stream;
 } fht_exec_opts;
 
 /* Fill `out` (except `data`) with the contiguous shape of the transform of `img`:

@@ -124,15 +124,19 @@ def _ptr(h):
     return ctypes.byref(h.desc) if h is not None else None
 
 
-def _opts(events):
-    """fht_exec_opts for a list of recorded torch.cuda.Event (timing hooks), or None."""
-    if not events:
+def _opts(events=None, aux_stream=None):
+    """fht_exec_opts for timing events (recorded torch.cuda.Event) and/or an auxiliary
+    torch.cuda.Stream for the pass-1 / pass-2 overlap of batched calls; None if neither."""
+    if not events and aux_stream is None:
         return None
-    arr = (ctypes.c_void_p * len(events))(*[ctypes.c_void_p(e.cuda_event) for e in events])
     o = _lib.FhtExecOpts()
-    o.events = ctypes.cast(arr, ctypes.POINTER(ctypes.c_void_p))
-    o.n_events = len(events)
-    o._keep = arr
+    if events:
+        arr = (ctypes.c_void_p * len(events))(*[ctypes.c_void_p(e.cuda_event) for e in events])
+        o.events = ctypes.cast(arr, ctypes.POINTER(ctypes.c_void_p))
+        o.n_events = len(events)
+        o._keep = arr
+    if aux_stream is not None:
+        o.aux_stream = aux_stream.cuda_stream
     return ctypes.byref(o)
 
 
@@ -147,7 +151,7 @@ def _finish(res, n, shifted, pair):
 
 def quadrant(t: torch.Tensor, q: int, pad: int | None = None, shifted: bool = False, pair: bool = False,
              workspace: torch.Tensor | None = None, out: HoughImage | None = None,
-             out_shifted: HoughImage | None = None, events=None):
+             out_shifted: HoughImage | None = None, events=None, aux_stream=None):
     """One quadrant (P:52-67). shifted=True returns fhtshift(H) written directly by the transform;
     pair=True returns (H, fhtshift(H)) from one pass."""
     img, t = _image(t)
@@ -156,13 +160,13 @@ def quadrant(t: torch.Tensor, q: int, pad: int | None = None, shifted: bool = Fa
     ws = _workspace(ws_n, t.device, workspace)
     n = _lib.check("fht_quadrant", _lib.lib.fht_quadrant(ctypes.byref(img), q, -1 if pad is None else pad,
                                                           _ptr(res[0]), _ptr(res[1]), ws.data_ptr(), ws_n,
-                                                          _stream(t), _opts(events)))
+                                                          _stream(t), _opts(events, aux_stream)))
     return _finish(res, n, shifted, pair)
 
 
 def full(t: torch.Tensor, layout: str = "quads", shifted: bool = False, pair: bool = False,
          workspace: torch.Tensor | None = None, out: HoughImage | None = None,
-         out_shifted: HoughImage | None = None, events=None):
+         out_shifted: HoughImage | None = None, events=None, aux_stream=None):
     """Full four-quadrant transform. See quadrant() for shifted / pair."""
     img, t = _image(t)
     lay = _LAYOUTS[layout]
@@ -170,7 +174,7 @@ def full(t: torch.Tensor, layout: str = "quads", shifted: bool = False, pair: bo
     ws_n = workspace_bytes(FHT_MODE_FULL, img)
     ws = _workspace(ws_n, t.device, workspace)
     n = _lib.check("fht_full", _lib.lib.fht_full(ctypes.byref(img), lay, _ptr(res[0]), _ptr(res[1]),
-                                                  ws.data_ptr(), ws_n, _stream(t), _opts(events)))
+                                                  ws.data_ptr(), ws_n, _stream(t), _opts(events, aux_stream)))
     return _finish(res, n, shifted, pair)
 
 
@@ -183,7 +187,7 @@ def angle_plan(h: int, w: int, theta_min_deg: float, theta_max_deg: float) -> Fh
 
 def angle_range(t: torch.Tensor, plan: FhtAnglePlan, shifted: bool = False, pair: bool = False,
                 workspace: torch.Tensor | None = None, out: HoughImage | None = None,
-                out_shifted: HoughImage | None = None, events=None):
+                out_shifted: HoughImage | None = None, events=None, aux_stream=None):
     """Angle-range-restricted transform. See quadrant() for shifted / pair."""
     img, t = _image(t)
     res = _descs(FHT_MODE_RANGE, img, plan, 0, 0, t.device, shifted, pair, out, out_shifted)
@@ -191,7 +195,7 @@ def angle_range(t: torch.Tensor, plan: FhtAnglePlan, shifted: bool = False, pair
     ws = _workspace(ws_n, t.device, workspace)
     n = _lib.check("fht_angle_range", _lib.lib.fht_angle_range(ctypes.byref(img), ctypes.byref(plan),
                                                                 _ptr(res[0]), _ptr(res[1]), ws.data_ptr(),
-                                                                ws_n, _stream(t), _opts(events)))
+                                                                ws_n, _stream(t), _opts(events, aux_stream)))
     return _finish(res, n, shifted, pair)
 
 

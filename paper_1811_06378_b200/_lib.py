@@ -59,7 +59,8 @@ class FhtHough(ctypes.Structure):
 
 
 class FhtExecOpts(ctypes.Structure):
-    _fields_ = [("events", ctypes.POINTER(ctypes.c_void_p)), ("n_events", ctypes.c_int32), ("_pad0", ctypes.c_int32)]
+    _fields_ = [("events", ctypes.POINTER(ctypes.c_void_p)), ("n_events", ctypes.c_int32), ("_pad0", ctypes.c_int32),
+                ("aux_stream", ctypes.c_void_p)]
 
 
 class FhtError(RuntimeError):

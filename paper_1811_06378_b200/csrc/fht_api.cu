@@ -165,7 +165,8 @@ struct ScratchPlan {
   int v2;
   int64_t pitch;       // elements
   int chunk;
-  size_t bytes;
+  int nbuf;            // scratch buffers: 2 when the batch needs several chunks (pass overlap)
+  size_t bytes;        // all buffers
 };
 ScratchPlan scratch_plan(const Frame& f, int nq, int64_t batch, const RangeDev* rg) {
   ScratchPlan sp{};
@@ -174,8 +175,10 @@ ScratchPlan scratch_plan(const Frame& f, int nq, int64_t batch, const RangeDev* 
     sp.pitch = v2_scratch_pitch(f, rg);
     const size_t touched = (size_t)nq * f.Hp * (size_t)sp.pitch * 4;
     sp.chunk = rg ? 1 : chunk_images(touched, batch);
-    sp.bytes = (size_t)sp.chunk * nq * f.Hp * (size_t)sp.pitch * 4;
+    sp.nbuf = batch > sp.chunk ? 2 : 1;
+    sp.bytes = (size_t)sp.nbuf * sp.chunk * nq * f.Hp * (size_t)sp.pitch * 4;
   } else {
+    sp.nbuf = 1;
     sp.pitch = rg ? ((rg->x_hi - rg->x_lo + 3) & ~3) : v1_scratch_width(f);
     const size_t per = (size_t)nq * f.Hp * (size_t)sp.pitch * 4;
     sp.chunk = rg ? 1 : chunk_images(per, batch);
@@ -496,7 +499,7 @@ int run_orientation(const fht_image* img, const Frame& f, const Slot* slots, int
     if (p2.ndest == 1) m2.out1 = m2.out0;
     if (!outs.d[0]) m2.out0_box = m2.out0;
     const bool f32 = img->dtype == FHT_F32;
-    const uint64_t scr_rows = (uint64_t)sp.chunk * p1.scratch_img_rows;
+    const uint64_t scr_rows = (uint64_t)sp.nbuf * sp.chunk * p1.scratch_img_rows;
     P1Maps m1;
     {  // pass-1 stores: scratch as [z*2^m + j][strip][column], one box {TX, 1, 2^m} per tile
       auto fn = encode_fn();
@@ -521,30 +524,79 @@ int run_orientation(const fht_image* img, const Frame& f, const Slot* slots, int
         !make_row_map(&m2.scr1, ws, f32, (uint64_t)span1, scr_rows, (uint64_t)sp.pitch, 36))
       return FHT_ERR_CUDA;
 
-    for (int64_t b0 = 0; b0 < img->batch; b0 += sp.chunk) {
+    // Chunks of the batch; with an auxiliary stream and two scratch buffers, pass 1 of chunk k+1
+    // (aux) overlaps pass 2 of chunk k (main): p2(k) waits for p1(k), p1(k+2) for p2(k).
+    const int nchunks = (int)((img->batch + sp.chunk - 1) / sp.chunk);
+    cudaStream_t aux = (log.opts && log.opts->aux_stream && sp.nbuf == 2 && nchunks > 1 &&
+                        (cudaStream_t)log.opts->aux_stream != st)
+                           ? (cudaStream_t)log.opts->aux_stream
+                           : nullptr;
+    cudaEvent_t ev_start = nullptr, ev_p1[2] = {nullptr, nullptr}, ev_p2[2] = {nullptr, nullptr};
+    auto destroy_events = [&]() {
+      for (cudaEvent_t e : {ev_start, ev_p1[0], ev_p1[1], ev_p2[0], ev_p2[1]})
+        if (e) cudaEventDestroy(e);
+    };
+    if (aux) {
+      bool ok = cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming) == cudaSuccess;
+      for (int b = 0; b < 2; ++b) {
+        ok = ok && cudaEventCreateWithFlags(&ev_p1[b], cudaEventDisableTiming) == cudaSuccess;
+        ok = ok && cudaEventCreateWithFlags(&ev_p2[b], cudaEventDisableTiming) == cudaSuccess;
+      }
+      ok = ok && cudaEventRecord(ev_start, st) == cudaSuccess && cudaStreamWaitEvent(aux, ev_start, 0) == cudaSuccess;
+      if (!ok) {
+        destroy_events();
+        return FHT_ERR_CUDA;
+      }
+    }
+    const int64_t chunk_rows = (int64_t)sp.chunk * p1.scratch_img_rows;
+    for (int k = 0; k < nchunks; ++k) {
+      const int64_t b0 = (int64_t)k * sp.chunk;
       const int nb = (int)((img->batch - b0) < sp.chunk ? (img->batch - b0) : sp.chunk);
+      const int buf = sp.nbuf == 2 ? (k & 1) : 0;
       p1.img0 = (int)b0;
       p2.img0 = (int)b0;
+      p1.z0 = buf * sp.chunk * nq;
+      p2.row0 = buf * chunk_rows;
       p1.ntiles = ntile1;
       dim3 g1((unsigned)(ntile1 * nstrips * nb * nq));
-      cudaError_t e;
-      log.before(st);
-      switch (img->dtype) {
-        case FHT_U8: e = launch_p1<uint8_t>(f.m, g1, m1, p1, st); break;
-        case FHT_I32: e = launch_p1<int32_t>(f.m, g1, m1, p1, st); break;
-        default: e = launch_p1<float>(f.m, g1, m1, p1, st); break;
+      cudaStream_t s1 = aux ? aux : st;
+      if (aux && k >= 2 && cudaStreamWaitEvent(aux, ev_p2[buf], 0) != cudaSuccess) {
+        destroy_events();
+        return FHT_ERR_CUDA;
       }
-      if (e != cudaSuccess) return FHT_ERR_CUDA;
-      log.after(st);
+      cudaError_t e;
+      log.before(s1);
+      switch (img->dtype) {
+        case FHT_U8: e = launch_p1<uint8_t>(f.m, g1, m1, p1, s1); break;
+        case FHT_I32: e = launch_p1<int32_t>(f.m, g1, m1, p1, s1); break;
+        default: e = launch_p1<float>(f.m, g1, m1, p1, s1); break;
+      }
+      if (e != cudaSuccess) {
+        destroy_events();
+        return FHT_ERR_CUDA;
+      }
+      log.after(s1);
       ++launches;
+      if (aux && (cudaEventRecord(ev_p1[buf], aux) != cudaSuccess || cudaStreamWaitEvent(st, ev_p1[buf], 0) != cudaSuccess)) {
+        destroy_events();
+        return FHT_ERR_CUDA;
+      }
       p2.ntiles = ntile2;
       p2.m = f.m;
       dim3 g2((unsigned)(ntile2 * ngroups * nb * nq));
       e = f32 ? launch_p2<float>(f.L, g2, m2, p2, st) : launch_p2<int>(f.L, g2, m2, p2, st);
-      if (e != cudaSuccess) return FHT_ERR_CUDA;
+      if (e != cudaSuccess) {
+        destroy_events();
+        return FHT_ERR_CUDA;
+      }
       log.after(st);
       ++launches;
+      if (aux && cudaEventRecord(ev_p2[buf], st) != cudaSuccess) {
+        destroy_events();
+        return FHT_ERR_CUDA;
+      }
     }
+    destroy_events();
     return launches;
   }
 

@@ -330,6 +330,7 @@ struct P1Params {
   int L;                             // log2(#strips)
   int TX;                            // tile width = TMA box (multiple of 4, <= TX1)
   int64_t scratch_img_rows;          // scratch rows per image
+  int z0;                            // first z (= image-in-chunk * nq + slot) of this scratch buffer
   P1Slot slot[4];
 };
 
@@ -356,7 +357,7 @@ __device__ __noinline__ void p1_tail(const CUtensorMap* tm_scr, const P1Params& 
   // ---- store F_m[strip][j] for all j in ONE box {TX, 1, NR} of the 3-D scratch view
   // [z*2^m + j][strip][column] (z = image-in-chunk * nq + slot); column X - xlo is 16-B aligned
   if (threadIdx.x == 0) {
-    const int z = (img - p.img0) * p.nq + (int)(sl.srow0 >> (R + p.L));
+    const int z = p.z0 + (img - p.img0) * p.nq + (int)(sl.srow0 >> (R + p.L));
     tma_store_3d(tm_scr, buf, X - sl.xlo, strip, z << R);
     tma_commit();
   }
@@ -562,6 +563,7 @@ struct P2Dest {
 
 struct P2Params {
   int64_t scratch_img_rows;
+  int64_t row0;            // first scratch row of this chunk's buffer
   int nq, img0;
   int ntiles;              // tiles per group (max over slots)
   int m;                   // log2(#groups)
@@ -614,7 +616,7 @@ __device__ __forceinline__ void p2_body(const CUtensorMap* tm_scr0, const CUtens
   constexpr int NA = 1 << S::a, NBk = 1 << S::b;  // sub-pass A blocks: one mbarrier each
   if (!black && threadIdx.x == 0) {
     for (int b = 0; b < NBk; ++b) mbar_init(bar + b);
-    const int64_t rbase = (int64_t)(img - p.img0) * p.scratch_img_rows + sl.srow0 + t0;
+    const int64_t rbase = p.row0 + (int64_t)(img - p.img0) * p.scratch_img_rows + sl.srow0 + t0;
     for (int b = 0; b < NBk; ++b) {
       mbar_expect_tx(bar + b, NA * (256 + 36) * 4);
       for (int i = b * NA; i < (b + 1) * NA; ++i) {

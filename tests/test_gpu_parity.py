@@ -302,3 +302,26 @@ def test_v2_batch_chunks(fht, O):
         quads = O.full_quadrants(imgs[b])
         for q in range(4):
             check(got[b, q], quads[q], False)
+
+
+def test_v2_aux_stream_overlap(fht, O):
+    """Pass 1 of chunk k+1 on an auxiliary stream overlapping pass 2 of chunk k (two scratch
+    buffers): bit-identical to the single-stream schedule, and the call is complete on the
+    caller's stream."""
+    from synth import random_image
+    imgs = np.stack([random_image((1024, 1024), "f32", seed=300 + b) for b in range(7)])
+    t = dev(imgs)
+    h1, s1 = fht.full(t, pair=True)
+    aux = torch.cuda.Stream()
+    h2, s2 = fht.full(t, pair=True, aux_stream=aux)
+    torch.cuda.current_stream().synchronize()          # only the caller's stream
+    assert torch.equal(h1.storage, h2.storage) and torch.equal(s1.storage, s2.storage)
+    quads = O.full_quadrants(imgs[5])
+    for q in range(4):
+        check(h2.view[5, q].cpu().numpy(), quads[q], False)
+    u8 = np.stack([random_image((512, 512), "u8", seed=400 + b) for b in range(40)])
+    tu = dev(u8)
+    a = fht.full(tu)
+    b = fht.full(tu, aux_stream=aux)
+    torch.cuda.current_stream().synchronize()
+    assert b.launches > 2 and torch.equal(a.storage, b.storage)

@@ -23,13 +23,15 @@ c = synth.CONFIGS[cid]
 imgs = synth.batch(cid)
 t = torch.from_numpy(imgs).cuda()
 outs = {}
+aux = torch.cuda.Stream() if os.environ.get("AB_AUX") == "1" else None
 plan = fht.angle_plan(c["h"], c["w"], c["theta_min"], c["theta_max"]) if c["mode"] == "range" else None
 def step(ev=None):
     if c["mode"] == "full":
         if cid in (2, 5):
-            outs["h"], outs["s"] = fht.full(t, pair=True, out=outs.get("h"), out_shifted=outs.get("s"), events=ev)
+            outs["h"], outs["s"] = fht.full(t, pair=True, out=outs.get("h"), out_shifted=outs.get("s"), events=ev,
+                                            aux_stream=None if ev else aux)
         else:
-            outs["h"] = fht.full(t, out=outs.get("h"), events=ev)
+            outs["h"] = fht.full(t, out=outs.get("h"), events=ev, aux_stream=None if ev else aux)
     elif c["mode"] == "range":
         outs["h"], outs["s"] = fht.angle_range(t, plan, pair=True, out=outs.get("h"), out_shifted=outs.get("s"), events=ev)
     else:
