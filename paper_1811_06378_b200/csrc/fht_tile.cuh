@@ -85,7 +85,10 @@ template <> struct Split<1> { static constexpr int a = 1, b = 0, nw = 4; };
 template <> struct Split<2> { static constexpr int a = 2, b = 0, nw = 4; };
 template <> struct Split<3> { static constexpr int a = 3, b = 0, nw = 4; };
 template <> struct Split<4> { static constexpr int a = 2, b = 2, nw = 4; };
-template <> struct Split<5> { static constexpr int a = 3, b = 2, nw = 4; };
+#ifndef FHT_SPLIT5_A
+#define FHT_SPLIT5_A 2  // 32-row tiles: sub-pass A levels (3: 8-row A blocks + 4-row B groups; 2: 4 + 8)
+#endif
+template <> struct Split<5> { static constexpr int a = FHT_SPLIT5_A, b = 5 - FHT_SPLIT5_A, nw = 4; };
 template <> struct Split<6> { static constexpr int a = 3, b = 3, nw = 8; };
 template <int R> constexpr int kMinBlocks = Split<R>::nw == 4 ? 5 : 2;  // occupancy target (regs <= 102 / 128)
 template <int R> constexpr int kTPW = ((1 << Split<R>::a) + Split<R>::nw - 1) / Split<R>::nw;  // B tasks/warp
