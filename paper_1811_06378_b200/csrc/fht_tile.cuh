@@ -47,6 +47,9 @@
 #define FHT_P2_DENSE 1    // pass-2 plain destination of interior tiles as one 2-D box (1)
 #endif
 
+#ifndef FHT_SCR_KEEP
+#define FHT_SCR_KEEP 1    // pass-1 scratch stores with an L2 evict-last hint
+#endif
 #ifndef FHT_PDL
 #define FHT_PDL 1         // programmatic dependent launch between the passes (griddepcontrol)
 #endif
@@ -132,6 +135,14 @@ __device__ __forceinline__ void tma_store_row_stream(const CUtensorMap* map, con
 __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* smem, int c0, int c1, int c2) {
   asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];"
                :: "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(smem)), "r"(c0), "r"(c1), "r"(c2) : "memory");
+}
+// Pass-1 scratch: keep it in L2 for pass 2 (evict-last)
+__device__ __forceinline__ void tma_store_3d_keep(const CUtensorMap* map, const void* smem, int c0, int c1, int c2) {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%2, %3, %4}], [%1], %5;"
+               :: "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(smem)), "r"(c0), "r"(c1), "r"(c2), "l"(pol)
+               : "memory");
 }
 __device__ __forceinline__ void tma_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void tma_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
@@ -361,7 +372,11 @@ __device__ __noinline__ void p1_tail(const CUtensorMap* tm_scr, const P1Params& 
   // [z*2^m + j][strip][column] (z = image-in-chunk * nq + slot); column X - xlo is 16-B aligned
   if (threadIdx.x == 0) {
     const int z = p.z0 + (img - p.img0) * p.nq + (int)(sl.srow0 >> (R + p.L));
+#if FHT_SCR_KEEP
+    tma_store_3d_keep(tm_scr, buf, X - sl.xlo, strip, z << R);
+#else
     tma_store_3d(tm_scr, buf, X - sl.xlo, strip, z << R);
+#endif
     tma_commit();
   }
   pdl_trigger();
