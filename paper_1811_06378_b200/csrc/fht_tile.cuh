@@ -50,6 +50,12 @@
 #ifndef FHT_SCR_KEEP
 #define FHT_SCR_KEEP 1    // pass-1 scratch stores with an L2 evict-last hint
 #endif
+#ifndef FHT_P2_WARPLOAD
+#define FHT_P2_WARPLOAD 1 // pass 2: each warp issues and waits for the TMA loads of its own sub-pass-A blocks
+#endif
+#ifndef FHT_P1_WARPLOAD
+#define FHT_P1_WARPLOAD 1 // pass 1 (TMA fill): same, per-block mbarriers instead of one for the tile
+#endif
 #ifndef FHT_PDL
 #define FHT_PDL 1         // programmatic dependent launch between the passes (griddepcontrol)
 #endif
@@ -356,17 +362,17 @@ struct P1Params {
 // inside the instruction cache.
 template <typename Tin, int R, int SIG, typename Tsrc>
 __device__ __noinline__ void p1_tail(const CUtensorMap* tm_scr, const P1Params& p, const P1Slot& sl, int img,
-                                     int strip, int X, const Tsrc* tsrc, int tpitch, int fa_pitch) {
+                                     int strip, int X, const Tsrc* tsrc, int tpitch, int fa_pitch, bool bars) {
   using A = typename AccOf<Tin>::type;
   using S = Split<R>;
-  constexpr int NR = 1 << R;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   A* buf = reinterpret_cast<A*>(smem_raw);
   unsigned char* tab = smem_raw + main_buf_bytes(R) + (sizeof(Tin) == 1 ? u8_tile_bytes(R) : 0);
   const int* rowoff = reinterpret_cast<const int*>(tab);
   const int* soff = rowoff + 64;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(tab + 768);
   A w[kTPW<R>][1 << S::b][VB];
-  tile_fht<R, SIG, A>(tsrc, tpitch, rowoff, buf, fa_pitch, w);
+  tile_fht<R, SIG, A>(tsrc, tpitch, rowoff, buf, fa_pitch, w, bars ? bar : nullptr);
   stage_rows<R, SIG, A>(w, buf, soff, p.TX, p.TX);  // dense [NR][TX]: the box layout
   // ---- store F_m[strip][j] for all j in ONE box {TX, 1, NR} of the 3-D scratch view
   // [z*2^m + j][strip][column] (z = image-in-chunk * nq + slot); column X - xlo is 16-B aligned
@@ -385,9 +391,10 @@ __device__ __noinline__ void p1_tail(const CUtensorMap* tm_scr, const P1Params& 
 
 template <typename Tin, int R, typename Tsrc>
 __device__ __forceinline__ void p1_tail_sig(int sigma, const CUtensorMap* tm_scr, const P1Params& p, const P1Slot& sl,
-                                            int img, int strip, int X, const Tsrc* tsrc, int tpitch, int fa_pitch) {
-  if (sigma > 0) p1_tail<Tin, R, 1>(tm_scr, p, sl, img, strip, X, tsrc, tpitch, fa_pitch);
-  else p1_tail<Tin, R, -1>(tm_scr, p, sl, img, strip, X, tsrc, tpitch, fa_pitch);
+                                            int img, int strip, int X, const Tsrc* tsrc, int tpitch, int fa_pitch,
+                                            bool bars = false) {
+  if (sigma > 0) p1_tail<Tin, R, 1>(tm_scr, p, sl, img, strip, X, tsrc, tpitch, fa_pitch, bars);
+  else p1_tail<Tin, R, -1>(tm_scr, p, sl, img, strip, X, tsrc, tpitch, fa_pitch, bars);
 }
 
 template <typename Tin, int R>
@@ -414,6 +421,29 @@ __device__ __forceinline__ void p1_body(const CUtensorMap* tm_img0, const CUtens
     const int a0 = Xa & ~(AL - 1);
     constexpr int TP = sizeof(Tin) == 1 ? TMA_PITCH_U8 : TMA_PITCH;
     Tin* tile = reinterpret_cast<Tin*>(sizeof(Tin) == 1 ? smem_raw + main_buf_bytes(R) : smem_raw);
+    constexpr uint32_t row_bytes = sizeof(Tin) == 1 ? 256 + 48 : (256 + 36) * 4;
+#if FHT_P1_WARPLOAD
+    // each warp issues (lane 0) and waits for (in tile_fht) the rows of its own sub-pass-A blocks
+    constexpr int NA = 1 << S::a, NBk = 1 << S::b, NW = S::nw;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int b = warp; b < NBk; b += NW) {
+      if (lane == 0) {
+        mbar_init(bar + b);
+        mbar_expect_tx(bar + b, NA * row_bytes);
+        for (int rho = b * NA; rho < (b + 1) * NA; ++rho) {
+          Tin* d = tile + rho * TP;
+          tma_load_3d(tm_img0, d, bar + b, a0, y0 + rho, img);
+          tma_load_3d(tm_img1, d + 256, bar + b, a0 + 256, y0 + rho, img);
+        }
+      }
+      if (lane < NA) {
+        rowoff[b * NA + lane] = Xa - a0;
+        soff[b * NA + lane] = 0;
+      }
+    }
+    __syncwarp();
+    constexpr bool bars = true;
+#else
     if (threadIdx.x < NR) {
       rowoff[threadIdx.x] = Xa - a0;
       soff[threadIdx.x] = 0;
@@ -421,7 +451,6 @@ __device__ __forceinline__ void p1_body(const CUtensorMap* tm_img0, const CUtens
     if (threadIdx.x == 0) mbar_init(bar);
     __syncthreads();
     if (threadIdx.x < 32) {
-      constexpr uint32_t row_bytes = sizeof(Tin) == 1 ? 256 + 48 : (256 + 36) * 4;
       if (threadIdx.x == 0) mbar_expect_tx(bar, NR * row_bytes);
       __syncwarp();
       for (int rho = threadIdx.x; rho < NR; rho += 32) {
@@ -431,10 +460,13 @@ __device__ __forceinline__ void p1_body(const CUtensorMap* tm_img0, const CUtens
       }
     }
     mbar_wait0(bar);
+    constexpr bool bars = false;
+#endif
     if constexpr (sizeof(Tin) == 1)
-      p1_tail_sig<Tin, R>(sl.sigma, tm_scr, p, sl, img, strip, X, static_cast<const Tin*>(tile), TP, FA_PITCH);
+      p1_tail_sig<Tin, R>(sl.sigma, tm_scr, p, sl, img, strip, X, static_cast<const Tin*>(tile), TP, FA_PITCH, bars);
     else
-      p1_tail_sig<Tin, R>(sl.sigma, tm_scr, p, sl, img, strip, X, reinterpret_cast<const A*>(tile), TP, TMA_PITCH);
+      p1_tail_sig<Tin, R>(sl.sigma, tm_scr, p, sl, img, strip, X, reinterpret_cast<const A*>(tile), TP, TMA_PITCH,
+                          bars);
     return;
   }
   if (threadIdx.x < NR) {
@@ -630,8 +662,30 @@ __device__ __forceinline__ void p2_body(const CUtensorMap* tm_scr0, const CUtens
 
   // ---- scratch rows t0 + i, column (x + sigma*j*i) - xlo1 for x = Xa + e: TMA from the
   // aligned-down column, zero outside [0, xhi1 - xlo1) = outside what pass 1 wrote. Issued first,
-  // by one thread, so the loads are in flight while the CTA plans its stores.
+  // so the loads are in flight while the CTA plans its stores.
   constexpr int NA = 1 << S::a, NBk = 1 << S::b;  // sub-pass A blocks: one mbarrier each
+#if FHT_P2_WARPLOAD
+  // every warp issues (lane 0) and waits for the rows of its own sub-pass-A blocks blk = warp,
+  // warp + NW, ...: no CTA-wide barrier between the issue and the butterflies, and the four warps
+  // issue in parallel. rowoff of a block's rows is written by the warp that reads them.
+  if (!black) {
+    const int64_t rbase = p.row0 + (int64_t)(img - p.img0) * p.scratch_img_rows + sl.srow0 + t0;
+    for (int b = warp; b < NBk; b += NW) {
+      if (lane == 0) {
+        mbar_init(bar + b);
+        mbar_expect_tx(bar + b, NA * (256 + 36) * 4);
+        for (int i = b * NA; i < (b + 1) * NA; ++i) {
+          const int a0 = (Xa + SIG * j * i - sl.xlo1) & ~3;
+          A* d = buf + i * TMA_PITCH;
+          tma_load_2d(tm_scr0, d, bar + b, a0, (int)(rbase + i));
+          tma_load_2d(tm_scr1, d + 256, bar + b, a0 + 256, (int)(rbase + i));
+        }
+      }
+      if (lane < NA) rowoff[b * NA + lane] = (Xa + SIG * j * (b * NA + lane) - sl.xlo1) & 3;
+    }
+    __syncwarp();
+  }
+#else
   if (!black && threadIdx.x == 0) {
     for (int b = 0; b < NBk; ++b) mbar_init(bar + b);
     const int64_t rbase = p.row0 + (int64_t)(img - p.img0) * p.scratch_img_rows + sl.srow0 + t0;
@@ -645,6 +699,7 @@ __device__ __forceinline__ void p2_body(const CUtensorMap* tm_scr0, const CUtens
       }
     }
   }
+#endif
 
   // ---- store plan per (destination, row): shift k, 16-byte aligned start, TMA or plain stores
   for (int it = threadIdx.x; it < p.ndest * NR; it += NT) {
@@ -681,8 +736,13 @@ __device__ __forceinline__ void p2_body(const CUtensorMap* tm_scr0, const CUtens
     info[d * NR + tau] = ri;
     soff[d * 64 + tau] = WO2 - r;
   }
+#if FHT_P2_WARPLOAD
+  // the plan (info, soff) is read after tile_fht's first __syncthreads; a black tile has none
+  if (black) __syncthreads();
+#else
   if (!black && threadIdx.x < NR) rowoff[threadIdx.x] = (Xa + SIG * j * (int)threadIdx.x - sl.xlo1) & 3;
   __syncthreads();
+#endif
 
   if (!black) tile_fht<R, SIG, A>(static_cast<const A*>(buf), TMA_PITCH, rowoff, buf, TMA_PITCH, w, bar);
 
