@@ -224,9 +224,11 @@ __device__ __forceinline__ void warp_fht(A (&v)[1 << NB][V]) {
 // sub-pass B leaves output row tau = jp*2^b + u, local column lane*VB + q in w[g][u][q]
 // (jp = warp + g*NW). Ends with __syncthreads (fa and src are free afterwards).
 // ------------------------------------------------------------------------------------------
-template <int R, int SIG, typename A, typename Tsrc>
-__device__ __forceinline__ void tile_fht(const Tsrc* src, int src_pitch, const int* rowoff, A* fa, int fa_pitch,
-                                         A (&w)[kTPW<R>][1 << Split<R>::b][VB], uint64_t* blk_bars = nullptr) {
+// The loader fills v[r][q] = input (row blk*2^a + r, x-order index e) for the lane's columns,
+// e = lane*VA + q (SIG = +1) or (WA - 1) - lane*VA - q (SIG = -1).
+template <int R, int SIG, typename A, typename LoadA>
+__device__ __forceinline__ void tile_fht_ld(const LoadA& load, A* fa, int fa_pitch,
+                                            A (&w)[kTPW<R>][1 << Split<R>::b][VB]) {
   using S = Split<R>;
   constexpr int a = S::a, b = S::b, NW = S::nw;
   constexpr int NA = 1 << a, NBk = 1 << b;
@@ -235,15 +237,8 @@ __device__ __forceinline__ void tile_fht(const Tsrc* src, int src_pitch, const i
   // sub-pass A: block blk = rows blk*2^a .. +2^a-1 -> fa row blk*2^a + j' = F_a[blk][j']
 #pragma unroll 1
   for (int blk = warp; blk < NBk; blk += NW) {
-    if (blk_bars) mbar_wait0(blk_bars + blk);  // this block's rows have landed (TMA)
     A v[NA][VA];
-#pragma unroll
-    for (int r = 0; r < NA; ++r) {
-      const int rho = blk * NA + r;
-      const Tsrc* p = src + rho * src_pitch + rowoff[rho] + (SIG > 0 ? lane * VA : (WA - 1) - lane * VA);
-#pragma unroll
-      for (int q = 0; q < VA; ++q) v[r][q] = static_cast<A>(p[SIG > 0 ? q : -q]);
-    }
+    load(blk, v);
     warp_fht<a, VA>(v);
     A* d = fa + (blk * NA) * fa_pitch + lane * VA;
 #pragma unroll
@@ -268,6 +263,26 @@ __device__ __forceinline__ void tile_fht(const Tsrc* src, int src_pitch, const i
     }
   }
   __syncthreads();
+}
+
+// Input rows from shared memory: element (rho, e) at src[rho*src_pitch + rowoff[rho] + e]; with
+// blk_bars, a block's rows are waited for (TMA) by the warp that reads them.
+template <int R, int SIG, typename A, typename Tsrc>
+__device__ __forceinline__ void tile_fht(const Tsrc* src, int src_pitch, const int* rowoff, A* fa, int fa_pitch,
+                                         A (&w)[kTPW<R>][1 << Split<R>::b][VB], uint64_t* blk_bars = nullptr) {
+  constexpr int NA = 1 << Split<R>::a;
+  const int lane = threadIdx.x & 31;
+  auto load = [&](int blk, A (&v)[NA][VA]) {
+    if (blk_bars) mbar_wait0(blk_bars + blk);  // this block's rows have landed (TMA)
+#pragma unroll
+    for (int r = 0; r < NA; ++r) {
+      const int rho = blk * NA + r;
+      const Tsrc* p = src + rho * src_pitch + rowoff[rho] + (SIG > 0 ? lane * VA : (WA - 1) - lane * VA);
+#pragma unroll
+      for (int q = 0; q < VA; ++q) v[r][q] = static_cast<A>(p[SIG > 0 ? q : -q]);
+    }
+  };
+  tile_fht_ld<R, SIG, A>(load, fa, fa_pitch, w);
 }
 
 template <int Q, typename A>
