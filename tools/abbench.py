@@ -39,6 +39,10 @@ def step(ev=None):
     return outs["h"].launches
 n = step()
 flush = torch.empty(128 << 20, dtype=torch.float32, device="cuda")
+def do_flush():
+    flush.zero_()  # > L2 write; AB_FLUSH=rw adds a read pass so the L2 is cold AND clean (no dirty write-back)
+    if os.environ.get("AB_FLUSH") == "rw":
+        flush.sum()
 for _ in range(5): step()
 torch.cuda.synchronize()
 steps = 30 if cid in (1, 2) else 8
@@ -47,7 +51,7 @@ for r in evs:
     for e in r: e.record()
 torch.cuda.synchronize()
 for i in range(steps):
-    flush.zero_()
+    do_flush()
     step(evs[i])
 torch.cuda.synchronize()
 tot = statistics.mean(evs[i][0].elapsed_time(evs[i][n]) for i in range(steps))
@@ -55,7 +59,7 @@ tot = statistics.mean(evs[i][0].elapsed_time(evs[i][n]) for i in range(steps))
 e0 = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
 e1 = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
 for i in range(steps):
-    flush.zero_()
+    do_flush()
     e0[i].record()
     step()
     e1[i].record()
@@ -80,6 +84,10 @@ def main():
     if "--rounds" in args:
         i = args.index("--rounds")
         rounds = int(args[i + 1])
+        del args[i:i + 2]
+    if "--flush" in args:  # w (default): write 512 MiB; rw: write then read 512 MiB
+        i = args.index("--flush")
+        os.environ["AB_FLUSH"] = args[i + 1]
         del args[i:i + 2]
     libs = args
     res = {}
