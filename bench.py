@@ -220,6 +220,7 @@ def main():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-shift-bench", action="store_true", help="skip the standalone fhtshift (SURVEY a7) lines")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--extra-configs", default="5,3,4,1",
                     help="other configs also timed (reported under 'configs', not the headline)")
@@ -392,7 +393,43 @@ def main():
         return {"value": px * world / (ms * 1e-3) / 1e9, "unit": "Gpixel/s", "h2d_bytes_per_step": hb,
                 "d2h_bytes_per_step": db, "ms_per_step": ms}
 
+    def shift_standalone(cfg_id, steps=20):
+        """SURVEY a7 standalone fhtshift (one warp per row, 16-byte rotation) on the config's Hough
+        image: read + write of every cell; working set > L2 for C5 (no flush needed)."""
+        cc = synth.CONFIGS[cfg_id]
+        t_in = torch.from_numpy(synth.batch(cfg_id)).to(dev)
+        if cc["mode"] == "range":
+            h = fht.angle_range(t_in, fht.angle_plan(cc["h"], cc["w"], cc["theta_min"], cc["theta_max"]))
+        else:
+            h = fht.full(t_in)
+        del t_in
+        out = fht.fhtshift(h)
+        for _ in range(3):
+            fht.fhtshift(h, out=out)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            fht.fhtshift(h, out=out)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+        nbytes = 2 * h.storage.numel() * h.storage.element_size()
+        res = {"workload": cc["name"], "mode": cc["mode"], "bytes_per_call": nbytes, "ms_per_call": ms,
+               "achieved_gbs": nbytes / (ms * 1e-3) / 1e9, "peak_gbs": peak_gbs,
+               "frac": nbytes / (ms * 1e-3) / 1e9 / peak_gbs, "launches_per_call": out.launches}
+        del h, out
+        torch.cuda.empty_cache()
+        return res
+
     head = run_config(args.config, args.steps, args.warmup, with_e2e=True)
+    shift_lines = []
+    if not args.no_shift_bench:
+        for cid in (5, 4):
+            try:
+                shift_lines.append(shift_standalone(cid))
+            except Exception as e:  # noqa: BLE001 -- report, do not hide
+                shift_lines.append({"workload": synth.CONFIGS[cid]["name"], "error": repr(e)})
     extra = {}
     extra_ids = [] if args.extra_configs in ("", "none") else [int(x) for x in args.extra_configs.split(",")]
     for cid in [x for x in extra_ids if x != args.config]:
@@ -440,6 +477,7 @@ def main():
         "gpu_launches": head["launches_per_step"] * args.steps,
         "clocks": head["clocks"],
         "configs": extra,
+        "fhtshift_standalone": shift_lines,
     }
     print(json.dumps(line), flush=True)
     if world > 1:

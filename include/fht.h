@@ -163,7 +163,10 @@ int fht_angle_range(const fht_image* img, const fht_angle_plan* plan, fht_hough*
 /* §5 fhtshift (R11): out[r][x] = in[r][(x - k_r) mod cols], k_r = ceil((n+s)/2) for
  * sigma=+1 quadrants, ceil((n-s)/2) for sigma=-1, and ceil((W'-len_s)/2) - start_s in RANGE
  * mode. `in` must be unshifted (FHT_ERR_STATE otherwise); `out` must have the same shape and
- * not alias `in`; on success out->shifted = 1. Bit copy: exact for every dtype. */
+ * not alias `in`; on success out->shifted = 1. Bit copy: exact for every dtype. One kernel (a warp
+ * per row, 16-byte loads/stores when cols, every stride and both bases are 16-byte aligned); RANGE
+ * mode first runs the per-row support-table kernel into a stream-ordered allocation of 2*rows ints
+ * (cudaMallocAsync / cudaFreeAsync on `stream`). Returns the number of kernels (1 or 2). */
 int fhtshift(const fht_hough* in, fht_hough* out, fht_stream_t stream);
 
 /* Human-readable name of a status code (static string). */

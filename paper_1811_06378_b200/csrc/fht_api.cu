@@ -1076,26 +1076,52 @@ int fhtshift(const fht_hough* in, fht_hough* out, fht_stream_t stream) {
   a.rows = (int)in->rows;
   a.W = (int)in->cols;
   a.nquad = (int)in->nquad;
+  a.rows_total = in->batch * in->nquad * in->rows;
   a.mode = in->mode;
   a.layout = in->layout;
   a.quadrant = in->quadrant;
+  a.vec = a.W % 4 == 0 && aligned16(in->data) && aligned16(out->data);
+  for (int64_t st : {in->batch_stride, in->quad_stride, in->row_stride, out->batch_stride, out->quad_stride,
+                     out->row_stride})
+    a.vec = a.vec && st % 4 == 0;
+  int* tabs = nullptr;
+  int launches = 0;
   if (in->mode == FHT_MODE_QUADRANT) {
     a.Hp = a.Wp = (int)in->rows;  // the quadrant's own row count
   } else if (in->mode == FHT_MODE_FULL) {
     a.Hp = (int)in->Hp;
     a.Wp = (int)in->Wp;
   } else {
-    a.g = in->plan.g;
-    a.h = (int)in->plan.h;
-    a.K = ilog2(in->plan.Hp);
-    a.w_content = (int)in->plan.w_content;
+    // per-row support start / length of the range frame (R17) by the §4 table kernel (its row
+    // blocks only), into a stream-ordered scratch of 2*rows ints
+    if (cudaMallocAsync(reinterpret_cast<void**>(&tabs), 2 * sizeof(int) * (size_t)in->rows, (cudaStream_t)stream) !=
+        cudaSuccess)
+      return FHT_ERR_CUDA;
+    RangeTableArgs ta{};
+    ta.g = in->plan.g;
+    ta.alpha = in->plan.alpha;
+    ta.h = (int)in->plan.h;
+    ta.w = (int)in->plan.w;
+    ta.w_content = (int)in->plan.w_content;
+    ta.Hp = (int)in->rows;
+    ta.K = ilog2(in->plan.Hp);
+    ta.start_tab = tabs;
+    ta.len_tab = tabs + in->rows;
+    const int nsb = (ta.Hp + kRangeRowsPerBlock - 1) / kRangeRowsPerBlock;  // no e_tab / colmap blocks
+    k_range_tables<<<nsb, kThreads, (size_t)ta.h * sizeof(int), (cudaStream_t)stream>>>(ta);
+    if (cudaGetLastError() != cudaSuccess) return FHT_ERR_CUDA;
+    a.start_tab = ta.start_tab;
+    a.len_tab = ta.len_tab;
+    ++launches;
   }
-  dim3 grid((unsigned)in->rows, (unsigned)(in->batch * in->nquad));
-  if (in->dtype == FHT_F32) k_fhtshift<float><<<grid, kThreads, 0, (cudaStream_t)stream>>>(a);
-  else k_fhtshift<int><<<grid, kThreads, 0, (cudaStream_t)stream>>>(a);
+  const int64_t nblk = (a.rows_total + kThreads / 32 - 1) / (kThreads / 32);
+  if (in->dtype == FHT_F32) k_fhtshift<float><<<(unsigned)nblk, kThreads, 0, (cudaStream_t)stream>>>(a);
+  else k_fhtshift<int><<<(unsigned)nblk, kThreads, 0, (cudaStream_t)stream>>>(a);
   if (cudaGetLastError() != cudaSuccess) return FHT_ERR_CUDA;
+  ++launches;
+  if (tabs && cudaFreeAsync(tabs, (cudaStream_t)stream) != cudaSuccess) return FHT_ERR_CUDA;
   out->shifted = 1;
-  return 1;
+  return launches;
 }
 
 }  // extern "C"

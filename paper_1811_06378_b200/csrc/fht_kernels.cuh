@@ -266,7 +266,10 @@ __device__ __forceinline__ int shear_e(double g, int y) {
 // are the lane (a per-lane constant) and the high bits are k (the same for the whole warp, from a
 // per-warp 128-entry table). The shear offsets e_y are computed once per block (shared memory).
 // Blocks [0, nsb) do kRangeRowsPerBlock rows with 8 warps; the remaining blocks write e_tab, colmap.
-constexpr int kRangeRowsPerBlock = 32;
+#ifndef FHT_RANGE_ROWS_PER_BLOCK
+#define FHT_RANGE_ROWS_PER_BLOCK 8
+#endif
+constexpr int kRangeRowsPerBlock = FHT_RANGE_ROWS_PER_BLOCK;  // one row per warp: 512 blocks for Hp = 4096
 __global__ void k_range_tables(const RangeTableArgs a) {
   extern __shared__ int e_s[];          // [h]
   __shared__ int dh_s[8][128];          // per warp: D of the high bits, y >> 5
@@ -328,71 +331,114 @@ struct ShiftArgs {
   int64_t in_img_stride, in_q_stride, in_row_stride;
   int64_t out_img_stride, out_q_stride, out_row_stride;
   int rows, W, nquad;
-  int mode, layout;   // fht_mode / fht_layout
-  int quadrant;       // QUADRANT mode
-  int Hp, Wp;         // quadrant row counts (QA/QB: Hp, QC/QD: Wp)
-  // range
-  double g;
-  int h, K, w_content;
+  int64_t rows_total;   // batch * nquad * rows
+  int mode, layout;     // fht_mode / fht_layout
+  int quadrant;         // QUADRANT mode
+  int Hp, Wp;           // quadrant row counts (QA/QB: Hp, QC/QD: Wp)
+  int vec;              // 16-byte path: W, every stride a multiple of 4 elements, bases 16-B aligned
+  const int* start_tab; // RANGE: per-row support start / length (k_range_tables)
+  const int* len_tab;
 };
 
 __device__ __forceinline__ int quadrant_sigma(int q) { return (q == 0 || q == 3) ? 1 : -1; }
 
+// k(s) of output row r (R11, R17): QUADRANT / FULL (QUADS or CONCAT row attribution,
+// P:111-113, R8) by the closed form, RANGE from the per-row support tables.
+__device__ __forceinline__ int shift_amount(const ShiftArgs& a, int r, int qs) {
+  if (a.mode == 2) {
+    int k = (ceil_half(a.W - __ldg(a.len_tab + r)) - __ldg(a.start_tab + r)) % a.W;
+    return k < 0 ? k + a.W : k;
+  }
+  int q, s;
+  if (a.mode == 1 && a.layout == 1) {
+    const int Hp = a.Hp, Wp = a.Wp;
+    if (r < Hp) { q = 0; s = Hp - 1 - r; }
+    else if (r < 2 * Hp - 1) { q = 1; s = r - (Hp - 1); }
+    else if (r < 2 * Hp - 2 + Wp) { q = 2; s = Wp - 1 - (r - (2 * Hp - 2)); }
+    else { q = 3; s = r - (2 * Hp + Wp - 3); }
+  } else {
+    q = a.mode == 0 ? a.quadrant : qs;
+    s = r;
+  }
+  const int n = (q < 2) ? a.Hp : a.Wp;
+  if (s >= n) return 0;
+  return (quadrant_sigma(q) > 0 ? ceil_half(n + s) : ceil_half(n - s)) % a.W;
+}
+
+template <typename T> struct Vec4;
+template <> struct Vec4<float> { using type = float4; };
+template <> struct Vec4<int> { using type = int4; };
+
+// out = src[4c - k .. 4c - k + 3] from the aligned chunks A = chunk(c - k) and B = the next one
+// (row-uniform misalignment O = (-k) mod 4)
+template <int O, typename V>
+__device__ __forceinline__ V rot_combine(const V& A, const V& B) {
+  if constexpr (O == 0) return A;
+  else if constexpr (O == 1) return V{A.y, A.z, A.w, B.x};
+  else if constexpr (O == 2) return V{A.z, A.w, B.x, B.y};
+  else return V{A.w, B.x, B.y, B.z};
+}
+
+// One warp rotates one row of W4 16-byte chunks: output chunk c <- source chunks ca, ca + 1
+// (mod W4) with ca = (cA0 + c) mod W4. Four chunks per lane in flight before their stores.
+template <int O, typename T>
+__device__ __forceinline__ void shift_row_vec(const T* src, T* dst, int W4, int cA0, int lane) {
+  using V = typename Vec4<T>::type;
+  const V* s4 = reinterpret_cast<const V*>(src);
+  V* d4 = reinterpret_cast<V*>(dst);
+  int ca = cA0 + lane;
+  if (ca >= W4) ca -= W4;
+  for (int c0 = lane; c0 < W4; c0 += 128) {
+    V o[4];
+    int cu = ca;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (c0 + 32 * u < W4) {
+        const V A = __ldg(s4 + cu);
+        V B = A;
+        if constexpr (O != 0) B = __ldg(s4 + (cu + 1 == W4 ? 0 : cu + 1));
+        o[u] = rot_combine<O>(A, B);
+      }
+      cu += 32;
+      while (cu >= W4) cu -= W4;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (c0 + 32 * u < W4) __stcs(d4 + c0 + 32 * u, o[u]);
+    ca = cu;
+  }
+}
+
+// Standalone fhtshift (R11): out[r][x] = in[r][(x - k_r) mod W]. One warp
+// per row (8 rows per block); 16-byte loads and streaming stores when everything is aligned.
 template <typename T>
 __global__ void __launch_bounds__(kThreads) k_fhtshift(const ShiftArgs a) {
-  const int r = blockIdx.x;
-  const int zq = blockIdx.y;  // image * nquad + quadrant slot
-  const int img = zq / a.nquad, qs = zq % a.nquad;
-  __shared__ int k_sh;
-  if (a.mode == 2) {  // RANGE: k = ceil((W - len)/2) - start, start/len by reduction over y < h
-    int mn = INT32_MAX, mx = INT32_MIN;
-    for (int y = threadIdx.x; y < a.h; y += blockDim.x) {
-      const int v = shear_e(a.g, y) - dyadic_offset(a.K, r, y);
-      mn = min(mn, v);
-      mx = max(mx, v);
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-      mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-      mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    }
-    __shared__ int smn[32], smx[32];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (lane == 0) { smn[warp] = mn; smx[warp] = mx; }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      for (int i = 1; i < (int)(blockDim.x >> 5); ++i) { mn = min(mn, smn[i]); mx = max(mx, smx[i]); }
-      const int len = mx - mn + a.w_content;
-      int k = (ceil_half(a.W - len) - mn) % a.W;
-      if (k < 0) k += a.W;
-      k_sh = k;
-    }
-  } else if (threadIdx.x == 0) {
-    int q, s;
-    if (a.mode == 1 && a.layout == 1) {  // CONCAT: attribute the row (R8)
-      const int Hp = a.Hp, Wp = a.Wp;
-      if (r < Hp) { q = 0; s = Hp - 1 - r; }
-      else if (r < 2 * Hp - 1) { q = 1; s = r - (Hp - 1); }
-      else if (r < 2 * Hp - 2 + Wp) { q = 2; s = Wp - 1 - (r - (2 * Hp - 2)); }
-      else { q = 3; s = r - (2 * Hp + Wp - 3); }
-    } else {
-      q = a.mode == 0 ? a.quadrant : qs;
-      s = r;
-    }
-    const int n = (q < 2) ? a.Hp : a.Wp;
-    int k = 0;
-    if (s < n) k = (quadrant_sigma(q) > 0 ? ceil_half(n + s) : ceil_half(n - s)) % a.W;
-    k_sh = k;
-  }
-  __syncthreads();
-  const int k = k_sh;
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+  if (row >= a.rows_total) return;
+  const int r = (int)(row % a.rows);
+  const int64_t zq = row / a.rows;  // image * nquad + quadrant slot
+  const int img = (int)(zq / a.nquad), qs = (int)(zq % a.nquad);
+  const int k = shift_amount(a, r, qs);
   const T* src = static_cast<const T*>(a.in) + (int64_t)img * a.in_img_stride + (int64_t)qs * a.in_q_stride +
                  (int64_t)r * a.in_row_stride;
   T* dst = static_cast<T*>(a.out) + (int64_t)img * a.out_img_stride + (int64_t)qs * a.out_q_stride +
            (int64_t)r * a.out_row_stride;
-  for (int x = threadIdx.x; x < a.W; x += blockDim.x) {
+  if (a.vec) {
+    const int base0 = k == 0 ? 0 : a.W - k;  // source index of output column 0
+    const int W4 = a.W >> 2, cA0 = base0 >> 2;
+    switch (base0 & 3) {
+      case 0: shift_row_vec<0>(src, dst, W4, cA0, lane); break;
+      case 1: shift_row_vec<1>(src, dst, W4, cA0, lane); break;
+      case 2: shift_row_vec<2>(src, dst, W4, cA0, lane); break;
+      default: shift_row_vec<3>(src, dst, W4, cA0, lane); break;
+    }
+    return;
+  }
+  for (int x = lane; x < a.W; x += 32) {
     int sx = x - k;
     if (sx < 0) sx += a.W;
-    dst[x] = src[sx];
+    __stcs(dst + x, __ldg(src + sx));
   }
 }
 
