@@ -110,6 +110,7 @@ struct RangeDev {
   const int* colmap;
   const int* start_tab;
   const int* len_tab;
+  double alpha;               // §4 scale: >= 1 lets pass 1 load image rows by TMA (dilation)
   int w_content, x_lo, x_hi;  // scratch signed x range (pass 1)
   int out_lo, out_hi;         // signed x range covered by pass 2 tiles
 };
@@ -399,7 +400,11 @@ int run_orientation(const fht_image* img, const Frame& f, const Slot* slots, int
     p1.scratch_img_rows = (int64_t)nq * f.Hp;
     const bool pitch16 = aligned16(img->data) && (img->row_stride * es) % 16 == 0 &&
                          (img->batch == 1 || (img->batch_stride * es) % 16 == 0);
-    p1.fill_tma = !rg && pitch16;
+#ifndef FHT_RANGE_TMA
+#define FHT_RANGE_TMA 1
+#endif
+    // range: TMA rows + shared-memory gather when a tile row's source span fits one row load
+    p1.fill_tma = pitch16 && (!rg || (FHT_RANGE_TMA && rg->alpha >= 1.0));
     p1.fill_vec = f.m >= 2 && (es == 1 ? ((reinterpret_cast<uintptr_t>(img->data) & 3) == 0 &&
                                           img->row_stride % 4 == 0 && (img->batch == 1 || img->batch_stride % 4 == 0))
                                        : pitch16);
@@ -765,6 +770,7 @@ Frame range_frame(const fht_image* img, const fht_angle_plan* plan) {
 RangeDev range_geometry(const Frame& f, const fht_angle_plan* plan) {
   RangeDev rg{};
   rg.w_content = (int)plan->w_content;
+  rg.alpha = plan->alpha;
   rg.x_lo = (int)plan->e_min - ((1 << f.m) - 1);
   rg.x_hi = (int)(plan->e_max + plan->w_content);
   // pass-2 signed columns: [min_s start_s, max_s start_s + W'); start_s in [e_min-(Hp-1), e_max]

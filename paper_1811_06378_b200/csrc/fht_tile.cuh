@@ -382,7 +382,12 @@ struct P1Params {
 // The butterfly part is instantiated per sign (SIG); the fills are sign-independent (they only
 // need the input origin Xa) and exist once per kernel, which keeps the kernel's code footprint
 // inside the instruction cache.
-template <typename Tin, int R, int SIG, typename Tsrc>
+constexpr int kNoRow = -2147483647 - 1;  // range fill: the row has no content in this tile
+
+// FILL = 1 (§4 range loader, sigma = +1): tsrc holds, per row rho, the image row y0 + rho from
+// column rowoff[rho] on (TMA); the transformed row T(x', y) = I[y][colmap[x' - e_y]] (P:146,
+// P:152) is gathered from it through colmap, e_y = erow[rho].
+template <typename Tin, int R, int SIG, typename Tsrc, int FILL = 0>
 __device__ __noinline__ void p1_tail(const CUtensorMap* tm_scr, const P1Params& p, const P1Slot& sl, int img,
                                      int strip, int X, const Tsrc* tsrc, int tpitch, int fa_pitch, bool bars) {
   using A = typename AccOf<Tin>::type;
@@ -394,7 +399,30 @@ __device__ __noinline__ void p1_tail(const CUtensorMap* tm_scr, const P1Params& 
   const int* soff = rowoff + 64;
   uint64_t* bar = reinterpret_cast<uint64_t*>(tab + 768);
   A w[kTPW<R>][1 << S::b][VB];
-  tile_fht<R, SIG, A>(tsrc, tpitch, rowoff, buf, fa_pitch, w, bars ? bar : nullptr);
+  if constexpr (FILL == 1) {
+    constexpr int NA = 1 << S::a;
+    const int* erow = soff + 64;
+    const int lane = threadIdx.x & 31;
+    auto load = [&](int blk, A (&v)[NA][VA]) {
+      mbar_wait0(bar + blk);
+#pragma unroll
+      for (int r = 0; r < NA; ++r) {
+        const int rho = blk * NA + r;
+        const int a0 = rowoff[rho], u0 = X + lane * VA - erow[rho];
+#pragma unroll
+        for (int q = 0; q < VA; ++q) {
+          const int u = u0 + q;
+          A val = A(0);
+          if (a0 != kNoRow && (unsigned)u < (unsigned)p.w_content)
+            val = static_cast<A>(tsrc[rho * tpitch + (__ldg(p.colmap + u) - a0)]);
+          v[r][q] = val;
+        }
+      }
+    };
+    tile_fht_ld<R, SIG, A>(load, buf, fa_pitch, w);
+  } else {
+    tile_fht<R, SIG, A>(tsrc, tpitch, rowoff, buf, fa_pitch, w, bars ? bar : nullptr);
+  }
   stage_rows<R, SIG, A>(w, buf, soff, p.TX, p.TX);  // dense [NR][TX]: the box layout
   // ---- store F_m[strip][j] for all j in ONE box {TX, 1, NR} of the 3-D scratch view
   // [z*2^m + j][strip][column] (z = image-in-chunk * nq + slot); column X - xlo is 16-B aligned
@@ -411,12 +439,16 @@ __device__ __noinline__ void p1_tail(const CUtensorMap* tm_scr, const P1Params& 
   if (threadIdx.x == 0) tma_wait_read();
 }
 
-template <typename Tin, int R, typename Tsrc>
+template <typename Tin, int R, typename Tsrc, int FILL = 0>
 __device__ __forceinline__ void p1_tail_sig(int sigma, const CUtensorMap* tm_scr, const P1Params& p, const P1Slot& sl,
                                             int img, int strip, int X, const Tsrc* tsrc, int tpitch, int fa_pitch,
                                             bool bars = false) {
-  if (sigma > 0) p1_tail<Tin, R, 1>(tm_scr, p, sl, img, strip, X, tsrc, tpitch, fa_pitch, bars);
-  else p1_tail<Tin, R, -1>(tm_scr, p, sl, img, strip, X, tsrc, tpitch, fa_pitch, bars);
+  if constexpr (FILL == 1) {  // the range frame is sigma = +1 only
+    p1_tail<Tin, R, 1, Tsrc, 1>(tm_scr, p, sl, img, strip, X, tsrc, tpitch, fa_pitch, true);
+  } else {
+    if (sigma > 0) p1_tail<Tin, R, 1>(tm_scr, p, sl, img, strip, X, tsrc, tpitch, fa_pitch, bars);
+    else p1_tail<Tin, R, -1>(tm_scr, p, sl, img, strip, X, tsrc, tpitch, fa_pitch, bars);
+  }
 }
 
 template <typename Tin, int R>
@@ -437,6 +469,52 @@ __device__ __forceinline__ void p1_body(const CUtensorMap* tm_img0, const CUtens
   const int y0 = strip * NR;
   const int Xa = sl.sigma > 0 ? X : X - (WA - WC);  // x of input index e = 0
 
+  if (p.range && p.fill_tma) {
+    // ---- §4 range loader by TMA (alpha >= 1: a tile row's 288 transformed columns come from at
+    // most 289 consecutive image columns, colmap being a dilation): row rho = image row y0 + rho
+    // from the aligned-down column of colmap[max(0, Xa - e_y)]; the transform is gathered from
+    // shared memory in the sub-pass-A loader. Every warp loads its own blocks' rows.
+    constexpr int AL = 16 / sizeof(Tin);
+    constexpr int TP = sizeof(Tin) == 1 ? TMA_PITCH_U8 : TMA_PITCH;
+    constexpr uint32_t row_bytes = sizeof(Tin) == 1 ? 256 + 48 : (256 + 36) * 4;
+    constexpr int NA = 1 << S::a, NBk = 1 << S::b, NW = S::nw;
+    Tin* tile = reinterpret_cast<Tin*>(sizeof(Tin) == 1 ? smem_raw + main_buf_bytes(R) : smem_raw);
+    int* erow = soff + 64;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int b = warp; b < NBk; b += NW) {
+      const int rho = b * NA + lane, y = y0 + rho;
+      int a0 = kNoRow, e = 0;
+      bool ne = false;
+      if (lane < NA) {
+        if (y < p.img_h) {
+          e = __ldg(p.e_tab + y);
+          const int u0 = Xa - e;
+          if (u0 < p.w_content && u0 + WA > 0) {
+            a0 = __ldg(p.colmap + max(0, u0)) & ~(AL - 1);
+            ne = true;
+          }
+        }
+        rowoff[rho] = a0;
+        erow[rho] = e;
+        soff[rho] = 0;
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, ne);
+      if (lane == 0) {
+        mbar_init(bar + b);
+        mbar_expect_tx(bar + b, (uint32_t)__popc(m) * row_bytes);
+      }
+      __syncwarp();
+      if (ne) {
+        Tin* d = tile + rho * TP;
+        tma_load_3d(tm_img0, d, bar + b, a0, y, img);
+        tma_load_3d(tm_img1, d + 256, bar + b, a0 + 256, y, img);
+      }
+    }
+    __syncwarp();
+    p1_tail_sig<Tin, R, Tin, 1>(1, tm_scr, p, sl, img, strip, X, static_cast<const Tin*>(tile), TP,
+                                sizeof(Tin) == 1 ? FA_PITCH : TMA_PITCH);
+    return;
+  }
   if (!sl.transposed && p.fill_tma) {
     // ---- TMA: NR image rows, columns [Xa, Xa + 288) from the 16-byte aligned column below
     constexpr int AL = 16 / sizeof(Tin);
