@@ -290,9 +290,11 @@ struct P1Maps {
 };
 template <typename Tin, int R>
 cudaError_t launch_p1_t(dim3 grid, const P1Maps& m, const v2::P1Params& a, cudaStream_t st) {
-  const size_t smem = v2::p1_smem_bytes(R, sizeof(Tin) == 1);
+  // range launches with the TMA loader also stage the strip's colmap slice (kColmapStageBytes)
+  const size_t smem = v2::p1_smem_bytes(R, sizeof(Tin) == 1) + (a.range && a.fill_tma ? v2::kColmapStageBytes : 0);
   static const cudaError_t attr =
-      cudaFuncSetAttribute(v2::k_p1<Tin, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(v2::k_p1<Tin, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)(v2::p1_smem_bytes(R, sizeof(Tin) == 1) + v2::kColmapStageBytes));
   if (attr != cudaSuccess) return attr;
   return launch_pdl(v2::k_p1<Tin, R>, grid, dim3(v2::Split<R>::nw * 32), smem, st, m.img0, m.img1, m.scr, a);
 }

@@ -114,6 +114,9 @@ constexpr size_t kTableBytes = 1024;
 __host__ __device__ constexpr size_t p1_smem_bytes(int R, bool u8) {
   return main_buf_bytes(R) + (u8 ? u8_tile_bytes(R) : 0) + kTableBytes;
 }
+// §4 range loader: the strip's colmap slice staged after the tables (2 KB keeps 5 CTAs/SM at R = 5)
+constexpr int kColmapStage = 512;
+constexpr size_t kColmapStageBytes = kColmapStage * 4;
 __host__ __device__ constexpr size_t p2_smem_bytes(int R) {
   return main_buf_bytes(R) + kTableBytes + 2 * (size_t)(1 << R) * 16;
 }
@@ -402,20 +405,38 @@ __device__ __noinline__ void p1_tail(const CUtensorMap* tm_scr, const P1Params& 
   if constexpr (FILL == 1) {
     constexpr int NA = 1 << S::a;
     const int* erow = soff + 64;
+    const int* cm_s = reinterpret_cast<const int*>(tab + kTableBytes);  // colmap[cm_lo + i]
+    const int cm_lo = reinterpret_cast<const int*>(tab)[224], cm_n = reinterpret_cast<const int*>(tab)[225];
     const int lane = threadIdx.x & 31;
     auto load = [&](int blk, A (&v)[NA][VA]) {
       mbar_wait0(bar + blk);
+      if (cm_n <= kColmapStage) {  // every u of the strip is inside the staged slice
 #pragma unroll
-      for (int r = 0; r < NA; ++r) {
-        const int rho = blk * NA + r;
-        const int a0 = rowoff[rho], u0 = X + lane * VA - erow[rho];
+        for (int r = 0; r < NA; ++r) {
+          const int rho = blk * NA + r;
+          const int a0 = rowoff[rho], u0 = X + lane * VA - erow[rho];
 #pragma unroll
-        for (int q = 0; q < VA; ++q) {
-          const int u = u0 + q;
-          A val = A(0);
-          if (a0 != kNoRow && (unsigned)u < (unsigned)p.w_content)
-            val = static_cast<A>(tsrc[rho * tpitch + (__ldg(p.colmap + u) - a0)]);
-          v[r][q] = val;
+          for (int q = 0; q < VA; ++q) {
+            const int u = u0 + q;
+            A val = A(0);
+            if (a0 != kNoRow && (unsigned)u < (unsigned)p.w_content)
+              val = static_cast<A>(tsrc[rho * tpitch + (cm_s[u - cm_lo] - a0)]);
+            v[r][q] = val;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < NA; ++r) {
+          const int rho = blk * NA + r;
+          const int a0 = rowoff[rho], u0 = X + lane * VA - erow[rho];
+#pragma unroll
+          for (int q = 0; q < VA; ++q) {
+            const int u = u0 + q;
+            A val = A(0);
+            if (a0 != kNoRow && (unsigned)u < (unsigned)p.w_content)
+              val = static_cast<A>(tsrc[rho * tpitch + (__ldg(p.colmap + u) - a0)]);
+            v[r][q] = val;
+          }
         }
       }
     };
@@ -510,7 +531,25 @@ __device__ __forceinline__ void p1_body(const CUtensorMap* tm_img0, const CUtens
         tma_load_3d(tm_img1, d + 256, bar + b, a0 + 256, y, img);
       }
     }
-    __syncwarp();
+    // the strip's colmap slice: e_y is monotonic in y (e_y = floor(g*y + 0.5)), so the u range of
+    // the strip is [Xa - e_max, Xa + 288 - e_min) from its first and last rows; staged while the
+    // row loads are in flight
+    {
+      int* cm_s = reinterpret_cast<int*>(reinterpret_cast<unsigned char*>(rowoff) + kTableBytes);
+      int ulo = 0, n = 0;
+      if (y0 < p.img_h) {
+        const int ea = __ldg(p.e_tab + y0), eb = __ldg(p.e_tab + min(y0 + NR - 1, p.img_h - 1));
+        ulo = max(0, Xa - max(ea, eb));
+        n = max(0, min(p.w_content, Xa + WA - min(ea, eb)) - ulo);
+      }
+      if (n <= kColmapStage)
+        for (int i = threadIdx.x; i < n; i += NT) cm_s[i] = __ldg(p.colmap + ulo + i);
+      if (threadIdx.x == 0) {
+        rowoff[224] = ulo;
+        rowoff[225] = n;
+      }
+      __syncthreads();
+    }
     p1_tail_sig<Tin, R, Tin, 1>(1, tm_scr, p, sl, img, strip, X, static_cast<const Tin*>(tile), TP,
                                 sizeof(Tin) == 1 ? FA_PITCH : TMA_PITCH);
     return;
