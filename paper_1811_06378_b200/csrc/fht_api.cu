@@ -775,9 +775,10 @@ RangeDev range_geometry(const Frame& f, const fht_angle_plan* plan) {
   rg.alpha = plan->alpha;
   rg.x_lo = (int)plan->e_min - ((1 << f.m) - 1);
   rg.x_hi = (int)(plan->e_max + plan->w_content);
-  // pass-2 signed columns: [min_s start_s, max_s start_s + W'); start_s in [e_min-(Hp-1), e_max]
+  // pass-2 signed columns: [min_s start_s, max_s start_s + W'); start_s >= e_min - (Hp-1) ...
   rg.out_lo = (int)plan->e_min - (f.Hp - 1);
-  rg.out_hi = (int)plan->e_max + (int)plan->W;
+  // ... and start_s = min_y (e_y - D_s(y)) <= e_min (D >= 0): no row stores at x >= e_min + W'
+  rg.out_hi = (int)plan->e_min + (int)plan->W;
   return rg;
 }
 

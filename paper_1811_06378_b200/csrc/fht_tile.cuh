@@ -960,8 +960,21 @@ k_p2(const __grid_constant__ CUtensorMap tm_scr0, const __grid_constant__ CUtens
   // tile n of part [lo, hi): X = lo + TX*k, owning TX columns; the last tile of a part sits at
   // hi - (TX + 4) and owns the rest, so its 16-byte aligned store box ends inside the part
   const bool pa = n < sl.ntiles_a;
-  const int lo = pa ? sl.xbeg : sl.xmid, hi = pa ? sl.xmid : sl.xend;
-  const int k = pa ? n : n - sl.ntiles_a, nk = pa ? sl.ntiles_a : sl.ntiles - sl.ntiles_a;
+  int lo = pa ? sl.xbeg : sl.xmid, nk = pa ? sl.ntiles_a : sl.ntiles - sl.ntiles_a;
+  const int hi = pa ? sl.xmid : sl.xend;
+  const int k = pa ? n : n - sl.ntiles_a;
+  if (p.range) {
+    // §4 frame: start_s = min_y (e_y - D_s(y)) is non-increasing in s (D_s(y) is) and
+    // D_s(y) <= Dmax(s) = sum_q ceil((s >> q) / 2), so no row t <= tmax of group j stores left of
+    // e_min - Dmax(tmax) (e_min = xbeg + Hp - 1): the group's tiles start there
+    const int tmax = (j << R) + (1 << R) - 1;
+    int dm = 0;
+    for (int s2 = tmax; s2 > 0; s2 >>= 1) dm += (s2 + 1) >> 1;
+    lo = max(lo, sl.xbeg + p.Hp - 1 - dm);
+    const int boxw = p.TX + WO2;
+    nk = hi <= lo ? 0 : (hi - lo <= boxw ? 1 : 1 + (hi - lo - boxw + p.TX - 1) / p.TX);
+    if (k >= nk) return;
+  }
   const int X = k + 1 < nk ? lo + p.TX * k : max(lo, hi - (p.TX + WO2));
   const int own = k + 1 < nk ? p.TX : hi - X;
   if (sl.sigma > 0) p2_body<A, R, 1>(&tm_scr0, &tm_scr1, &tm0, &tm1, &tm0_box, p, sl, img, j, X, own);
