@@ -502,6 +502,7 @@ __device__ __forceinline__ void p1_body(const CUtensorMap* tm_img0, const CUtens
     Tin* tile = reinterpret_cast<Tin*>(sizeof(Tin) == 1 ? smem_raw + main_buf_bytes(R) : smem_raw);
     int* erow = soff + 64;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    bool any_row = false;  // some row of the tile has transformed content (the warp's blocks)
     for (int b = warp; b < NBk; b += NW) {
       const int rho = b * NA + lane, y = y0 + rho;
       int a0 = kNoRow, e = 0;
@@ -520,6 +521,7 @@ __device__ __forceinline__ void p1_body(const CUtensorMap* tm_img0, const CUtens
         soff[rho] = 0;
       }
       const unsigned m = __ballot_sync(0xffffffffu, ne);
+      any_row |= m != 0u;
       if (lane == 0) {
         mbar_init(bar + b);
         mbar_expect_tx(bar + b, (uint32_t)__popc(m) * row_bytes);
@@ -548,7 +550,21 @@ __device__ __forceinline__ void p1_body(const CUtensorMap* tm_img0, const CUtens
         rowoff[224] = ulo;
         rowoff[225] = n;
       }
-      __syncthreads();
+      if (!__syncthreads_or(any_row)) {
+        // no row of the tile has content (no load was issued): F_m is 0 over the whole tile
+        A* z = reinterpret_cast<A*>(smem_raw);
+        for (int idx = threadIdx.x; idx < NR * p.TX; idx += NT) z[idx] = A(0);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          const int zz = p.z0 + (img - p.img0) * p.nq + (int)(sl.srow0 >> (R + p.L));
+          tma_store_3d_keep(tm_scr, z, X - sl.xlo, strip, zz << R);
+          tma_commit();
+        }
+        pdl_trigger();
+        if (threadIdx.x == 0) tma_wait_read();
+        return;
+      }
     }
     p1_tail_sig<Tin, R, Tin, 1>(1, tm_scr, p, sl, img, strip, X, static_cast<const Tin*>(tile), TP,
                                 sizeof(Tin) == 1 ? FA_PITCH : TMA_PITCH);
