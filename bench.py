@@ -422,7 +422,44 @@ def main():
         torch.cuda.empty_cache()
         return res
 
+    def range_pruned(steps=20):
+        """SURVEY §8(f) f2 on config 4's image: shear-only plan, rows s <= S_max only (2196 of 4096 for
+        [-15, 15]); the Hough rows and their fhtshift written in one pass, as config 4 does."""
+        cc = synth.CONFIGS[4]
+        t_in = torch.from_numpy(synth.batch(4)).to(dev)
+        plan = fht.angle_plan(cc["h"], cc["w"], cc["theta_min"], cc["theta_max"], pruned=True)
+        outs = {}
+
+        def step():
+            outs["h"], outs["s"] = fht.angle_range(t_in, plan, pair=True, out=outs.get("h"), out_shifted=outs.get("s"))
+            return outs["h"].launches
+        n = step()
+        for _ in range(3):
+            step()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            step()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+        nbytes = t_in.numel() * 4 + 2 * plan.rows * plan.W * 4
+        res = {"workload": "c4_range_pruned_f32_4096", "rows": plan.rows, "W": plan.W, "ms_per_step": ms,
+               "gpix_s": cc["h"] * cc["w"] / (ms * 1e-3) / 1e9, "compulsory_bytes": nbytes,
+               "step_gbs": nbytes / (ms * 1e-3) / 1e9, "step_frac_of_measured_hbm": nbytes / (ms * 1e-3) / 1e9 / peak_gbs,
+               "launches_per_step": n, "l2": "working set > L2 (no flush needed)"}
+        del t_in, outs
+        torch.cuda.empty_cache()
+        return res
+
     head = run_config(args.config, args.steps, args.warmup, with_e2e=True)
+    pruned_line = None
+    if not args.no_shift_bench:
+        try:
+            pruned_line = range_pruned()
+        except Exception as e:  # noqa: BLE001 -- report, do not hide
+            pruned_line = {"workload": "c4_range_pruned_f32_4096", "error": repr(e)}
     shift_lines = []
     if not args.no_shift_bench:
         for cid in (5, 4):
@@ -478,6 +515,7 @@ def main():
         "clocks": head["clocks"],
         "configs": extra,
         "fhtshift_standalone": shift_lines,
+        "angle_range_pruned": pruned_line,
     }
     print(json.dumps(line), flush=True)
     if world > 1:

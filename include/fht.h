@@ -85,6 +85,7 @@ typedef struct {
   int64_t w_content; /* w' = ceil(alpha*w) */
   int64_t W;         /* W' */
   int64_t e_min, e_max; /* min / max of e_y over y < h */
+  int64_t rows;         /* output rows: Hp (fht_angle_plan_make), S_max + 1 (fht_angle_plan_make_pruned) */
 } fht_angle_plan;
 
 /* Output (Hough image) descriptor. Fill it with fht_hough_describe(), then set `data`. */
@@ -154,6 +155,17 @@ int fht_full(const fht_image* img, int layout, fht_hough* out, fht_hough* out_sh
 int fht_angle_plan_make(int64_t h, int64_t w, double theta_min_deg, double theta_max_deg,
                         fht_angle_plan* out);
 
+/* Shift-range-pruned plan (north_star "computes only the stages and shift ranges
+ * the restriction needs"): shear only (alpha = 1, w' = w, colmap = identity,
+ * e_y = floor(-k_lo*y + 0.5)), so the slopes [k_lo, k_hi] become QA rows s = (k - k_lo)*(Hp-1) of
+ * the sheared image and only rows s <= S_max = ceil((k_hi - k_lo)*(Hp-1)) are computed and stored
+ * (plan.rows = S_max + 1 <= Hp). W' follows R17 with the spread taken over those rows. Requires
+ * k_hi - k_lo <= 1 (otherwise FHT_ERR_UNSUPPORTED: use fht_angle_plan_make's scaled frame); other
+ * errors as fht_angle_plan_make. fht_angle_range computes a pruned plan on the v2 kernels only
+ * (FHT_ERR_UNSUPPORTED for the degenerate frames of the v1 path). */
+int fht_angle_plan_make_pruned(int64_t h, int64_t w, double theta_min_deg, double theta_max_deg,
+                               fht_angle_plan* out);
+
 /* Angle-range-restricted transform: QA of the virtually sheared+scaled image, the
  * shear and scale fused into the first FHT iteration (pass-1 loader). f32/u8/i32 input. */
 int fht_angle_range(const fht_image* img, const fht_angle_plan* plan, fht_hough* out,
@@ -163,10 +175,10 @@ int fht_angle_range(const fht_image* img, const fht_angle_plan* plan, fht_hough*
 /* §5 fhtshift (R11): out[r][x] = in[r][(x - k_r) mod cols], k_r = ceil((n+s)/2) for
  * sigma=+1 quadrants, ceil((n-s)/2) for sigma=-1, and ceil((W'-len_s)/2) - start_s in RANGE
  * mode. `in` must be unshifted (FHT_ERR_STATE otherwise); `out` must have the same shape and
- * not alias `in`; on success out->shifted = 1. Bit copy: exact for every dtype. One kernel (a warp
- * per row, 16-byte loads/stores when cols, every stride and both bases are 16-byte aligned); RANGE
- * mode first runs the per-row support-table kernel into a stream-ordered allocation of 2*rows ints
- * (cudaMallocAsync / cudaFreeAsync on `stream`). Returns the number of kernels (1 or 2). */
+ * not alias `in`; on success out->shifted = 1. Bit copy: exact for every dtype. One kernel: a warp
+ * per row, 16-byte loads/stores when cols, every stride and both bases are 16-byte aligned; in RANGE
+ * mode each block first reduces its rows' support (start_s, len_s) from an e_y table in shared
+ * memory. Allocates nothing. Returns 1 (kernels enqueued). */
 int fhtshift(const fht_hough* in, fht_hough* out, fht_stream_t stream);
 
 /* Human-readable name of a status code (static string). */

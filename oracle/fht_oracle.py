@@ -309,6 +309,7 @@ class AnglePlan:
     w_content: int     # w' = ceil(alpha * w)
     W: int             # W'
     g: float           # shear in transformed pixels per row: alpha * (-k_lo)
+    rows: int = 0      # output rows: Hp (§4 plan) or S_max + 1 (pruned plan); 0 means Hp
 
 
 def shear_offsets(g: float, n: int) -> np.ndarray:
@@ -347,7 +348,36 @@ def angle_plan(h: int, w: int, theta_min_deg: float, theta_max_deg: float,
     D = pattern_offsets(Hp)[:, :h]                       # [s][y], y < h only (rows >= h are empty)
     spread = (e[None, :] - D).max(axis=1) - (e[None, :] - D).min(axis=1)
     W = w_content + max(Hp, int(spread.max()) + 1)       # R17: no two unwrapped lines fold together
-    return AnglePlan(theta_min_deg, theta_max_deg, k_lo, k_hi, alpha, h, w, Hp, w_content, W, g)
+    return AnglePlan(theta_min_deg, theta_max_deg, k_lo, k_hi, alpha, h, w, Hp, w_content, W, g, Hp)
+
+
+def angle_plan_pruned(h: int, w: int, theta_min_deg: float, theta_max_deg: float,
+                      k_lo: float | None = None, k_hi: float | None = None) -> AnglePlan:
+    """Shift-range-pruned plan: shear only (P:132 shear law; alpha = 1, so colmap is the identity
+    and w' = w). The slopes [k_lo, k_hi] become slopes [0, k_hi - k_lo] of the sheared image, i.e. its QA
+    rows s = (k - k_lo)(Hp - 1) (R19), so only rows s <= S_max = ceil((k_hi - k_lo)(Hp - 1)) are
+    needed -- the paper's point that the restricted transform costs less. Needs k_hi - k_lo <= 1
+    (the rows must fit QA); W' by R17 over the kept rows."""
+    if not (-90.0 < theta_min_deg < theta_max_deg < 90.0):
+        raise ValueError("need -90 < theta_min < theta_max < 90")
+    if k_lo is None:
+        k_lo = math.tan(math.radians(theta_min_deg))
+    if k_hi is None:
+        k_hi = math.tan(math.radians(theta_max_deg))
+    if not k_hi - k_lo <= 1.0:
+        raise ValueError("pruned plan needs k_hi - k_lo <= 1")
+    Hp = next_pow2(h)
+    rows = min(Hp, int(math.ceil((k_hi - k_lo) * (Hp - 1) - _EPS)) + 1)
+    g = -k_lo
+    e = shear_offsets(g, h)
+    D = pattern_offsets(Hp)[:rows, :h]
+    spread = (e[None, :] - D).max(axis=1) - (e[None, :] - D).min(axis=1)
+    W = w + max(Hp, int(spread.max()) + 1)
+    return AnglePlan(theta_min_deg, theta_max_deg, k_lo, k_hi, 1.0, h, w, Hp, w, W, g, rows)
+
+
+def plan_rows(plan: AnglePlan) -> int:
+    return plan.rows if plan.rows else plan.Hp
 
 
 def transformed_image(img: np.ndarray, plan: AnglePlan) -> np.ndarray:
@@ -370,7 +400,8 @@ def angle_range(img: np.ndarray, plan: AnglePlan, tier: int = 2) -> np.ndarray:
     """H_{+1}(T) with cyclic width W' -- the QA transform of the sheared and scaled image."""
     T = transformed_image(img, plan)
     fr = Frame(rows=T, sigma=+1, h=plan.h, w=plan.W, Hp=plan.Hp, W=plan.W)
-    return hough_of_frame_recursive(fr) if tier == 2 else hough_of_frame_direct(fr)
+    H = hough_of_frame_recursive(fr) if tier == 2 else hough_of_frame_direct(fr)
+    return H[: plan_rows(plan)]      # a pruned plan keeps rows s <= S_max of the same transform
 
 
 def range_cells_direct(img: np.ndarray, plan: AnglePlan, cells) -> np.ndarray:
@@ -398,7 +429,7 @@ def angle_of_row(s: int, plan: AnglePlan) -> float:
 def range_support(plan: AnglePlan) -> tuple[np.ndarray, np.ndarray]:
     """(start_s, len_s): the unwrapped meaningful run of each output row (R11 generic rule)."""
     e = shear_offsets(plan.g, plan.h)
-    D = pattern_offsets(plan.Hp)[:, : plan.h]
+    D = pattern_offsets(plan.Hp)[: plan_rows(plan), : plan.h]
     v = e[None, :] - D
     start = v.min(axis=1)
     length = v.max(axis=1) - start + plan.w_content

@@ -178,10 +178,12 @@ def full(t: torch.Tensor, layout: str = "quads", shifted: bool = False, pair: bo
     return _finish(res, n, shifted, pair)
 
 
-def angle_plan(h: int, w: int, theta_min_deg: float, theta_max_deg: float) -> FhtAnglePlan:
+def angle_plan(h: int, w: int, theta_min_deg: float, theta_max_deg: float, pruned: bool = False) -> FhtAnglePlan:
+    """§4 plan (scale + shear, all Hp rows), or with pruned=True the shift-range-pruned plan (shear
+    only, rows s <= S_max)."""
     p = FhtAnglePlan()
-    _lib.check("fht_angle_plan_make", _lib.lib.fht_angle_plan_make(h, w, float(theta_min_deg),
-                                                                    float(theta_max_deg), ctypes.byref(p)))
+    name = "fht_angle_plan_make_pruned" if pruned else "fht_angle_plan_make"
+    _lib.check(name, getattr(_lib.lib, name)(h, w, float(theta_min_deg), float(theta_max_deg), ctypes.byref(p)))
     return p
 
 

@@ -25,7 +25,7 @@ STATUS = {
 
 EXPORTED = (
     "fht_hough_describe", "fht_workspace_bytes", "fht_quadrant", "fht_full", "fht_angle_plan_make",
-    "fht_angle_range", "fhtshift", "fht_status_string",
+    "fht_angle_plan_make_pruned", "fht_angle_range", "fhtshift", "fht_status_string",
 )
 
 
@@ -43,6 +43,7 @@ class FhtAnglePlan(ctypes.Structure):
         ("k_lo", ctypes.c_double), ("k_hi", ctypes.c_double), ("alpha", ctypes.c_double), ("g", ctypes.c_double),
         ("h", ctypes.c_int64), ("w", ctypes.c_int64), ("Hp", ctypes.c_int64),
         ("w_content", ctypes.c_int64), ("W", ctypes.c_int64), ("e_min", ctypes.c_int64), ("e_max", ctypes.c_int64),
+        ("rows", ctypes.c_int64),
     ]
 
 
@@ -81,13 +82,14 @@ def _load():
     lib.fht_quadrant.argtypes = [P(FhtImage), i32, i64, P(FhtHough), P(FhtHough), vp, sz, vp, P(FhtExecOpts)]
     lib.fht_full.argtypes = [P(FhtImage), i32, P(FhtHough), P(FhtHough), vp, sz, vp, P(FhtExecOpts)]
     lib.fht_angle_plan_make.argtypes = [i64, i64, dbl, dbl, P(FhtAnglePlan)]
+    lib.fht_angle_plan_make_pruned.argtypes = [i64, i64, dbl, dbl, P(FhtAnglePlan)]
     lib.fht_angle_range.argtypes = [P(FhtImage), P(FhtAnglePlan), P(FhtHough), P(FhtHough), vp, sz, vp,
                                     P(FhtExecOpts)]
     lib.fhtshift.argtypes = [P(FhtHough), P(FhtHough), vp]
     lib.fht_status_string.argtypes = [i32]
     lib.fht_status_string.restype = ctypes.c_char_p
-    for name in ("fht_hough_describe", "fht_quadrant", "fht_full", "fht_angle_plan_make", "fht_angle_range",
-                 "fhtshift"):
+    for name in ("fht_hough_describe", "fht_quadrant", "fht_full", "fht_angle_plan_make", "fht_angle_plan_make_pruned",
+                 "fht_angle_range", "fhtshift"):
         getattr(lib, name).restype = i32
     return lib
 

@@ -111,6 +111,7 @@ struct RangeDev {
   const int* start_tab;
   const int* len_tab;
   double alpha;               // §4 scale: >= 1 lets pass 1 load image rows by TMA (dilation)
+  int rows;                   // output rows (plan.rows; < Hp for a pruned plan, f2)
   int w_content, x_lo, x_hi;  // scratch signed x range (pass 1)
   int out_lo, out_hi;         // signed x range covered by pass 2 tiles
 };
@@ -389,7 +390,9 @@ int run_orientation(const fht_image* img, const Frame& f, const Slot* slots, int
   const fht_hough* any = outs.d[0] ? outs.d[0] : outs.d[1];
 
   if (sp.v2) {
-    const int nstrips = 1 << f.L, ngroups = 1 << f.m;
+    const int nstrips = 1 << f.L;
+    // pass-2 groups j = rows t >> L: a pruned range plan (f2) needs only t < rows
+    const int ngroups = rg && rg->rows < f.Hp ? (rg->rows + nstrips - 1) / nstrips : 1 << f.m;
     const size_t es = dtype_size(img->dtype);
     v2::P1Params p1{};
     p1.img = img->data;
@@ -478,10 +481,12 @@ int run_orientation(const fht_image* img, const Frame& f, const Slot* slots, int
       s.rsign = slots[q].row_sign;
       s.skip = slots[q].skip_t;
     }
+    p2.rows_out = 1 << 30;
     if (rg) {
       p2.range = 1;
       p2.start_tab = rg->start_tab;
       p2.len_tab = rg->len_tab;
+      p2.rows_out = rg->rows;
     }
     P2Maps m2;
     CUtensorMap* tm_out[2] = {&m2.out0, &m2.out1};
@@ -512,7 +517,7 @@ int run_orientation(const fht_image* img, const Frame& f, const Slot* slots, int
       auto fn = encode_fn();
       cuuint64_t dims[3] = {(cuuint64_t)sp.pitch, (cuuint64_t)nstrips, (cuuint64_t)(scr_rows / nstrips)};
       cuuint64_t strides[2] = {(cuuint64_t)(sp.pitch * 4), (cuuint64_t)(sp.pitch * 4 * nstrips)};
-      cuuint32_t box[3] = {(cuuint32_t)p1.TX, 1, (cuuint32_t)(1 << f.m)};
+      cuuint32_t box[3] = {(cuuint32_t)p1.TX, 1, (cuuint32_t)ngroups};  // shifts j < ngroups only
       cuuint32_t e[3] = {1, 1, 1};
       if (!fn || fn(&m1.scr, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_INT32, 3, ws, dims, strides,
                     box, e, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
@@ -590,6 +595,7 @@ int run_orientation(const fht_image* img, const Frame& f, const Slot* slots, int
       }
       p2.ntiles = ntile2;
       p2.m = f.m;
+      p2.ngroups = ngroups;
       dim3 g2((unsigned)(ntile2 * ngroups * nb * nq));
       e = f32 ? launch_p2<float>(f.L, g2, m2, p2, st) : launch_p2<int>(f.L, g2, m2, p2, st);
       if (e != cudaSuccess) {
@@ -773,6 +779,7 @@ RangeDev range_geometry(const Frame& f, const fht_angle_plan* plan) {
   RangeDev rg{};
   rg.w_content = (int)plan->w_content;
   rg.alpha = plan->alpha;
+  rg.rows = (int)plan->rows;
   rg.x_lo = (int)plan->e_min - ((1 << f.m) - 1);
   rg.x_hi = (int)(plan->e_max + plan->w_content);
   // pass-2 signed columns: [min_s start_s, max_s start_s + W'); start_s >= e_min - (Hp-1) ...
@@ -806,17 +813,25 @@ const char* fht_status_string(int s) {
   return "unknown status";
 }
 
-int fht_angle_plan_make(int64_t h, int64_t w, double tmin, double tmax, fht_angle_plan* out) {
+namespace {
+int plan_make(int64_t h, int64_t w, double tmin, double tmax, bool pruned, fht_angle_plan* out) {
   if (!out || h < 1 || w < 1) return FHT_ERR_ARG;
   if (!(tmin > -90.0 && tmin < tmax && tmax < 90.0)) return FHT_ERR_ARG;
   const double deg = M_PI / 180.0;
   const double k_lo = std::tan(tmin * deg), k_hi = std::tan(tmax * deg);
-  const double alpha = 1.0 / (k_hi - k_lo);
+  const double alpha = pruned ? 1.0 : 1.0 / (k_hi - k_lo);
   if (!(alpha * (double)w >= 1.0)) return FHT_ERR_ARG;
+  if (pruned && !(k_hi - k_lo <= 1.0)) return FHT_ERR_UNSUPPORTED;
   const int64_t Hp = next_pow2(h);
   if (Hp > 4096 || h > 4096) return FHT_ERR_UNSUPPORTED;
-  const int64_t w_content = (int64_t)std::ceil(alpha * (double)w - 1e-9);
+  const int64_t w_content = pruned ? w : (int64_t)std::ceil(alpha * (double)w - 1e-9);
   const double g = alpha * (-k_lo);
+  // f2: rows s = (k - k_lo)(Hp - 1) for k in [k_lo, k_hi] (R19 in the sheared frame)
+  int64_t rows = Hp;
+  if (pruned) {
+    const int64_t s_max = (int64_t)std::ceil((k_hi - k_lo) * (double)(Hp - 1) - 1e-9);
+    rows = s_max + 1 < Hp ? s_max + 1 : Hp;
+  }
   // e_y and the largest per-row spread of e_y - D_s(y) over y < h (R17)
   const int K = ilog2(Hp);
   int* e = new int[h];
@@ -828,7 +843,7 @@ int fht_angle_plan_make(int64_t h, int64_t w, double tmin, double tmax, fht_angl
     e_max = e[y] > e_max ? e[y] : e_max;
   }
   int64_t spread_max = 0;
-  for (int64_t s = 0; s < Hp; ++s) {
+  for (int64_t s = 0; s < rows; ++s) {
     // D_s(y) by lowest-set-bit recurrence: bit p of y carries weight ceil((s >> (K-1-p))/2)
     int mn = 1 << 30, mx = -(1 << 30);
     for (int64_t y = 0; y < h; ++y) {
@@ -860,8 +875,18 @@ int fht_angle_plan_make(int64_t h, int64_t w, double tmin, double tmax, fht_angl
   p.W = w_content + (Hp > spread_max + 1 ? Hp : spread_max + 1);
   p.e_min = e_min;
   p.e_max = e_max;
+  p.rows = rows;
   *out = p;
   return FHT_OK;
+}
+}  // namespace
+
+int fht_angle_plan_make(int64_t h, int64_t w, double tmin, double tmax, fht_angle_plan* out) {
+  return plan_make(h, w, tmin, tmax, false, out);
+}
+
+int fht_angle_plan_make_pruned(int64_t h, int64_t w, double tmin, double tmax, fht_angle_plan* out) {
+  return plan_make(h, w, tmin, tmax, true, out);
 }
 
 int fht_hough_describe(int mode, int layout, int quadrant, const fht_image* img, const fht_angle_plan* plan,
@@ -898,8 +923,9 @@ int fht_hough_describe(int mode, int layout, int quadrant, const fht_image* img,
     d.cols = d.Hp + d.Wp;
   } else if (mode == FHT_MODE_RANGE) {
     if (!plan || plan->h != img->h || plan->w != img->w) return FHT_ERR_ARG;
+    if (plan->rows < 1 || plan->rows > plan->Hp) return FHT_ERR_ARG;
     d.nquad = 1;
-    d.rows = plan->Hp;
+    d.rows = plan->rows;
     d.cols = plan->W;
     d.plan = *plan;
   } else {
@@ -1026,6 +1052,7 @@ int fht_angle_range(const fht_image* img, const fht_angle_plan* plan, fht_hough*
   if ((s = check_frame_supported(f))) return s;
   RangeDev rg = range_geometry(f, plan);
   const ScratchPlan sp = scratch_plan(f, 1, 1, &rg);
+  if (plan->rows < f.Hp && !sp.v2) return FHT_ERR_UNSUPPORTED;  // pruned plans: v2 kernels only
   // workspace: [scratch][e_tab h][colmap w'][start Hp][len Hp]
   const size_t scratch = (sp.bytes + 255) & ~size_t(255);
   int* tab = reinterpret_cast<int*>(static_cast<char*>(ws) + scratch);
@@ -1093,44 +1120,25 @@ int fhtshift(const fht_hough* in, fht_hough* out, fht_stream_t stream) {
   for (int64_t st : {in->batch_stride, in->quad_stride, in->row_stride, out->batch_stride, out->quad_stride,
                      out->row_stride})
     a.vec = a.vec && st % 4 == 0;
-  int* tabs = nullptr;
-  int launches = 0;
+  size_t smem = 0;
   if (in->mode == FHT_MODE_QUADRANT) {
     a.Hp = a.Wp = (int)in->rows;  // the quadrant's own row count
   } else if (in->mode == FHT_MODE_FULL) {
     a.Hp = (int)in->Hp;
     a.Wp = (int)in->Wp;
   } else {
-    // per-row support start / length of the range frame (R17) by the §4 table kernel (its row
-    // blocks only), into a stream-ordered scratch of 2*rows ints
-    if (cudaMallocAsync(reinterpret_cast<void**>(&tabs), 2 * sizeof(int) * (size_t)in->rows, (cudaStream_t)stream) !=
-        cudaSuccess)
-      return FHT_ERR_CUDA;
-    RangeTableArgs ta{};
-    ta.g = in->plan.g;
-    ta.alpha = in->plan.alpha;
-    ta.h = (int)in->plan.h;
-    ta.w = (int)in->plan.w;
-    ta.w_content = (int)in->plan.w_content;
-    ta.Hp = (int)in->rows;
-    ta.K = ilog2(in->plan.Hp);
-    ta.start_tab = tabs;
-    ta.len_tab = tabs + in->rows;
-    const int nsb = (ta.Hp + kRangeRowsPerBlock - 1) / kRangeRowsPerBlock;  // no e_tab / colmap blocks
-    k_range_tables<<<nsb, kThreads, (size_t)ta.h * sizeof(int), (cudaStream_t)stream>>>(ta);
-    if (cudaGetLastError() != cudaSuccess) return FHT_ERR_CUDA;
-    a.start_tab = ta.start_tab;
-    a.len_tab = ta.len_tab;
-    ++launches;
+    a.g = in->plan.g;
+    a.h = (int)in->plan.h;
+    a.K = ilog2(in->plan.Hp);
+    a.w_content = (int)in->plan.w_content;
+    smem = (size_t)a.h * sizeof(int);  // e_y table of the block (h <= 4096)
   }
   const int64_t nblk = (a.rows_total + kThreads / 32 - 1) / (kThreads / 32);
-  if (in->dtype == FHT_F32) k_fhtshift<float><<<(unsigned)nblk, kThreads, 0, (cudaStream_t)stream>>>(a);
-  else k_fhtshift<int><<<(unsigned)nblk, kThreads, 0, (cudaStream_t)stream>>>(a);
+  if (in->dtype == FHT_F32) k_fhtshift<float><<<(unsigned)nblk, kThreads, smem, (cudaStream_t)stream>>>(a);
+  else k_fhtshift<int><<<(unsigned)nblk, kThreads, smem, (cudaStream_t)stream>>>(a);
   if (cudaGetLastError() != cudaSuccess) return FHT_ERR_CUDA;
-  ++launches;
-  if (tabs && cudaFreeAsync(tabs, (cudaStream_t)stream) != cudaSuccess) return FHT_ERR_CUDA;
   out->shifted = 1;
-  return launches;
+  return 1;
 }
 
 }  // extern "C"

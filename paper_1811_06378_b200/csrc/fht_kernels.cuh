@@ -270,6 +270,38 @@ __device__ __forceinline__ int shear_e(double g, int y) {
 #define FHT_RANGE_ROWS_PER_BLOCK 8
 #endif
 constexpr int kRangeRowsPerBlock = FHT_RANGE_ROWS_PER_BLOCK;  // one row per warp: 512 blocks for Hp = 4096
+
+// min / max over y < h of e_y - D_s(y) for row s, by one warp (every lane gets the result). e_s: the
+// block's shared e_y table; dh: the warp's 128-entry scratch (reused: ends with __syncwarp).
+__device__ __forceinline__ void row_support_warp(int K, int h, int s, const int* e_s, int* dh, int lane, int& mn,
+                                                 int& mx) {
+  auto wbit = [&](int bit) { return bit < K ? ((s >> (K - 1 - bit)) + 1) >> 1 : 0; };
+  int dl = 0;  // bits 0..4 of y = lane
+  for (int b = 0; b < 5; ++b)
+    if ((lane >> b) & 1) dl += wbit(b);
+  for (int k = lane; k < 128; k += 32) {  // bits 5..11 of y = k
+    int d = 0;
+    for (int b = 0; b < 7; ++b)
+      if ((k >> b) & 1) d += wbit(5 + b);
+    dh[k] = d;
+  }
+  __syncwarp();
+  mn = INT32_MAX;
+  mx = INT32_MIN;
+  for (int k = 0; 32 * k < h; ++k) {
+    const int y = 32 * k + lane;
+    if (y < h) {
+      const int v = e_s[y] - dl - dh[k];
+      mn = min(mn, v);
+      mx = max(mx, v);
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  __syncwarp();  // dh reused by the warp's next row
+}
 __global__ void k_range_tables(const RangeTableArgs a) {
   extern __shared__ int e_s[];          // [h]
   __shared__ int dh_s[8][128];          // per warp: D of the high bits, y >> 5
@@ -281,35 +313,12 @@ __global__ void k_range_tables(const RangeTableArgs a) {
     const int s_end = min(a.Hp, ((int)blockIdx.x + 1) * kRangeRowsPerBlock);
     int* dh = dh_s[warp];
     for (int s = blockIdx.x * kRangeRowsPerBlock + warp; s < s_end; s += nw) {
-      auto wbit = [&](int bit) { return bit < a.K ? ((s >> (a.K - 1 - bit)) + 1) >> 1 : 0; };
-      int dl = 0;  // bits 0..4 of y = lane
-      for (int b = 0; b < 5; ++b)
-        if ((lane >> b) & 1) dl += wbit(b);
-      for (int k = lane; k < 128; k += 32) {  // bits 5..11 of y = k
-        int d = 0;
-        for (int b = 0; b < 7; ++b)
-          if ((k >> b) & 1) d += wbit(5 + b);
-        dh[k] = d;
-      }
-      __syncwarp();
-      int mn = INT32_MAX, mx = INT32_MIN;
-      for (int k = 0; 32 * k < a.h; ++k) {
-        const int y = 32 * k + lane;
-        if (y < a.h) {
-          const int v = e_s[y] - dl - dh[k];
-          mn = min(mn, v);
-          mx = max(mx, v);
-        }
-      }
-      for (int o = 16; o > 0; o >>= 1) {
-        mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-        mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      }
+      int mn, mx;
+      row_support_warp(a.K, a.h, s, e_s, dh, lane, mn, mx);
       if (lane == 0) {
         a.start_tab[s] = mn;
         a.len_tab[s] = mx - mn + a.w_content;
       }
-      __syncwarp();  // dh reused by the warp's next row
     }
     return;
   }
@@ -336,8 +345,8 @@ struct ShiftArgs {
   int quadrant;         // QUADRANT mode
   int Hp, Wp;           // quadrant row counts (QA/QB: Hp, QC/QD: Wp)
   int vec;              // 16-byte path: W, every stride a multiple of 4 elements, bases 16-B aligned
-  const int* start_tab; // RANGE: per-row support start / length (k_range_tables)
-  const int* len_tab;
+  double g;             // RANGE: shear e_y = floor(g*y + 0.5), y < h; K = log2 Hp; w' (R17 support)
+  int h, K, w_content;
 };
 
 __device__ __forceinline__ int quadrant_sigma(int q) { return (q == 0 || q == 3) ? 1 : -1; }
@@ -345,10 +354,6 @@ __device__ __forceinline__ int quadrant_sigma(int q) { return (q == 0 || q == 3)
 // k(s) of output row r (R11, R17): QUADRANT / FULL (QUADS or CONCAT row attribution,
 // P:111-113, R8) by the closed form, RANGE from the per-row support tables.
 __device__ __forceinline__ int shift_amount(const ShiftArgs& a, int r, int qs) {
-  if (a.mode == 2) {
-    int k = (ceil_half(a.W - __ldg(a.len_tab + r)) - __ldg(a.start_tab + r)) % a.W;
-    return k < 0 ? k + a.W : k;
-  }
   int q, s;
   if (a.mode == 1 && a.layout == 1) {
     const int Hp = a.Hp, Wp = a.Wp;
@@ -415,11 +420,25 @@ template <typename T>
 __global__ void __launch_bounds__(kThreads) k_fhtshift(const ShiftArgs a) {
   const int lane = threadIdx.x & 31;
   const int64_t row = (int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+  int k_range = 0;
+  if (a.mode == 2) {
+    // RANGE (R11 generic rule, R17 support): k = ceil((W' - len)/2) - start, start/len of the row by
+    // the §4 table method -- e_y once per block in shared memory, then one warp per row
+    extern __shared__ int e_s[];  // [h]
+    __shared__ int dh_s[kThreads / 32][128];
+    for (int y = threadIdx.x; y < a.h; y += blockDim.x) e_s[y] = shear_e(a.g, y);
+    __syncthreads();
+    if (row >= a.rows_total) return;
+    int mn, mx;
+    row_support_warp(a.K, a.h, (int)(row % a.rows), e_s, dh_s[threadIdx.x >> 5], lane, mn, mx);
+    k_range = (ceil_half(a.W - (mx - mn + a.w_content)) - mn) % a.W;
+    if (k_range < 0) k_range += a.W;
+  }
   if (row >= a.rows_total) return;
   const int r = (int)(row % a.rows);
   const int64_t zq = row / a.rows;  // image * nquad + quadrant slot
   const int img = (int)(zq / a.nquad), qs = (int)(zq % a.nquad);
-  const int k = shift_amount(a, r, qs);
+  const int k = a.mode == 2 ? k_range : shift_amount(a, r, qs);
   const T* src = static_cast<const T*>(a.in) + (int64_t)img * a.in_img_stride + (int64_t)qs * a.in_q_stride +
                  (int64_t)r * a.in_row_stride;
   T* dst = static_cast<T*>(a.out) + (int64_t)img * a.out_img_stride + (int64_t)qs * a.out_q_stride +

@@ -771,7 +771,9 @@ struct P2Params {
   int64_t row0;            // first scratch row of this chunk's buffer
   int nq, img0;
   int ntiles;              // tiles per group (max over slots)
-  int m;                   // log2(#groups)
+  int m;                   // log2(#groups of the transform)
+  int ngroups;             // groups launched (2^m, or ceil(rows_out / 2^L) for a pruned range plan)
+  int rows_out;            // output rows t >= rows_out are neither computed for nor stored (f2)
   int TX;                  // tile stride (columns owned per tile); store box = TX + 4
   int W, Hp, wc;
   int range;
@@ -882,7 +884,7 @@ __device__ __forceinline__ void p2_body(const CUtensorMap* tm_scr0, const CUtens
     ri.d0 = d0;
     ri.mlo = max(X, vlo);
     ri.mhi = min(X + own, vhi);
-    if (t == sl.skip) {
+    if (t == sl.skip || t >= p.rows_out) {
       ri.mhi = ri.mlo;
     } else if (!p.no_tma && xs0 >= vlo && xs0 + min(box, p.W - d0) <= vhi) {
       ri.d0 |= kTmaBit;
@@ -914,6 +916,7 @@ __device__ __forceinline__ void p2_body(const CUtensorMap* tm_scr0, const CUtens
     // plain destination of an interior QUADS tile: every row has the same aligned start and no
     // remainder, rows ascend -> ONE 2-D box {box, NR} from a dense [NR][box] staging plane
     const bool dense = FHT_P2_DENSE && !p.range && !D.shifted && sl.rsign == 1 && (sl.skip < t0 || sl.skip > tmax) &&
+                       tmax < p.rows_out &&
                        (inf[0].d0 & kTmaBit) && inf[0].mlo >= inf[0].mhi;
     const int pitch = dense ? box : ST_PITCH;
     if (!black) {
@@ -967,8 +970,8 @@ k_p2(const __grid_constant__ CUtensorMap tm_scr0, const __grid_constant__ CUtens
   int id = blockIdx.x;
   const int n = id % p.ntiles;
   id /= p.ntiles;
-  const int j = id & ((1 << p.m) - 1);
-  id >>= p.m;
+  const int j = id % p.ngroups;
+  id /= p.ngroups;
   const int qi = id % p.nq;
   const int img = p.img0 + id / p.nq;
   const P2Slot& sl = p.slot[qi];

@@ -24,11 +24,19 @@ def test_header_symbols_exported():
         assert hasattr(L.lib, name)
 
 
-def test_struct_sizes_match_header():
+def test_struct_sizes_match_header(tmp_path):
+    """The ctypes mirrors have the C compiler's sizeof for every struct include/fht.h declares."""
+    import subprocess
     L = _lib()
-    assert ctypes.sizeof(L.FhtImage) == 56
-    assert ctypes.sizeof(L.FhtAnglePlan) == 6 * 8 + 7 * 8
-    assert ctypes.sizeof(L.FhtHough) == 8 + 6 * 4 + 11 * 8 + ctypes.sizeof(L.FhtAnglePlan)
+    src = tmp_path / "sz.c"
+    src.write_text('#include <stdio.h>\n#include "fht.h"\nint main(void) { printf("%zu %zu %zu %zu", '
+                   'sizeof(fht_image), sizeof(fht_angle_plan), sizeof(fht_hough), sizeof(fht_exec_opts)); return 0; }\n')
+    inc = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include")
+    subprocess.run(["gcc", "-I", inc, str(src), "-o", str(tmp_path / "sz")], check=True)
+    got = [int(x) for x in subprocess.run([str(tmp_path / "sz")], capture_output=True, text=True, check=True).stdout.split()]
+    assert got == [ctypes.sizeof(L.FhtImage), ctypes.sizeof(L.FhtAnglePlan), ctypes.sizeof(L.FhtHough),
+                   ctypes.sizeof(L.FhtExecOpts)]
+    assert ctypes.sizeof(L.FhtAnglePlan) == 6 * 8 + 8 * 8
 
 
 def _img(L, h, w, b=1, dt=2, data=4096):
@@ -66,6 +74,25 @@ def test_plan_matches_oracle_rule():
         assert (p.Hp, p.w_content, p.W) == (o.Hp, o.w_content, o.W)
         e = O.shear_offsets(o.g, h)
         assert (p.e_min, p.e_max) == (e.min(), e.max())
+
+
+def test_pruned_plan_matches_oracle_rule():
+    """fht_angle_plan_make_pruned (f2): same scalars, rows and W' as the oracle's pruned plan."""
+    from oracle import fht_oracle as O
+    L = _lib()
+    for h, w, a, b in [(4096, 4096, -15, 15), (64, 48, 5, 40), (33, 17, -20, 0), (16, 16, 0, 45), (128, 96, -26, 18)]:
+        p = L.FhtAnglePlan()
+        assert L.lib.fht_angle_plan_make_pruned(h, w, a, b, ctypes.byref(p)) == 0
+        o = O.angle_plan_pruned(h, w, a, b)
+        assert (p.k_lo, p.k_hi, p.alpha, p.g) == (o.k_lo, o.k_hi, 1.0, o.g)
+        assert (p.Hp, p.w_content, p.W, p.rows) == (o.Hp, o.w_content, o.W, o.rows)
+        d = L.FhtHough()
+        img = _img(L, h, w)
+        assert L.lib.fht_hough_describe(L.FHT_MODE_RANGE, 0, 0, ctypes.byref(img), ctypes.byref(p), ctypes.byref(d)) == 0
+        assert (d.rows, d.cols) == (o.rows, o.W)
+    p = L.FhtAnglePlan()
+    assert L.lib.fht_angle_plan_make(64, 64, -15, 15, ctypes.byref(p)) == 0 and p.rows == p.Hp
+    assert L.lib.fht_angle_plan_make_pruned(64, 64, -30, 30, ctypes.byref(p)) == -5   # k_hi - k_lo > 1
 
 
 def test_plan_errors():

@@ -115,6 +115,58 @@ def test_angle_range_small(fht, O, shape, dt):
         assert np.array_equal(fr.view[0, 0].cpu().numpy(), want_s)
 
 
+PRUNED_RANGES = [(-15, 15), (5, 40), (-30, -2), (0, 45), (-26, 18), (1, 2), (0, 10)]
+
+
+@pytest.mark.parametrize("shape", [(16, 16), (33, 17), (64, 48), (128, 128), (200, 136)], ids=str)
+@pytest.mark.parametrize("dt", ["u8", "f32"])
+def test_angle_range_pruned_small(fht, O, shape, dt):
+    """f2: shear-only plan, rows s <= S_max only; all cells against the oracle (same transform, first
+    rows), its fhtshift standalone and fused."""
+    from synth import random_image
+    img = random_image(shape, dt, seed=shape[0] + 5 * shape[1])
+    t = dev(img)
+    for tmin, tmax in PRUNED_RANGES:
+        p = fht.angle_plan(*shape, tmin, tmax, pruned=True)
+        op = O.angle_plan_pruned(*shape, tmin, tmax, k_lo=p.k_lo, k_hi=p.k_hi)
+        assert (op.W, op.rows) == (p.W, p.rows)
+        r = fht.angle_range(t, p)
+        rs = fht.fhtshift(r)
+        fr, fs = fht.angle_range(t, p, pair=True)
+        torch.cuda.synchronize()
+        got = r.view[0, 0].cpu().numpy()
+        assert got.shape == (op.rows, op.W)
+        check(got, O.angle_range(img, op), dt != "f32")
+        want_s = O.fhtshift_range(got, op)
+        assert np.array_equal(rs.view[0, 0].cpu().numpy(), want_s)
+        assert np.array_equal(fr.view[0, 0].cpu().numpy(), got)
+        assert np.array_equal(fs.view[0, 0].cpu().numpy(), want_s)
+
+
+def test_angle_range_pruned_c4_image(fht, O):
+    """f2 on config 4's 4096^2 f32 image, [-15, 15]: 2196 of 4096 rows; sampled cells by the direct
+    pattern sums, row conservation on every row, fhtshift rows."""
+    import synth
+    img = synth.batch(4)[0]
+    p = fht.angle_plan(4096, 4096, -15.0, 15.0, pruned=True)
+    op = O.angle_plan_pruned(4096, 4096, -15.0, 15.0, k_lo=p.k_lo, k_hi=p.k_hi)
+    assert (p.rows, p.W) == (op.rows, op.W) == (2196, 8192)
+    r, rs = fht.angle_range(dev(img), p, pair=True)
+    torch.cuda.synchronize()
+    got = r.view[0, 0].cpu().numpy()
+    rng = np.random.default_rng(44)
+    start, length = O.range_support(op)
+    extra = [(sr, int((start[sr] + dx) % op.W)) for sr in (0, 1, 1097, 2195) for dx in (-1, 0, 1, int(length[sr]) - 1)]
+    cells = _sample_cells(op.rows, op.W, 2048, rng, extra)
+    check(np.array([got[a, b] for a, b in cells], dtype=np.float32), O.range_cells_direct(img, op, cells), False)
+    total = float(img.astype(np.float64).sum())
+    assert np.all(np.abs(got.astype(np.float64).sum(axis=1) - total) <= 1e-4 * total)
+    gs = rs.view[0, 0].cpu().numpy()
+    k = O.fhtshift_amounts_range(op)
+    for row in (0, 17, 1098, 2195):
+        assert np.array_equal(gs[row], np.roll(got[row], int(k[row])))
+
+
 def test_strided_batch_input(fht, O):
     """Non-contiguous rows (a column slice of a wider tensor) and a batch of 3."""
     from synth import random_image

@@ -287,6 +287,51 @@ def test_range_peak_location():
         assert abs(s_peak - p.alpha * (k - p.k_lo) * (P - 1)) <= 2.0
 
 
+# ---------------------------------------------------------------- shift-range-pruned plan (f2)
+@pytest.mark.parametrize("shape", [(8, 8), (16, 11), (5, 7), (32, 32), (64, 40)])
+@pytest.mark.parametrize("tmax", [10.0, 30.0, 45.0])
+def test_pruned_zero_shear_is_qa_rows(shape, tmax):
+    """theta in [0, tmax] needs no shear (k_lo = 0): the pruned transform is exactly the first
+    ceil(tan(tmax)(Hp - 1)) + 1 rows of the QA quadrant (SURVEY §8(f) f2 pin; R19 row -> slope)."""
+    img = random_image(shape, "i32", seed=shape[0] * 7 + int(tmax))
+    p = O.angle_plan_pruned(*shape, 0.0, tmax)
+    Hp = O.next_pow2(shape[0])
+    assert p.rows == min(Hp, math.ceil(math.tan(math.radians(tmax)) * (Hp - 1) - 1e-9) + 1)
+    qa = O.hough_recursive(img, O.QA)
+    assert p.W == qa.shape[1]
+    assert (O.angle_range(img, p) == qa[: p.rows]).all()
+
+
+def test_pruned_conservation_and_tiers():
+    """alpha = 1: T holds every pixel once, so every kept row sums to the image total; tier 1
+    (direct pattern sums) equals tier 2 on every kept cell."""
+    img = random_image((32, 24), "i32", seed=11)
+    for tmin, tmax in [(-15, 15), (5, 40), (-30, -2), (-26, 18)]:
+        p = O.angle_plan_pruned(32, 24, tmin, tmax)
+        R = O.angle_range(img, p)
+        assert R.shape == (p.rows, p.W)
+        assert (R.sum(axis=1) == img.sum()).all()
+        assert (R == O.angle_range(img, p, tier=1)).all()
+        start, length = O.range_support(p)
+        assert len(start) == p.rows and (length <= p.W).all()
+
+
+def test_pruned_peak_location():
+    """A digital line of slope k in [k_lo, k_hi] peaks at row (k - k_lo)(Hp - 1) of the sheared frame
+    (within 2 rows: the shear is rounded per row)."""
+    P = 64
+    for tmin, tmax, k in [(-15, 15, 0.1), (-15, 15, -0.2), (10, 40, 0.5), (-40, -10, -0.4)]:
+        img = np.zeros((P, P), dtype=np.int64)
+        ys = np.arange(P)
+        xs = np.floor(20 + k * ys + 0.5).astype(int) if k > 0 else np.floor(44 + k * ys + 0.5).astype(int)
+        img[ys, xs] = 1
+        p = O.angle_plan_pruned(P, P, tmin, tmax)
+        R = O.angle_range(img, p)
+        s_peak = np.unravel_index(np.argmax(R), R.shape)[0]
+        assert abs(s_peak - (k - p.k_lo) * (P - 1)) <= 2.0
+        assert R.max() >= P // 2          # the line's pixels concentrate in one cell (not exact: DDA != dyadic)
+
+
 def test_range_support_no_fold():
     """R17: with W' chosen by the rule, each row's unwrapped support fits in W' columns."""
     for tmin, tmax in [(-15, 15), (5, 40), (-80, 80), (1, 2)]:
