@@ -30,6 +30,13 @@ Functions and what pins them (tests/test_oracle_pins.py):
   self-consistency and the approximate peak location are checked.
 * `fhtshift_amounts` / `fhtshift` -- §5 (R11). Pinned by permutation, contiguity of
   the meaningful run, width law w + s and P:160's quoted row-0 / last-row shifts.
+* `pattern_on_original` / `cell_segment` -- §3.2 steps 1-2 and §3.3 attribution
+  (P:111-113): a Hough cell back to its discrete pattern on the original image. Pinned by SPEC's
+  worked cases (S:195-197, S:257-258 golden), the round trip (drawing the pixels and
+  transforming gives the pixel count at that cell, a maximal cell) and the black-zone
+  characterisation (S:201; P:81).
+* `hough_peaks` -- top-k 3x3 local maxima of a Hough plane (R25 in DESIGN.md). Pinned
+  by planted-peak examples, the cyclic column neighbourhood and the plateau rule.
 """
 from __future__ import annotations
 
@@ -490,3 +497,77 @@ def fhtshift_concat(full: np.ndarray, Hp: int, Wp: int) -> np.ndarray:
 
 def fhtshift_range(hough: np.ndarray, plan: AnglePlan) -> np.ndarray:
     return fhtshift_rows(hough, fhtshift_amounts_range(plan))
+
+
+# ----------------------------------------------------------------------------------------
+# §3.2 / §3.3: from a Hough cell back to the original image; peaks
+# ----------------------------------------------------------------------------------------
+def pattern_on_original(h: int, w: int, quadrant: int, s: int, x0: int, n: int, W: int) -> list[tuple[int, int]]:
+    """Pixels (x, y) of the original h x w image on the pattern of cell (s, x0) of `quadrant`.
+
+    P:71 step 1: the pattern of the padded frame, frame column (x0 + sigma * D_s(y)) for frame rows
+    y < n (n = the frame's padded row count). P:73-75 step 2: columns mod W (case b: the pattern
+    leaving the right side re-enters on the left) and only pixels inside the original frame (case a);
+    none left means the black zone (case c). QC/QD frames are the transposed image:
+    frame (row y, column x) is original pixel (x = y, y = x).
+    """
+    transposed, sigma = QUADRANT_FRAME[quadrant]
+    fh, fw = (w, h) if transposed else (h, w)
+    D = pattern_offsets(n)[s]
+    pix = []
+    for y in range(min(fh, n)):
+        xf = (x0 + sigma * int(D[y])) % W
+        if xf < fw:
+            pix.append((y, xf) if transposed else (xf, y))
+    return pix
+
+
+def cell_segment(mode: str, h: int, w: int, row: int, col: int, quadrant: int = QA, layout: str = "quads"):
+    """Cell (row, col) of a QUADRANT or FULL Hough plane -> (quadrant, s, pixels). FULL QUADS: plane
+    `quadrant`, s = row; CONCAT: P:111-113 attribution (R8); padding as the transform's (R9)."""
+    if mode == "quadrant":
+        transposed = QUADRANT_FRAME[quadrant][0]
+        n = next_pow2(w if transposed else h)
+        W = (h if transposed else w) + n
+        q, s = quadrant, row
+    else:
+        Hp, Wp = next_pow2(h), next_pow2(w)
+        W = Hp + Wp
+        q, s = (quadrant, row) if layout == "quads" else attribute_row(row, Hp, Wp)
+        n = Wp if QUADRANT_FRAME[q][0] else Hp
+    if s >= n:
+        return q, s, []
+    return q, s, pattern_on_original(h, w, q, s, col, n, W)
+
+
+def hough_peaks(H: np.ndarray, k: int) -> list[tuple[float, int, int]]:
+    """Top-k peaks of one Hough plane H[s][x0] (R25): a cell is a peak when it beats each of its up to
+    8 neighbours -- columns cyclic (x0 is taken mod W), rows not -- where a beats b iff
+    v(a) > v(b), or v(a) == v(b) and a comes first in row-major order (a plateau keeps its first
+    cell). Peaks ordered by value descending, then row-major index ascending; at most k."""
+    R, W = H.shape
+    peaks = []
+    for r in range(R):
+        for c in range(W):
+            v = H[r, c]
+            ok = True
+            for dr in (-1, 0, 1):
+                rr = r + dr
+                if rr < 0 or rr >= R:
+                    continue
+                for dc in (-1, 0, 1):
+                    if dr == 0 and dc == 0:
+                        continue
+                    cc = (c + dc) % W
+                    if rr == r and cc == c:
+                        continue
+                    u = H[rr, cc]
+                    if u > v or (u == v and rr * W + cc < r * W + c):
+                        ok = False
+                        break
+                if not ok:
+                    break
+            if ok:
+                peaks.append((v, r, c))
+    peaks.sort(key=lambda t: (-t[0], t[1] * W + t[2]))
+    return peaks[:k]

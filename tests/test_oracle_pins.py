@@ -419,3 +419,74 @@ def test_cells_direct_equals_full():
         H = O.hough_of_frame_direct(fr)
         cells = [(s, x) for s in range(fr.Hp) for x in range(fr.W)]
         assert (O.hough_cells_direct(fr, cells) == H.ravel()).all()
+
+
+# ---------------------------------------------------------------- §3.2 / §3.3 recovery, peaks (f3)
+@pytest.mark.parametrize("ex", GOLDEN["pattern_on_original"], ids=lambda e: e["cite"])
+def test_pattern_on_original_golden(ex):
+    q = O.QUADRANT_NAMES.index(ex["quadrant"])
+    n = O.next_pow2(ex["h"])
+    pix = O.pattern_on_original(ex["h"], ex["w"], q, ex["s"], ex["x0"], n, ex["w"] + n)
+    assert [list(p) for p in pix] == ex["pixels"]
+
+
+@pytest.mark.parametrize("ex", GOLDEN["concat_cell_segment"], ids=lambda e: e["cite"])
+def test_concat_cell_segment_golden(ex):
+    q, s, pix = O.cell_segment("full", ex["h"], ex["w"], ex["row"], ex["col"], layout="concat")
+    assert (O.QUADRANT_NAMES[q], s) == (ex["quadrant"], ex["s"])
+    assert [list(p) for p in pix] == ex["pixels"]
+
+
+def test_segment_round_trip():
+    """drawing a recovered pattern into a blank image and transforming gives its pixel count at
+    that cell, and no cell exceeds it (the tier-2 recursion does not use the pattern table)."""
+    rng = np.random.default_rng(8)
+    for _ in range(60):
+        h, w = int(rng.integers(1, 17)), int(rng.integers(1, 17))
+        q = int(rng.integers(0, 4))
+        tr = O.QUADRANT_FRAME[q][0]
+        n = O.next_pow2(w if tr else h)
+        W = (h if tr else w) + n
+        s, x0 = int(rng.integers(0, n)), int(rng.integers(0, W))
+        pix = O.pattern_on_original(h, w, q, s, x0, n, W)
+        if not pix:
+            continue
+        img = np.zeros((h, w), dtype=np.int64)
+        for x, y in pix:
+            img[y, x] = 1
+        H = O.hough_recursive(img, q)
+        assert H[s, x0] == len(pix) == H.max()
+
+
+def test_black_zone_characterisation():
+    """for QA (h a power of two) the pattern misses the image exactly when x0 >= w and
+    x0 + s < W; for h < Hp the pattern ends at row h - 1, so s becomes its offset there, D_s(h - 1)."""
+    for h, w in [(4, 4), (8, 5), (16, 16), (5, 12), (3, 7)]:
+        n = O.next_pow2(h)
+        W = w + n
+        for s in range(n):
+            reach = s if h == n else int(O.pattern_offsets(n)[s][h - 1])
+            for x0 in range(W):
+                empty = not O.pattern_on_original(h, w, O.QA, s, x0, n, W)
+                assert empty == (x0 >= w and x0 + reach < W)
+
+
+def test_full_cell_segment_quads_matches_quadrant():
+    """FULL/QUADS recovery equals the quadrant's own recovery when the image is already square."""
+    for q in range(4):
+        for row, col in [(0, 0), (3, 5), (7, 15), (5, 9)]:
+            _, _, a = O.cell_segment("full", 8, 8, row, col, quadrant=q)
+            _, _, b = O.cell_segment("quadrant", 8, 8, row, col, quadrant=q)
+            assert a == b
+
+
+def test_hough_peaks_planted():
+    """R25 rule on a planted plane: cyclic columns ((0,7) neighbours (0,0)), ties to the earlier cell,
+    order by value then row-major index."""
+    H = np.zeros((4, 8), dtype=np.int64)
+    H[1, 2], H[2, 6], H[0, 7], H[0, 0] = 5, 7, 3, 3
+    assert O.hough_peaks(H, 3) == [(7, 2, 6), (5, 1, 2), (3, 0, 0)]
+    P = np.array([[1, 4, 4, 4, 1, 0], [0, 0, 0, 0, 0, 0]], dtype=np.int64)    # plateau: first cell only
+    assert O.hough_peaks(P, 2) == [(4, 0, 1)]                                # zeros all lose to an earlier neighbour
+    F = np.array([[0.5, -1.0, 0.25], [0.5, 2.0, -3.0]], dtype=np.float64)
+    assert O.hough_peaks(F, 5) == [(2.0, 1, 1)]
