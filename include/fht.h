@@ -184,6 +184,35 @@ int fhtshift(const fht_hough* in, fht_hough* out, fht_stream_t stream);
 /* Human-readable name of a status code (static string). */
 const char* fht_status_string(int status);
 
+/* ---- Peaks and line recovery ---------------------------------------------- */
+
+/* Top-k peaks of every Hough plane (plane = image b, quadrant slot q; batch*nquad planes of
+ * rows x cols; R25). A cell beats a neighbour when its value is larger, or equal and it
+ * comes first in row-major order; a peak beats each of its up to 8 neighbours (columns cyclic:
+ * x0 is taken mod W; rows not). The k (1..32) peaks with the largest values (ties: smaller
+ * row-major index first) are written to values[plane*k + i] (the Hough dtype), rows[...] and
+ * cols[...] (int32), all DEVICE pointers owned by the caller; a plane with fewer than k peaks pads
+ * with row = col = -1, value 0. ws: fht_peaks_workspace_bytes(h) device bytes. Two kernels (a
+ * streaming pass over bands of rows, a per-plane merge). Errors: ARG (k outside 1..32, NULL),
+ * DTYPE, WORKSPACE, UNSUPPORTED (rows*cols >= 2^32). Returns 2 (kernels enqueued). */
+size_t fht_peaks_workspace_bytes(const fht_hough* h);
+int fht_peaks(const fht_hough* h, int32_t k, void* values, int32_t* rows, int32_t* cols, void* ws,
+              size_t ws_bytes, fht_stream_t stream);
+
+/* The pattern of one Hough cell on the original image (§3.2 steps 1-2; CONCAT rows are
+ * attributed by P:111-113, R8): frame column (col + sigma*D_s(y)) mod W of frame rows y < n, kept
+ * where it lies inside the original frame (QC/QD: transposed). The kept pixels form one run;
+ * out gets its first (x0, y0) and last (x1, y1) pixel in frame-row order and the pixel count npix
+ * (0 = the cell is in the black zone), plus the quadrant and its shift s. Host-only,
+ * no device access. QUADRANT and FULL descriptors (`slot` = the QUADS plane; 0 otherwise);
+ * RANGE returns FHT_ERR_UNSUPPORTED. */
+typedef struct {
+  int32_t quadrant, s;
+  int64_t npix;
+  int64_t x0, y0, x1, y1;
+} fht_segment;
+int fht_cell_segment(const fht_hough* h, int64_t slot, int64_t row, int64_t col, fht_segment* out);
+
 #ifdef __cplusplus
 }
 #endif

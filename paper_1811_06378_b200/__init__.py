@@ -210,3 +210,29 @@ def fhtshift(h: HoughImage, out: HoughImage | None = None) -> HoughImage:
     out.desc.shifted = 0
     out.launches = _lib.check("fhtshift", _lib.lib.fhtshift(ctypes.byref(h.desc), ctypes.byref(out.desc), _stream(h.storage)))
     return out
+
+
+def peaks(h: HoughImage, k: int = 16, workspace: torch.Tensor | None = None):
+    """Top-k peaks of every Hough plane (DESIGN R25): (values, rows, cols), each
+    [batch][nquad][k] on the device; missing peaks have row = col = -1."""
+    d = h.desc
+    shape = (d.batch, d.nquad, k)
+    vals = torch.empty(shape, dtype=h.storage.dtype, device=h.storage.device)
+    rows = torch.empty(shape, dtype=torch.int32, device=h.storage.device)
+    cols = torch.empty(shape, dtype=torch.int32, device=h.storage.device)
+    ws_n = _lib.lib.fht_peaks_workspace_bytes(ctypes.byref(d))
+    ws = _workspace(ws_n, h.storage.device, workspace)
+    _lib.check("fht_peaks", _lib.lib.fht_peaks(ctypes.byref(d), int(k), vals.data_ptr(), rows.data_ptr(),
+                                                 cols.data_ptr(), ws.data_ptr(), ws_n, _stream(h.storage)))
+    return vals, rows, cols
+
+
+def cell_segment(h: HoughImage, row: int, col: int, slot: int = 0) -> dict | None:
+    """The pattern of Hough cell (row, col) on the original image (CONCAT rows by P:111-113):
+    {"quadrant", "s", "npix", "first": (x, y), "last": (x, y)}, or None in the black zone."""
+    sg = _lib.FhtSegment()
+    _lib.check("fht_cell_segment", _lib.lib.fht_cell_segment(ctypes.byref(h.desc), int(slot), int(row), int(col),
+                                                               ctypes.byref(sg)))
+    if sg.npix == 0:
+        return None
+    return {"quadrant": sg.quadrant, "s": sg.s, "npix": sg.npix, "first": (sg.x0, sg.y0), "last": (sg.x1, sg.y1)}

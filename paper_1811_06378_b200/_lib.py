@@ -25,7 +25,8 @@ STATUS = {
 
 EXPORTED = (
     "fht_hough_describe", "fht_workspace_bytes", "fht_quadrant", "fht_full", "fht_angle_plan_make",
-    "fht_angle_plan_make_pruned", "fht_angle_range", "fhtshift", "fht_status_string",
+    "fht_angle_plan_make_pruned", "fht_angle_range", "fhtshift", "fht_status_string", "fht_peaks_workspace_bytes",
+    "fht_peaks", "fht_cell_segment",
 )
 
 
@@ -44,6 +45,13 @@ class FhtAnglePlan(ctypes.Structure):
         ("h", ctypes.c_int64), ("w", ctypes.c_int64), ("Hp", ctypes.c_int64),
         ("w_content", ctypes.c_int64), ("W", ctypes.c_int64), ("e_min", ctypes.c_int64), ("e_max", ctypes.c_int64),
         ("rows", ctypes.c_int64),
+    ]
+
+
+class FhtSegment(ctypes.Structure):
+    _fields_ = [
+        ("quadrant", ctypes.c_int32), ("s", ctypes.c_int32), ("npix", ctypes.c_int64),
+        ("x0", ctypes.c_int64), ("y0", ctypes.c_int64), ("x1", ctypes.c_int64), ("y1", ctypes.c_int64),
     ]
 
 
@@ -86,10 +94,14 @@ def _load():
     lib.fht_angle_range.argtypes = [P(FhtImage), P(FhtAnglePlan), P(FhtHough), P(FhtHough), vp, sz, vp,
                                     P(FhtExecOpts)]
     lib.fhtshift.argtypes = [P(FhtHough), P(FhtHough), vp]
+    lib.fht_peaks_workspace_bytes.argtypes = [P(FhtHough)]
+    lib.fht_peaks_workspace_bytes.restype = sz
+    lib.fht_peaks.argtypes = [P(FhtHough), i32, vp, vp, vp, vp, sz, vp]
+    lib.fht_cell_segment.argtypes = [P(FhtHough), i64, i64, i64, P(FhtSegment)]
     lib.fht_status_string.argtypes = [i32]
     lib.fht_status_string.restype = ctypes.c_char_p
     for name in ("fht_hough_describe", "fht_quadrant", "fht_full", "fht_angle_plan_make", "fht_angle_plan_make_pruned",
-                 "fht_angle_range", "fhtshift"):
+                 "fht_angle_range", "fhtshift", "fht_peaks", "fht_cell_segment"):
         getattr(lib, name).restype = i32
     return lib
 

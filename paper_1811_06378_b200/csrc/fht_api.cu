@@ -20,6 +20,7 @@
 #include "../../include/fht.h"
 #include "fht_kernels.cuh"
 #include "fht_tile.cuh"
+#include "fht_peaks.cuh"
 
 namespace {
 
@@ -796,6 +797,17 @@ size_t range_tables_bytes(const fht_angle_plan* plan) {
 
 }  // namespace
 
+namespace {
+// peaks: rows per band so that the band pass has >= 4 CTAs per SM
+int peaks_band(const fht_hough* h) {
+  const int64_t planes = h->batch * h->nquad;
+  int64_t band = (h->rows * planes + 4 * 148 - 1) / (4 * 148);
+  if (band < 8) band = 8;
+  if (band > h->rows) band = h->rows;
+  return (int)band;
+}
+}  // namespace
+
 extern "C" {
 
 const char* fht_status_string(int s) {
@@ -1139,6 +1151,107 @@ int fhtshift(const fht_hough* in, fht_hough* out, fht_stream_t stream) {
   if (cudaGetLastError() != cudaSuccess) return FHT_ERR_CUDA;
   out->shifted = 1;
   return 1;
+}
+
+size_t fht_peaks_workspace_bytes(const fht_hough* h) {
+  if (!h || h->batch < 1 || h->nquad < 1 || h->rows < 1 || h->cols < 1) return 0;
+  const int band = peaks_band(h);
+  const int64_t nbands = (h->rows + band - 1) / band;
+  // [planes][nbands][32] list keys, then [planes] thresholds
+  return (size_t)(h->batch * h->nquad * nbands) * pk::kMaxK * sizeof(uint64_t) +
+         (size_t)(h->batch * h->nquad) * sizeof(uint64_t);
+}
+
+int fht_peaks(const fht_hough* h, int32_t k, void* values, int32_t* rows, int32_t* cols, void* ws, size_t ws_bytes,
+              fht_stream_t stream) {
+  if (!h || !h->data || !values || !rows || !cols) return FHT_ERR_ARG;
+  if (h->dtype != FHT_I32 && h->dtype != FHT_F32) return FHT_ERR_DTYPE;
+  if (k < 1 || k > pk::kMaxK || h->batch < 1 || h->nquad < 1 || h->rows < 1 || h->cols < 1) return FHT_ERR_ARG;
+  if (h->rows * h->cols >= (int64_t(1) << 32) - 1 || h->rows >= (int64_t(1) << 31)) return FHT_ERR_UNSUPPORTED;
+  const size_t need = fht_peaks_workspace_bytes(h);
+  if (!ws || ws_bytes < need) return FHT_ERR_WORKSPACE;
+  pk::PeakArgs a{};
+  a.data = h->data;
+  a.bstride = h->batch_stride;
+  a.qstride = h->quad_stride;
+  a.rstride = h->row_stride;
+  a.nquad = (int)h->nquad;
+  a.R = (int)h->rows;
+  a.W = (int)h->cols;
+  a.band = peaks_band(h);
+  a.nbands = (a.R + a.band - 1) / a.band;
+  a.part = static_cast<uint64_t*>(ws);
+  a.thr = reinterpret_cast<unsigned long long*>(a.part + (int64_t)(h->batch * h->nquad) * a.nbands * pk::kMaxK);
+  a.values = values;
+  a.rows = rows;
+  a.cols = cols;
+  a.k = k;
+  a.planes = (int)(h->batch * h->nquad);
+  const dim3 g1((unsigned)a.nbands, (unsigned)a.planes), g2((unsigned)((a.planes + pk::kWarps - 1) / pk::kWarps));
+  const cudaStream_t st = (cudaStream_t)stream;
+  if (cudaMemsetAsync(a.thr, 0, (size_t)a.planes * sizeof(uint64_t), st) != cudaSuccess) return FHT_ERR_CUDA;
+  if (h->dtype == FHT_F32) {
+    pk::k_peaks_band<float><<<g1, pk::kWarps * 32, 0, st>>>(a);
+    pk::k_peaks_merge<float><<<g2, pk::kWarps * 32, 0, st>>>(a);
+  } else {
+    pk::k_peaks_band<int><<<g1, pk::kWarps * 32, 0, st>>>(a);
+    pk::k_peaks_merge<int><<<g2, pk::kWarps * 32, 0, st>>>(a);
+  }
+  if (cudaGetLastError() != cudaSuccess) return FHT_ERR_CUDA;
+  return 2;
+}
+
+int fht_cell_segment(const fht_hough* h, int64_t slot, int64_t row, int64_t col, fht_segment* out) {
+  if (!h || !out) return FHT_ERR_ARG;
+  if (row < 0 || row >= h->rows || col < 0 || col >= h->cols || slot < 0 || slot >= h->nquad) return FHT_ERR_ARG;
+  int q;
+  int64_t s;
+  int64_t n;
+  if (h->mode == FHT_MODE_QUADRANT) {
+    q = h->quadrant;
+    s = row;
+    n = h->rows;
+  } else if (h->mode == FHT_MODE_FULL) {
+    if (h->layout == FHT_LAYOUT_QUADS) {
+      q = (int)slot;
+      s = row;
+    } else {  // CONCAT: P:111-113 thresholds, a shared row belongs to the earlier quadrant (R8)
+      const int64_t Hp = h->Hp, Wp = h->Wp;
+      if (row < Hp) { q = FHT_QA; s = Hp - 1 - row; }
+      else if (row < 2 * Hp - 1) { q = FHT_QB; s = row - (Hp - 1); }
+      else if (row < 2 * Hp - 2 + Wp) { q = FHT_QC; s = Wp - 1 - (row - (2 * Hp - 2)); }
+      else { q = FHT_QD; s = row - (2 * Hp + Wp - 3); }
+    }
+    n = q >= 2 ? h->Wp : h->Hp;
+  } else {
+    return FHT_ERR_UNSUPPORTED;  // RANGE: the resampled frame has no single-pixel inverse
+  }
+  const bool tr = q >= 2;
+  const int sigma = (q == FHT_QA || q == FHT_QD) ? 1 : -1;
+  const int64_t fh = tr ? h->w : h->h, fw = tr ? h->h : h->w, W = h->cols;
+  fht_segment sg{};
+  sg.quadrant = q;
+  sg.s = (int32_t)s;
+  if (s < n) {
+    // P:71 step 1: frame column (x0 + sigma*D_s(y)) of frame row y; P:73-77 step 2: mod W, keep the
+    // original frame (QC/QD frames are the transposed image)
+    const int K = ilog2(n);
+    for (int64_t y = 0; y < fh && y < n; ++y) {
+      int64_t xf = (col + sigma * (int64_t)dyadic_offset(K, (int)s, (int)y)) % W;
+      if (xf < 0) xf += W;
+      if (xf >= fw) continue;
+      const int64_t px = tr ? y : xf, py = tr ? xf : y;
+      if (sg.npix == 0) {
+        sg.x0 = px;
+        sg.y0 = py;
+      }
+      sg.x1 = px;
+      sg.y1 = py;
+      ++sg.npix;
+    }
+  }
+  *out = sg;
+  return FHT_OK;
 }
 
 }  // extern "C"

@@ -162,3 +162,30 @@ def test_status_strings():
     L = _lib()
     for s in range(-8, 1):
         assert L.lib.fht_status_string(s)
+
+
+def test_cell_segment_matches_oracle():
+    """fht_cell_segment (host) == the oracle's §3.2/§3.3 recovery on every cell of small frames:
+    QUADRANT (all four), FULL QUADS and CONCAT; count and first/last pixel."""
+    from oracle import fht_oracle as O
+    L = _lib()
+    for h, w in [(4, 4), (5, 7), (8, 3), (6, 6)]:
+        img = _img(L, h, w)
+        cases = [(L.FHT_MODE_QUADRANT, 0, q) for q in range(4)] + [(L.FHT_MODE_FULL, L.FHT_LAYOUT_QUADS, 0),
+                                                                   (L.FHT_MODE_FULL, L.FHT_LAYOUT_CONCAT, 0)]
+        for mode, layout, quad in cases:
+            d = L.FhtHough()
+            assert L.lib.fht_hough_describe(mode, layout, quad, ctypes.byref(img), None, ctypes.byref(d)) == 0
+            for slot in range(d.nquad):
+                for row in range(d.rows):
+                    for col in range(d.cols):
+                        sg = L.FhtSegment()
+                        assert L.lib.fht_cell_segment(ctypes.byref(d), slot, row, col, ctypes.byref(sg)) == 0
+                        if mode == L.FHT_MODE_QUADRANT:
+                            q, s, pix = O.cell_segment("quadrant", h, w, row, col, quadrant=quad)
+                        else:
+                            q, s, pix = O.cell_segment("full", h, w, row, col, quadrant=slot,
+                                                       layout="quads" if layout == L.FHT_LAYOUT_QUADS else "concat")
+                        assert (sg.quadrant, sg.s, sg.npix) == (q, s, len(pix))
+                        if pix:
+                            assert (sg.x0, sg.y0, sg.x1, sg.y1) == (*pix[0], *pix[-1])

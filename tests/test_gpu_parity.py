@@ -377,3 +377,57 @@ def test_v2_aux_stream_overlap(fht, O):
     b = fht.full(tu, aux_stream=aux)
     torch.cuda.current_stream().synchronize()
     assert b.launches > 2 and torch.equal(a.storage, b.storage)
+
+
+# ------------------------------------------------------------------ peaks + recovery (f3)
+def _check_peaks(fht, O, H, k):
+    """GPU top-k vs the oracle's rule on the SAME (GPU-computed) Hough values, every plane."""
+    vals, rows, cols = fht.peaks(H, k)
+    torch.cuda.synchronize()
+    planes = H.view.cpu().numpy()
+    v, r, c = vals.cpu().numpy(), rows.cpu().numpy(), cols.cpu().numpy()
+    for b in range(planes.shape[0]):
+        for q in range(planes.shape[1]):
+            want = O.hough_peaks(planes[b, q], k)
+            n = len(want)
+            assert [(int(r[b, q, i]), int(c[b, q, i])) for i in range(n)] == [(wr, wc) for _, wr, wc in want]
+            assert np.array_equal(v[b, q, :n], np.array([wv for wv, _, _ in want], dtype=v.dtype))
+            assert (r[b, q, n:] == -1).all() and (c[b, q, n:] == -1).all()
+
+
+@pytest.mark.parametrize("shape", [(16, 16), (33, 17), (64, 48), (128, 96)], ids=str)
+@pytest.mark.parametrize("dt", ["u8", "f32"])
+def test_peaks_small(fht, O, shape, dt):
+    from synth import random_image
+    img = random_image(shape, dt, seed=shape[0] * 3 + shape[1])
+    t = dev(img)
+    for k in (1, 7, 32):
+        _check_peaks(fht, O, fht.full(t), k)
+        _check_peaks(fht, O, fht.quadrant(t, 2), k)
+    _check_peaks(fht, O, fht.full(t, layout="concat"), 16)
+    _check_peaks(fht, O, fht.angle_range(t, fht.angle_plan(*shape, -15, 15)), 16)
+
+
+def test_peaks_c3_batch_and_segments(fht, O):
+    """Config 3 (64 u8 edge maps, planted near-horizontal lines): all 256 planes' top-16 against the
+    oracle rule (sampled planes), and the recovered pattern of each image's strongest peak carries
+    exactly its value (round trip on the real data: the cell sums those pixels, here 0/1 ones)."""
+    import synth
+    imgs = synth.batch(3)
+    h = fht.full(dev(imgs))
+    vals, rows, cols = fht.peaks(h, 16)
+    torch.cuda.synchronize()
+    planes = h.view.cpu().numpy()
+    v, r, c = vals.cpu().numpy(), rows.cpu().numpy(), cols.cpu().numpy()
+    rng = np.random.default_rng(33)
+    for b in rng.choice(64, 6, replace=False):
+        for q in range(4):
+            want = O.hough_peaks(planes[b, q], 16)
+            assert [(int(r[b, q, i]), int(c[b, q, i]), int(v[b, q, i])) for i in range(16)] == \
+                   [(wr, wc, int(wv)) for wv, wr, wc in want]
+    for b in range(0, 64, 9):
+        q = int(np.argmax(v[b, :, 0]))
+        seg = fht.cell_segment(h, int(r[b, q, 0]), int(c[b, q, 0]), slot=q)
+        _, _, pix = O.cell_segment("full", 512, 512, int(r[b, q, 0]), int(c[b, q, 0]), quadrant=q)
+        assert seg["npix"] == len(pix) and (seg["first"], seg["last"]) == (pix[0], pix[-1])
+        assert int(sum(int(imgs[b][y, x]) for x, y in pix)) == int(v[b, q, 0])
