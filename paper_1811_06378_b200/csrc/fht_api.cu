@@ -1190,11 +1190,16 @@ int fht_peaks(const fht_hough* h, int32_t k, void* values, int32_t* rows, int32_
   const dim3 g1((unsigned)a.nbands, (unsigned)a.planes), g2((unsigned)((a.planes + pk::kWarps - 1) / pk::kWarps));
   const cudaStream_t st = (cudaStream_t)stream;
   if (cudaMemsetAsync(a.thr, 0, (size_t)a.planes * sizeof(uint64_t), st) != cudaSuccess) return FHT_ERR_CUDA;
+  // 16-byte columns when every row start is 16-byte aligned and W is a multiple of 4
+  const bool vec = a.W % 4 == 0 && a.W >= 4 && aligned16(h->data) && a.rstride % 4 == 0 && a.qstride % 4 == 0 &&
+                   a.bstride % 4 == 0;
   if (h->dtype == FHT_F32) {
-    pk::k_peaks_band<float><<<g1, pk::kWarps * 32, 0, st>>>(a);
+    if (vec) pk::k_peaks_band4<float><<<g1, pk::kWarps * 32, 0, st>>>(a);
+    else pk::k_peaks_band<float><<<g1, pk::kWarps * 32, 0, st>>>(a);
     pk::k_peaks_merge<float><<<g2, pk::kWarps * 32, 0, st>>>(a);
   } else {
-    pk::k_peaks_band<int><<<g1, pk::kWarps * 32, 0, st>>>(a);
+    if (vec) pk::k_peaks_band4<int><<<g1, pk::kWarps * 32, 0, st>>>(a);
+    else pk::k_peaks_band<int><<<g1, pk::kWarps * 32, 0, st>>>(a);
     pk::k_peaks_merge<int><<<g2, pk::kWarps * 32, 0, st>>>(a);
   }
   if (cudaGetLastError() != cudaSuccess) return FHT_ERR_CUDA;

@@ -143,6 +143,103 @@ __global__ void __launch_bounds__(kWarps * 32) k_peaks_band(const PeakArgs a) {
   }
 }
 
+template <typename A> struct V4Of;
+template <> struct V4Of<float> { using type = float4; };
+template <> struct V4Of<int> { using type = int4; };
+template <typename V> __device__ __forceinline__ auto vget(const V& v, int j) {
+  return j == 0 ? v.x : j == 1 ? v.y : j == 2 ? v.z : v.w;
+}
+
+// 16-byte variant (W, the strides and the base a multiple of 4 elements): lane l holds columns
+// c0 + 4l .. c0 + 4l + 3 of a 128-column strip, so the per-row filter, ballot and loop overhead
+// is paid once per 4 cells; neighbours inside the lane come from registers.
+template <typename A>
+__global__ void __launch_bounds__(kWarps * 32) k_peaks_band4(const PeakArgs a) {
+  using V = typename V4Of<A>::type;
+  __shared__ uint64_t lists[kWarps][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int plane = blockIdx.y;
+  const A* base = static_cast<const A*>(a.data) + (int64_t)(plane / a.nquad) * a.bstride +
+                  (int64_t)(plane % a.nquad) * a.qstride;
+  const int R = a.R, W = a.W;
+  const int r0 = blockIdx.x * a.band, r1 = min(R, r0 + a.band);
+  uint64_t list = 0, lmin = 0, published = 0;
+  unsigned long long* gthr = a.thr + plane;
+  for (int c0 = warp * 128; c0 < W; c0 += kWarps * 128) {
+    const int cb = c0 + 4 * lane;  // first column of the lane
+    const bool valid = cb < W;     // W % 4 == 0: all four or none
+    auto ldv = [&](int r) -> V { return *reinterpret_cast<const V*>(base + (int64_t)r * a.rstride + cb); };
+    bool hp = r0 > 0;
+    V vp = (hp && valid) ? ldv(r0 - 1) : V{};
+    V vc = valid ? ldv(r0) : V{};
+    for (int rb = r0; rb < r1; rb += kRowsInFlight) {
+      const uint64_t floor = max(lmin, (uint64_t)__ldcg(gthr));
+      V nx[kRowsInFlight];
+#pragma unroll
+      for (int u = 0; u < kRowsInFlight; ++u) {
+        const int rr = rb + 1 + u;
+        nx[u] = (valid && rr < R && rr <= r1) ? ldv(rr) : V{};
+      }
+#pragma unroll
+      for (int u = 0; u < kRowsInFlight; ++u) {
+        const int r = rb + u;
+        if (r >= r1) break;
+        const bool hn = r + 1 < R;
+        const V vn = nx[u];
+        const uint32_t th = (uint32_t)(max(lmin, floor) >> 32);
+        unsigned cm = 0;  // candidate columns of the lane
+        if (valid) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) cm |= (ord_bits(vget(vc, j)) >= th) ? (1u << j) : 0u;
+        }
+        if (__any_sync(0xffffffffu, cm != 0)) {
+          const A* rowc = base + (int64_t)r * a.rstride;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            uint64_t key = 0;
+            if (cm & (1u << j)) {
+              const int c = cb + j;
+              const A v = vget(vc, j);
+              const int cl = c == 0 ? W - 1 : c - 1, cr = c + 1 >= W ? 0 : c + 1;
+              // same row (W >= 4 here): left earlier unless it wraps, right later unless it wraps
+              const A l = j > 0 ? vget(vc, j - 1) : __ldg(rowc + cl);
+              const A rt = j < 3 ? vget(vc, j + 1) : __ldg(rowc + cr);
+              bool peak = (c == 0 ? !(l > v) : !(l >= v)) && (c == W - 1 ? !(rt >= v) : !(rt > v));
+              if (peak && hp) {
+                const A* rp = rowc - a.rstride;
+                const A pl = j > 0 ? vget(vp, j - 1) : __ldg(rp + cl);
+                const A pr = j < 3 ? vget(vp, j + 1) : __ldg(rp + cr);
+                peak = !(vget(vp, j) >= v) && !(pl >= v) && !(pr >= v);
+              }
+              if (peak && hn) {
+                const A* rn = rowc + a.rstride;
+                const A nl = j > 0 ? vget(vn, j - 1) : __ldg(rn + cl);
+                const A nr = j < 3 ? vget(vn, j + 1) : __ldg(rn + cr);
+                peak = !(vget(vn, j) > v) && !(nl > v) && !(nr > v);
+              }
+              if (peak) key = ((uint64_t)ord_bits(v) << 32) | (uint64_t)(0xFFFFFFFFu - (uint32_t)(r * W + c));
+            }
+            list_offer(list, lmin, key, lane, floor);
+          }
+        }
+        vp = vc;
+        vc = vn;
+        hp = true;
+      }
+      if (lane == 0 && lmin > published) {
+        atomicMax(gthr, (unsigned long long)lmin);
+        published = lmin;
+      }
+    }
+  }
+  lists[warp][lane] = list;
+  __syncthreads();
+  if (warp == 0) {
+    for (int w2 = 1; w2 < kWarps; ++w2) list_offer(list, lmin, lists[w2][lane], lane);
+    a.part[((int64_t)plane * a.nbands + blockIdx.x) * 32 + lane] = list;
+  }
+}
+
 template <typename A>
 __global__ void __launch_bounds__(kWarps * 32) k_peaks_merge(const PeakArgs a) {
   const int lane = threadIdx.x & 31;
