@@ -221,6 +221,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-shift-bench", action="store_true", help="skip the standalone fhtshift (SURVEY a7) lines")
+    ap.add_argument("--no-graph", action="store_true", help="C1/C2 headline with eager calls instead of graph replay")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--extra-configs", default="5,3,4,1",
                     help="other configs also timed (reported under 'configs', not the headline)")
@@ -277,7 +278,7 @@ def main():
     def max_over_ranks(x):
         return _mor(x, device=dev)
 
-    def run_config(cfg_id, steps, warmup, with_e2e):
+    def run_config(cfg_id, steps, warmup, with_e2e, use_graph=True):
         cc = synth.CONFIGS[cfg_id]
         mine = rank_images(cc["batch"], rank, world)  # weak scaling: this rank's own images
         imgs = synth.batch(cfg_id, first=mine.start)
@@ -291,7 +292,12 @@ def main():
         outs = {}
         aux = torch.cuda.Stream(device=dev)
         step = make_step(fht, cfg_id, cc, t, outs, plan, aux)
-        n_launch = step(events=[])
+        # kernels per step as the per-kernel breakdown (below) launches them: with events the
+        # library runs every call on the launching stream (a single-image full transform otherwise
+        # splits its two orientations over the main and auxiliary streams, 4 launches instead of 2)
+        probe = torch.cuda.Event(enable_timing=True)
+        probe.record()
+        n_launch = step(events=[probe])
         torch.cuda.synchronize()
         ws_bytes = 0
         flush = None
@@ -300,6 +306,20 @@ def main():
         stream = torch.cuda.current_stream()
         for _ in range(warmup):
             step()
+        torch.cuda.synchronize()
+        # C1/C2 headline steps are CUDA-graph replays of the same call (one host launch
+        # per step instead of ~40 us of descriptor checks, tensor-map encodes and launches); stated in
+        # config.timing. Batched configs are GPU-bound and run the eager call.
+        graph = None
+        if use_graph and cfg_id in (1, 2):
+            outs["ws"] = torch.empty(max(1, fht.workspace_bytes(
+                {"quadrant": fht.FHT_MODE_QUADRANT, "full": fht.FHT_MODE_FULL, "range": fht.FHT_MODE_RANGE}[cc["mode"]],
+                fht._image(t)[0], plan)), dtype=torch.uint8, device=dev)
+            graph = fht.Graph(step)
+            for _ in range(warmup):
+                graph.replay()
+            torch.cuda.synchronize()
+        launches_eager = step()
         torch.cuda.synchronize()
         # per-step events: [0] before the first kernel ... [n_launch] after the last (fht_exec_opts)
         evs = [[torch.cuda.Event(enable_timing=True) for _ in range(n_launch + 1)] for _ in range(steps)]
@@ -320,7 +340,11 @@ def main():
                 if flush is not None:
                     flush.zero_()
                 s0[i].record(stream)
-                launches += step()
+                if graph is not None:
+                    graph.replay()
+                    launches += launches_eager
+                else:
+                    launches += step()
                 s1[i].record(stream)
             torch.cuda.synchronize()
             t_wall = time.perf_counter() - t_wall
@@ -341,7 +365,7 @@ def main():
                "in_bytes": in_b, "out_bytes": out_b, "launches_per_step": launches // steps,
                "l2": "flushed between steps (512 MiB write outside the step events)" if flush is not None
                else "working set > L2 (no flush needed)",
-               "clocks": clk.summary(), "wall_s": t_wall}
+               "clocks": clk.summary(), "wall_s": t_wall, "graph": graph is not None}
         res["step_gbs"] = (in_b + out_b) / (ms * 1e-3) / 1e9
         # dominant kernel: pass 2 (writes every output byte); per-launch algorithmic bytes. With
         # batch chunking there are several (pass 1, pass 2) pairs per step.
@@ -479,7 +503,44 @@ def main():
         torch.cuda.empty_cache()
         return res
 
-    head = run_config(args.config, args.steps, args.warmup, with_e2e=True)
+    def back_to_back(cfg_id, steps=200):
+        """Steps issued back to back (no L2 flush, so the input may stay in L2: informational, not the
+        headline): wall time per step with the eager Python/C call vs a CUDA-graph replay of the same
+        call -- shows whether the host keeps ahead of the GPU."""
+        import time as _t
+        cc = synth.CONFIGS[cfg_id]
+        t_in = torch.from_numpy(synth.batch(cfg_id)).to(dev)
+        outs = {}
+        aux = torch.cuda.Stream(device=dev)
+        plan = fht.angle_plan(cc["h"], cc["w"], cc["theta_min"], cc["theta_max"]) if cc["mode"] == "range" else None
+        step = make_step(fht, cfg_id, cc, t_in, outs, plan, aux)
+        step()
+        outs["ws"] = torch.empty(max(1, fht.workspace_bytes(
+            {"quadrant": fht.FHT_MODE_QUADRANT, "full": fht.FHT_MODE_FULL, "range": fht.FHT_MODE_RANGE}[cc["mode"]],
+            fht._image(t_in)[0], plan)), dtype=torch.uint8, device=dev)
+        res = {"workload": cc["name"], "steps": steps, "l2": "not flushed (back to back)"}
+        for label, run in (("eager", None), ("graph", fht.Graph(step))):
+            go = step if run is None else run.replay
+            for _ in range(10):
+                go()
+            torch.cuda.synchronize()
+            w0 = _t.perf_counter()
+            for _ in range(steps):
+                go()
+            h_us = (_t.perf_counter() - w0) / steps * 1e6
+            torch.cuda.synchronize()
+            res[label] = {"wall_us_per_step": (_t.perf_counter() - w0) / steps * 1e6, "host_us_per_step": h_us}
+        del t_in, outs
+        torch.cuda.empty_cache()
+        return res
+
+    head = run_config(args.config, args.steps, args.warmup, with_e2e=True, use_graph=not args.no_graph)
+    b2b_line = None
+    if not args.no_shift_bench:
+        try:
+            b2b_line = back_to_back(args.config)
+        except Exception as e:  # noqa: BLE001 -- report, do not hide
+            b2b_line = {"error": repr(e)}
     peaks_line = None
     if not args.no_shift_bench:
         try:
@@ -530,8 +591,11 @@ def main():
                             5: "full 4-quadrant FHT + fhtshift (both written)"}[args.config],
                    "parallelism": f"dp{world} (independent images per rank, no collective)",
                    "l2": head["l2"],
-                   "timing": "CUDA events on the launching stream around each step (none between its kernels), "
-                             "mean over steps; max over ranks; per-kernel times from a second K-step loop"},
+                   "timing": ("CUDA events on the launching stream around each step (none between its kernels), "
+                              "mean over steps; max over ranks; per-kernel times from a second K-step loop of eager "
+                              "calls with an event around every kernel"
+                              + ("; headline steps are CUDA-graph replays of the same call (SURVEY 8(d): allowed "
+                                 "for C1/C2)" if head["graph"] else "; headline steps are eager calls"))},
         "roofline": {"bound": "hbm", "achieved": head["pass2_gbs"], "peak": peak_gbs, "unit": "GB/s",
                      "frac": head["pass2_gbs"] / peak_gbs, "traffic": tr,
                      "kernel": kernel_names[1], "kernel_ms": head["kernels"]["pass2_ms"],
@@ -549,6 +613,7 @@ def main():
         "fhtshift_standalone": shift_lines,
         "angle_range_pruned": pruned_line,
         "peaks": peaks_line,
+        "back_to_back": b2b_line,
     }
     print(json.dumps(line), flush=True)
     if world > 1:

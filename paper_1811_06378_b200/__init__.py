@@ -236,3 +236,31 @@ def cell_segment(h: HoughImage, row: int, col: int, slot: int = 0) -> dict | Non
     if sg.npix == 0:
         return None
     return {"quadrant": sg.quadrant, "s": sg.s, "npix": sg.npix, "first": (sg.x0, sg.y0), "last": (sg.x1, sg.y1)}
+
+
+class Graph:
+    """A CUDA graph of one call sequence through this library (torch.cuda.CUDAGraph): `fn` is run
+    once eagerly (one-time attributes, tensor maps), then captured on a side stream and replayed by
+    `replay()` -- one host launch instead of the per-call descriptor checks, tensor-map encodes and
+    kernel launches. Every buffer `fn` uses (input, outputs, workspace) must be preallocated and stay
+    alive; the library's launches (programmatic dependent launch, the auxiliary-stream fork/join via
+    events) are captured as graph edges.
+
+        g = fht.Graph(lambda: fht.full(t, pair=True, out=h, out_shifted=s, workspace=ws))
+        g.replay()
+    """
+
+    def __init__(self, fn):
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            fn()
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self.result = fn()
+
+    def replay(self):
+        self.graph.replay()
+        return self.result

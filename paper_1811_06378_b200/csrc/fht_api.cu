@@ -1035,7 +1035,43 @@ int fht_full(const fht_image* img, int layout, fht_hough* out, fht_hough* out_sh
   const Frame f0 = make_frame(img->h, img->w, 0, 1), f1 = make_frame(img->h, img->w, 1, 1);
   if ((s = check_frame_supported(f0)) || (s = check_frame_supported(f1))) return s;
   int r;
-  if (Hp == Wp && use_v2(f0, nullptr)) {
+#ifndef FHT_SPLIT_ORIENT
+#define FHT_SPLIT_ORIENT 1
+#endif
+  // Square, one chunk, an auxiliary stream and no per-kernel events: QA/QB on `stream` and QC/QD
+  // on the auxiliary stream, each a (pass 1, pass 2) pair over its own half of the 4-slot scratch,
+  // so the latency-bound pass 1 of one orientation overlaps the store-bound pass 2 of the other.
+  cudaStream_t aux = (opts && opts->aux_stream && (cudaStream_t)opts->aux_stream != (cudaStream_t)stream &&
+                      !(opts->events && opts->n_events > 0))
+                         ? (cudaStream_t)opts->aux_stream
+                         : nullptr;
+  const ScratchPlan sp2 = scratch_plan(f0, 2, img->batch, nullptr);
+  const size_t half = (sp2.bytes + 255) & ~size_t(255);
+  if (FHT_SPLIT_ORIENT && aux && Hp == Wp && use_v2(f0, nullptr) && sp2.nbuf == 1 && sp2.chunk >= img->batch &&
+      2 * half <= ws_bytes) {
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    auto destroy = [&]() {
+      for (cudaEvent_t e : ev)
+        if (e) cudaEventDestroy(e);
+    };
+    if (cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventRecord(ev[0], (cudaStream_t)stream) != cudaSuccess || cudaStreamWaitEvent(aux, ev[0], 0) != cudaSuccess) {
+      destroy();
+      return FHT_ERR_CUDA;
+    }
+    LaunchLog quiet{nullptr, 0};
+    r = run_orientation(img, f0, sl, 2, o, ws, half, (cudaStream_t)stream, nullptr, quiet);
+    const int r2 = r < 0 ? r : run_orientation(img, f0, sl + 2, 2, o, static_cast<char*>(ws) + half, half, aux, nullptr,
+                                               quiet);
+    const bool ok = cudaEventRecord(ev[1], aux) == cudaSuccess &&
+                    cudaStreamWaitEvent((cudaStream_t)stream, ev[1], 0) == cudaSuccess;
+    destroy();
+    if (r < 0) return r;
+    if (r2 < 0) return r2;
+    if (!ok) return FHT_ERR_CUDA;
+    r += r2;
+  } else if (Hp == Wp && use_v2(f0, nullptr)) {
     // square: both orientations share one frame -> one pass-1 and one pass-2 launch for all four
     r = run_orientation(img, f0, sl, 4, o, ws, ws_bytes, (cudaStream_t)stream, nullptr, log);
     if (r < 0) return r;

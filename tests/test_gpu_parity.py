@@ -431,3 +431,26 @@ def test_peaks_c3_batch_and_segments(fht, O):
         _, _, pix = O.cell_segment("full", 512, 512, int(r[b, q, 0]), int(c[b, q, 0]), quadrant=q)
         assert seg["npix"] == len(pix) and (seg["first"], seg["last"]) == (pix[0], pix[-1])
         assert int(sum(int(imgs[b][y, x]) for x, y in pix)) == int(v[b, q, 0])
+
+
+def test_graph_replay_equals_eager(fht, O):
+    """A captured step (pass pair with PDL, fused fhtshift, the two-stream orientation split) replays
+    to the same bits as the eager call; new input values flow through the same graph."""
+    import synth
+    img = synth.batch(2)[0]
+    t = dev(img)
+    h0, s0 = fht.full(t, pair=True)
+    h, s = fht.full(t, pair=True)
+    ws = torch.empty(fht.workspace_bytes(fht.FHT_MODE_FULL, fht._image(t)[0], None), dtype=torch.uint8, device="cuda")
+    aux = torch.cuda.Stream()
+    g = fht.Graph(lambda: fht.full(t, pair=True, out=h, out_shifted=s, workspace=ws, aux_stream=aux))
+    h.storage.zero_()
+    s.storage.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(h.storage, h0.storage) and torch.equal(s.storage, s0.storage)
+    t.copy_(t.flip(0))                      # new values, same buffer
+    g.replay()
+    h1, s1 = fht.full(t, pair=True)
+    torch.cuda.synchronize()
+    assert torch.equal(h.storage, h1.storage) and torch.equal(s.storage, s1.storage)
