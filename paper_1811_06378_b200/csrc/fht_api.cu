@@ -137,14 +137,18 @@ bool use_v2(const Frame& f, const RangeDev* rg) {
 
 // v2 pass-1 columns [lo, hi) rounded up to a multiple of 4 (16-byte aligned TMA rows); the
 // extra columns hold zeros (no pixel reaches them), so pass 2 may read them freely.
-void v2_pass1_range(const Frame& f, int sigma, const RangeDev* rg, int& lo, int& hi) {
+// pass-1 scratch element bytes: u8 input keeps F_m in uint16, else the accumulator
+int scratch_es(int dtype) { return dtype == FHT_U8 ? 2 : 4; }
+// spans rounded to 16 bytes of scratch elements (tile starts and row pitch stay TMA-aligned)
+void v2_pass1_range(const Frame& f, int sigma, const RangeDev* rg, int& lo, int& hi, int es) {
   pass1_range(f, sigma, rg, lo, hi);
-  hi = lo + ((hi - lo + 3) & ~3);
+  const int al = 16 / es;
+  hi = lo + ((hi - lo + al - 1) & ~(al - 1));
 }
-int64_t v2_scratch_pitch(const Frame& f, const RangeDev* rg) {
+int64_t v2_scratch_pitch(const Frame& f, const RangeDev* rg, int es) {
   int lo, hi, w = 0;
   for (int s = -1; s <= 1; s += 2) {
-    v2_pass1_range(f, s, rg, lo, hi);
+    v2_pass1_range(f, s, rg, lo, hi, es);
     w = (hi - lo) > w ? (hi - lo) : w;
   }
   return w;
@@ -171,15 +175,15 @@ struct ScratchPlan {
   int nbuf;            // scratch buffers: 2 when the batch needs several chunks (pass overlap)
   size_t bytes;        // all buffers
 };
-ScratchPlan scratch_plan(const Frame& f, int nq, int64_t batch, const RangeDev* rg) {
+ScratchPlan scratch_plan(const Frame& f, int nq, int64_t batch, const RangeDev* rg, int es) {
   ScratchPlan sp{};
   sp.v2 = use_v2(f, rg);
   if (sp.v2) {
-    sp.pitch = v2_scratch_pitch(f, rg);
-    const size_t touched = (size_t)nq * f.Hp * (size_t)sp.pitch * 4;
+    sp.pitch = v2_scratch_pitch(f, rg, es);
+    const size_t touched = (size_t)nq * f.Hp * (size_t)sp.pitch * es;
     sp.chunk = rg ? 1 : chunk_images(touched, batch);
     sp.nbuf = batch > sp.chunk ? 2 : 1;
-    sp.bytes = (size_t)sp.nbuf * sp.chunk * nq * f.Hp * (size_t)sp.pitch * 4;
+    sp.bytes = (size_t)sp.nbuf * sp.chunk * nq * f.Hp * (size_t)sp.pitch * es;
   } else {
     sp.nbuf = 1;
     sp.pitch = rg ? ((rg->x_hi - rg->x_lo + 3) & ~3) : v1_scratch_width(f);
@@ -205,14 +209,16 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 // 2-D row-major tensor [rows][cols] with a box_rows x box_cols box (default: one row per copy).
 bool make_row_map(CUtensorMap* m, const void* base, bool f32, uint64_t cols, uint64_t rows, uint64_t pitch_elems,
-                  uint32_t box_cols, uint32_t box_rows = 1) {
+                  uint32_t box_cols, uint32_t box_rows = 1, bool u16 = false) {
   auto fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[2] = {cols, rows};
-  cuuint64_t strides[1] = {pitch_elems * 4};
+  cuuint64_t strides[1] = {pitch_elems * (u16 ? 2 : 4)};
   cuuint32_t box[2] = {box_cols, box_rows};
   cuuint32_t es[2] = {1, 1};
-  return fn(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_INT32, 2, const_cast<void*>(base), dims,
+  const CUtensorMapDataType dt = u16 ? CU_TENSOR_MAP_DATA_TYPE_UINT16
+                                     : f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_INT32;
+  return fn(m, dt, 2, const_cast<void*>(base), dims,
             strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
             CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -315,24 +321,24 @@ cudaError_t launch_p1(int r, dim3 grid, const P1Maps& m, const v2::P1Params& a, 
 struct P2Maps {
   CUtensorMap scr0, scr1, out0, out1, out0_box;
 };
-template <typename A, int R>
+template <typename A, int R, typename Tscr>
 cudaError_t launch_p2_t(dim3 grid, const P2Maps& m, const v2::P2Params& a, cudaStream_t st) {
   const size_t smem = v2::p2_smem_bytes(R);
   static const cudaError_t attr =
-      cudaFuncSetAttribute(v2::k_p2<A, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(v2::k_p2<A, R, Tscr>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (attr != cudaSuccess) return attr;
-  return launch_pdl(v2::k_p2<A, R>, grid, dim3(v2::Split<R>::nw * 32), smem, st, m.scr0, m.scr1, m.out0, m.out1,
+  return launch_pdl(v2::k_p2<A, R, Tscr>, grid, dim3(v2::Split<R>::nw * 32), smem, st, m.scr0, m.scr1, m.out0, m.out1,
                     m.out0_box, a);
 }
-template <typename A>
+template <typename A, typename Tscr = A>
 cudaError_t launch_p2(int r, dim3 grid, const P2Maps& m, const v2::P2Params& a, cudaStream_t st) {
   switch (r) {
-    case 1: return launch_p2_t<A, 1>(grid, m, a, st);
-    case 2: return launch_p2_t<A, 2>(grid, m, a, st);
-    case 3: return launch_p2_t<A, 3>(grid, m, a, st);
-    case 4: return launch_p2_t<A, 4>(grid, m, a, st);
-    case 5: return launch_p2_t<A, 5>(grid, m, a, st);
-    case 6: return launch_p2_t<A, 6>(grid, m, a, st);
+    case 1: return launch_p2_t<A, 1, Tscr>(grid, m, a, st);
+    case 2: return launch_p2_t<A, 2, Tscr>(grid, m, a, st);
+    case 3: return launch_p2_t<A, 3, Tscr>(grid, m, a, st);
+    case 4: return launch_p2_t<A, 4, Tscr>(grid, m, a, st);
+    case 5: return launch_p2_t<A, 5, Tscr>(grid, m, a, st);
+    case 6: return launch_p2_t<A, 6, Tscr>(grid, m, a, st);
   }
   return cudaErrorInvalidValue;
 }
@@ -385,7 +391,8 @@ struct LaunchLog {
 // Run the two passes for one orientation over all images, chunked. Returns launches or error.
 int run_orientation(const fht_image* img, const Frame& f, const Slot* slots, int nq, const Outs& outs, void* ws,
                     size_t ws_bytes, cudaStream_t st, const RangeDev* rg, LaunchLog& log) {
-  const ScratchPlan sp = scratch_plan(f, nq, img->batch, rg);
+  const int ses = scratch_es(img->dtype);
+  const ScratchPlan sp = scratch_plan(f, nq, img->batch, rg, ses);
   if (!ws || ws_bytes < sp.bytes) return FHT_ERR_WORKSPACE;
   int launches = 0;
   const fht_hough* any = outs.d[0] ? outs.d[0] : outs.d[1];
@@ -419,7 +426,7 @@ int run_orientation(const fht_image* img, const Frame& f, const Slot* slots, int
       v2::P1Slot& s = p1.slot[q];
       s.sigma = slots[q].sigma;
       s.transposed = slots[q].transposed;
-      v2_pass1_range(f, s.sigma, rg, s.xlo, s.xhi);
+      v2_pass1_range(f, s.sigma, rg, s.xlo, s.xhi, ses);
       s.srow0 = (int64_t)q * f.Hp;
       span1 = (s.xhi - s.xlo) < span1 ? (s.xhi - s.xlo) : span1;
     }
@@ -517,10 +524,12 @@ int run_orientation(const fht_image* img, const Frame& f, const Slot* slots, int
     {  // pass-1 stores: scratch as [z*2^m + j][strip][column], one box {TX, 1, 2^m} per tile
       auto fn = encode_fn();
       cuuint64_t dims[3] = {(cuuint64_t)sp.pitch, (cuuint64_t)nstrips, (cuuint64_t)(scr_rows / nstrips)};
-      cuuint64_t strides[2] = {(cuuint64_t)(sp.pitch * 4), (cuuint64_t)(sp.pitch * 4 * nstrips)};
+      cuuint64_t strides[2] = {(cuuint64_t)(sp.pitch * ses), (cuuint64_t)(sp.pitch * ses * nstrips)};
       cuuint32_t box[3] = {(cuuint32_t)p1.TX, 1, (cuuint32_t)ngroups};  // shifts j < ngroups only
       cuuint32_t e[3] = {1, 1, 1};
-      if (!fn || fn(&m1.scr, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_INT32, 3, ws, dims, strides,
+      const CUtensorMapDataType sdt = ses == 2 ? CU_TENSOR_MAP_DATA_TYPE_UINT16
+                                               : f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_INT32;
+      if (!fn || fn(&m1.scr, sdt, 3, ws, dims, strides,
                     box, e, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return FHT_ERR_CUDA;
@@ -533,8 +542,9 @@ int run_orientation(const fht_image* img, const Frame& f, const Slot* slots, int
       m1.img1 = m1.scr;
     }
     // scratch as pass 2 reads it: columns [0, span1) = what pass 1 wrote; TMA zero-fills the rest
-    if (!make_row_map(&m2.scr0, ws, f32, (uint64_t)span1, scr_rows, (uint64_t)sp.pitch, 256) ||
-        !make_row_map(&m2.scr1, ws, f32, (uint64_t)span1, scr_rows, (uint64_t)sp.pitch, 36))
+    if (!make_row_map(&m2.scr0, ws, f32, (uint64_t)span1, scr_rows, (uint64_t)sp.pitch, 256, 1, ses == 2) ||
+        !make_row_map(&m2.scr1, ws, f32, (uint64_t)span1, scr_rows, (uint64_t)sp.pitch, ses == 2 ? 40 : 36, 1,
+                      ses == 2))
       return FHT_ERR_CUDA;
 
     // Chunks of the batch; with an auxiliary stream and two scratch buffers, pass 1 of chunk k+1
@@ -598,7 +608,8 @@ int run_orientation(const fht_image* img, const Frame& f, const Slot* slots, int
       p2.m = f.m;
       p2.ngroups = ngroups;
       dim3 g2((unsigned)(ntile2 * ngroups * nb * nq));
-      e = f32 ? launch_p2<float>(f.L, g2, m2, p2, st) : launch_p2<int>(f.L, g2, m2, p2, st);
+      e = f32 ? launch_p2<float>(f.L, g2, m2, p2, st)
+              : ses == 2 ? launch_p2<int, uint16_t>(f.L, g2, m2, p2, st) : launch_p2<int>(f.L, g2, m2, p2, st);
       if (e != cudaSuccess) {
         destroy_events();
         return FHT_ERR_CUDA;
@@ -956,18 +967,18 @@ size_t fht_workspace_bytes(int mode, const fht_image* img, const fht_angle_plan*
     if (!plan) return 0;
     const Frame f = range_frame(img, plan);
     const RangeDev rg = range_geometry(f, plan);
-    const ScratchPlan sp = scratch_plan(f, 1, 1, &rg);
+    const ScratchPlan sp = scratch_plan(f, 1, 1, &rg, scratch_es(img->dtype));
     return ((sp.bytes + 255) & ~size_t(255)) + range_tables_bytes(plan);
   }
   size_t need = 0;
   if (mode == FHT_MODE_FULL && next_pow2(img->h) == next_pow2(img->w)) {
     const Frame f = make_frame(img->h, img->w, 0, 1);
-    if (use_v2(f, nullptr)) return scratch_plan(f, 4, img->batch, nullptr).bytes;  // one 4-slot pass
+    if (use_v2(f, nullptr)) return scratch_plan(f, 4, img->batch, nullptr, scratch_es(img->dtype)).bytes;  // one 4-slot pass
   }
   for (int tr = 0; tr < 2; ++tr) {
     const Frame f = make_frame(img->h, img->w, tr, mode == FHT_MODE_FULL);
     const int nq = mode == FHT_MODE_FULL ? 2 : 1;
-    const ScratchPlan sp = scratch_plan(f, nq, img->batch, nullptr);
+    const ScratchPlan sp = scratch_plan(f, nq, img->batch, nullptr, scratch_es(img->dtype));
     need = sp.bytes > need ? sp.bytes : need;
   }
   return need;
@@ -1045,7 +1056,7 @@ int fht_full(const fht_image* img, int layout, fht_hough* out, fht_hough* out_sh
                       !(opts->events && opts->n_events > 0))
                          ? (cudaStream_t)opts->aux_stream
                          : nullptr;
-  const ScratchPlan sp2 = scratch_plan(f0, 2, img->batch, nullptr);
+  const ScratchPlan sp2 = scratch_plan(f0, 2, img->batch, nullptr, scratch_es(img->dtype));
   const size_t half = (sp2.bytes + 255) & ~size_t(255);
   if (FHT_SPLIT_ORIENT && aux && Hp == Wp && use_v2(f0, nullptr) && sp2.nbuf == 1 && sp2.chunk >= img->batch &&
       2 * half <= ws_bytes) {
@@ -1099,7 +1110,7 @@ int fht_angle_range(const fht_image* img, const fht_angle_plan* plan, fht_hough*
   const Frame f = range_frame(img, plan);
   if ((s = check_frame_supported(f))) return s;
   RangeDev rg = range_geometry(f, plan);
-  const ScratchPlan sp = scratch_plan(f, 1, 1, &rg);
+  const ScratchPlan sp = scratch_plan(f, 1, 1, &rg, scratch_es(img->dtype));
   if (plan->rows < f.Hp && !sp.v2) return FHT_ERR_UNSUPPORTED;  // pruned plans: v2 kernels only
   // workspace: [scratch][e_tab h][colmap w'][start Hp][len Hp]
   const size_t scratch = (sp.bytes + 255) & ~size_t(255);

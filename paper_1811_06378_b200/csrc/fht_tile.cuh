@@ -102,6 +102,9 @@ template <> struct Split<4> { static constexpr int a = 2, b = 2, nw = 4; };
 #endif
 template <> struct Split<5> { static constexpr int a = FHT_SPLIT5_A, b = 5 - FHT_SPLIT5_A, nw = 4; };
 template <> struct Split<6> { static constexpr int a = 3, b = 3, nw = 8; };
+// pass-1 scratch element: u8 input keeps F_m (<= 255 * 2^m <= 16320 for m <= 6) in uint16
+template <typename Tin> struct ScrOf { using type = typename AccOf<Tin>::type; };
+template <> struct ScrOf<uint8_t> { using type = uint16_t; };
 template <int R> constexpr int kMinBlocks = Split<R>::nw == 4 ? 5 : 2;  // occupancy target (regs <= 102 / 128)
 template <int R> constexpr int kTPW = ((1 << Split<R>::a) + Split<R>::nw - 1) / Split<R>::nw;  // B tasks/warp
 
@@ -295,22 +298,29 @@ __device__ __forceinline__ void tile_fht(const Tsrc* src, int src_pitch, const i
   tile_fht_ld<R, SIG, A>(load, fa, fa_pitch, w);
 }
 
-template <int Q, typename A>
+// Sg: the staged element type (A, or uint16_t for the u8 pipeline's pass-1 scratch)
+template <int Q, typename Sg, typename A>
 __device__ __forceinline__ void st_pred(uint32_t a, int idx, int box, A v) {
-  const uint32_t bits = *reinterpret_cast<const uint32_t*>(&v);
-  asm volatile("{ .reg .pred p; setp.lt.u32 p, %1, %2; @p st.shared.b32 [%0+%3], %4; }"
-               :: "r"(a), "r"(idx), "r"(box), "n"(Q * 4), "r"(bits) : "memory");
+  if constexpr (sizeof(Sg) == 2) {
+    const uint16_t bits = static_cast<uint16_t>(v);  // exact: u8 pass-1 sums are <= 255 * 2^6
+    asm volatile("{ .reg .pred p; setp.lt.u32 p, %1, %2; @p st.shared.b16 [%0+%3], %4; }"
+                 :: "r"(a), "r"(idx), "r"(box), "n"(Q * 2), "h"(bits) : "memory");
+  } else {
+    const uint32_t bits = *reinterpret_cast<const uint32_t*>(&v);
+    asm volatile("{ .reg .pred p; setp.lt.u32 p, %1, %2; @p st.shared.b32 [%0+%3], %4; }"
+                 :: "r"(a), "r"(idx), "r"(box), "n"(Q * 4), "r"(bits) : "memory");
+  }
 }
-template <int SIG, typename A, int... Q>
+template <int SIG, typename Sg, typename A, int... Q>
 __device__ __forceinline__ void st_pred_row(uint32_t a, int lo, int box, const A (&v)[VB], std::integer_sequence<int, Q...>) {
-  (st_pred<Q>(a, lo + Q, box, v[SIG > 0 ? Q : VB - 1 - Q]), ...);
+  (st_pred<Q, Sg>(a, lo + Q, box, v[SIG > 0 ? Q : VB - 1 - Q]), ...);
 }
 
 // Write the register results into a staging plane of row pitch `pitch`: output row tau, window
 // index s stored at s - soff[tau] when 0 <= that < box. Explicitly predicated st.shared (one
 // ISETP + one STS per element, no branches). Then fence for the TMA engine and synchronise.
-template <int R, int SIG, typename A>
-__device__ __forceinline__ void stage_rows(A (&w)[kTPW<R>][1 << Split<R>::b][VB], A* stg, const int* soff, int box,
+template <int R, int SIG, typename A, typename Sg = A>
+__device__ __forceinline__ void stage_rows(A (&w)[kTPW<R>][1 << Split<R>::b][VB], Sg* stg, const int* soff, int box,
                                            int pitch) {
   using S = Split<R>;
   constexpr int NA = 1 << S::a, NBk = 1 << S::b, NW = S::nw;
@@ -327,12 +337,12 @@ __device__ __forceinline__ void stage_rows(A (&w)[kTPW<R>][1 << Split<R>::b][VB]
 #if FHT_STAGE_ASM
         const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(stg + tau * pitch + lo));
         // element q of the lane sits at staging index lo + q
-        st_pred_row<SIG>(a, lo, box, w[g][u], std::make_integer_sequence<int, VB>{});
+        st_pred_row<SIG, Sg>(a, lo, box, w[g][u], std::make_integer_sequence<int, VB>{});
 #else
-        A* dst = stg + tau * pitch;
+        Sg* dst = stg + tau * pitch;
 #pragma unroll
         for (int q = 0; q < VB; ++q)
-          if ((unsigned)(lo + q) < (unsigned)box) dst[lo + q] = w[g][u][SIG > 0 ? q : VB - 1 - q];
+          if ((unsigned)(lo + q) < (unsigned)box) dst[lo + q] = static_cast<Sg>(w[g][u][SIG > 0 ? q : VB - 1 - q]);
 #endif
       }
     }
@@ -444,7 +454,9 @@ __device__ __noinline__ void p1_tail(const CUtensorMap* tm_scr, const P1Params& 
   } else {
     tile_fht<R, SIG, A>(tsrc, tpitch, rowoff, buf, fa_pitch, w, bars ? bar : nullptr);
   }
-  stage_rows<R, SIG, A>(w, buf, soff, p.TX, p.TX);  // dense [NR][TX]: the box layout
+  // dense [NR][TX] in the scratch type (u8 input: uint16), the box layout
+  using Sc = typename ScrOf<Tin>::type;
+  stage_rows<R, SIG, A, Sc>(w, reinterpret_cast<Sc*>(buf), soff, p.TX, p.TX);
   // ---- store F_m[strip][j] for all j in ONE box {TX, 1, NR} of the 3-D scratch view
   // [z*2^m + j][strip][column] (z = image-in-chunk * nq + slot); column X - xlo is 16-B aligned
   if (threadIdx.x == 0) {
@@ -792,7 +804,7 @@ struct RowInfo {  // per (destination, output row), shared memory, 16 B
 };
 constexpr int kTmaBit = 1 << 30;
 
-template <typename A, int R, int SIG>
+template <typename A, int R, int SIG, typename Tscr>
 __device__ __forceinline__ void p2_body(const CUtensorMap* tm_scr0, const CUtensorMap* tm_scr1,
                                         const CUtensorMap* tm0, const CUtensorMap* tm1, const CUtensorMap* tm0_box,
                                         const P2Params& p, const P2Slot& sl, int img, int j, int X, int own) {
@@ -827,18 +839,22 @@ __device__ __forceinline__ void p2_body(const CUtensorMap* tm_scr0, const CUtens
   // issue in parallel. rowoff of a block's rows is written by the warp that reads them.
   if (!black) {
     const int64_t rbase = p.row0 + (int64_t)(img - p.img0) * p.scratch_img_rows + sl.srow0 + t0;
+    // scratch rows of Tscr: loads start at the 16-byte aligned column below (kAl elements) and
+    // take 256 + kBox1 columns (kBox1 * sizeof(Tscr) a multiple of 16); row i lands at byte
+    // i * TMA_PITCH * 4 of the buffer, where its fa row will be written in place
+    constexpr int kAl = 16 / (int)sizeof(Tscr), kBox1 = sizeof(Tscr) == 2 ? 40 : 36;
     for (int b = warp; b < NBk; b += NW) {
       if (lane == 0) {
         mbar_init(bar + b);
-        mbar_expect_tx(bar + b, NA * (256 + 36) * 4);
+        mbar_expect_tx(bar + b, NA * (256 + kBox1) * (uint32_t)sizeof(Tscr));
         for (int i = b * NA; i < (b + 1) * NA; ++i) {
-          const int a0 = (Xa + SIG * j * i - sl.xlo1) & ~3;
-          A* d = buf + i * TMA_PITCH;
+          const int a0 = (Xa + SIG * j * i - sl.xlo1) & ~(kAl - 1);
+          Tscr* d = reinterpret_cast<Tscr*>(buf + i * TMA_PITCH);
           tma_load_2d(tm_scr0, d, bar + b, a0, (int)(rbase + i));
           tma_load_2d(tm_scr1, d + 256, bar + b, a0 + 256, (int)(rbase + i));
         }
       }
-      if (lane < NA) rowoff[b * NA + lane] = (Xa + SIG * j * (b * NA + lane) - sl.xlo1) & 3;
+      if (lane < NA) rowoff[b * NA + lane] = (Xa + SIG * j * (b * NA + lane) - sl.xlo1) & (kAl - 1);
     }
     __syncwarp();
   }
@@ -901,7 +917,9 @@ __device__ __forceinline__ void p2_body(const CUtensorMap* tm_scr0, const CUtens
   __syncthreads();
 #endif
 
-  if (!black) tile_fht<R, SIG, A>(static_cast<const A*>(buf), TMA_PITCH, rowoff, buf, TMA_PITCH, w, bar);
+  if (!black)
+    tile_fht<R, SIG, A>(reinterpret_cast<const Tscr*>(buf), TMA_PITCH * 4 / (int)sizeof(Tscr), rowoff, buf, TMA_PITCH,
+                        w, bar);
 
   // ---- stores, one destination at a time (the staging plane is reused)
   bool issued = false;
@@ -959,7 +977,7 @@ __device__ __forceinline__ void p2_body(const CUtensorMap* tm_scr0, const CUtens
 
 // tm_scr0: scratch, one row x 256 columns; tm_scr1: one row x 36 columns; tm0 / tm1: destinations
 // (one-row boxes); tm0_box: destination 0 with box {TX + 4, 2^R} (dense interior tiles)
-template <typename A, int R>
+template <typename A, int R, typename Tscr = A>
 __global__ void __launch_bounds__(Split<R>::nw * 32, kMinBlocks<R>)
 k_p2(const __grid_constant__ CUtensorMap tm_scr0, const __grid_constant__ CUtensorMap tm_scr1,
      const __grid_constant__ CUtensorMap tm0, const __grid_constant__ CUtensorMap tm1,
@@ -996,8 +1014,8 @@ k_p2(const __grid_constant__ CUtensorMap tm_scr0, const __grid_constant__ CUtens
   }
   const int X = k + 1 < nk ? lo + p.TX * k : max(lo, hi - (p.TX + WO2));
   const int own = k + 1 < nk ? p.TX : hi - X;
-  if (sl.sigma > 0) p2_body<A, R, 1>(&tm_scr0, &tm_scr1, &tm0, &tm1, &tm0_box, p, sl, img, j, X, own);
-  else p2_body<A, R, -1>(&tm_scr0, &tm_scr1, &tm0, &tm1, &tm0_box, p, sl, img, j, X, own);
+  if (sl.sigma > 0) p2_body<A, R, 1, Tscr>(&tm_scr0, &tm_scr1, &tm0, &tm1, &tm0_box, p, sl, img, j, X, own);
+  else p2_body<A, R, -1, Tscr>(&tm_scr0, &tm_scr1, &tm0, &tm1, &tm0_box, p, sl, img, j, X, own);
 }
 
 }  // namespace v2
