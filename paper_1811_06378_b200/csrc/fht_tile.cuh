@@ -59,6 +59,9 @@
 #ifndef FHT_OUT_EVICT_FIRST
 #define FHT_OUT_EVICT_FIRST 0 // Hough-row TMA stores with an L2 evict-first hint (measured: 0 is ~0.5% faster)
 #endif
+#ifndef FHT_P2_BLACK
+#define FHT_P2_BLACK 1    // pass 2: black-zone tiles store zeros without loads or butterflies
+#endif
 #ifndef FHT_PDL
 #define FHT_PDL 1         // programmatic dependent launch between the passes (griddepcontrol)
 #endif
@@ -827,7 +830,7 @@ __device__ __forceinline__ void p2_body(const CUtensorMap* tm_scr0, const CUtens
   A w[kTPW<R>][1 << S::b][VB];
 
   bool black = false;  // the whole window is outside every row's pattern support
-  if (!p.range) black = SIG > 0 ? (Xw + WC - 1 < -tmax) : (Xw >= p.wc + tmax);
+  if (FHT_P2_BLACK && !p.range) black = SIG > 0 ? (Xw + WC - 1 < -tmax) : (Xw >= p.wc + tmax);
 
   // ---- scratch rows t0 + i, column (x + sigma*j*i) - xlo1 for x = Xa + e: TMA from the
   // aligned-down column, zero outside [0, xhi1 - xlo1) = outside what pass 1 wrote. Issued first,
