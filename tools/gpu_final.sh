@@ -3,12 +3,14 @@
 mkdir -p gpurun_out/final
 timeout 900 python -m pytest tests -m gpu -q 2>&1 | tail -5 > gpurun_out/final/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/final/smoke.log 2>&1
-timeout 900 python bench.py > gpurun_out/final/bench.json 2>gpurun_out/final/bench.err
+S=$(date +%s); timeout 900 python bench.py > gpurun_out/final/bench.json 2>gpurun_out/final/bench.err; echo "default bench wall $(( $(date +%s) - S )) s" > gpurun_out/final/bench_wall.txt
 B="python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-shift-bench --extra-configs none"
 $B > gpurun_out/final/plain_c2.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/final/launches_c2.csv $B > gpurun_out/final/ncu_l.log 2>&1
-$B > gpurun_out/final/plain_c2b.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:k_p -s 8 -c 2 -o gpurun_out/final/prof_c2 $B > gpurun_out/final/ncu_f2.log 2>&1
+# full capture of the launch the roofline describes: one stream, merged 4-slot pass pair (eager)
+BM="$B --no-graph --no-aux"
+$BM > gpurun_out/final/plain_c2b.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:k_p -s 8 -c 2 -o gpurun_out/final/prof_c2 $BM > gpurun_out/final/ncu_f2.log 2>&1
 B5="python bench.py --config 5 --steps 3 --warmup 3 --no-cpu-baseline --no-shift-bench --extra-configs none"
 $B5 > gpurun_out/final/plain_c5.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:k_p -s 64 -c 2 -o gpurun_out/final/prof_c5 $B5 > gpurun_out/final/ncu_f5.log 2>&1
