@@ -342,6 +342,31 @@ def test_v2_full_pair(fht, O, shape, dt):
     assert np.array_equal(sc.view[0, 0].cpu().numpy(), O.fhtshift_concat(gc, Hp, Wp))
 
 
+@pytest.mark.parametrize("side,dt", [(2048, "u8"), (4096, "f32")], ids=["2048-u8", "4096-f32"])
+def test_full_large(fht, O, side, dt):
+    """Largest tilings at full size: u8 2048^2 (R = 6 pass 1 with the uint16 scratch) and f32 4096^2
+    (R = 6 in both passes). Sampled cells of every quadrant by the direct pattern sums, and every row
+    of every quadrant conserves the image total."""
+    from synth import random_image
+    img = random_image((side, side), dt, seed=side + 17)
+    h = fht.full(dev(img))
+    torch.cuda.synchronize()
+    got = h.view[0].cpu().numpy()
+    total = img.astype(np.float64).sum()
+    rng = np.random.default_rng(side)
+    for q in range(4):
+        fr = O.quadrant_frame(img, q, square_to=(side, side))
+        cells = _sample_cells(fr.Hp, fr.W, 96, rng)
+        want = O.hough_cells_direct(fr, cells)
+        vals = np.array([got[q, a, c] for a, c in cells], dtype=got.dtype)
+        check(vals, want, dt != "f32")
+        sums = got[q].astype(np.float64).sum(axis=1)
+        if dt == "f32":
+            assert np.all(np.abs(sums - total) <= 1e-4 * total)
+        else:
+            assert np.all(sums == total)
+
+
 def test_v2_batch_chunks(fht, O):
     """A batch large enough to need several pass-1 scratch chunks (48 MiB budget)."""
     from synth import random_image
