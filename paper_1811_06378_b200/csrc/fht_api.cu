@@ -26,7 +26,19 @@ namespace {
 
 using namespace fht;
 
-constexpr size_t kScratchBudget = size_t(48) << 20;  // touched pass-1 scratch bytes per chunk
+// Pass-1 scratch bytes per batch chunk. Measured (profiles/r01_v2/ab_scratch_budget*.log): fewer, fuller
+// launches beat keeping a chunk's scratch L2-resident -- C5 1528 us at 48 MiB (1 image per chunk),
+// 1391 us with the whole 16-image batch (1.1 GB) in one chunk; C3 318 -> 302 us. 2 GiB of a B200's
+// 180 GB (two buffers when a batch needs several chunks).
+#ifndef FHT_SCRATCH_BUDGET_MB
+#define FHT_SCRATCH_BUDGET_MB 2048
+#endif
+// (the environment variable FHT_SCRATCH_BUDGET_MB overrides it: tests of the multi-chunk schedule)
+size_t scratch_budget() {
+  const char* e = std::getenv("FHT_SCRATCH_BUDGET_MB");
+  const long mb = e ? std::atol(e) : 0;
+  return size_t(mb > 0 ? mb : FHT_SCRATCH_BUDGET_MB) << 20;
+}
 
 int64_t next_pow2(int64_t n) {
   int64_t p = 1;
@@ -161,10 +173,11 @@ int v1_scratch_width(const Frame& f) {
 }
 
 int chunk_images(size_t per_image_touched, int64_t batch) {
-  int64_t c = (int64_t)(kScratchBudget / (per_image_touched ? per_image_touched : 1));
+  int64_t c = (int64_t)(scratch_budget() / (per_image_touched ? per_image_touched : 1));
   if (c < 1) c = 1;
   if (c > batch) c = batch;
-  return (int)c;
+  const int64_t n = (batch + c - 1) / c;  // balanced: 17 images at most 16 per chunk -> 9 + 8
+  return (int)((batch + n - 1) / n);
 }
 
 // Scratch bytes (address extent) and chunk for one orientation with nq slots.

@@ -367,8 +367,9 @@ def test_full_large(fht, O, side, dt):
             assert np.all(sums == total)
 
 
-def test_v2_batch_chunks(fht, O):
-    """A batch large enough to need several pass-1 scratch chunks (48 MiB budget)."""
+def test_v2_batch_chunks(fht, O, monkeypatch):
+    """A batch split into several pass-1 scratch chunks (budget lowered to 48 MiB for the test)."""
+    monkeypatch.setenv("FHT_SCRATCH_BUDGET_MB", "48")
     from synth import random_image
     imgs = np.stack([random_image((1024, 1024), "f32", seed=100 + b) for b in range(7)])
     h = fht.full(dev(imgs))
@@ -381,10 +382,11 @@ def test_v2_batch_chunks(fht, O):
             check(got[b, q], quads[q], False)
 
 
-def test_v2_aux_stream_overlap(fht, O):
+def test_v2_aux_stream_overlap(fht, O, monkeypatch):
     """Pass 1 of chunk k+1 on an auxiliary stream overlapping pass 2 of chunk k (two scratch
     buffers): bit-identical to the single-stream schedule, and the call is complete on the
-    caller's stream."""
+    caller's stream (budget lowered to 48 MiB so the batches need several chunks)."""
+    monkeypatch.setenv("FHT_SCRATCH_BUDGET_MB", "48")
     from synth import random_image
     imgs = np.stack([random_image((1024, 1024), "f32", seed=300 + b) for b in range(7)])
     t = dev(imgs)
