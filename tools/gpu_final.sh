@@ -11,9 +11,10 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpuru
 BM="$B --no-graph --no-aux"
 $BM > gpurun_out/final/plain_c2b.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:k_p -s 8 -c 2 -o gpurun_out/final/prof_c2 $BM > gpurun_out/final/ncu_f2.log 2>&1
-B5="python bench.py --config 5 --steps 3 --warmup 3 --no-cpu-baseline --no-shift-bench --extra-configs none"
+# C5: the whole batch is one chunk; one stream so the captured pair is the per-kernel loop's launch
+B5="python bench.py --config 5 --steps 3 --warmup 3 --no-cpu-baseline --no-shift-bench --extra-configs none --no-aux"
 $B5 > gpurun_out/final/plain_c5.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:k_p -s 64 -c 2 -o gpurun_out/final/prof_c5 $B5 > gpurun_out/final/ncu_f5.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_p -s 6 -c 2 -o gpurun_out/final/prof_c5 $B5 > gpurun_out/final/ncu_f5.log 2>&1
 B4="python bench.py --config 4 --steps 3 --warmup 3 --no-cpu-baseline --no-shift-bench --extra-configs none"
 $B4 > gpurun_out/final/plain_c4.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:k_p -s 8 -c 2 -o gpurun_out/final/prof_c4 $B4 > gpurun_out/final/ncu_f4.log 2>&1
