@@ -86,6 +86,8 @@ typedef struct {
   int64_t W;         /* W' */
   int64_t e_min, e_max; /* min / max of e_y over y < h */
   int64_t rows;         /* output rows: Hp (fht_angle_plan_make), S_max + 1 (fht_angle_plan_make_pruned) */
+  int64_t transposed;   /* 1: mostly-horizontal plan -- the frame is the transposed image and h, w
+                           above are the FRAME's (image w, h); angles are measured from horizontal */
 } fht_angle_plan;
 
 /* Output (Hough image) descriptor. Fill it with fht_hough_describe(), then set `data`. */
@@ -165,6 +167,17 @@ int fht_angle_plan_make(int64_t h, int64_t w, double theta_min_deg, double theta
  * (FHT_ERR_UNSUPPORTED for the degenerate frames of the v1 path). */
 int fht_angle_plan_make_pruned(int64_t h, int64_t w, double theta_min_deg, double theta_max_deg,
                                fht_angle_plan* out);
+
+/* General plan (SURVEY §8(f) f4 "mostly-horizontal range"). flags: FHT_PLAN_PRUNED (as
+ * fht_angle_plan_make_pruned) and/or FHT_PLAN_HORIZONTAL: the range is of inclinations from the
+ * HORIZONTAL (tan = dy/dx) and the plan is built on the transposed image, the frame of the
+ * mostly-horizontal quadrants QC/QD -- so a range near horizontal keeps alpha near 1
+ * instead of being squeezed by the vertical frame's scale. Horizontal [0, 45] equals QD exactly,
+ * [-45, 0] QC with rows reversed. h, w are the IMAGE's; the plan stores the frame's (swapped).
+ * Errors as fht_angle_plan_make / fht_angle_plan_make_pruned. */
+enum { FHT_PLAN_PRUNED = 1, FHT_PLAN_HORIZONTAL = 2 };
+int fht_angle_plan_make_ex(int64_t h, int64_t w, double theta_min_deg, double theta_max_deg, int32_t flags,
+                           fht_angle_plan* out);
 
 /* Angle-range-restricted transform: QA of the virtually sheared+scaled image, the
  * shear and scale fused into the first FHT iteration (pass-1 loader). f32/u8/i32 input. */

@@ -317,6 +317,7 @@ class AnglePlan:
     W: int             # W'
     g: float           # shear in transformed pixels per row: alpha * (-k_lo)
     rows: int = 0      # output rows: Hp (§4 plan) or S_max + 1 (pruned plan); 0 means Hp
+    transposed: bool = False  # mostly-horizontal plan: built on the transposed image (h, w are its)
 
 
 def shear_offsets(g: float, n: int) -> np.ndarray:
@@ -387,6 +388,21 @@ def plan_rows(plan: AnglePlan) -> int:
     return plan.rows if plan.rows else plan.Hp
 
 
+def angle_plan_horizontal(h: int, w: int, phi_min_deg: float, phi_max_deg: float, pruned: bool = False,
+                          k_lo: float | None = None, k_hi: float | None = None) -> AnglePlan:
+    """Mostly-horizontal lines (the transposed image serves the mostly-horizontal quadrants):
+    the same plan built on I^T (h, w of the plan are w, h of the image), angles phi measured from the
+    horizontal, tan phi = dy/dx."""
+    make = angle_plan_pruned if pruned else angle_plan
+    p = make(w, h, phi_min_deg, phi_max_deg, k_lo=k_lo, k_hi=k_hi)
+    p.transposed = True
+    return p
+
+
+def _plan_image(img: np.ndarray, plan: AnglePlan) -> np.ndarray:
+    return np.asarray(img).T if plan.transposed else np.asarray(img)
+
+
 def transformed_image(img: np.ndarray, plan: AnglePlan) -> np.ndarray:
     """Materialise T (Hp x W'): T[y][x'] = I[y][colmap[(x' - e_y) mod W']] if that index < w'."""
     a = _as_acc(np.asarray(img))
@@ -405,7 +421,7 @@ def transformed_image(img: np.ndarray, plan: AnglePlan) -> np.ndarray:
 
 def angle_range(img: np.ndarray, plan: AnglePlan, tier: int = 2) -> np.ndarray:
     """H_{+1}(T) with cyclic width W' -- the QA transform of the sheared and scaled image."""
-    T = transformed_image(img, plan)
+    T = transformed_image(_plan_image(img, plan), plan)
     fr = Frame(rows=T, sigma=+1, h=plan.h, w=plan.W, Hp=plan.Hp, W=plan.W)
     H = hough_of_frame_recursive(fr) if tier == 2 else hough_of_frame_direct(fr)
     return H[: plan_rows(plan)]      # a pruned plan keeps rows s <= S_max of the same transform
@@ -414,7 +430,7 @@ def angle_range(img: np.ndarray, plan: AnglePlan, tier: int = 2) -> np.ndarray:
 def range_cells_direct(img: np.ndarray, plan: AnglePlan, cells) -> np.ndarray:
     """The §4 definition evaluated at listed (s, x0) cells without materialising T:
     sum_y T[y][(x0 + D_s(y)) mod W'] with T as in `transformed_image`."""
-    a = _as_acc(np.asarray(img))
+    a = _as_acc(_plan_image(img, plan))
     colmap = scale_colmap(plan.alpha, plan.w, plan.w_content)
     e = shear_offsets(plan.g, plan.h)
     ys = np.arange(plan.h)

@@ -178,12 +178,15 @@ def full(t: torch.Tensor, layout: str = "quads", shifted: bool = False, pair: bo
     return _finish(res, n, shifted, pair)
 
 
-def angle_plan(h: int, w: int, theta_min_deg: float, theta_max_deg: float, pruned: bool = False) -> FhtAnglePlan:
-    """§4 plan (scale + shear, all Hp rows), or with pruned=True the shift-range-pruned plan (shear
-    only, rows s <= S_max)."""
+def angle_plan(h: int, w: int, theta_min_deg: float, theta_max_deg: float, pruned: bool = False,
+               horizontal: bool = False) -> FhtAnglePlan:
+    """§4 plan (scale + shear, all Hp rows); pruned=True: the shift-range-pruned plan (shear only,
+    rows s <= S_max); horizontal=True: angles from the horizontal, the plan built on
+    the transposed image (mostly-horizontal lines, f4)."""
     p = FhtAnglePlan()
-    name = "fht_angle_plan_make_pruned" if pruned else "fht_angle_plan_make"
-    _lib.check(name, getattr(_lib.lib, name)(h, w, float(theta_min_deg), float(theta_max_deg), ctypes.byref(p)))
+    flags = (_lib.FHT_PLAN_PRUNED if pruned else 0) | (_lib.FHT_PLAN_HORIZONTAL if horizontal else 0)
+    _lib.check("fht_angle_plan_make_ex", _lib.lib.fht_angle_plan_make_ex(h, w, float(theta_min_deg),
+                                                                          float(theta_max_deg), flags, ctypes.byref(p)))
     return p
 
 

@@ -18,6 +18,8 @@ FHT_QA, FHT_QB, FHT_QC, FHT_QD = 0, 1, 2, 3
 FHT_MODE_QUADRANT, FHT_MODE_FULL, FHT_MODE_RANGE = 0, 1, 2
 FHT_LAYOUT_QUADS, FHT_LAYOUT_CONCAT = 0, 1
 
+FHT_PLAN_PRUNED, FHT_PLAN_HORIZONTAL = 1, 2
+
 STATUS = {
     0: "FHT_OK", -1: "FHT_ERR_ARG", -2: "FHT_ERR_DTYPE", -3: "FHT_ERR_SHAPE", -4: "FHT_ERR_ALIGN",
     -5: "FHT_ERR_UNSUPPORTED", -6: "FHT_ERR_WORKSPACE", -7: "FHT_ERR_STATE", -8: "FHT_ERR_CUDA",
@@ -25,7 +27,7 @@ STATUS = {
 
 EXPORTED = (
     "fht_hough_describe", "fht_workspace_bytes", "fht_quadrant", "fht_full", "fht_angle_plan_make",
-    "fht_angle_plan_make_pruned", "fht_angle_range", "fhtshift", "fht_status_string", "fht_peaks_workspace_bytes",
+    "fht_angle_plan_make_pruned", "fht_angle_plan_make_ex", "fht_angle_range", "fhtshift", "fht_status_string", "fht_peaks_workspace_bytes",
     "fht_peaks", "fht_cell_segment",
 )
 
@@ -44,7 +46,7 @@ class FhtAnglePlan(ctypes.Structure):
         ("k_lo", ctypes.c_double), ("k_hi", ctypes.c_double), ("alpha", ctypes.c_double), ("g", ctypes.c_double),
         ("h", ctypes.c_int64), ("w", ctypes.c_int64), ("Hp", ctypes.c_int64),
         ("w_content", ctypes.c_int64), ("W", ctypes.c_int64), ("e_min", ctypes.c_int64), ("e_max", ctypes.c_int64),
-        ("rows", ctypes.c_int64),
+        ("rows", ctypes.c_int64), ("transposed", ctypes.c_int64),
     ]
 
 
@@ -91,6 +93,7 @@ def _load():
     lib.fht_full.argtypes = [P(FhtImage), i32, P(FhtHough), P(FhtHough), vp, sz, vp, P(FhtExecOpts)]
     lib.fht_angle_plan_make.argtypes = [i64, i64, dbl, dbl, P(FhtAnglePlan)]
     lib.fht_angle_plan_make_pruned.argtypes = [i64, i64, dbl, dbl, P(FhtAnglePlan)]
+    lib.fht_angle_plan_make_ex.argtypes = [i64, i64, dbl, dbl, i32, P(FhtAnglePlan)]
     lib.fht_angle_range.argtypes = [P(FhtImage), P(FhtAnglePlan), P(FhtHough), P(FhtHough), vp, sz, vp,
                                     P(FhtExecOpts)]
     lib.fhtshift.argtypes = [P(FhtHough), P(FhtHough), vp]
@@ -101,6 +104,7 @@ def _load():
     lib.fht_status_string.argtypes = [i32]
     lib.fht_status_string.restype = ctypes.c_char_p
     for name in ("fht_hough_describe", "fht_quadrant", "fht_full", "fht_angle_plan_make", "fht_angle_plan_make_pruned",
+                 "fht_angle_plan_make_ex",
                  "fht_angle_range", "fhtshift", "fht_peaks", "fht_cell_segment"):
         getattr(lib, name).restype = i32
     return lib

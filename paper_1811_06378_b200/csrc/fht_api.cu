@@ -124,6 +124,7 @@ struct RangeDev {
   const int* start_tab;
   const int* len_tab;
   double alpha;               // §4 scale: >= 1 lets pass 1 load image rows by TMA (dilation)
+  int transposed;             // mostly-horizontal plan: frame rows are image columns (gather fill)
   int rows;                   // output rows (plan.rows; < Hp for a pruned plan, f2)
   int w_content, x_lo, x_hi;  // scratch signed x range (pass 1)
   int out_lo, out_hi;         // signed x range covered by pass 2 tiles
@@ -430,7 +431,7 @@ int run_orientation(const fht_image* img, const Frame& f, const Slot* slots, int
 #define FHT_RANGE_TMA 1
 #endif
     // range: TMA rows + shared-memory gather when a tile row's source span fits one row load
-    p1.fill_tma = pitch16 && (!rg || (FHT_RANGE_TMA && rg->alpha >= 1.0));
+    p1.fill_tma = pitch16 && (!rg || (FHT_RANGE_TMA && rg->alpha >= 1.0 && !rg->transposed));
     p1.fill_vec = f.m >= 2 && (es == 1 ? ((reinterpret_cast<uintptr_t>(img->data) & 3) == 0 &&
                                           img->row_stride % 4 == 0 && (img->batch == 1 || img->batch_stride % 4 == 0))
                                        : pitch16);
@@ -787,15 +788,20 @@ int plan_e(double g, int64_t y) {
   return (int)std::floor(p + 0.5);
 }
 
+// the plan's frame is the image, or its transpose for a mostly-horizontal plan
+bool plan_matches(const fht_image* img, const fht_angle_plan* plan) {
+  return plan->transposed ? (plan->h == img->w && plan->w == img->h) : (plan->h == img->h && plan->w == img->w);
+}
+
 Frame range_frame(const fht_image* img, const fht_angle_plan* plan) {
   Frame f{};
-  f.transposed = 0;
+  f.transposed = plan->transposed ? 1 : 0;
   f.Hp = (int)plan->Hp;
   f.K = ilog2(f.Hp);
   f.wc = (int)plan->w_content;
   f.W = (int)plan->W;
-  f.rows_avail = (int)img->h;
-  f.cols_avail = (int)img->w;
+  f.rows_avail = (int)plan->h;
+  f.cols_avail = (int)plan->w;
   split_levels(f);
   return f;
 }
@@ -804,6 +810,7 @@ RangeDev range_geometry(const Frame& f, const fht_angle_plan* plan) {
   RangeDev rg{};
   rg.w_content = (int)plan->w_content;
   rg.alpha = plan->alpha;
+  rg.transposed = plan->transposed ? 1 : 0;
   rg.rows = (int)plan->rows;
   rg.x_lo = (int)plan->e_min - ((1 << f.m) - 1);
   rg.x_hi = (int)(plan->e_max + plan->w_content);
@@ -925,6 +932,15 @@ int fht_angle_plan_make_pruned(int64_t h, int64_t w, double tmin, double tmax, f
   return plan_make(h, w, tmin, tmax, true, out);
 }
 
+int fht_angle_plan_make_ex(int64_t h, int64_t w, double tmin, double tmax, int32_t flags, fht_angle_plan* out) {
+  if (flags & ~(FHT_PLAN_PRUNED | FHT_PLAN_HORIZONTAL)) return FHT_ERR_ARG;
+  const bool hz = (flags & FHT_PLAN_HORIZONTAL) != 0;
+  // mostly-horizontal: the vertical plan of the transposed image (frame h, w = image w, h)
+  const int r = plan_make(hz ? w : h, hz ? h : w, tmin, tmax, (flags & FHT_PLAN_PRUNED) != 0, out);
+  if (r == FHT_OK) out->transposed = hz ? 1 : 0;
+  return r;
+}
+
 int fht_hough_describe(int mode, int layout, int quadrant, const fht_image* img, const fht_angle_plan* plan,
                        fht_hough* out) {
   if (!img || !out) return FHT_ERR_ARG;
@@ -958,7 +974,7 @@ int fht_hough_describe(int mode, int layout, int quadrant, const fht_image* img,
     }
     d.cols = d.Hp + d.Wp;
   } else if (mode == FHT_MODE_RANGE) {
-    if (!plan || plan->h != img->h || plan->w != img->w) return FHT_ERR_ARG;
+    if (!plan || !plan_matches(img, plan)) return FHT_ERR_ARG;
     if (plan->rows < 1 || plan->rows > plan->Hp) return FHT_ERR_ARG;
     d.nquad = 1;
     d.rows = plan->rows;
@@ -1114,7 +1130,7 @@ int fht_angle_range(const fht_image* img, const fht_angle_plan* plan, fht_hough*
                     void* ws, size_t ws_bytes, fht_stream_t stream, const fht_exec_opts* opts) {
   int s = check_image(img);
   if (s) return s;
-  if (!plan || plan->h != img->h || plan->w != img->w) return FHT_ERR_ARG;
+  if (!plan || !plan_matches(img, plan)) return FHT_ERR_ARG;
   fht_hough want;
   if ((s = fht_hough_describe(FHT_MODE_RANGE, 0, 0, img, plan, &want))) return s;
   if ((s = validate_outs(img, out, out_shifted, want, ws, ws_bytes))) return s;
@@ -1128,15 +1144,15 @@ int fht_angle_range(const fht_image* img, const fht_angle_plan* plan, fht_hough*
   // workspace: [scratch][e_tab h][colmap w'][start Hp][len Hp]
   const size_t scratch = (sp.bytes + 255) & ~size_t(255);
   int* tab = reinterpret_cast<int*>(static_cast<char*>(ws) + scratch);
-  rg.e_tab = tab;
-  rg.colmap = tab + img->h;
-  rg.start_tab = tab + img->h + plan->w_content;
+  rg.e_tab = tab;  // frame rows (image columns for a transposed plan)
+  rg.colmap = tab + plan->h;
+  rg.start_tab = tab + plan->h + plan->w_content;
   rg.len_tab = rg.start_tab + f.Hp;
   RangeTableArgs ta{};
   ta.g = plan->g;
   ta.alpha = plan->alpha;
-  ta.h = (int)img->h;
-  ta.w = (int)img->w;
+  ta.h = (int)plan->h;  // the frame's rows / columns
+  ta.w = (int)plan->w;
   ta.w_content = (int)plan->w_content;
   ta.Hp = f.Hp;
   ta.K = f.K;
@@ -1145,14 +1161,15 @@ int fht_angle_range(const fht_image* img, const fht_angle_plan* plan, fht_hough*
   ta.start_tab = const_cast<int*>(rg.start_tab);
   ta.len_tab = const_cast<int*>(rg.len_tab);
   const int nb_tab = (f.Hp + kRangeRowsPerBlock - 1) / kRangeRowsPerBlock +
-                     (int)((std::max<int64_t>(img->h, plan->w_content) + kThreads - 1) / kThreads);
+                     (int)((std::max<int64_t>(plan->h, plan->w_content) + kThreads - 1) / kThreads);
   LaunchLog log{opts, 0};
   log.before((cudaStream_t)stream);
-  k_range_tables<<<nb_tab, kThreads, (size_t)img->h * sizeof(int), (cudaStream_t)stream>>>(ta);
+  k_range_tables<<<nb_tab, kThreads, (size_t)plan->h * sizeof(int), (cudaStream_t)stream>>>(ta);
   if (cudaGetLastError() != cudaSuccess) return FHT_ERR_CUDA;
   log.after((cudaStream_t)stream);
   Slot sl{};
   sl.sigma = 1;
+  sl.transposed = plan->transposed ? 1 : 0;  // mostly-horizontal: the loader reads I[colmap[u]][y]
   sl.row_sign = 1;
   sl.skip_t = -1;
   Outs o{{out, out_shifted}};

@@ -643,10 +643,13 @@ __device__ __forceinline__ void p1_body(const CUtensorMap* tm_img0, const CUtens
     rowoff[threadIdx.x] = 0;
     soff[threadIdx.x] = 0;
   }
-  if (!sl.transposed) {
+  if (!sl.transposed || p.range) {
     // ---- scalar fill (angle-range gather T(x, y) = I[y][colmap[x - e_y]], or odd pitches), in
     // batches of CH elements per thread: every gather of a batch is in flight before its stores
-    // (the colmap -> pixel chain is two dependent loads; 4 in flight per thread was latency-bound)
+    // (the colmap -> pixel chain is two dependent loads; 4 in flight per thread was latency-bound).
+    // A mostly-horizontal range plan (transposed slot) gathers T(x, y) = I[colmap[x - e_y]][y]:
+    // frame row y is image column y.
+    const int frows = sl.transposed ? p.img_w : p.img_h;
     constexpr int ITS = (NR * WA + NT - 1) / NT;
     constexpr int CH = ITS >= 12 ? 12 : ITS;
 #pragma unroll 1
@@ -659,7 +662,7 @@ __device__ __forceinline__ void p1_body(const CUtensorMap* tm_img0, const CUtens
         const int rho = idx / WA, e = idx - rho * WA;
         const int y = y0 + rho, x = Xa + e;
         cm[c] = -1;
-        if (it0 + c < ITS && idx < NR * WA && y < p.img_h) {
+        if (it0 + c < ITS && idx < NR * WA && y < frows) {
           if (!p.range) {
             if (x >= 0 && x < p.img_w) cm[c] = x;
           } else {  // P:146; R13, R14
@@ -672,7 +675,9 @@ __device__ __forceinline__ void p1_body(const CUtensorMap* tm_img0, const CUtens
       for (int c = 0; c < CH; ++c) {  // stage 2: the pixels
         const int idx = threadIdx.x + (it0 + c) * NT;
         const int rho = idx / WA;
-        v[c] = cm[c] >= 0 ? static_cast<A>(__ldg(src + (int64_t)(y0 + rho) * p.img_rstride + cm[c])) : A(0);
+        const int64_t off = sl.transposed ? (int64_t)cm[c] * p.img_rstride + (y0 + rho)
+                                          : (int64_t)(y0 + rho) * p.img_rstride + cm[c];
+        v[c] = cm[c] >= 0 ? static_cast<A>(__ldg(src + off)) : A(0);
       }
 #pragma unroll
       for (int c = 0; c < CH; ++c) {  // stage 3: shared memory

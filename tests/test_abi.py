@@ -36,7 +36,7 @@ def test_struct_sizes_match_header(tmp_path):
     got = [int(x) for x in subprocess.run([str(tmp_path / "sz")], capture_output=True, text=True, check=True).stdout.split()]
     assert got == [ctypes.sizeof(L.FhtImage), ctypes.sizeof(L.FhtAnglePlan), ctypes.sizeof(L.FhtHough),
                    ctypes.sizeof(L.FhtExecOpts)]
-    assert ctypes.sizeof(L.FhtAnglePlan) == 6 * 8 + 8 * 8
+    assert ctypes.sizeof(L.FhtAnglePlan) == 6 * 8 + 9 * 8
 
 
 def _img(L, h, w, b=1, dt=2, data=4096):
@@ -93,6 +93,30 @@ def test_pruned_plan_matches_oracle_rule():
     p = L.FhtAnglePlan()
     assert L.lib.fht_angle_plan_make(64, 64, -15, 15, ctypes.byref(p)) == 0 and p.rows == p.Hp
     assert L.lib.fht_angle_plan_make_pruned(64, 64, -30, 30, ctypes.byref(p)) == -5   # k_hi - k_lo > 1
+
+
+def test_plan_ex_matches_oracle():
+    """fht_angle_plan_make_ex: HORIZONTAL builds the plan on the transposed image (frame h, w swapped),
+    PRUNED as before, both combined; descriptors follow the frame."""
+    from oracle import fht_oracle as O
+    L = _lib()
+    for h, w, a, b, flags in [(64, 48, -15, 15, 2), (33, 17, 5, 40, 2), (128, 96, -20, 10, 3), (16, 16, 0, 45, 2)]:
+        p = L.FhtAnglePlan()
+        assert L.lib.fht_angle_plan_make_ex(h, w, a, b, flags, ctypes.byref(p)) == 0
+        o = O.angle_plan_horizontal(h, w, a, b, pruned=bool(flags & 1))
+        assert p.transposed == 1 and (p.h, p.w) == (o.h, o.w) == (w, h)
+        assert (p.k_lo, p.k_hi, p.alpha, p.g) == (o.k_lo, o.k_hi, o.alpha, o.g)
+        assert (p.Hp, p.w_content, p.W, p.rows) == (o.Hp, o.w_content, o.W, O.plan_rows(o))
+        d = L.FhtHough()
+        img = _img(L, h, w)
+        assert L.lib.fht_hough_describe(L.FHT_MODE_RANGE, 0, 0, ctypes.byref(img), ctypes.byref(p), ctypes.byref(d)) == 0
+        assert (d.rows, d.cols) == (O.plan_rows(o), o.W)
+        bad = _img(L, w, h) if w != h else None
+        if bad is not None:   # the plan's frame is the transposed image: an h x w plan does not fit w x h
+            assert L.lib.fht_hough_describe(L.FHT_MODE_RANGE, 0, 0, ctypes.byref(bad), ctypes.byref(p),
+                                            ctypes.byref(d)) == -1
+    p = L.FhtAnglePlan()
+    assert L.lib.fht_angle_plan_make_ex(16, 16, -10, 10, 4, ctypes.byref(p)) == -1    # unknown flag
 
 
 def test_plan_errors():

@@ -4,6 +4,8 @@ Bar: integer input -> bit-exact int32; float32 input -> |gpu - o
 ATOL + RTOL |o64| with RTOL = 1e-5, ATOL = 1e-3 (north_star; R21). fhtshift is a bit copy
 and is compared exactly against the oracle's rotation of the GPU's own unshifted output.
 """
+import math
+
 import numpy as np
 import pytest
 import torch
@@ -141,6 +143,52 @@ def test_angle_range_pruned_small(fht, O, shape, dt):
         assert np.array_equal(rs.view[0, 0].cpu().numpy(), want_s)
         assert np.array_equal(fr.view[0, 0].cpu().numpy(), got)
         assert np.array_equal(fs.view[0, 0].cpu().numpy(), want_s)
+
+
+HORIZONTAL_RANGES = [(-15, 15), (5, 40), (-30, -2), (0, 45), (-80, 80)]
+
+
+@pytest.mark.parametrize("shape", [(16, 16), (33, 17), (64, 48), (96, 200)], ids=str)
+@pytest.mark.parametrize("dt", ["u8", "f32"])
+def test_angle_range_horizontal_small(fht, O, shape, dt):
+    """f4: mostly-horizontal plans (the transposed image's frame, the loader gathering I[colmap][y]),
+    scaled and pruned; all cells against the oracle, fhtshift fused and standalone."""
+    from synth import random_image
+    img = random_image(shape, dt, seed=shape[0] * 5 + shape[1])
+    t = dev(img)
+    for tmin, tmax in HORIZONTAL_RANGES:
+        for pruned in (False, True):
+            if pruned and math.tan(math.radians(tmax)) - math.tan(math.radians(tmin)) > 1.0:
+                continue
+            p = fht.angle_plan(*shape, tmin, tmax, pruned=pruned, horizontal=True)
+            op = O.angle_plan_horizontal(*shape, tmin, tmax, pruned=pruned, k_lo=p.k_lo, k_hi=p.k_hi)
+            assert (op.W, O.plan_rows(op)) == (p.W, p.rows)
+            r, rs = fht.angle_range(t, p, pair=True)
+            s2 = fht.fhtshift(r)
+            torch.cuda.synchronize()
+            got = r.view[0, 0].cpu().numpy()
+            check(got, O.angle_range(img, op), dt != "f32")
+            want_s = O.fhtshift_range(got, op)
+            assert np.array_equal(rs.view[0, 0].cpu().numpy(), want_s)
+            assert np.array_equal(s2.view[0, 0].cpu().numpy(), want_s)
+
+
+def test_angle_range_horizontal_large(fht, O):
+    """A 1024 x 2048 f32 image, lines within 20 deg of the horizontal: sampled cells by the direct
+    pattern sums of the transposed frame, row conservation on every row."""
+    from synth import random_image
+    img = random_image((1024, 2048), "f32", seed=2048)
+    p = fht.angle_plan(1024, 2048, -20.0, 20.0, horizontal=True)
+    op = O.angle_plan_horizontal(1024, 2048, -20.0, 20.0, k_lo=p.k_lo, k_hi=p.k_hi)
+    r = fht.angle_range(dev(img), p)
+    torch.cuda.synchronize()
+    got = r.view[0, 0].cpu().numpy()
+    assert got.shape == (op.Hp, op.W)
+    rng = np.random.default_rng(20)
+    cells = _sample_cells(op.Hp, op.W, 1024, rng)
+    check(np.array([got[a, b] for a, b in cells], dtype=np.float32), O.range_cells_direct(img, op, cells), False)
+    T_total = float(O.transformed_image(img.T, op).astype(np.float64).sum())
+    assert np.all(np.abs(got.astype(np.float64).sum(axis=1) - T_total) <= 1e-4 * abs(T_total) + 1e-2)
 
 
 def test_angle_range_pruned_c4_image(fht, O):

@@ -332,6 +332,20 @@ def test_pruned_peak_location():
         assert R.max() >= P // 2          # the line's pixels concentrate in one cell (not exact: DDA != dyadic)
 
 
+@pytest.mark.parametrize("shape", [(8, 8), (16, 11), (5, 7), (32, 20)])
+def test_horizontal_plan_is_qd_qc(shape):
+    """Mostly-horizontal plans (f4): [0, 45] from the horizontal is exactly QD (I^T, +), and
+    [-45, 0] is QC (I^T, -) with rows reversed -- the transposed counterparts of the QA / QB pins."""
+    img = random_image(shape, "i32", seed=shape[0] * 11 + shape[1])
+    p = O.angle_plan_horizontal(*shape, 0.0, 45.0)
+    qd = O.hough_recursive(img, O.QD)
+    assert (p.h, p.w) == (shape[1], shape[0]) and p.W == qd.shape[1]
+    assert (O.angle_range(img, p) == qd).all()
+    q = O.angle_plan_horizontal(*shape, -45.0, 0.0)
+    qc = O.hough_recursive(img, O.QC)
+    assert (O.angle_range(img, q) == qc[::-1]).all()
+
+
 def test_range_support_no_fold():
     """R17: with W' chosen by the rule, each row's unwrapped support fits in W' columns."""
     for tmin, tmax in [(-15, 15), (5, 40), (-80, 80), (1, 2)]:
