@@ -608,6 +608,7 @@ def main():
                      "share_of_step": head["kernels"]["pass2_share_of_step"], "peak_source": peak_src},
         "step_roofline": {"bytes": head["in_bytes"] + head["out_bytes"], "achieved": head["step_gbs"],
                           "peak": peak_gbs, "frac": head["step_gbs"] / peak_gbs,
+                          "frac_vs_nominal_8tbs": head["step_gbs"] / 8000.0,
                           "note": "compulsory bytes (one read of the image + one write of every output) / step time"},
         "kernels": head["kernels"],
         "cpu_baseline": cpu,
