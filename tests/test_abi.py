@@ -213,3 +213,31 @@ def test_cell_segment_matches_oracle():
                         assert (sg.quadrant, sg.s, sg.npix) == (q, s, len(pix))
                         if pix:
                             assert (sg.x0, sg.y0, sg.x1, sg.y1) == (*pix[0], *pix[-1])
+
+
+def test_peaks_and_segment_errors():
+    """Synchronous argument checks of the f3 entry points (no device work is enqueued)."""
+    L = _lib()
+    img = _img(L, 16, 16)
+    d = L.FhtHough()
+    assert L.lib.fht_hough_describe(L.FHT_MODE_FULL, L.FHT_LAYOUT_QUADS, 0, ctypes.byref(img), None, ctypes.byref(d)) == 0
+    d.data = 4096
+    n = L.lib.fht_peaks_workspace_bytes(ctypes.byref(d))
+    assert n > 0
+    ws = 8192
+    assert L.lib.fht_peaks(ctypes.byref(d), 0, 4096, 4096, 4096, ws, n, None) == -1       # k < 1
+    assert L.lib.fht_peaks(ctypes.byref(d), 33, 4096, 4096, 4096, ws, n, None) == -1      # k > 32
+    assert L.lib.fht_peaks(ctypes.byref(d), 8, None, 4096, 4096, ws, n, None) == -1       # NULL output
+    assert L.lib.fht_peaks(ctypes.byref(d), 8, 4096, 4096, 4096, ws, n - 1, None) == -6   # workspace too small
+    du = L.FhtHough.from_buffer_copy(d)
+    du.dtype = L.FHT_U8
+    assert L.lib.fht_peaks(ctypes.byref(du), 8, 4096, 4096, 4096, ws, n, None) == -2      # dtype
+    sg = L.FhtSegment()
+    assert L.lib.fht_cell_segment(ctypes.byref(d), 0, d.rows, 0, ctypes.byref(sg)) == -1  # row out of range
+    assert L.lib.fht_cell_segment(ctypes.byref(d), 4, 0, 0, ctypes.byref(sg)) == -1       # slot out of range
+    assert L.lib.fht_cell_segment(ctypes.byref(d), 0, 0, d.cols, ctypes.byref(sg)) == -1  # col out of range
+    p = L.FhtAnglePlan()
+    assert L.lib.fht_angle_plan_make(16, 16, -15, 15, ctypes.byref(p)) == 0
+    dr = L.FhtHough()
+    assert L.lib.fht_hough_describe(L.FHT_MODE_RANGE, 0, 0, ctypes.byref(img), ctypes.byref(p), ctypes.byref(dr)) == 0
+    assert L.lib.fht_cell_segment(ctypes.byref(dr), 0, 0, 0, ctypes.byref(sg)) == -5      # RANGE: unsupported
