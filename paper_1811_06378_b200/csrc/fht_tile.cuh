@@ -62,6 +62,9 @@
 #ifndef FHT_P2_BLACK
 #define FHT_P2_BLACK 1    // pass 2: black-zone tiles store zeros without loads or butterflies
 #endif
+#ifndef FHT_P2_REVERSE_DEST
+#define FHT_P2_REVERSE_DEST 1  // pass 2: store the second destination (fhtshift) first (measured ~1% faster)
+#endif
 #ifndef FHT_PDL
 #define FHT_PDL 1         // programmatic dependent launch between the passes (griddepcontrol)
 #endif
@@ -931,11 +934,12 @@ __device__ __forceinline__ void p2_body(const CUtensorMap* tm_scr0, const CUtens
 
   // ---- stores, one destination at a time (the staging plane is reused)
   bool issued = false;
-  for (int d = 0; d < p.ndest; ++d) {
+  for (int dd = 0; dd < p.ndest; ++dd) {
+    const int d = FHT_P2_REVERSE_DEST ? p.ndest - 1 - dd : dd;
     const P2Dest& D = p.dest[d];
     const RowInfo* inf = info + d * NR;
     const int* so = soff + d * 64;
-    if (d > 0) {
+    if (dd > 0) {
       if (issued) tma_wait_read();
       __syncthreads();
     }
