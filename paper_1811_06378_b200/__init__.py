@@ -78,11 +78,14 @@ def _image(t: torch.Tensor) -> tuple[FhtImage, torch.Tensor]:
     return img, t
 
 
-def _alloc_out(mode: int, layout: int, q: int, img: FhtImage, plan, device) -> tuple[FhtHough, torch.Tensor]:
+def _alloc_out(mode: int, layout: int, q: int, img: FhtImage, plan, device, pad=None) -> tuple[FhtHough, torch.Tensor]:
     d = FhtHough()
-    _lib.check("fht_hough_describe",
-               _lib.lib.fht_hough_describe(mode, layout, q, ctypes.byref(img),
-                                           ctypes.byref(plan) if plan is not None else None, ctypes.byref(d)))
+    if pad is not None:
+        _lib.check("fht_hough_describe_pad", _lib.lib.fht_hough_describe_pad(q, ctypes.byref(img), pad, ctypes.byref(d)))
+    else:
+        _lib.check("fht_hough_describe",
+                   _lib.lib.fht_hough_describe(mode, layout, q, ctypes.byref(img),
+                                               ctypes.byref(plan) if plan is not None else None, ctypes.byref(d)))
     storage = torch.empty(d.batch * d.batch_stride, dtype=_DT_OUT[d.dtype], device=device)
     d.data = storage.data_ptr()
     return d, storage
@@ -104,7 +107,7 @@ def _stream(t: torch.Tensor):
     return ctypes.c_void_p(torch.cuda.current_stream(t.device).cuda_stream)
 
 
-def _descs(kind, img, plan, q, layout, device, shifted, pair, out, out_shifted):
+def _descs(kind, img, plan, q, layout, device, shifted, pair, out, out_shifted, pad=None):
     """The (plain, shifted) output pair a transform call writes; None where not requested."""
     want_plain = pair or not shifted
     want_shift = pair or shifted
@@ -114,7 +117,7 @@ def _descs(kind, img, plan, q, layout, device, shifted, pair, out, out_shifted):
             res.append(None)
             continue
         if given is None:
-            d, storage = _alloc_out(kind, layout, q, img, plan, device)
+            d, storage = _alloc_out(kind, layout, q, img, plan, device, pad)
             given = HoughImage(storage, d)
         res.append(given)
     return res
@@ -152,10 +155,11 @@ def _finish(res, n, shifted, pair):
 def quadrant(t: torch.Tensor, q: int, pad: int | None = None, shifted: bool = False, pair: bool = False,
              workspace: torch.Tensor | None = None, out: HoughImage | None = None,
              out_shifted: HoughImage | None = None, events=None, aux_stream=None):
-    """One quadrant (P:52-67). shifted=True returns fhtshift(H) written directly by the transform;
-    pair=True returns (H, fhtshift(H)) from one pass."""
+    """One quadrant. pad: extension columns (None = Hp; any pad >= h_frame - 1 on the GPU).
+    shifted=True returns fhtshift(H) written directly by the transform; pair=True returns
+    (H, fhtshift(H)) from one pass."""
     img, t = _image(t)
-    res = _descs(FHT_MODE_QUADRANT, img, None, q, 0, t.device, shifted, pair, out, out_shifted)
+    res = _descs(FHT_MODE_QUADRANT, img, None, q, 0, t.device, shifted, pair, out, out_shifted, pad)
     ws_n = workspace_bytes(FHT_MODE_QUADRANT, img)
     ws = _workspace(ws_n, t.device, workspace)
     n = _lib.check("fht_quadrant", _lib.lib.fht_quadrant(ctypes.byref(img), q, -1 if pad is None else pad,

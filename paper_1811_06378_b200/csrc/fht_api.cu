@@ -83,14 +83,14 @@ void split_levels(Frame& f) {
   }
 }
 
-Frame make_frame(int64_t h, int64_t w, int transposed, int full) {
+Frame make_frame(int64_t h, int64_t w, int transposed, int full, int64_t pad = -1) {
   Frame f{};
   f.transposed = transposed;
   const int64_t rows = transposed ? w : h, cols = transposed ? h : w;
   f.Hp = (int)next_pow2(rows);
   f.K = ilog2(f.Hp);
   f.wc = full ? (int)next_pow2(cols) : (int)cols;  // R9: FULL pads both dims to powers of two
-  f.W = f.wc + f.Hp;
+  f.W = f.wc + (pad < 0 ? f.Hp : (int)pad);          // extended by pad (default Hp) columns
   f.rows_avail = (int)rows;
   f.cols_avail = (int)cols;
   split_levels(f);
@@ -485,7 +485,7 @@ int run_orientation(const fht_image* img, const Frame& f, const Slot* slots, int
         s.xbeg = rg->out_lo;
         s.xend = rg->out_hi;
       } else {
-        s.xbeg = s.sigma > 0 ? -f.Hp : 0;
+        s.xbeg = s.sigma > 0 ? -(f.W - f.wc) : 0;  // signed columns [-pad, wc) (sigma = +1), [0, W)
         s.xend = s.xbeg + p2.W;
       }
       // sigma = +1 rows wrap at x = 0 (x < 0 is stored at x + W): no tile straddles it
@@ -994,6 +994,17 @@ int fht_hough_describe(int mode, int layout, int quadrant, const fht_image* img,
   return FHT_OK;
 }
 
+int fht_hough_describe_pad(int quadrant, const fht_image* img, int64_t pad_cols, fht_hough* out) {
+  int s = fht_hough_describe(FHT_MODE_QUADRANT, 0, quadrant, img, nullptr, out);
+  if (s || pad_cols == -1) return s;
+  if (pad_cols < 0) return FHT_ERR_ARG;
+  out->cols = (quadrant >= 2 ? img->h : img->w) + pad_cols;
+  out->row_stride = (out->cols + 3) & ~int64_t(3);
+  out->quad_stride = out->rows * out->row_stride;
+  out->batch_stride = out->nquad * out->quad_stride;
+  return FHT_OK;
+}
+
 size_t fht_workspace_bytes(int mode, const fht_image* img, const fht_angle_plan* plan) {
   if (!img || img->batch < 1 || img->h < 1 || img->w < 1) return 0;
   if (mode == FHT_MODE_RANGE) {
@@ -1022,11 +1033,17 @@ int fht_quadrant(const fht_image* img, int quadrant, int64_t pad_cols, fht_hough
   int s = check_image(img);
   if (s) return s;
   if (quadrant < 0 || quadrant > 3) return FHT_ERR_ARG;
+  // pad (R22): any pad >= h_frame - 1 keeps every line's signed columns apart mod
+  // w + pad (rows >= h are zero, so no pattern reaches further than h - 1 columns); a smaller
+  // pad folds lines cyclically and would need a fold pass (not built: UNSUPPORTED)
+  const int64_t hf = quadrant >= 2 ? img->w : img->h;
+  if (pad_cols < -1) return FHT_ERR_ARG;
+  if (pad_cols != -1 && pad_cols < hf - 1) return FHT_ERR_UNSUPPORTED;
   fht_hough want;
-  s = fht_hough_describe(FHT_MODE_QUADRANT, 0, quadrant, img, nullptr, &want);
+  s = fht_hough_describe_pad(quadrant, img, pad_cols, &want);
   if (s) return s;
-  const Frame f = make_frame(img->h, img->w, quadrant >= 2, 0);
-  if (pad_cols != -1 && pad_cols != f.Hp) return FHT_ERR_UNSUPPORTED;
+  const Frame f = make_frame(img->h, img->w, quadrant >= 2, 0, pad_cols);
+  if (pad_cols != -1 && pad_cols != f.Hp && !use_v2(f, nullptr)) return FHT_ERR_UNSUPPORTED;
   if ((s = validate_outs(img, out, out_shifted, want, ws, ws_bytes))) return s;
   if ((out && out->quadrant != quadrant) || (out_shifted && out_shifted->quadrant != quadrant)) return FHT_ERR_ARG;
   if ((s = check_frame_supported(f))) return s;

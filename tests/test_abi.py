@@ -241,3 +241,19 @@ def test_peaks_and_segment_errors():
     dr = L.FhtHough()
     assert L.lib.fht_hough_describe(L.FHT_MODE_RANGE, 0, 0, ctypes.byref(img), ctypes.byref(p), ctypes.byref(dr)) == 0
     assert L.lib.fht_cell_segment(ctypes.byref(dr), 0, 0, 0, ctypes.byref(sg)) == -5      # RANGE: unsupported
+
+
+def test_pad_describe_and_limits():
+    """fht_hough_describe_pad: cols = w_frame + pad; fht_quadrant rejects pads that would fold lines
+    (pad < h_frame - 1) before any device work."""
+    L = _lib()
+    img = _img(L, 100, 60)
+    d = L.FhtHough()
+    assert L.lib.fht_hough_describe_pad(0, ctypes.byref(img), 99, ctypes.byref(d)) == 0
+    assert (d.rows, d.cols) == (128, 60 + 99) and d.row_stride % 4 == 0
+    assert L.lib.fht_hough_describe_pad(2, ctypes.byref(img), 59, ctypes.byref(d)) == 0
+    assert (d.rows, d.cols) == (64, 100 + 59)
+    assert L.lib.fht_hough_describe_pad(0, ctypes.byref(img), -1, ctypes.byref(d)) == 0 and d.cols == 60 + 128
+    assert L.lib.fht_hough_describe_pad(0, ctypes.byref(img), -2, ctypes.byref(d)) == -1
+    assert L.lib.fht_quadrant(ctypes.byref(img), 0, 98, ctypes.byref(d), None, None, 0, None, None) == -5
+    assert L.lib.fht_quadrant(ctypes.byref(img), 2, 58, ctypes.byref(d), None, None, 0, None, None) == -5
