@@ -135,6 +135,9 @@ int fht_hough_describe(int mode, int layout, int quadrant, const fht_image* img,
  * (w_frame = w for QA/QB, h for QC/QD); pad_cols = -1 means Hp (= fht_hough_describe). */
 int fht_hough_describe_pad(int quadrant, const fht_image* img, int64_t pad_cols, fht_hough* out);
 
+/* Workspace for fht_quadrant with this pad (a pad below h_frame - 1 adds the pad = Hp image). */
+size_t fht_quadrant_workspace_bytes(const fht_image* img, int quadrant, int64_t pad_cols);
+
 /* Device workspace (bytes) the call needs for `img` (pass-1 scratch + tables). */
 size_t fht_workspace_bytes(int mode, const fht_image* img, const fht_angle_plan* plan);
 
@@ -145,11 +148,12 @@ size_t fht_workspace_bytes(int mode, const fht_image* img, const fht_angle_plan*
  * pitch, and must not overlap each other, the image or the workspace. On success
  * out->shifted = 0 and out_shifted->shifted = 1. */
 
-/* One quadrant. pad_cols: -1 (= Hp), or any pad >= h_frame - 1 (h_frame = h
- * for QA/QB, w for QC/QD; the paper's literal "extended by h" included): every line's
- * columns stay apart mod w_frame + pad. Smaller pads fold lines cyclically and return
- * FHT_ERR_UNSUPPORTED on the GPU (the oracle handles any pad). Outputs from
- * fht_hough_describe_pad(quadrant, img, pad_cols, ...) (pad -1: fht_hough_describe). */
+/* One quadrant. pad_cols: -1 (= Hp) or any pad >= 0 (R22). For pad >=
+ * h_frame - 1 (h_frame = h for QA/QB, w for QC/QD; the paper's literal "extended by h" included)
+ * every line's columns stay apart mod w_frame + pad and the two passes write the image directly;
+ * a smaller pad folds lines cyclically ("mod(w+h)"): the pad = Hp transform goes into the
+ * workspace and one more kernel folds it mod w_frame + pad. Outputs from
+ * fht_hough_describe_pad(quadrant, img, pad_cols, ...); workspace fht_quadrant_workspace_bytes(). */
 int fht_quadrant(const fht_image* img, int quadrant, int64_t pad_cols, fht_hough* out,
                  fht_hough* out_shifted, void* ws, size_t ws_bytes, fht_stream_t stream,
                  const fht_exec_opts* opts);

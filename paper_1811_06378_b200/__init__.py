@@ -155,12 +155,12 @@ def _finish(res, n, shifted, pair):
 def quadrant(t: torch.Tensor, q: int, pad: int | None = None, shifted: bool = False, pair: bool = False,
              workspace: torch.Tensor | None = None, out: HoughImage | None = None,
              out_shifted: HoughImage | None = None, events=None, aux_stream=None):
-    """One quadrant. pad: extension columns (None = Hp; any pad >= h_frame - 1 on the GPU).
+    """One quadrant. pad: extension columns (None = Hp; smaller than h_frame - 1 folds lines).
     shifted=True returns fhtshift(H) written directly by the transform; pair=True returns
     (H, fhtshift(H)) from one pass."""
     img, t = _image(t)
     res = _descs(FHT_MODE_QUADRANT, img, None, q, 0, t.device, shifted, pair, out, out_shifted, pad)
-    ws_n = workspace_bytes(FHT_MODE_QUADRANT, img)
+    ws_n = int(_lib.lib.fht_quadrant_workspace_bytes(ctypes.byref(img), q, -1 if pad is None else pad))
     ws = _workspace(ws_n, t.device, workspace)
     n = _lib.check("fht_quadrant", _lib.lib.fht_quadrant(ctypes.byref(img), q, -1 if pad is None else pad,
                                                           _ptr(res[0]), _ptr(res[1]), ws.data_ptr(), ws_n,

@@ -28,7 +28,7 @@ STATUS = {
 EXPORTED = (
     "fht_hough_describe", "fht_workspace_bytes", "fht_quadrant", "fht_full", "fht_angle_plan_make",
     "fht_angle_plan_make_pruned", "fht_angle_plan_make_ex", "fht_angle_range", "fhtshift", "fht_status_string", "fht_peaks_workspace_bytes",
-    "fht_peaks", "fht_cell_segment", "fht_hough_describe_pad",
+    "fht_peaks", "fht_cell_segment", "fht_hough_describe_pad", "fht_quadrant_workspace_bytes",
 )
 
 
@@ -102,6 +102,8 @@ def _load():
     lib.fht_peaks.argtypes = [P(FhtHough), i32, vp, vp, vp, vp, sz, vp]
     lib.fht_cell_segment.argtypes = [P(FhtHough), i64, i64, i64, P(FhtSegment)]
     lib.fht_hough_describe_pad.argtypes = [i32, P(FhtImage), i64, P(FhtHough)]
+    lib.fht_quadrant_workspace_bytes.argtypes = [P(FhtImage), i32, i64]
+    lib.fht_quadrant_workspace_bytes.restype = sz
     lib.fht_status_string.argtypes = [i32]
     lib.fht_status_string.restype = ctypes.c_char_p
     for name in ("fht_hough_describe", "fht_quadrant", "fht_full", "fht_angle_plan_make", "fht_angle_plan_make_pruned",

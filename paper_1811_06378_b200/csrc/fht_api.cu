@@ -1005,6 +1005,16 @@ int fht_hough_describe_pad(int quadrant, const fht_image* img, int64_t pad_cols,
   return FHT_OK;
 }
 
+size_t fht_quadrant_workspace_bytes(const fht_image* img, int quadrant, int64_t pad_cols) {
+  const size_t base = fht_workspace_bytes(FHT_MODE_QUADRANT, img, nullptr);
+  if (!img || pad_cols == -1 || quadrant < 0 || quadrant > 3) return base;
+  const int64_t hf = quadrant >= 2 ? img->w : img->h;
+  if (pad_cols >= hf - 1) return base;
+  fht_hough d;
+  if (fht_hough_describe(FHT_MODE_QUADRANT, 0, quadrant, img, nullptr, &d)) return 0;
+  return (((size_t)(d.batch * d.batch_stride) * 4 + 255) & ~size_t(255)) + base;  // + the pad = Hp image
+}
+
 size_t fht_workspace_bytes(int mode, const fht_image* img, const fht_angle_plan* plan) {
   if (!img || img->batch < 1 || img->h < 1 || img->w < 1) return 0;
   if (mode == FHT_MODE_RANGE) {
@@ -1035,13 +1045,53 @@ int fht_quadrant(const fht_image* img, int quadrant, int64_t pad_cols, fht_hough
   if (quadrant < 0 || quadrant > 3) return FHT_ERR_ARG;
   // pad (R22): any pad >= h_frame - 1 keeps every line's signed columns apart mod
   // w + pad (rows >= h are zero, so no pattern reaches further than h - 1 columns); a smaller
-  // pad folds lines cyclically and would need a fold pass (not built: UNSUPPORTED)
+  // pad folds lines cyclically: computed as the default transform + a fold
   const int64_t hf = quadrant >= 2 ? img->w : img->h;
   if (pad_cols < -1) return FHT_ERR_ARG;
-  if (pad_cols != -1 && pad_cols < hf - 1) return FHT_ERR_UNSUPPORTED;
   fht_hough want;
   s = fht_hough_describe_pad(quadrant, img, pad_cols, &want);
   if (s) return s;
+  if (pad_cols != -1 && pad_cols < hf - 1) {
+    // lines fold cyclically mod w + pad: the default (pad = Hp) transform into the workspace, then
+    // the fold (k_fold; R22). Workspace: [temporary Hough image][scratch]
+    if ((s = validate_outs(img, out, out_shifted, want, ws, ws_bytes))) return s;
+    if ((out && out->quadrant != quadrant) || (out_shifted && out_shifted->quadrant != quadrant)) return FHT_ERR_ARG;
+    fht_hough tmpd;
+    if ((s = fht_hough_describe(FHT_MODE_QUADRANT, 0, quadrant, img, nullptr, &tmpd))) return s;
+    const size_t tmp_bytes = ((size_t)(tmpd.batch * tmpd.batch_stride) * 4 + 255) & ~size_t(255);
+    const size_t need = fht_quadrant_workspace_bytes(img, quadrant, pad_cols);
+    if (!ws || ws_bytes < need) return FHT_ERR_WORKSPACE;
+    tmpd.data = ws;
+    const int r = fht_quadrant(img, quadrant, -1, &tmpd, nullptr, static_cast<char*>(ws) + tmp_bytes,
+                               ws_bytes - tmp_bytes, stream, opts);
+    if (r < 0) return r;
+    FoldArgs fa{};
+    fa.tmp = ws;
+    fa.tmp_pitch = tmpd.row_stride;
+    fa.tmp_batch = tmpd.batch_stride;
+    if (out) {
+      fa.out = out->data;
+      fa.out_pitch = out->row_stride;
+      fa.out_batch = out->batch_stride;
+    }
+    if (out_shifted) {
+      fa.outs = out_shifted->data;
+      fa.outs_pitch = out_shifted->row_stride;
+      fa.outs_batch = out_shifted->batch_stride;
+    }
+    fa.Hp = (int)tmpd.rows;
+    fa.W = (int)want.cols;
+    fa.Wt = (int)tmpd.cols;
+    fa.sigma = (quadrant == FHT_QA || quadrant == FHT_QD) ? 1 : -1;
+    fa.xlo = fa.sigma > 0 ? -fa.Hp : 0;  // the default run's tiling window [xlo, xlo + Wt)
+    fa.total = tmpd.batch * (int64_t)fa.Hp * fa.W;
+    const int64_t nblk = std::min<int64_t>((fa.total + kThreads - 1) / kThreads, 148 * 16);
+    if (tmpd.dtype == FHT_F32) k_fold<float><<<(unsigned)nblk, kThreads, 0, (cudaStream_t)stream>>>(fa);
+    else k_fold<int><<<(unsigned)nblk, kThreads, 0, (cudaStream_t)stream>>>(fa);
+    if (cudaGetLastError() != cudaSuccess) return FHT_ERR_CUDA;
+    mark_outs(out, out_shifted);
+    return r + 1;
+  }
   const Frame f = make_frame(img->h, img->w, quadrant >= 2, 0, pad_cols);
   if (pad_cols != -1 && pad_cols != f.Hp && !use_v2(f, nullptr)) return FHT_ERR_UNSUPPORTED;
   if ((s = validate_outs(img, out, out_shifted, want, ws, ws_bytes))) return s;

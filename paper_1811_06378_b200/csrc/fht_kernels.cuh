@@ -461,4 +461,47 @@ __global__ void __launch_bounds__(kThreads) k_fhtshift(const ShiftArgs a) {
   }
 }
 
+// ------------------------------------------------------------------------------------------
+// Fold for quadrant pads below h_frame - 1 (R22; "mod(w+h)"): the cyclic transform of
+// width W = w + pad is the signed transform summed over columns congruent mod W. The signed
+// transform comes from the default (pad = Hp) run, whose Wt = w + Hp columns hold every signed
+// column of the window [xlo, xlo + Wt) exactly once, at x mod Wt.
+// ------------------------------------------------------------------------------------------
+struct FoldArgs {
+  const void* tmp;
+  int64_t tmp_pitch, tmp_batch;  // elements
+  void* out;                     // may be NULL
+  int64_t out_pitch, out_batch;
+  void* outs;                    // fhtshift destination, may be NULL
+  int64_t outs_pitch, outs_batch;
+  int Hp, W, Wt, xlo, sigma;
+  int64_t total;                 // batch * Hp * W
+};
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_fold(const FoldArgs a) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int x0 = (int)(i % a.W);
+    const int64_t rs = i / a.W;
+    const int s = (int)(rs % a.Hp);
+    const int64_t b = rs / a.Hp;
+    const T* row = static_cast<const T*>(a.tmp) + b * a.tmp_batch + (int64_t)s * a.tmp_pitch;
+    // signed columns x = x0 + m W inside the window, ascending
+    int x = x0 + ((a.xlo - x0) > 0 ? ((a.xlo - x0) + a.W - 1) / a.W : -((x0 - a.xlo) / a.W)) * a.W;
+    T acc = T(0);
+    for (; x < a.xlo + a.Wt; x += a.W) {
+      int c = x % a.Wt;
+      c += c < 0 ? a.Wt : 0;
+      acc += row[c];
+    }
+    if (a.out) static_cast<T*>(a.out)[b * a.out_batch + (int64_t)s * a.out_pitch + x0] = acc;
+    if (a.outs) {
+      const int k = (a.sigma > 0 ? ceil_half(a.Hp + s) : ceil_half(a.Hp - s)) % a.W;
+      int xs = x0 + k;
+      xs -= xs >= a.W ? a.W : 0;
+      static_cast<T*>(a.outs)[b * a.outs_batch + (int64_t)s * a.outs_pitch + xs] = acc;
+    }
+  }
+}
+
 }  // namespace fht

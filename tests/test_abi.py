@@ -156,7 +156,8 @@ def test_argument_errors_are_synchronous():
     dq = L.FhtHough()
     assert L.lib.fht_hough_describe(0, 0, 0, ctypes.byref(img), None, ctypes.byref(dq)) == 0
     dq.data = 1 << 20
-    assert L.lib.fht_quadrant(ctypes.byref(img), 0, 5, ctypes.byref(dq), None, 1 << 24, ws_n, None, None) == -5
+    # pad 5 is supported (R22) but needs a descriptor of w + 5 columns: the pad = Hp one is a SHAPE error
+    assert L.lib.fht_quadrant(ctypes.byref(img), 0, 5, ctypes.byref(dq), None, 1 << 24, ws_n, None, None) == -3
     ds = L.FhtHough.from_buffer_copy(d)
     ds.shifted = 1
     d3 = L.FhtHough.from_buffer_copy(d)
@@ -244,8 +245,8 @@ def test_peaks_and_segment_errors():
 
 
 def test_pad_describe_and_limits():
-    """fht_hough_describe_pad: cols = w_frame + pad; fht_quadrant rejects pads that would fold lines
-    (pad < h_frame - 1) before any device work."""
+    """fht_hough_describe_pad: cols = w_frame + pad; a pad below h_frame - 1 (folding) needs the pad = Hp
+    image in the workspace."""
     L = _lib()
     img = _img(L, 100, 60)
     d = L.FhtHough()
@@ -255,5 +256,7 @@ def test_pad_describe_and_limits():
     assert (d.rows, d.cols) == (64, 100 + 59)
     assert L.lib.fht_hough_describe_pad(0, ctypes.byref(img), -1, ctypes.byref(d)) == 0 and d.cols == 60 + 128
     assert L.lib.fht_hough_describe_pad(0, ctypes.byref(img), -2, ctypes.byref(d)) == -1
-    assert L.lib.fht_quadrant(ctypes.byref(img), 0, 98, ctypes.byref(d), None, None, 0, None, None) == -5
-    assert L.lib.fht_quadrant(ctypes.byref(img), 2, 58, ctypes.byref(d), None, None, 0, None, None) == -5
+    # pads below h_frame - 1 fold: the pad = Hp image (128 x 188 f32, row stride 188) is added to the workspace
+    base = L.lib.fht_quadrant_workspace_bytes(ctypes.byref(img), 0, -1)
+    assert L.lib.fht_quadrant_workspace_bytes(ctypes.byref(img), 0, 99) == base
+    assert L.lib.fht_quadrant_workspace_bytes(ctypes.byref(img), 0, 98) == base + ((128 * 188 * 4 + 255) // 256) * 256

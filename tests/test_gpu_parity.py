@@ -218,15 +218,16 @@ def test_angle_range_pruned_c4_image(fht, O):
 @pytest.mark.parametrize("shape", [(33, 17), (100, 60), (64, 48), (20, 300)], ids=str)
 @pytest.mark.parametrize("dt", ["u8", "f32"])
 def test_quadrant_pads(fht, O, shape, dt):
-    """Pads other than Hp (P:65-67 "extending ... by h"; R22): h_frame - 1, h_frame (the paper's), Hp + 9;
-    every quadrant, Hough and fused fhtshift against the oracle's cyclic frame of that width."""
+    """Pads other than Hp ("extending ... by h"; R22): from 0 (lines fold: default transform +
+    fold kernel) through h_frame - 1, h_frame (the paper's) to Hp + 9 (direct); every quadrant, Hough and
+    fused fhtshift against the oracle's cyclic frame of that width."""
     from synth import random_image
     img = random_image(shape, dt, seed=shape[0] + 13 * shape[1])
     t = dev(img)
     for q in range(4):
         hf = shape[1] if q >= 2 else shape[0]
         Hp = O.next_pow2(hf)
-        for pad in sorted({hf - 1, hf, Hp + 9}):
+        for pad in sorted({0, 1, 3, hf // 2, hf - 2, hf - 1, hf, Hp + 9} - {-1}):
             h, s = fht.quadrant(t, q, pad=pad, pair=True)
             torch.cuda.synchronize()
             got = h.view[0, 0].cpu().numpy()
