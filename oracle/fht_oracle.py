@@ -25,11 +25,15 @@ Functions and what pins them (tests/test_oracle_pins.py):
   row count 2(w+h)-3, attribution thresholds (S:248-250 golden).
 * `angle_plan` / `transformed_image` / `angle_range` -- §4 shear + scale (P:124, P:132,
   P:144-152; R12-R17). Pinned by: identity plan [0,45] == QA exactly, [-45,0] == QB with
-  rows reversed, row conservation, scale/shear laws for the plan scalars. The nearest-
-  neighbour resampling choice (R14) is **parity unpinned** against the paper: only its
-  self-consistency and the approximate peak location are checked.
+  rows reversed, row conservation, scale/shear laws for the plan scalars. `shear_offsets`
+  (R13) by hand-derived goldens (tests/golden/plan_readings.json) and the property e_y - g y in
+  (-1/2, 1/2] in exact rational arithmetic; `scale_colmap` (R14) by goldens and the nearest-
+  neighbour property |(c + 1/2) alpha - (u + 1/2)| <= alpha/2 of the scale law with the
+  floor/ceil(alpha) multiplicity law for dilations; `angle_of_row` (R19) by the endpoint slopes
+  (row 0 = theta_min, row Hp - 1 = theta_max exactly, tan equally spaced) and a rasterised line.
 * `fhtshift_amounts` / `fhtshift` -- §5 (R11). Pinned by permutation, contiguity of
-  the meaningful run, width law w + s and P:160's quoted row-0 / last-row shifts.
+  the meaningful run, width law w + s, P:160's quoted row-0 / last-row shifts, and
+  exact centring of the all-ones run for every pad (R11's generic rule, not only pad = Hp).
 * `pattern_on_original` / `cell_segment` -- §3.2 steps 1-2 and §3.3 attribution
   (P:111-113): a Hough cell back to its discrete pattern on the original image. Pinned by SPEC's
   worked cases (S:195-197, S:257-258 golden), the round trip (drawing the pixels and
@@ -444,7 +448,10 @@ def range_cells_direct(img: np.ndarray, plan: AnglePlan, cells) -> np.ndarray:
 
 
 def angle_of_row(s: int, plan: AnglePlan) -> float:
-    """R19 metadata: row s of the range output holds lines of slope k_lo + s / (alpha (Hp - 1))."""
+    """R19 (P:52 'shift = h tg(phi)'): row s holds patterns of endpoint slope s / (Hp - 1) in the
+    transformed image (D_s(Hp - 1) = s); the scale law divides by alpha and the shear law
+    (P:132) adds k_lo back: slope k_lo + s / (alpha (Hp - 1)), returned as degrees (from vertical;
+    from horizontal for a transposed plan)."""
     k = plan.k_lo + s / (plan.alpha * (plan.Hp - 1)) if plan.Hp > 1 else plan.k_lo
     return math.degrees(math.atan(k))
 
@@ -466,14 +473,24 @@ def _ceil_half(v: int) -> int:
     return -((-v) // 2)
 
 
-def fhtshift_amounts_quadrant(Hp: int, W: int, sigma: int) -> np.ndarray:
-    """Right-rotation of row s: ceil((Hp + s)/2) for sigma=+1, ceil((Hp - s)/2) for sigma=-1.
+def fhtshift_amounts_quadrant(Hp: int, W: int, sigma: int, w_frame: int | None = None) -> np.ndarray:
+    """Right-rotation k_s of row s by R11's generic rule k = ceil((W - len)/2) - start, so that the
+    row's meaningful run lands centred (P:172 'concentrated around its center in a single zone').
 
-    P:160: 'row zero will shift by h and the last row by h/2 ... rows are shifted by h - i/2',
-    i counted on the flipped image, i = Hp - s (R11).
+    The run of row s is the cells a line of the w_frame-wide frame can reach (width law P:156,
+    w + h tg(alpha) -> w_frame + s): signed x0 in [-s, w_frame) for sigma=+1 (start = -s), in
+    [0, w_frame + s) for sigma=-1 (start = 0); len = w_frame + s. With pad = W - w_frame this is
+    ceil((pad + s)/2) (sigma=+1) and ceil((pad - s)/2) (sigma=-1). For the paper's pad = Hp it is
+    P:160's 'row zero will shift by h and the last row by h/2 ... rows are shifted by h - i/2',
+    i counted on the flipped image, i = Hp - s (R11). `w_frame` defaults to W - Hp.
     """
-    return np.array([(_ceil_half(Hp + s) if sigma > 0 else _ceil_half(Hp - s)) % W for s in range(Hp)],
-                    dtype=np.int64)
+    wf = W - Hp if w_frame is None else w_frame
+    out = []
+    for s in range(Hp):
+        start = -s if sigma > 0 else 0
+        length = wf + s
+        out.append((_ceil_half(W - length) - start) % W)
+    return np.array(out, dtype=np.int64)
 
 
 def fhtshift_amounts_range(plan: AnglePlan) -> np.ndarray:
@@ -491,9 +508,11 @@ def fhtshift_rows(hough: np.ndarray, k: np.ndarray) -> np.ndarray:
     return out
 
 
-def fhtshift_quadrant(hough: np.ndarray, sigma: int) -> np.ndarray:
+def fhtshift_quadrant(hough: np.ndarray, sigma: int, pad: int | None = None) -> np.ndarray:
+    """fhtshift of one quadrant image [Hp][W]; `pad` = the frame's extension W - w_frame (None: Hp,
+    the paper's h x h extension and every full-mode quadrant)."""
     Hp, W = hough.shape
-    return fhtshift_rows(hough, fhtshift_amounts_quadrant(Hp, W, sigma))
+    return fhtshift_rows(hough, fhtshift_amounts_quadrant(Hp, W, sigma, W - (Hp if pad is None else pad)))
 
 
 def fhtshift_quads(quads: list[np.ndarray]) -> list[np.ndarray]:

@@ -504,3 +504,122 @@ def test_hough_peaks_planted():
     assert O.hough_peaks(P, 2) == [(4, 0, 1)]                                # zeros all lose to an earlier neighbour
     F = np.array([[0.5, -1.0, 0.25], [0.5, 2.0, -3.0]], dtype=np.float64)
     assert O.hough_peaks(F, 5) == [(2.0, 1, 1)]
+
+
+# ---------------------------------------------------------------- round 2: the open readings pinned
+PLAN_GOLDEN = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "plan_readings.json")))
+
+
+@pytest.mark.parametrize("ex", PLAN_GOLDEN["shear_offsets"], ids=lambda e: str(e["g"]))
+def test_shear_offsets_golden(ex):
+    """R13: hand-derived shear offsets, ties rounding up."""
+    assert O.shear_offsets(ex["g"], len(ex["e"])).tolist() == ex["e"]
+
+
+@pytest.mark.parametrize("g", [0.5, -0.5, 0.25, 1.0 / 3.0, -0.7, 2.5, 0.0, 1.8660254037844388,
+                               0.26794919243112275, -11.430052302761343])
+def test_shear_offsets_nearest_ties_up(g):
+    """R13 as a property: e_y is the integer nearest g*y with ties up, i.e. e_y - g*y in (-1/2, 1/2]
+    (exact rational arithmetic on the double g). A floor shear (e - gy in (-1, 0]) or round-half-down
+    (e - gy = -1/2 at a tie) fails."""
+    from fractions import Fraction
+    e = O.shear_offsets(g, 3000)
+    G = Fraction(g)
+    for y in range(3000):
+        d = Fraction(int(e[y])) - G * y
+        assert Fraction(-1, 2) < d <= Fraction(1, 2), (g, y, d)
+
+
+@pytest.mark.parametrize("ex", PLAN_GOLDEN["scale_colmap"], ids=lambda e: str(e["alpha"]))
+def test_scale_colmap_golden(ex):
+    """R14 (P:124 scale law): hand-derived nearest-neighbour maps."""
+    wc = math.ceil(ex["alpha"] * ex["w"] - 1e-9)
+    assert O.scale_colmap(ex["alpha"], ex["w"], wc).tolist() == ex["colmap"]
+
+
+@pytest.mark.parametrize("alpha", [1.8660254037844388, 2.0, 3.3, 1.0, 1.25, 0.7, 0.5, 0.25, 5.0])
+@pytest.mark.parametrize("w", [7, 64, 100, 4096])
+def test_scale_colmap_nearest_neighbour(alpha, w):
+    """R14 as properties of nearest-neighbour resampling under the scale law x' = alpha x:
+    transformed column u (centre u + 1/2) takes the source column c whose scaled centre (c + 1/2) alpha
+    is nearest, |(c + 1/2) alpha - (u + 1/2)| <= alpha / 2 (clamped to w - 1 only past the right edge);
+    for alpha >= 1 (a dilation) the map is onto and every interior source column is taken floor(alpha)
+    or ceil(alpha) times. A corner-aligned map floor(u / alpha + 1/2) fails the first property."""
+    wc = math.ceil(alpha * w - 1e-9)
+    cm = O.scale_colmap(alpha, w, wc)
+    assert len(cm) == wc and cm.min() >= 0 and cm.max() <= w - 1
+    assert (np.diff(cm) >= 0).all()
+    for u in range(wc):
+        c = int(cm[u])
+        if (u + 0.5) / alpha >= w:                      # past the last source centre band: clamped
+            assert c == w - 1
+            continue
+        assert abs((c + 0.5) * alpha - (u + 0.5)) <= alpha / 2 + 1e-12, (u, c)
+    if alpha >= 1.0:
+        counts = np.bincount(cm, minlength=w)
+        assert (counts >= 1).all()
+        inner = counts[1:-1]
+        assert ((inner == math.floor(alpha)) | (inner == math.ceil(alpha))).all()
+
+
+@pytest.mark.parametrize("shape,tmin,tmax", [((64, 64), -15, 15), ((32, 40), 5, 40), ((128, 16), -60, 10),
+                                             ((16, 16), -80, 80), ((256, 100), 1, 2)])
+def test_angle_of_row_endpoints(shape, tmin, tmax):
+    """R19 (P:52 'shift = h tg(phi)'): row s of the §4 frame holds patterns whose endpoint slope is
+    s / (Hp - 1) (D_s(0) = 0, D_s(Hp - 1) = s) in the transformed image; undoing the scale law
+     and shear law gives the image slope. So row 0 is theta_min, row Hp - 1 is theta_max
+    exactly, and tan(angle) is equally spaced in s. A formula without the scale (alpha) or in radians
+    fails the far endpoint."""
+    p = O.angle_plan(*shape, tmin, tmax)
+    a = np.array([O.angle_of_row(s, p) for s in range(p.Hp)])
+    assert a[0] == pytest.approx(tmin, abs=1e-9) and a[-1] == pytest.approx(tmax, abs=1e-9)
+    t = np.tan(np.radians(a))
+    assert np.allclose(np.diff(t), (t[-1] - t[0]) / (p.Hp - 1), rtol=1e-9, atol=1e-12)
+    assert (np.diff(a) > 0).all()
+    # pruned plan: shear only (alpha = 1), row S_max is the first row at or past theta_max
+    if math.tan(math.radians(tmax)) - math.tan(math.radians(tmin)) <= 1.0:
+        q = O.angle_plan_pruned(*shape, tmin, tmax)
+        assert O.angle_of_row(0, q) == pytest.approx(tmin, abs=1e-9)
+        assert O.angle_of_row(q.rows - 1, q) >= tmax - 1e-9
+        if q.rows >= 2:
+            assert O.angle_of_row(q.rows - 2, q) < tmax
+
+
+def test_angle_of_row_peak():
+    """A rasterised line of known inclination peaks at a row whose angle_of_row is within 2 rows'
+    worth of the line's angle (the shear and the digital line are rounded per row)."""
+    P = 128
+    for tmin, tmax, deg in [(-15, 15, 6.0), (-15, 15, -9.0), (10, 40, 25.0), (-40, -10, -20.0)]:
+        k = math.tan(math.radians(deg))
+        img = np.zeros((P, P), dtype=np.int64)
+        ys = np.arange(P)
+        xs = np.floor((30 if k > 0 else 90) + k * ys + 0.5).astype(int)
+        img[ys, xs] = 1
+        p = O.angle_plan(P, P, tmin, tmax)
+        s_peak = int(np.unravel_index(np.argmax(O.angle_range(img, p)), (p.Hp, p.W))[0])
+        dk = 2.0 / (p.alpha * (p.Hp - 1))           # slope step of 2 rows
+        assert abs(math.tan(math.radians(O.angle_of_row(s_peak, p))) - k) <= dk
+
+
+@pytest.mark.parametrize("P,w", [(8, 8), (16, 16), (16, 5), (8, 20)])
+@pytest.mark.parametrize("q", [0, 1, 2, 3])
+def test_fhtshift_centred_any_pad(P, w, q):
+    """R11's generic rule for every pad (P:156 width law w + s, P:172 'concentrated around its center in
+    a single zone'): for an all-ones P x w frame (h = Hp) and any pad >= s, row s's meaningful run of
+    w_frame + s cells lands exactly at [ceil((W - len)/2), ...) -- centred, one zone. A shift taken from
+    Hp instead of the pad (off by (pad - Hp)/2) fails."""
+    shape = (P, w) if q < 2 else (w, P)                   # the frame is P rows x w columns
+    img = np.ones(shape, dtype=np.int64)
+    sigma = O.QUADRANT_FRAME[q][1]
+    for pad in sorted({P - 1, P, P + 1, P + 7, 2 * P + 3, 40}):
+        H = O.hough_recursive(img, q, pad)
+        W = w + pad
+        assert H.shape == (P, W)
+        S = O.fhtshift_quadrant(H, sigma, pad)
+        for s in range(P):
+            assert sorted(S[s].tolist()) == sorted(H[s].tolist())      # a rotation of the row
+            if s > pad:
+                continue                                               # the run wraps onto itself
+            L = w + s
+            nz = np.flatnonzero(S[s])
+            assert len(nz) == L and nz[0] == -((L - W) // 2) and nz[-1] == nz[0] + L - 1, (pad, s)
