@@ -4,13 +4,14 @@
  * practical applications and the structure of Hough image" (arXiv 1811.06378).
  *
  * Citations: P:n = PAPER.md line n (section in brackets); S:n = SPEC.md line n.
- * Readings R1..R23 are listed in DESIGN.md ("Readings of the paper").
+ * Readings R1..R26 are listed in DESIGN.md ("Readings of the paper").
  *
  * Conventions common to every call
  * --------------------------------
  *  - Every buffer pointer in fht_image / fht_hough and every workspace pointer is a DEVICE
  *    pointer allocated and owned by the caller. The library allocates no device memory, keeps
- *    no global mutable state and retains no pointer after a call returns. All device work is
+ *    no global mutable state (beyond a per-device record of which kernels have had their dynamic
+ *    shared-memory limit raised) and retains no pointer after a call returns. All device work is
  *    enqueued on `stream` (0 = legacy default stream); buffers must stay alive until it ends.
  *  - Strides are in ELEMENTS. Pointers must be aligned to their element size (FHT_ERR_ALIGN
  *    otherwise). Output descriptors from fht_hough_describe() have 16-byte row pitches; the
@@ -85,10 +86,10 @@ typedef struct {
   int64_t w_content; /* w' = ceil(alpha*w) */
   int64_t W;         /* W' */
   int64_t e_min, e_max; /* min / max of e_y over y < h */
-  int64_t rows;         /* output rows: Hp (fht_angle_plan_make), S_max + 1 (fht_angle_plan_make_pruned) */
+  int64_t rows;         /* output rows: Hp (fht_angle_plan), S_max + 1 (fht_angle_plan_make_pruned) */
   int64_t transposed;   /* 1: mostly-horizontal plan -- the frame is the transposed image and h, w
                            above are the FRAME's (image w, h); angles are measured from horizontal */
-} fht_angle_plan;
+} fht_angle_plan_t;
 
 /* Output (Hough image) descriptor. Fill it with fht_hough_describe(), then set `data`. */
 typedef struct {
@@ -102,7 +103,7 @@ typedef struct {
   int64_t batch, nquad, rows, cols;       /* nquad = 4 for FULL/QUADS, else 1 */
   int64_t batch_stride, quad_stride, row_stride;
   int64_t h, w, Hp, Wp;                   /* source image dims; Hp/Wp = padded powers of two */
-  fht_angle_plan plan;                    /* valid iff mode == RANGE */
+  fht_angle_plan_t plan;                    /* valid iff mode == RANGE */
 } fht_hough;
 
 /* Optional per-call execution options (may be NULL).
@@ -129,7 +130,7 @@ typedef struct {
  *   RANGE: rows = plan->Hp, cols = plan->W.
  * `plan` may be NULL unless mode == RANGE. Returns FHT_OK or a negative fht_status. */
 int fht_hough_describe(int mode, int layout, int quadrant, const fht_image* img,
-                       const fht_angle_plan* plan, fht_hough* out);
+                       const fht_angle_plan_t* plan, fht_hough* out);
 
 /* Quadrant-mode descriptor with a pad other than Hp (R22): cols = w_frame + pad_cols
  * (w_frame = w for QA/QB, h for QC/QD); pad_cols = -1 means Hp (= fht_hough_describe). */
@@ -139,7 +140,7 @@ int fht_hough_describe_pad(int quadrant, const fht_image* img, int64_t pad_cols,
 size_t fht_quadrant_workspace_bytes(const fht_image* img, int quadrant, int64_t pad_cols);
 
 /* Device workspace (bytes) the call needs for `img` (pass-1 scratch + tables). */
-size_t fht_workspace_bytes(int mode, const fht_image* img, const fht_angle_plan* plan);
+size_t fht_workspace_bytes(int mode, const fht_image* img, const fht_angle_plan_t* plan);
 
 /* Output pair of the transform calls below. `out` receives the Hough image H; `out_shifted`
  * receives fhtshift(H) (§5), written by the same pass-2 kernel from the same
@@ -162,21 +163,30 @@ int fht_quadrant(const fht_image* img, int quadrant, int64_t pad_cols, fht_hough
 int fht_full(const fht_image* img, int layout, fht_hough* out, fht_hough* out_shifted, void* ws,
              size_t ws_bytes, fht_stream_t stream, const fht_exec_opts* opts);
 
-/* Host-only: build the §4 plan. FHT_ERR_ARG if theta_min >= theta_max,
- * |theta| >= 90 deg, or alpha*w < 1. Deterministic double arithmetic, no FMA (R16). */
-int fht_angle_plan_make(int64_t h, int64_t w, double theta_min_deg, double theta_max_deg,
-                        fht_angle_plan* out);
+/* Host-only: build the §4 plan (P:124 scale law, P:132 shear law, P:144 composition) for an h x w
+ * image and inclinations [theta_min, theta_max] (degrees from vertical, R12). FHT_ERR_ARG if
+ * theta_min >= theta_max, |theta| >= 90 deg, or alpha*w < 1; FHT_ERR_UNSUPPORTED for h > 4096.
+ * Deterministic double arithmetic, no FMA (R16). O(Hp log Hp) host work: W' (R17) takes the
+ * per-row spread of e_y - D_s(y) from the FHT block recursion with (min, max) in place of +. */
+int fht_angle_plan(int64_t h, int64_t w, double theta_min_deg, double theta_max_deg, fht_angle_plan_t* out);
+
+/* Host-only: the inclination (degrees; from vertical, or from horizontal for a transposed plan) of
+ * the lines row s of a range output holds (R19, "shift = h tg(phi)"): row s's patterns have
+ * endpoint slope s/(Hp-1) in the transformed frame; undoing the scale and shear gives
+ * tan = k_lo + s / (alpha (Hp - 1)). Row 0 is theta_min; row Hp-1 of a §4 plan is theta_max.
+ * FHT_ERR_ARG for NULL pointers or s outside [0, Hp). */
+int fht_angle_of_row(const fht_angle_plan_t* plan, int64_t s, double* deg);
 
 /* Shift-range-pruned plan (north_star "computes only the stages and shift ranges
  * the restriction needs"): shear only (alpha = 1, w' = w, colmap = identity,
  * e_y = floor(-k_lo*y + 0.5)), so the slopes [k_lo, k_hi] become QA rows s = (k - k_lo)*(Hp-1) of
  * the sheared image and only rows s <= S_max = ceil((k_hi - k_lo)*(Hp-1)) are computed and stored
  * (plan.rows = S_max + 1 <= Hp). W' follows R17 with the spread taken over those rows. Requires
- * k_hi - k_lo <= 1 (otherwise FHT_ERR_UNSUPPORTED: use fht_angle_plan_make's scaled frame); other
- * errors as fht_angle_plan_make. fht_angle_range computes a pruned plan on the v2 kernels only
+ * k_hi - k_lo <= 1 (otherwise FHT_ERR_UNSUPPORTED: use fht_angle_plan's scaled frame); other
+ * errors as fht_angle_plan. fht_angle_range_plan computes a pruned plan on the v2 kernels only
  * (FHT_ERR_UNSUPPORTED for the degenerate frames of the v1 path). */
 int fht_angle_plan_make_pruned(int64_t h, int64_t w, double theta_min_deg, double theta_max_deg,
-                               fht_angle_plan* out);
+                               fht_angle_plan_t* out);
 
 /* General plan (SURVEY §8(f) f4 "mostly-horizontal range"). flags: FHT_PLAN_PRUNED (as
  * fht_angle_plan_make_pruned) and/or FHT_PLAN_HORIZONTAL: the range is of inclinations from the
@@ -184,20 +194,35 @@ int fht_angle_plan_make_pruned(int64_t h, int64_t w, double theta_min_deg, doubl
  * mostly-horizontal quadrants QC/QD -- so a range near horizontal keeps alpha near 1
  * instead of being squeezed by the vertical frame's scale. Horizontal [0, 45] equals QD exactly,
  * [-45, 0] QC with rows reversed. h, w are the IMAGE's; the plan stores the frame's (swapped).
- * Errors as fht_angle_plan_make / fht_angle_plan_make_pruned. */
+ * Errors as fht_angle_plan / fht_angle_plan_make_pruned. */
 enum { FHT_PLAN_PRUNED = 1, FHT_PLAN_HORIZONTAL = 2 };
 int fht_angle_plan_make_ex(int64_t h, int64_t w, double theta_min_deg, double theta_max_deg, int32_t flags,
-                           fht_angle_plan* out);
+                           fht_angle_plan_t* out);
 
-/* Angle-range-restricted transform: QA of the virtually sheared+scaled image, the
- * shear and scale fused into the first FHT iteration (pass-1 loader). f32/u8/i32 input. */
-int fht_angle_range(const fht_image* img, const fht_angle_plan* plan, fht_hough* out,
+/* Angle-range-restricted transform (§4, "perform a transform for an arbitrary range of
+ * angles [gamma1; gamma2]"): QA of the virtually sheared+scaled image, the shear and
+ * scale fused into the first FHT iteration (pass-1 loader). f32/u8/i32 input. The §4 plan of
+ * (img->h, img->w, theta_min, theta_max) is built inside the call (fht_angle_plan); the outputs
+ * must be described with that plan (fht_hough_describe(FHT_MODE_RANGE, ..., &plan, ...)), else
+ * FHT_ERR_SHAPE. Workspace: fht_angle_range_workspace_bytes(). Errors as fht_angle_plan plus the
+ * output / workspace errors of the other transform calls. Returns the kernels enqueued (3). */
+int fht_angle_range(const fht_image* img, double theta_min_deg, double theta_max_deg, fht_hough* out,
                     fht_hough* out_shifted, void* ws, size_t ws_bytes, fht_stream_t stream,
                     const fht_exec_opts* opts);
+size_t fht_angle_range_workspace_bytes(const fht_image* img, double theta_min_deg, double theta_max_deg);
 
-/* §5 fhtshift (R11): out[r][x] = in[r][(x - k_r) mod cols], k_r = ceil((n+s)/2) for
- * sigma=+1 quadrants, ceil((n-s)/2) for sigma=-1, and ceil((W'-len_s)/2) - start_s in RANGE
- * mode. `in` must be unshifted (FHT_ERR_STATE otherwise); `out` must have the same shape and
+/* The same transform for a prepared plan: a §4 plan, a shift-range-pruned plan or a mostly-
+ * horizontal plan (fht_angle_plan_make_pruned / _ex). Workspace: fht_workspace_bytes(FHT_MODE_RANGE,
+ * img, plan). */
+int fht_angle_range_plan(const fht_image* img, const fht_angle_plan_t* plan, fht_hough* out,
+                         fht_hough* out_shifted, void* ws, size_t ws_bytes, fht_stream_t stream,
+                         const fht_exec_opts* opts);
+
+/* §5 fhtshift (R11): out[r][x] = in[r][(x - k_r) mod cols] with R11's generic rule
+ * k = ceil((W - len_s)/2) - start_s, which centres row s's meaningful run: for quadrants
+ * len_s = w_frame + s, so k_r = ceil((pad+s)/2) for sigma=+1 and ceil((pad-s)/2) for sigma=-1 with
+ * pad = cols - w_frame (= n, the row count, in FULL mode and for the default quadrant pad); RANGE
+ * mode takes (start_s, len_s) from the row's support. `in` must be unshifted (FHT_ERR_STATE otherwise); `out` must have the same shape and
  * not alias `in`; on success out->shifted = 1. Bit copy: exact for every dtype. One kernel: a warp
  * per row, 16-byte loads/stores when cols, every stride and both bases are 16-byte aligned; in RANGE
  * mode each block first reduces its rows' support (start_s, len_s) from an e_y table in shared
@@ -217,7 +242,8 @@ const char* fht_status_string(int status);
  * cols[...] (int32), all DEVICE pointers owned by the caller; a plane with fewer than k peaks pads
  * with row = col = -1, value 0. ws: fht_peaks_workspace_bytes(h) device bytes. Two kernels (a
  * streaming pass over bands of rows, a per-plane merge). Errors: ARG (k outside 1..32, NULL),
- * DTYPE, WORKSPACE, UNSUPPORTED (rows*cols >= 2^32). Returns 2 (kernels enqueued). */
+ * DTYPE, WORKSPACE, UNSUPPORTED (rows*cols >= 2^32, or more than 65535 planes). Returns 2 (kernels
+ * enqueued). */
 size_t fht_peaks_workspace_bytes(const fht_hough* h);
 int fht_peaks(const fht_hough* h, int32_t k, void* values, int32_t* rows, int32_t* cols, void* ws,
               size_t ws_bytes, fht_stream_t stream);

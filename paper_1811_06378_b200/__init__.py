@@ -8,7 +8,9 @@ library, or calling with a non-CUDA tensor, raises.
     full(img, layout="quads", shifted=False, pair=False)   -> HoughImage | (H, S)  (P:89-113)
     quadrant(img, q, pad=None, shifted=False, pair=False)  -> HoughImage | (H, S)  (P:52-67)
     angle_plan(h, w, theta_min, theta_max)          -> FhtAnglePlan (P:124, P:132, P:144)
-    angle_range(img, plan, shifted=False, pair=False)      -> HoughImage | (H, S)  (P:146-152)
+    angle_range(img, theta_min, theta_max, shifted=False, pair=False) -> HoughImage | (H, S)  (P:117, P:146-152)
+    angle_range(img, plan, ...)                     -> the same for a prepared (pruned / horizontal) plan
+    angle_of_row(plan, s)                           -> degrees (R19, P:52)
     fhtshift(hough)                                 -> HoughImage   (P:154-172)
 
 `shifted=True` makes the transform write the fhtshift-ed image directly (fused store);
@@ -25,7 +27,7 @@ from ._lib import (FHT_F32, FHT_I32, FHT_LAYOUT_CONCAT, FHT_LAYOUT_QUADS, FHT_MO
                    FHT_MODE_RANGE, FHT_QA, FHT_QB, FHT_QC, FHT_QD, FHT_U8, FhtAnglePlan, FhtError, FhtHough,
                    FhtImage)
 
-__all__ = ["full", "quadrant", "angle_plan", "angle_range", "fhtshift", "HoughImage", "FhtError",
+__all__ = ["full", "quadrant", "angle_plan", "angle_range", "angle_of_row", "fhtshift", "HoughImage", "FhtError",
            "QA", "QB", "QC", "QD", "workspace_bytes", "LIB_PATH"]
 
 QA, QB, QC, QD = FHT_QA, FHT_QB, FHT_QC, FHT_QD
@@ -194,17 +196,38 @@ def angle_plan(h: int, w: int, theta_min_deg: float, theta_max_deg: float, prune
     return p
 
 
-def angle_range(t: torch.Tensor, plan: FhtAnglePlan, shifted: bool = False, pair: bool = False,
-                workspace: torch.Tensor | None = None, out: HoughImage | None = None,
+def angle_of_row(plan: FhtAnglePlan, s: int) -> float:
+    """Inclination (degrees) of the lines row s of a range output holds (R19)."""
+    d = ctypes.c_double()
+    _lib.check("fht_angle_of_row", _lib.lib.fht_angle_of_row(ctypes.byref(plan), int(s), ctypes.byref(d)))
+    return d.value
+
+
+def angle_range(t: torch.Tensor, theta_min, theta_max: float | None = None, shifted: bool = False,
+                pair: bool = False, workspace: torch.Tensor | None = None, out: HoughImage | None = None,
                 out_shifted: HoughImage | None = None, events=None, aux_stream=None):
-    """Angle-range-restricted transform. See quadrant() for shifted / pair."""
+    """Angle-range-restricted transform (§4, P:117 "a transform for an arbitrary range of angles";
+    P:146-152): `angle_range(t, theta_min, theta_max)` calls fht_angle_range, which builds the §4 plan
+    itself; `angle_range(t, plan)` calls fht_angle_range_plan with a prepared plan (pruned or
+    mostly-horizontal plans). See quadrant() for shifted / pair."""
     img, t = _image(t)
+    if isinstance(theta_min, FhtAnglePlan):
+        plan, by_angles = theta_min, False
+    else:
+        plan, by_angles = angle_plan(int(img.h), int(img.w), float(theta_min), float(theta_max)), True
     res = _descs(FHT_MODE_RANGE, img, plan, 0, 0, t.device, shifted, pair, out, out_shifted)
-    ws_n = workspace_bytes(FHT_MODE_RANGE, img, plan)
-    ws = _workspace(ws_n, t.device, workspace)
-    n = _lib.check("fht_angle_range", _lib.lib.fht_angle_range(ctypes.byref(img), ctypes.byref(plan),
-                                                                _ptr(res[0]), _ptr(res[1]), ws.data_ptr(),
-                                                                ws_n, _stream(t), _opts(events, aux_stream)))
+    if by_angles:
+        ws_n = int(_lib.lib.fht_angle_range_workspace_bytes(ctypes.byref(img), float(theta_min), float(theta_max)))
+        ws = _workspace(ws_n, t.device, workspace)
+        n = _lib.check("fht_angle_range", _lib.lib.fht_angle_range(
+            ctypes.byref(img), float(theta_min), float(theta_max), _ptr(res[0]), _ptr(res[1]), ws.data_ptr(), ws_n,
+            _stream(t), _opts(events, aux_stream)))
+    else:
+        ws_n = workspace_bytes(FHT_MODE_RANGE, img, plan)
+        ws = _workspace(ws_n, t.device, workspace)
+        n = _lib.check("fht_angle_range_plan", _lib.lib.fht_angle_range_plan(
+            ctypes.byref(img), ctypes.byref(plan), _ptr(res[0]), _ptr(res[1]), ws.data_ptr(), ws_n, _stream(t),
+            _opts(events, aux_stream)))
     return _finish(res, n, shifted, pair)
 
 

@@ -26,8 +26,9 @@ STATUS = {
 }
 
 EXPORTED = (
-    "fht_hough_describe", "fht_workspace_bytes", "fht_quadrant", "fht_full", "fht_angle_plan_make",
-    "fht_angle_plan_make_pruned", "fht_angle_plan_make_ex", "fht_angle_range", "fhtshift", "fht_status_string", "fht_peaks_workspace_bytes",
+    "fht_hough_describe", "fht_workspace_bytes", "fht_quadrant", "fht_full", "fht_angle_plan", "fht_angle_of_row",
+    "fht_angle_plan_make_pruned", "fht_angle_plan_make_ex", "fht_angle_range", "fht_angle_range_workspace_bytes",
+    "fht_angle_range_plan", "fhtshift", "fht_status_string", "fht_peaks_workspace_bytes",
     "fht_peaks", "fht_cell_segment", "fht_hough_describe_pad", "fht_quadrant_workspace_bytes",
 )
 
@@ -91,11 +92,15 @@ def _load():
     lib.fht_workspace_bytes.restype = sz
     lib.fht_quadrant.argtypes = [P(FhtImage), i32, i64, P(FhtHough), P(FhtHough), vp, sz, vp, P(FhtExecOpts)]
     lib.fht_full.argtypes = [P(FhtImage), i32, P(FhtHough), P(FhtHough), vp, sz, vp, P(FhtExecOpts)]
-    lib.fht_angle_plan_make.argtypes = [i64, i64, dbl, dbl, P(FhtAnglePlan)]
+    lib.fht_angle_plan.argtypes = [i64, i64, dbl, dbl, P(FhtAnglePlan)]
+    lib.fht_angle_of_row.argtypes = [P(FhtAnglePlan), i64, P(dbl)]
     lib.fht_angle_plan_make_pruned.argtypes = [i64, i64, dbl, dbl, P(FhtAnglePlan)]
     lib.fht_angle_plan_make_ex.argtypes = [i64, i64, dbl, dbl, i32, P(FhtAnglePlan)]
-    lib.fht_angle_range.argtypes = [P(FhtImage), P(FhtAnglePlan), P(FhtHough), P(FhtHough), vp, sz, vp,
-                                    P(FhtExecOpts)]
+    lib.fht_angle_range.argtypes = [P(FhtImage), dbl, dbl, P(FhtHough), P(FhtHough), vp, sz, vp, P(FhtExecOpts)]
+    lib.fht_angle_range_workspace_bytes.argtypes = [P(FhtImage), dbl, dbl]
+    lib.fht_angle_range_workspace_bytes.restype = sz
+    lib.fht_angle_range_plan.argtypes = [P(FhtImage), P(FhtAnglePlan), P(FhtHough), P(FhtHough), vp, sz, vp,
+                                         P(FhtExecOpts)]
     lib.fhtshift.argtypes = [P(FhtHough), P(FhtHough), vp]
     lib.fht_peaks_workspace_bytes.argtypes = [P(FhtHough)]
     lib.fht_peaks_workspace_bytes.restype = sz
@@ -106,9 +111,9 @@ def _load():
     lib.fht_quadrant_workspace_bytes.restype = sz
     lib.fht_status_string.argtypes = [i32]
     lib.fht_status_string.restype = ctypes.c_char_p
-    for name in ("fht_hough_describe", "fht_quadrant", "fht_full", "fht_angle_plan_make", "fht_angle_plan_make_pruned",
-                 "fht_angle_plan_make_ex",
-                 "fht_angle_range", "fhtshift", "fht_peaks", "fht_cell_segment", "fht_hough_describe_pad"):
+    for name in ("fht_hough_describe", "fht_quadrant", "fht_full", "fht_angle_plan", "fht_angle_of_row",
+                 "fht_angle_plan_make_pruned", "fht_angle_plan_make_ex", "fht_angle_range", "fht_angle_range_plan",
+                 "fhtshift", "fht_peaks", "fht_cell_segment", "fht_hough_describe_pad"):
         getattr(lib, name).restype = i32
     return lib
 

@@ -11,6 +11,7 @@
 //                        frames v2 does not tile (Hp <= 2 or fewer than 8 columns).
 #include <cudaTypedefs.h>
 
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -173,9 +174,13 @@ int v1_scratch_width(const Frame& f) {
   return (ws + 3) & ~3;
 }
 
+// at most kMaxChunk images per launch: the v1 grid puts image x slot in gridDim.z (<= 65535, 4 slots)
+// and the v2 flat grids stay below 2^31 CTAs
+constexpr int64_t kMaxChunk = 16383;
 int chunk_images(size_t per_image_touched, int64_t batch) {
   int64_t c = (int64_t)(scratch_budget() / (per_image_touched ? per_image_touched : 1));
   if (c < 1) c = 1;
+  if (c > kMaxChunk) c = kMaxChunk;
   if (c > batch) c = batch;
   const int64_t n = (batch + c - 1) / c;  // balanced: 17 images at most 16 per chunk -> 9 + 8
   return (int)((batch + n - 1) / n);
@@ -237,14 +242,30 @@ bool make_row_map(CUtensorMap* m, const void* base, bool f32, uint64_t cols, uin
             CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// ---------------------------------------------------------------- dynamic shared memory opt-in
+// cudaFuncAttributeMaxDynamicSharedMemorySize is a per-device (per-context) attribute: `done` (one
+// per kernel instantiation) records, one bit per device ordinal, where it has been set, so a
+// process that drives several GPUs opts in on each of them (a pure cache of device state).
+template <typename K>
+cudaError_t smem_optin(K kern, size_t bytes, std::atomic<unsigned long long>& done) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
+  return e;
+}
+
 // ---------------------------------------------------------------- v1 launch helpers
 template <typename Tin, int LOGR>
 cudaError_t launch_pass1_t(dim3 grid, const Pass1Args& a, cudaStream_t st) {
   using A = typename AccOf<Tin>::type;
   constexpr int R = 1 << LOGR;
   const size_t smem = 2 * (size_t)R * tile_pitch(R) * sizeof(A);
-  static const cudaError_t attr =
-      cudaFuncSetAttribute(k_pass1<Tin, LOGR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  static std::atomic<unsigned long long> done{0};
+  const cudaError_t attr = smem_optin(k_pass1<Tin, LOGR>, smem, done);
   if (attr != cudaSuccess) return attr;
   k_pass1<Tin, LOGR><<<grid, kThreads, smem, st>>>(a);
   return cudaGetLastError();
@@ -268,8 +289,8 @@ template <typename A, int LOGR>
 cudaError_t launch_pass2_t(dim3 grid, const Pass2Args& a, cudaStream_t st) {
   constexpr int R = 1 << LOGR;
   const size_t smem = 2 * (size_t)R * tile_pitch(R) * sizeof(A);
-  static const cudaError_t attr =
-      cudaFuncSetAttribute(k_pass2<A, LOGR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  static std::atomic<unsigned long long> done{0};
+  const cudaError_t attr = smem_optin(k_pass2<A, LOGR>, smem, done);
   if (attr != cudaSuccess) return attr;
   k_pass2<A, LOGR><<<grid, kThreads, smem, st>>>(a);
   return cudaGetLastError();
@@ -314,9 +335,9 @@ template <typename Tin, int R>
 cudaError_t launch_p1_t(dim3 grid, const P1Maps& m, const v2::P1Params& a, cudaStream_t st) {
   // range launches with the TMA loader also stage the strip's colmap slice (kColmapStageBytes)
   const size_t smem = v2::p1_smem_bytes(R, sizeof(Tin) == 1) + (a.range && a.fill_tma ? v2::kColmapStageBytes : 0);
-  static const cudaError_t attr =
-      cudaFuncSetAttribute(v2::k_p1<Tin, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)(v2::p1_smem_bytes(R, sizeof(Tin) == 1) + v2::kColmapStageBytes));
+  static std::atomic<unsigned long long> done{0};
+  const cudaError_t attr =
+      smem_optin(v2::k_p1<Tin, R>, v2::p1_smem_bytes(R, sizeof(Tin) == 1) + v2::kColmapStageBytes, done);
   if (attr != cudaSuccess) return attr;
   return launch_pdl(v2::k_p1<Tin, R>, grid, dim3(v2::Split<R>::nw * 32), smem, st, m.img0, m.img1, m.scr, a);
 }
@@ -338,8 +359,8 @@ struct P2Maps {
 template <typename A, int R, typename Tscr>
 cudaError_t launch_p2_t(dim3 grid, const P2Maps& m, const v2::P2Params& a, cudaStream_t st) {
   const size_t smem = v2::p2_smem_bytes(R);
-  static const cudaError_t attr =
-      cudaFuncSetAttribute(v2::k_p2<A, R, Tscr>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  static std::atomic<unsigned long long> done{0};
+  const cudaError_t attr = smem_optin(v2::k_p2<A, R, Tscr>, smem, done);
   if (attr != cudaSuccess) return attr;
   return launch_pdl(v2::k_p2<A, R, Tscr>, grid, dim3(v2::Split<R>::nw * 32), smem, st, m.scr0, m.scr1, m.out0, m.out1,
                     m.out0_box, a);
@@ -764,6 +785,7 @@ size_t hough_extent_bytes(const fht_hough* h) {
 int validate_outs(const fht_image* img, const fht_hough* out, const fht_hough* out_s, const fht_hough& want,
                   const void* ws, size_t ws_bytes) {
   if (!out && !out_s) return FHT_ERR_ARG;
+  if (ws && overlaps(ws, ws_bytes, img->data, image_extent_bytes(img))) return FHT_ERR_ARG;  // fht.h: no aliasing
   const fht_hough* o[2] = {out, out_s};
   for (int d = 0; d < 2; ++d) {
     if (!o[d]) continue;
@@ -789,11 +811,11 @@ int plan_e(double g, int64_t y) {
 }
 
 // the plan's frame is the image, or its transpose for a mostly-horizontal plan
-bool plan_matches(const fht_image* img, const fht_angle_plan* plan) {
+bool plan_matches(const fht_image* img, const fht_angle_plan_t* plan) {
   return plan->transposed ? (plan->h == img->w && plan->w == img->h) : (plan->h == img->h && plan->w == img->w);
 }
 
-Frame range_frame(const fht_image* img, const fht_angle_plan* plan) {
+Frame range_frame(const fht_image* img, const fht_angle_plan_t* plan) {
   Frame f{};
   f.transposed = plan->transposed ? 1 : 0;
   f.Hp = (int)plan->Hp;
@@ -806,7 +828,7 @@ Frame range_frame(const fht_image* img, const fht_angle_plan* plan) {
   return f;
 }
 
-RangeDev range_geometry(const Frame& f, const fht_angle_plan* plan) {
+RangeDev range_geometry(const Frame& f, const fht_angle_plan_t* plan) {
   RangeDev rg{};
   rg.w_content = (int)plan->w_content;
   rg.alpha = plan->alpha;
@@ -821,7 +843,7 @@ RangeDev range_geometry(const Frame& f, const fht_angle_plan* plan) {
   return rg;
 }
 
-size_t range_tables_bytes(const fht_angle_plan* plan) {
+size_t range_tables_bytes(const fht_angle_plan_t* plan) {
   const size_t tables = (size_t)(plan->h + plan->w_content + 2 * plan->Hp + 64) * 4;
   return (tables + 255) & ~size_t(255);
 }
@@ -861,7 +883,7 @@ const char* fht_status_string(int s) {
 }
 
 namespace {
-int plan_make(int64_t h, int64_t w, double tmin, double tmax, bool pruned, fht_angle_plan* out) {
+int plan_make(int64_t h, int64_t w, double tmin, double tmax, bool pruned, fht_angle_plan_t* out) {
   if (!out || h < 1 || w < 1) return FHT_ERR_ARG;
   if (!(tmin > -90.0 && tmin < tmax && tmax < 90.0)) return FHT_ERR_ARG;
   const double deg = M_PI / 180.0;
@@ -879,36 +901,47 @@ int plan_make(int64_t h, int64_t w, double tmin, double tmax, bool pruned, fht_a
     const int64_t s_max = (int64_t)std::ceil((k_hi - k_lo) * (double)(Hp - 1) - 1e-9);
     rows = s_max + 1 < Hp ? s_max + 1 : Hp;
   }
-  // e_y and the largest per-row spread of e_y - D_s(y) over y < h (R17)
-  const int K = ilog2(Hp);
-  int* e = new int[h];
-  int* D = new int[h];
+  // e_y and the largest per-row spread of e_y - D_s(y) over y < h (R17). The min and max over y of
+  // e_y - D_s(y) for every s come from the FHT's own block recursion with (min, max) in place of +
+  // (D_t of a 2^k-row block = D_{t>>1} on its top half, ceil(t/2) + D_{t>>1} on its bottom half):
+  //   mn_k[b][t] = min(mn_{k-1}[2b][t>>1], mn_{k-1}[2b+1][t>>1] - ceil(t/2))   (mx likewise),
+  // Hp log2 Hp steps instead of Hp * h (a plan costs microseconds, so fht_angle_range can build it per call).
   int e_min = 1 << 30, e_max = -(1 << 30);
-  for (int64_t y = 0; y < h; ++y) {
-    e[y] = plan_e(g, y);
-    e_min = e[y] < e_min ? e[y] : e_min;
-    e_max = e[y] > e_max ? e[y] : e_max;
+  const int64_t kInf = int64_t(1) << 40;
+  int64_t* mn = new int64_t[Hp];
+  int64_t* mx = new int64_t[Hp];
+  int64_t* mn2 = new int64_t[Hp];
+  int64_t* mx2 = new int64_t[Hp];
+  for (int64_t y = 0; y < Hp; ++y) {
+    if (y < h) {
+      const int e = plan_e(g, y);
+      e_min = e < e_min ? e : e_min;
+      e_max = e > e_max ? e : e_max;
+      mn[y] = mx[y] = e;
+    } else {  // padding rows hold no pixel: neutral for min / max
+      mn[y] = kInf;
+      mx[y] = -kInf;
+    }
+  }
+  for (int64_t half = 1; half < Hp; half <<= 1) {  // level: blocks of 2*half rows, shifts t < 2*half
+    for (int64_t b = 0; b < Hp / (2 * half); ++b)
+      for (int64_t t = 0; t < 2 * half; ++t) {
+        const int64_t top = (2 * b) * half + (t >> 1), bot = (2 * b + 1) * half + (t >> 1), c = (t + 1) >> 1;
+        const int64_t lo_b = mn[bot] == kInf ? kInf : mn[bot] - c, hi_b = mx[bot] == -kInf ? -kInf : mx[bot] - c;
+        mn2[b * 2 * half + t] = mn[top] < lo_b ? mn[top] : lo_b;
+        mx2[b * 2 * half + t] = mx[top] > hi_b ? mx[top] : hi_b;
+      }
+    std::swap(mn, mn2);
+    std::swap(mx, mx2);
   }
   int64_t spread_max = 0;
-  for (int64_t s = 0; s < rows; ++s) {
-    // D_s(y) by lowest-set-bit recurrence: bit p of y carries weight ceil((s >> (K-1-p))/2)
-    int mn = 1 << 30, mx = -(1 << 30);
-    for (int64_t y = 0; y < h; ++y) {
-      if (y == 0) D[0] = 0;
-      else {
-        const int64_t low = y & (-y);
-        const int p = ilog2(low);
-        D[y] = D[y & (y - 1)] + (int)(((s >> (K - 1 - p)) + 1) >> 1);
-      }
-      const int v = e[y] - D[y];
-      mn = v < mn ? v : mn;
-      mx = v > mx ? v : mx;
-    }
-    if (mx - mn > spread_max) spread_max = mx - mn;
-  }
-  delete[] e;
-  delete[] D;
-  fht_angle_plan p{};
+  for (int64_t s = 0; s < rows; ++s)
+    if (mx[s] - mn[s] > spread_max) spread_max = mx[s] - mn[s];
+  delete[] mn;
+  delete[] mx;
+  delete[] mn2;
+  delete[] mx2;
+  fht_angle_plan_t p{};
   p.theta_min_deg = tmin;
   p.theta_max_deg = tmax;
   p.k_lo = k_lo;
@@ -928,15 +961,24 @@ int plan_make(int64_t h, int64_t w, double tmin, double tmax, bool pruned, fht_a
 }
 }  // namespace
 
-int fht_angle_plan_make(int64_t h, int64_t w, double tmin, double tmax, fht_angle_plan* out) {
+int fht_angle_plan(int64_t h, int64_t w, double tmin, double tmax, fht_angle_plan_t* out) {
   return plan_make(h, w, tmin, tmax, false, out);
 }
 
-int fht_angle_plan_make_pruned(int64_t h, int64_t w, double tmin, double tmax, fht_angle_plan* out) {
+int fht_angle_of_row(const fht_angle_plan_t* plan, int64_t s, double* deg) {
+  // R19 ("shift = h tg(phi)"): row s holds patterns of endpoint slope s / (Hp - 1) in the
+  // transformed frame (D_s(Hp - 1) = s); undo the scale and the shear
+  if (!plan || !deg || plan->Hp < 1 || s < 0 || s >= plan->Hp || !(plan->alpha > 0.0)) return FHT_ERR_ARG;
+  const double k = plan->Hp > 1 ? plan->k_lo + (double)s / (plan->alpha * (double)(plan->Hp - 1)) : plan->k_lo;
+  *deg = std::atan(k) * (180.0 / M_PI);
+  return FHT_OK;
+}
+
+int fht_angle_plan_make_pruned(int64_t h, int64_t w, double tmin, double tmax, fht_angle_plan_t* out) {
   return plan_make(h, w, tmin, tmax, true, out);
 }
 
-int fht_angle_plan_make_ex(int64_t h, int64_t w, double tmin, double tmax, int32_t flags, fht_angle_plan* out) {
+int fht_angle_plan_make_ex(int64_t h, int64_t w, double tmin, double tmax, int32_t flags, fht_angle_plan_t* out) {
   if (flags & ~(FHT_PLAN_PRUNED | FHT_PLAN_HORIZONTAL)) return FHT_ERR_ARG;
   const bool hz = (flags & FHT_PLAN_HORIZONTAL) != 0;
   // mostly-horizontal: the vertical plan of the transposed image (frame h, w = image w, h)
@@ -945,7 +987,7 @@ int fht_angle_plan_make_ex(int64_t h, int64_t w, double tmin, double tmax, int32
   return r;
 }
 
-int fht_hough_describe(int mode, int layout, int quadrant, const fht_image* img, const fht_angle_plan* plan,
+int fht_hough_describe(int mode, int layout, int quadrant, const fht_image* img, const fht_angle_plan_t* plan,
                        fht_hough* out) {
   if (!img || !out) return FHT_ERR_ARG;
   if (img->dtype != FHT_U8 && img->dtype != FHT_I32 && img->dtype != FHT_F32) return FHT_ERR_DTYPE;
@@ -1015,7 +1057,7 @@ size_t fht_quadrant_workspace_bytes(const fht_image* img, int quadrant, int64_t 
   return (((size_t)(d.batch * d.batch_stride) * 4 + 255) & ~size_t(255)) + base;  // + the pad = Hp image
 }
 
-size_t fht_workspace_bytes(int mode, const fht_image* img, const fht_angle_plan* plan) {
+size_t fht_workspace_bytes(int mode, const fht_image* img, const fht_angle_plan_t* plan) {
   if (!img || img->batch < 1 || img->h < 1 || img->w < 1) return 0;
   if (mode == FHT_MODE_RANGE) {
     if (!plan) return 0;
@@ -1038,8 +1080,12 @@ size_t fht_workspace_bytes(int mode, const fht_image* img, const fht_angle_plan*
   return need;
 }
 
-int fht_quadrant(const fht_image* img, int quadrant, int64_t pad_cols, fht_hough* out, fht_hough* out_shifted,
-                 void* ws, size_t ws_bytes, fht_stream_t stream, const fht_exec_opts* opts) {
+}  // extern "C"
+
+namespace {
+// fht_quadrant with the caller's launch log (events / counts shared with the fold path's inner call)
+int quadrant_run(const fht_image* img, int quadrant, int64_t pad_cols, fht_hough* out, fht_hough* out_shifted,
+                 void* ws, size_t ws_bytes, fht_stream_t stream, LaunchLog& log) {
   int s = check_image(img);
   if (s) return s;
   if (quadrant < 0 || quadrant > 3) return FHT_ERR_ARG;
@@ -1062,8 +1108,8 @@ int fht_quadrant(const fht_image* img, int quadrant, int64_t pad_cols, fht_hough
     const size_t need = fht_quadrant_workspace_bytes(img, quadrant, pad_cols);
     if (!ws || ws_bytes < need) return FHT_ERR_WORKSPACE;
     tmpd.data = ws;
-    const int r = fht_quadrant(img, quadrant, -1, &tmpd, nullptr, static_cast<char*>(ws) + tmp_bytes,
-                               ws_bytes - tmp_bytes, stream, opts);
+    const int r = quadrant_run(img, quadrant, -1, &tmpd, nullptr, static_cast<char*>(ws) + tmp_bytes,
+                               ws_bytes - tmp_bytes, stream, log);
     if (r < 0) return r;
     FoldArgs fa{};
     fa.tmp = ws;
@@ -1083,12 +1129,15 @@ int fht_quadrant(const fht_image* img, int quadrant, int64_t pad_cols, fht_hough
     fa.W = (int)want.cols;
     fa.Wt = (int)tmpd.cols;
     fa.sigma = (quadrant == FHT_QA || quadrant == FHT_QD) ? 1 : -1;
+    fa.pad = (int)(want.cols - (quadrant >= 2 ? img->h : img->w));  // fused fhtshift: R11 rule of this pad
     fa.xlo = fa.sigma > 0 ? -fa.Hp : 0;  // the default run's tiling window [xlo, xlo + Wt)
     fa.total = tmpd.batch * (int64_t)fa.Hp * fa.W;
     const int64_t nblk = std::min<int64_t>((fa.total + kThreads - 1) / kThreads, 148 * 16);
+    // the inner run's last log.after() recorded the event that opens this launch
     if (tmpd.dtype == FHT_F32) k_fold<float><<<(unsigned)nblk, kThreads, 0, (cudaStream_t)stream>>>(fa);
     else k_fold<int><<<(unsigned)nblk, kThreads, 0, (cudaStream_t)stream>>>(fa);
     if (cudaGetLastError() != cudaSuccess) return FHT_ERR_CUDA;
+    log.after((cudaStream_t)stream);
     mark_outs(out, out_shifted);
     return r + 1;
   }
@@ -1105,10 +1154,18 @@ int fht_quadrant(const fht_image* img, int quadrant, int64_t pad_cols, fht_hough
   sl.row_sign = 1;
   sl.skip_t = -1;
   Outs o{{out, out_shifted}};
-  LaunchLog log{opts, 0};
   const int r = run_orientation(img, f, &sl, 1, o, ws, ws_bytes, (cudaStream_t)stream, nullptr, log);
   if (r > 0) mark_outs(out, out_shifted);
   return r;
+}
+}  // namespace
+
+extern "C" {
+
+int fht_quadrant(const fht_image* img, int quadrant, int64_t pad_cols, fht_hough* out, fht_hough* out_shifted,
+                 void* ws, size_t ws_bytes, fht_stream_t stream, const fht_exec_opts* opts) {
+  LaunchLog log{opts, 0};
+  return quadrant_run(img, quadrant, pad_cols, out, out_shifted, ws, ws_bytes, stream, log);
 }
 
 int fht_full(const fht_image* img, int layout, fht_hough* out, fht_hough* out_shifted, void* ws, size_t ws_bytes,
@@ -1197,8 +1254,32 @@ int fht_full(const fht_image* img, int layout, fht_hough* out, fht_hough* out_sh
   return r;
 }
 
-int fht_angle_range(const fht_image* img, const fht_angle_plan* plan, fht_hough* out, fht_hough* out_shifted,
-                    void* ws, size_t ws_bytes, fht_stream_t stream, const fht_exec_opts* opts) {
+size_t fht_angle_range_workspace_bytes(const fht_image* img, double theta_min_deg, double theta_max_deg) {
+  fht_angle_plan_t p;
+  if (!img || fht_angle_plan(img->h, img->w, theta_min_deg, theta_max_deg, &p) != FHT_OK) return 0;
+  return fht_workspace_bytes(FHT_MODE_RANGE, img, &p);
+}
+
+int fht_angle_range(const fht_image* img, double theta_min_deg, double theta_max_deg, fht_hough* out,
+                    fht_hough* out_shifted, void* ws, size_t ws_bytes, fht_stream_t stream, const fht_exec_opts* opts) {
+  // P:117 "perform a transform for an arbitrary range of angles [gamma1; gamma2]": the §4 plan is
+  // built here (host, O(Hp log Hp)) and must describe the same transform as the outputs
+  int s = check_image(img);
+  if (s) return s;
+  fht_angle_plan_t p;
+  if ((s = fht_angle_plan(img->h, img->w, theta_min_deg, theta_max_deg, &p))) return s;
+  for (const fht_hough* o : {(const fht_hough*)out, (const fht_hough*)out_shifted}) {
+    if (!o) continue;
+    if (o->mode != FHT_MODE_RANGE || o->plan.transposed || o->plan.rows != p.rows || o->plan.W != p.W ||
+        o->plan.w_content != p.w_content || o->plan.theta_min_deg != theta_min_deg ||
+        o->plan.theta_max_deg != theta_max_deg)
+      return FHT_ERR_SHAPE;
+  }
+  return fht_angle_range_plan(img, &p, out, out_shifted, ws, ws_bytes, stream, opts);
+}
+
+int fht_angle_range_plan(const fht_image* img, const fht_angle_plan_t* plan, fht_hough* out, fht_hough* out_shifted,
+                         void* ws, size_t ws_bytes, fht_stream_t stream, const fht_exec_opts* opts) {
   int s = check_image(img);
   if (s) return s;
   if (!plan || !plan_matches(img, plan)) return FHT_ERR_ARG;
@@ -1283,6 +1364,7 @@ int fhtshift(const fht_hough* in, fht_hough* out, fht_stream_t stream) {
   size_t smem = 0;
   if (in->mode == FHT_MODE_QUADRANT) {
     a.Hp = a.Wp = (int)in->rows;  // the quadrant's own row count
+    a.pad = (int)(in->cols - (in->quadrant >= 2 ? in->h : in->w));  // W - w_frame (R11 generic rule)
   } else if (in->mode == FHT_MODE_FULL) {
     a.Hp = (int)in->Hp;
     a.Wp = (int)in->Wp;
@@ -1316,6 +1398,7 @@ int fht_peaks(const fht_hough* h, int32_t k, void* values, int32_t* rows, int32_
   if (h->dtype != FHT_I32 && h->dtype != FHT_F32) return FHT_ERR_DTYPE;
   if (k < 1 || k > pk::kMaxK || h->batch < 1 || h->nquad < 1 || h->rows < 1 || h->cols < 1) return FHT_ERR_ARG;
   if (h->rows * h->cols >= (int64_t(1) << 32) - 1 || h->rows >= (int64_t(1) << 31)) return FHT_ERR_UNSUPPORTED;
+  if (h->batch * h->nquad > 65535) return FHT_ERR_UNSUPPORTED;  // planes are gridDim.y of the band pass
   const size_t need = fht_peaks_workspace_bytes(h);
   if (!ws || ws_bytes < need) return FHT_ERR_WORKSPACE;
   pk::PeakArgs a{};

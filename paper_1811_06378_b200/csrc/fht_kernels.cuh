@@ -223,7 +223,7 @@ __global__ void __launch_bounds__(kThreads) k_pass2(const Pass2Args a) {
     if (!a.range) {
       lo = a.xbeg[qi];
       hi = lo + a.W;
-      if (a.shift) k = sigma > 0 ? ceil_half(a.Hp + t) : ceil_half(a.Hp - t);
+      if (a.shift) k = sigma > 0 ? ceil_half(a.W - a.wc + t) : ceil_half(a.W - a.wc - t);  // R11, pad = W - wc
     } else {
       lo = a.start_tab[t];
       hi = lo + a.W;
@@ -344,6 +344,7 @@ struct ShiftArgs {
   int mode, layout;     // fht_mode / fht_layout
   int quadrant;         // QUADRANT mode
   int Hp, Wp;           // quadrant row counts (QA/QB: Hp, QC/QD: Wp)
+  int pad;              // QUADRANT mode: the frame's extension W - w_frame (FULL: pad = the row count)
   int vec;              // 16-byte path: W, every stride a multiple of 4 elements, bases 16-B aligned
   double g;             // RANGE: shear e_y = floor(g*y + 0.5), y < h; K = log2 Hp; w' (R17 support)
   int h, K, w_content;
@@ -367,7 +368,11 @@ __device__ __forceinline__ int shift_amount(const ShiftArgs& a, int r, int qs) {
   }
   const int n = (q < 2) ? a.Hp : a.Wp;
   if (s >= n) return 0;
-  return (quadrant_sigma(q) > 0 ? ceil_half(n + s) : ceil_half(n - s)) % a.W;
+  // R11 generic rule k = ceil((W - len)/2) - start, len = w_frame + s: ceil((pad + s)/2) for sigma=+1
+  // (start = -s), ceil((pad - s)/2) for sigma=-1 (start = 0); pad = W - w_frame (full mode: n)
+  const int pad = a.mode == 0 ? a.pad : n;
+  int k = (quadrant_sigma(q) > 0 ? ceil_half(pad + s) : ceil_half(pad - s)) % a.W;
+  return k < 0 ? k + a.W : k;
 }
 
 template <typename T> struct Vec4;
@@ -475,6 +480,7 @@ struct FoldArgs {
   void* outs;                    // fhtshift destination, may be NULL
   int64_t outs_pitch, outs_batch;
   int Hp, W, Wt, xlo, sigma;
+  int pad;                       // W - w_frame (the fused fhtshift's R11 rule)
   int64_t total;                 // batch * Hp * W
 };
 
@@ -496,7 +502,8 @@ __global__ void __launch_bounds__(kThreads) k_fold(const FoldArgs a) {
     }
     if (a.out) static_cast<T*>(a.out)[b * a.out_batch + (int64_t)s * a.out_pitch + x0] = acc;
     if (a.outs) {
-      const int k = (a.sigma > 0 ? ceil_half(a.Hp + s) : ceil_half(a.Hp - s)) % a.W;
+      int k = (a.sigma > 0 ? ceil_half(a.pad + s) : ceil_half(a.pad - s)) % a.W;  // R11 generic rule
+      k += k < 0 ? a.W : 0;
       int xs = x0 + k;
       xs -= xs >= a.W ? a.W : 0;
       static_cast<T*>(a.outs)[b * a.outs_batch + (int64_t)s * a.outs_pitch + xs] = acc;

@@ -895,13 +895,16 @@ __device__ __forceinline__ void p2_body(const CUtensorMap* tm_scr0, const CUtens
       vhi = vlo + p.W;
       if (D.shifted) k = (((p.W - __ldg(p.len_tab + t)) + 1) >> 1) - vlo;
     } else if (D.shifted) {
-      k = SIG > 0 ? ceil_half(p.Hp + t) : ceil_half(p.Hp - t);
+      // R11 generic rule ceil((W - len)/2) - start with len = wc + t: ceil((pad + t)/2) (sigma = +1,
+      // start = -t) or ceil((pad - t)/2) (sigma = -1, start = 0), pad = W - wc
+      const int pad = p.W - p.wc;
+      k = SIG > 0 ? ceil_half(pad + t) : ceil_half(pad - t);
     }
     // X in [xbeg, xend), k in [0, W): one conditional add/subtract replaces the modulo (range
     // mode: k is arbitrary, keep the division)
     int v = X + k;
     if (p.range) v = mod_pos(v, p.W);
-    else { v += v < 0 ? p.W : 0; v -= v >= p.W ? p.W : 0; }
+    else { v += v < 0 ? p.W : 0; v -= v >= p.W ? p.W : 0; }  // X + k in (-W, 2W) for every pad >= h - 1
     const int r = v & 3;
     const int xs0 = X - r;
     int d0 = v - r;

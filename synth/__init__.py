@@ -132,9 +132,12 @@ def batch(config_id: int, count: int | None = None, first: int = 0) -> np.ndarra
     return np.stack([gen[config_id](i) for i in idx])
 
 
-def random_image(shape, dtype: str, seed: int, density: float | None = None) -> np.ndarray:
-    """Small seeded random image for unit/parity tests: u8 / i32 in [0,255], f32 N(0,1)."""
+def random_image(shape, dtype: str, seed: int, density: float | None = None, bound: int | None = None) -> np.ndarray:
+    """Small seeded random image for unit/parity tests: u8 / i32 in [0,255], f32 N(0,1); "i32w": int32
+    uniform in [-bound, bound] (signed, large magnitudes; the caller picks a bound its sums fit in)."""
     g = np.random.Generator(np.random.PCG64(np.random.SeedSequence([BASE_SEED, 99, seed])))
+    if dtype == "i32w":
+        return g.integers(-bound, bound + 1, size=shape).astype(np.int32)
     if dtype == "u8":
         a = g.integers(0, 256, size=shape, dtype=np.uint8)
         if density is not None:

@@ -2,6 +2,7 @@
 declares, and the host-only calls (describe, workspace sizing, plan, argument checks) behave
 as documented. No compute call runs here (no GPU)."""
 import ctypes
+import math
 import os
 import re
 
@@ -30,7 +31,7 @@ def test_struct_sizes_match_header(tmp_path):
     L = _lib()
     src = tmp_path / "sz.c"
     src.write_text('#include <stdio.h>\n#include "fht.h"\nint main(void) { printf("%zu %zu %zu %zu", '
-                   'sizeof(fht_image), sizeof(fht_angle_plan), sizeof(fht_hough), sizeof(fht_exec_opts)); return 0; }\n')
+                   'sizeof(fht_image), sizeof(fht_angle_plan_t), sizeof(fht_hough), sizeof(fht_exec_opts)); return 0; }\n')
     inc = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include")
     subprocess.run(["gcc", "-I", inc, str(src), "-o", str(tmp_path / "sz")], check=True)
     got = [int(x) for x in subprocess.run([str(tmp_path / "sz")], capture_output=True, text=True, check=True).stdout.split()]
@@ -68,7 +69,7 @@ def test_plan_matches_oracle_rule():
     L = _lib()
     for h, w, a, b in [(4096, 4096, -15, 15), (64, 48, 5, 40), (33, 17, -45, 0), (16, 16, 0, 45), (32, 32, -80, 80)]:
         p = L.FhtAnglePlan()
-        assert L.lib.fht_angle_plan_make(h, w, a, b, ctypes.byref(p)) == 0
+        assert L.lib.fht_angle_plan(h, w, a, b, ctypes.byref(p)) == 0
         o = O.angle_plan(h, w, a, b)
         assert (p.k_lo, p.k_hi, p.alpha, p.g) == (o.k_lo, o.k_hi, o.alpha, o.g)
         assert (p.Hp, p.w_content, p.W) == (o.Hp, o.w_content, o.W)
@@ -91,7 +92,7 @@ def test_pruned_plan_matches_oracle_rule():
         assert L.lib.fht_hough_describe(L.FHT_MODE_RANGE, 0, 0, ctypes.byref(img), ctypes.byref(p), ctypes.byref(d)) == 0
         assert (d.rows, d.cols) == (o.rows, o.W)
     p = L.FhtAnglePlan()
-    assert L.lib.fht_angle_plan_make(64, 64, -15, 15, ctypes.byref(p)) == 0 and p.rows == p.Hp
+    assert L.lib.fht_angle_plan(64, 64, -15, 15, ctypes.byref(p)) == 0 and p.rows == p.Hp
     assert L.lib.fht_angle_plan_make_pruned(64, 64, -30, 30, ctypes.byref(p)) == -5   # k_hi - k_lo > 1
 
 
@@ -122,11 +123,11 @@ def test_plan_ex_matches_oracle():
 def test_plan_errors():
     L = _lib()
     p = L.FhtAnglePlan()
-    assert L.lib.fht_angle_plan_make(16, 16, 10, 10, ctypes.byref(p)) == -1
-    assert L.lib.fht_angle_plan_make(16, 16, -90, 10, ctypes.byref(p)) == -1
-    assert L.lib.fht_angle_plan_make(16, 16, 20, 10, ctypes.byref(p)) == -1
-    assert L.lib.fht_angle_plan_make(1, 1, -89.9, 89.9, ctypes.byref(p)) == -1      # alpha * w < 1
-    assert L.lib.fht_angle_plan_make(0, 16, -10, 10, ctypes.byref(p)) == -1
+    assert L.lib.fht_angle_plan(16, 16, 10, 10, ctypes.byref(p)) == -1
+    assert L.lib.fht_angle_plan(16, 16, -90, 10, ctypes.byref(p)) == -1
+    assert L.lib.fht_angle_plan(16, 16, 20, 10, ctypes.byref(p)) == -1
+    assert L.lib.fht_angle_plan(1, 1, -89.9, 89.9, ctypes.byref(p)) == -1      # alpha * w < 1
+    assert L.lib.fht_angle_plan(0, 16, -10, 10, ctypes.byref(p)) == -1
 
 
 def test_argument_errors_are_synchronous():
@@ -238,7 +239,7 @@ def test_peaks_and_segment_errors():
     assert L.lib.fht_cell_segment(ctypes.byref(d), 4, 0, 0, ctypes.byref(sg)) == -1       # slot out of range
     assert L.lib.fht_cell_segment(ctypes.byref(d), 0, 0, d.cols, ctypes.byref(sg)) == -1  # col out of range
     p = L.FhtAnglePlan()
-    assert L.lib.fht_angle_plan_make(16, 16, -15, 15, ctypes.byref(p)) == 0
+    assert L.lib.fht_angle_plan(16, 16, -15, 15, ctypes.byref(p)) == 0
     dr = L.FhtHough()
     assert L.lib.fht_hough_describe(L.FHT_MODE_RANGE, 0, 0, ctypes.byref(img), ctypes.byref(p), ctypes.byref(dr)) == 0
     assert L.lib.fht_cell_segment(ctypes.byref(dr), 0, 0, 0, ctypes.byref(sg)) == -5      # RANGE: unsupported
@@ -260,3 +261,85 @@ def test_pad_describe_and_limits():
     base = L.lib.fht_quadrant_workspace_bytes(ctypes.byref(img), 0, -1)
     assert L.lib.fht_quadrant_workspace_bytes(ctypes.byref(img), 0, 99) == base
     assert L.lib.fht_quadrant_workspace_bytes(ctypes.byref(img), 0, 98) == base + ((128 * 188 * 4 + 255) // 256) * 256
+
+
+def test_plan_fast_spread_matches_oracle_many():
+    """fht_angle_plan's W' (R17) comes from the (min, max) block recursion; the oracle takes the spread
+    of e_y - D_s(y) over all (s, y) explicitly. Same W' (and pruned rows) on random shapes and angles,
+    non-power-of-two heights included (padding rows hold no pixel)."""
+    import random
+    from oracle import fht_oracle as O
+    L = _lib()
+    rnd = random.Random(7)
+    for _ in range(60):
+        h, w = rnd.randint(1, 300), rnd.randint(4, 300)
+        a = rnd.uniform(-85, 80)
+        b = rnd.uniform(a + 0.5, min(89, a + 120))
+        p = L.FhtAnglePlan()
+        r = L.lib.fht_angle_plan(h, w, a, b, ctypes.byref(p))
+        try:
+            o = O.angle_plan(h, w, a, b)
+        except ValueError:
+            assert r == -1
+            continue
+        assert r == 0 and (p.W, p.w_content, p.Hp) == (o.W, o.w_content, o.Hp), (h, w, a, b)
+        if math.tan(math.radians(b)) - math.tan(math.radians(a)) <= 1.0:
+            assert L.lib.fht_angle_plan_make_pruned(h, w, a, b, ctypes.byref(p)) == 0
+            o = O.angle_plan_pruned(h, w, a, b)
+            assert (p.W, p.rows) == (o.W, o.rows), (h, w, a, b)
+
+
+def test_angle_of_row_matches_oracle():
+    """fht_angle_of_row (R19) against the oracle's angle_of_row (pinned by the endpoint slopes)."""
+    from oracle import fht_oracle as O
+    L = _lib()
+    for h, w, a, b, flags in [(4096, 4096, -15, 15, 0), (64, 48, 5, 40, 0), (33, 17, -45, 0, 0),
+                              (128, 96, -20, 10, 1), (64, 48, -15, 15, 2)]:
+        p = L.FhtAnglePlan()
+        assert L.lib.fht_angle_plan_make_ex(h, w, a, b, flags, ctypes.byref(p)) == 0
+        o = (O.angle_plan_horizontal(h, w, a, b, pruned=bool(flags & 1)) if flags & 2 else
+             (O.angle_plan_pruned if flags & 1 else O.angle_plan)(h, w, a, b))
+        d = ctypes.c_double()
+        for s in sorted({0, 1, p.Hp // 2, p.rows - 1, p.Hp - 1}):
+            assert L.lib.fht_angle_of_row(ctypes.byref(p), s, ctypes.byref(d)) == 0
+            assert d.value == pytest.approx(O.angle_of_row(s, o), abs=1e-12)
+        assert L.lib.fht_angle_of_row(ctypes.byref(p), p.Hp, ctypes.byref(d)) == -1
+        assert L.lib.fht_angle_of_row(ctypes.byref(p), -1, ctypes.byref(d)) == -1
+    p = L.FhtAnglePlan()
+    assert L.lib.fht_angle_plan(256, 256, -15, 15, ctypes.byref(p)) == 0
+    d = ctypes.c_double()
+    assert L.lib.fht_angle_of_row(ctypes.byref(p), 0, ctypes.byref(d)) == 0 and d.value == pytest.approx(-15, abs=1e-12)
+    assert L.lib.fht_angle_of_row(ctypes.byref(p), 255, ctypes.byref(d)) == 0 and d.value == pytest.approx(15, abs=1e-12)
+
+
+def test_angle_range_by_angles_checks():
+    """fht_angle_range(img, theta_min, theta_max, ...) builds the §4 plan itself: its workspace
+    size equals fht_workspace_bytes for that plan, and outputs described with another plan, or angle
+    errors, are rejected synchronously."""
+    L = _lib()
+    img = _img(L, 64, 48)
+    p = L.FhtAnglePlan()
+    assert L.lib.fht_angle_plan(64, 48, -15, 15, ctypes.byref(p)) == 0
+    n = L.lib.fht_angle_range_workspace_bytes(ctypes.byref(img), -15.0, 15.0)
+    assert n == L.lib.fht_workspace_bytes(L.FHT_MODE_RANGE, ctypes.byref(img), ctypes.byref(p)) and n > 0
+    assert L.lib.fht_angle_range_workspace_bytes(ctypes.byref(img), 15.0, -15.0) == 0
+    d = L.FhtHough()
+    assert L.lib.fht_hough_describe(L.FHT_MODE_RANGE, 0, 0, ctypes.byref(img), ctypes.byref(p), ctypes.byref(d)) == 0
+    d.data = 1 << 40
+    ws = 1 << 44
+    # outputs described for [-15, 15] but the call asks for [-10, 15]
+    assert L.lib.fht_angle_range(ctypes.byref(img), -10.0, 15.0, ctypes.byref(d), None, ws, n, None, None) == -3
+    assert L.lib.fht_angle_range(ctypes.byref(img), 15.0, -15.0, ctypes.byref(d), None, ws, n, None, None) == -1
+    assert L.lib.fht_angle_range(ctypes.byref(img), -15.0, 15.0, None, None, ws, n, None, None) == -1
+    assert L.lib.fht_angle_range(ctypes.byref(img), -15.0, 15.0, ctypes.byref(d), None, ws, 16, None, None) == -6
+
+
+def test_workspace_may_not_alias_image():
+    """fht.h: no buffer may overlap another -- a workspace over the image is FHT_ERR_ARG."""
+    L = _lib()
+    img = _img(L, 64, 64, data=1 << 40)
+    d = L.FhtHough()
+    assert L.lib.fht_hough_describe(L.FHT_MODE_FULL, 0, 0, ctypes.byref(img), None, ctypes.byref(d)) == 0
+    d.data = 1 << 42
+    n = L.lib.fht_workspace_bytes(L.FHT_MODE_FULL, ctypes.byref(img), None)
+    assert L.lib.fht_full(ctypes.byref(img), 0, ctypes.byref(d), None, (1 << 40) + 64, n, None, None) == -1

@@ -234,7 +234,10 @@ def test_quadrant_pads(fht, O, shape, dt):
             want = O.hough_recursive(img, q, pad)
             assert got.shape == want.shape
             check(got, want, dt != "f32")
-            assert np.array_equal(s.view[0, 0].cpu().numpy(), O.fhtshift_quadrant(got, O.QUADRANT_FRAME[q][1]))
+            assert np.array_equal(s.view[0, 0].cpu().numpy(), O.fhtshift_quadrant(got, O.QUADRANT_FRAME[q][1], pad))
+            s2 = fht.fhtshift(h)                                       # standalone kernel, same R11 rule
+            torch.cuda.synchronize()
+            assert np.array_equal(s2.view[0, 0].cpu().numpy(), s.view[0, 0].cpu().numpy())
 
 
 def test_strided_batch_input(fht, O):
@@ -551,3 +554,185 @@ def test_graph_replay_equals_eager(fht, O):
     h1, s1 = fht.full(t, pair=True)
     torch.cuda.synchronize()
     assert torch.equal(h.storage, h1.storage) and torch.equal(s.storage, s1.storage)
+
+
+# ------------------------------------------------------------------ round 2: the benched calls themselves
+# bench.py times these exact calls (same arguments, streams and graph capture); here they are compared
+# with the oracle on EVERY cell of every output. Oracle work runs in a fork pool of host processes
+# (numpy only; the children never touch CUDA).
+_G = {}
+
+
+def _pool_map(fn, items):
+    import multiprocessing as mp
+    import os
+    n = max(1, min(len(items), 16, len(os.sched_getaffinity(0))))
+    with mp.get_context("fork").Pool(n) as pool:
+        errs = [r for r in pool.imap_unordered(fn, items) if r is not None]
+    assert not errs, errs[:5]
+
+
+def _tol_err(got, want):
+    err = np.abs(got.astype(np.float64) - want)
+    bad = err > ATOL + RTOL * np.abs(want)
+    return None if not bad.any() else f"{int(bad.sum())} cells out of tolerance, max err {err.max()}"
+
+
+def _full_unit(args):
+    """(b, q): oracle quadrant q of image b vs the GPU planes in _G; plain and fhtshift-ed outputs."""
+    from oracle import fht_oracle as O
+    b, q = args
+    img = _G["imgs"][b]
+    Hp, Wp = O.full_padding(*img.shape)
+    fr = O.quadrant_frame(img, q, square_to=(Hp, Wp))
+    want = O.hough_of_frame_recursive(fr)
+    n = want.shape[0]
+    integer = _G["integer"]
+    msgs = []
+    if "h" in _G:
+        got = _G["h"][b, q, :n]
+        if integer:
+            if not np.array_equal(got.astype(np.int64), want):
+                msgs.append(f"img {b} q {q}: plain mismatch")
+        else:
+            e = _tol_err(got, want)
+            if e:
+                msgs.append(f"img {b} q {q}: plain {e}")
+    if "s" in _G:
+        gs = _G["s"][b, q, :n]
+        want_s = O.fhtshift_quadrant(want, fr.sigma)
+        e = (None if np.array_equal(gs.astype(np.int64), want_s) else "mismatch") if integer else _tol_err(gs, want_s)
+        if e:
+            msgs.append(f"img {b} q {q}: shifted {e}")
+        if "h" in _G and not np.array_equal(gs, O.fhtshift_quadrant(_G["h"][b, q, :n], fr.sigma)):
+            msgs.append(f"img {b} q {q}: shifted is not the exact rotation of the plain output")
+    return "; ".join(msgs) or None
+
+
+def test_config1_bench_step(fht, O):
+    """C1 as bench.py times it: the QA call captured in a CUDA graph and replayed."""
+    import synth
+    img = synth.batch(1)[0]
+    t = dev(img)
+    h = fht.quadrant(t, fht.QA)
+    ws = torch.empty(fht.workspace_bytes(fht.FHT_MODE_QUADRANT, fht._image(t)[0]), dtype=torch.uint8, device="cuda")
+    g = fht.Graph(lambda: fht.quadrant(t, fht.QA, out=h, workspace=ws))
+    h.storage.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    check(h.view[0, 0].cpu().numpy(), O.hough_direct(img, O.QA), True)
+
+
+def test_config2_bench_step(fht, O):
+    """C2 as bench.py times it: full(pair=True, aux_stream) -- the two-stream orientation split --
+    captured in a CUDA graph; both outputs, every cell, against the oracle."""
+    import synth
+    img = synth.batch(2)[0]
+    t = dev(img)
+    h, s = fht.full(t, pair=True)
+    ws = torch.empty(fht.workspace_bytes(fht.FHT_MODE_FULL, fht._image(t)[0]), dtype=torch.uint8, device="cuda")
+    aux = torch.cuda.Stream()
+    g = fht.Graph(lambda: fht.full(t, pair=True, out=h, out_shifted=s, workspace=ws, aux_stream=aux))
+    h.storage.zero_()
+    s.storage.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    _G.clear()
+    _G.update(imgs=img[None], integer=False, h=h.view.cpu().numpy(), s=s.view.cpu().numpy())
+    _pool_map(_full_unit, [(0, q) for q in range(4)])
+
+
+def test_config3_bench_step(fht, O):
+    """C3 as bench.py times it: full(aux_stream) over the 64-image u8 batch; all 256 planes, every cell,
+    bit-exact."""
+    import synth
+    imgs = synth.batch(3)
+    aux = torch.cuda.Stream()
+    h = fht.full(dev(imgs), aux_stream=aux)
+    torch.cuda.synchronize()
+    _G.clear()
+    _G.update(imgs=imgs, integer=True, h=h.view.cpu().numpy())
+    _pool_map(_full_unit, [(b, q) for b in range(imgs.shape[0]) for q in range(4)])
+
+
+def test_config5_bench_step(fht, O):
+    """C5 as bench.py times it: full(pair=True, aux_stream) over the 16 x 2048^2 batch; both outputs of
+    all 16 images, every cell, against the oracle. The single-destination step (shifted=True) must
+    write the same bits as the pair's fhtshift output."""
+    import synth
+    imgs = synth.batch(5)
+    t = dev(imgs)
+    aux = torch.cuda.Stream()
+    h, s = fht.full(t, pair=True, aux_stream=aux)
+    s1 = fht.full(t, shifted=True, aux_stream=aux)
+    torch.cuda.synchronize()
+    assert torch.equal(s1.storage, s.storage)
+    del s1, t
+    _G.clear()
+    _G.update(imgs=imgs, integer=False, h=h.view.cpu().numpy(), s=s.view.cpu().numpy())
+    del h, s
+    torch.cuda.empty_cache()
+    _pool_map(_full_unit, [(b, q) for b in range(imgs.shape[0]) for q in range(4)])
+    _G.clear()
+
+
+def test_config4_bench_step(fht, O):
+    """C4 as bench.py times it: angle_range(t, -15, 15, pair=True) (fht_angle_range builds the §4 plan);
+    both outputs, every cell, against the oracle's tier-2 recursion on the materialised T."""
+    import synth
+    img = synth.batch(4)[0]
+    r, rs = fht.angle_range(dev(img), -15.0, 15.0, pair=True)
+    torch.cuda.synchronize()
+    p = r.plan
+    assert (p.W, p.w_content, p.rows) == (11740, 7644, 4096)
+    op = O.angle_plan(4096, 4096, -15.0, 15.0, k_lo=p.k_lo, k_hi=p.k_hi)
+    want = O.angle_range(img, op)
+    got = r.view[0, 0].cpu().numpy()
+    check(got, want, False)
+    gs = rs.view[0, 0].cpu().numpy()
+    check(gs, O.fhtshift_range(want, op), False)
+    assert np.array_equal(gs, O.fhtshift_range(got, op))
+
+
+@pytest.mark.parametrize("dt", ["f32", "u8"])
+def test_angle_range_steep_colmap_fallback(fht, O, dt):
+    """A steep narrow range on a 2048-row image: [-85, -84.6] deg has g = alpha (-k_lo) ~ 13.4 columns
+    per row, so a 64-row strip's transformed columns span ~860 image columns -- beyond the 512-entry
+    shared-memory colmap slice, the pass-1 loader's global colmap branch. Every cell vs the oracle."""
+    from synth import random_image
+    img = random_image((2048, 40), dt, seed=8584)
+    p = fht.angle_plan(2048, 40, -85.0, -84.6)
+    assert p.alpha >= 1.0 and p.g * 63 > 512
+    r, rs = fht.angle_range(dev(img), -85.0, -84.6, pair=True)
+    torch.cuda.synchronize()
+    op = O.angle_plan(2048, 40, -85.0, -84.6, k_lo=p.k_lo, k_hi=p.k_hi)
+    assert (op.W, op.w_content) == (p.W, p.w_content)
+    want = O.angle_range(img, op)
+    got = r.view[0, 0].cpu().numpy()
+    check(got, want, dt != "f32")
+    assert np.array_equal(rs.view[0, 0].cpu().numpy(), O.fhtshift_range(got, op))
+
+
+@pytest.mark.parametrize("shape", [(3, 5), (64, 64), (100, 37), (300, 700), (257, 255), (1024, 64)], ids=str)
+def test_i32_signed_large_values(fht, O, shape):
+    """int32 input with negative and large values (|v| <= (2^31 - 1) / P, so every sum fits int32):
+    quadrants and the full transform, bit-exact against the int64 oracle."""
+    from synth import random_image
+    P = max(O.full_padding(*shape))
+    img = random_image(shape, "i32w", seed=shape[0] * 3 + shape[1], bound=(2 ** 31 - 1) // P)
+    assert img.min() < -(2 ** 20) // P and img.max() > (2 ** 20) // P
+    t = dev(img)
+    for q in range(4):
+        h, s = fht.quadrant(t, q, pair=True)
+        torch.cuda.synchronize()
+        want = O.hough_recursive(img, q)
+        got = h.view[0, 0].cpu().numpy()
+        check(got, want, True)
+        assert np.array_equal(s.view[0, 0].cpu().numpy(), O.fhtshift_quadrant(got, O.QUADRANT_FRAME[q][1]))
+    hq, sq = fht.full(t, pair=True)
+    torch.cuda.synchronize()
+    quads = O.full_quadrants(img)
+    for q in range(4):
+        n = quads[q].shape[0]
+        check(hq.view[0, q, :n].cpu().numpy(), quads[q], True)
+        check(sq.view[0, q, :n].cpu().numpy(), O.fhtshift_quadrant(quads[q], O.QUADRANT_FRAME[q][1]), True)
