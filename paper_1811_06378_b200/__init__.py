@@ -211,13 +211,15 @@ def angle_range(t: torch.Tensor, theta_min, theta_max: float | None = None, shif
     itself; `angle_range(t, plan)` calls fht_angle_range_plan with a prepared plan (pruned or
     mostly-horizontal plans). See quadrant() for shifted / pair."""
     img, t = _image(t)
-    if isinstance(theta_min, FhtAnglePlan):
-        plan, by_angles = theta_min, False
-    else:
-        plan, by_angles = angle_plan(int(img.h), int(img.w), float(theta_min), float(theta_max)), True
+    by_angles = not isinstance(theta_min, FhtAnglePlan)
+    plan = None if by_angles else theta_min
+    need_out = ((pair or not shifted) and out is None) or ((pair or shifted) and out_shifted is None)
+    if by_angles and need_out:  # the plan only describes outputs the caller did not pass
+        plan = angle_plan(int(img.h), int(img.w), float(theta_min), float(theta_max))
     res = _descs(FHT_MODE_RANGE, img, plan, 0, 0, t.device, shifted, pair, out, out_shifted)
     if by_angles:
-        ws_n = int(_lib.lib.fht_angle_range_workspace_bytes(ctypes.byref(img), float(theta_min), float(theta_max)))
+        ws_n = (workspace.numel() * workspace.element_size() if workspace is not None else
+                int(_lib.lib.fht_angle_range_workspace_bytes(ctypes.byref(img), float(theta_min), float(theta_max))))
         ws = _workspace(ws_n, t.device, workspace)
         n = _lib.check("fht_angle_range", _lib.lib.fht_angle_range(
             ctypes.byref(img), float(theta_min), float(theta_max), _ptr(res[0]), _ptr(res[1]), ws.data_ptr(), ws_n,

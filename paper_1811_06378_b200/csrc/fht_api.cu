@@ -907,11 +907,9 @@ int plan_make(int64_t h, int64_t w, double tmin, double tmax, bool pruned, fht_a
   //   mn_k[b][t] = min(mn_{k-1}[2b][t>>1], mn_{k-1}[2b+1][t>>1] - ceil(t/2))   (mx likewise),
   // Hp log2 Hp steps instead of Hp * h (a plan costs microseconds, so fht_angle_range can build it per call).
   int e_min = 1 << 30, e_max = -(1 << 30);
-  const int64_t kInf = int64_t(1) << 40;
-  int64_t* mn = new int64_t[Hp];
-  int64_t* mx = new int64_t[Hp];
-  int64_t* mn2 = new int64_t[Hp];
-  int64_t* mx2 = new int64_t[Hp];
+  constexpr int kInf = 1 << 29;  // neutral element (padding rows); |e_y|, D < 2^28 keep it apart
+  int* buf = new int[4 * Hp];
+  int *mn = buf, *mx = buf + Hp, *mn2 = buf + 2 * Hp, *mx2 = buf + 3 * Hp;
   for (int64_t y = 0; y < Hp; ++y) {
     if (y < h) {
       const int e = plan_e(g, y);
@@ -924,23 +922,21 @@ int plan_make(int64_t h, int64_t w, double tmin, double tmax, bool pruned, fht_a
     }
   }
   for (int64_t half = 1; half < Hp; half <<= 1) {  // level: blocks of 2*half rows, shifts t < 2*half
-    for (int64_t b = 0; b < Hp / (2 * half); ++b)
+    for (int64_t b = 0; b < Hp; b += 2 * half)
       for (int64_t t = 0; t < 2 * half; ++t) {
-        const int64_t top = (2 * b) * half + (t >> 1), bot = (2 * b + 1) * half + (t >> 1), c = (t + 1) >> 1;
-        const int64_t lo_b = mn[bot] == kInf ? kInf : mn[bot] - c, hi_b = mx[bot] == -kInf ? -kInf : mx[bot] - c;
-        mn2[b * 2 * half + t] = mn[top] < lo_b ? mn[top] : lo_b;
-        mx2[b * 2 * half + t] = mx[top] > hi_b ? mx[top] : hi_b;
+        const int64_t top = b + (t >> 1), bot = top + half;
+        const int c = (int)((t + 1) >> 1);
+        const int lo = mn[bot] - c, hi = mx[bot] - c;
+        mn2[b + t] = mn[top] < lo ? mn[top] : lo;
+        mx2[b + t] = mx[top] > hi ? mx[top] : hi;
       }
     std::swap(mn, mn2);
     std::swap(mx, mx2);
   }
   int64_t spread_max = 0;
   for (int64_t s = 0; s < rows; ++s)
-    if (mx[s] - mn[s] > spread_max) spread_max = mx[s] - mn[s];
-  delete[] mn;
-  delete[] mx;
-  delete[] mn2;
-  delete[] mx2;
+    if ((int64_t)mx[s] - mn[s] > spread_max) spread_max = (int64_t)mx[s] - mn[s];
+  delete[] buf;
   fht_angle_plan_t p{};
   p.theta_min_deg = tmin;
   p.theta_max_deg = tmax;
