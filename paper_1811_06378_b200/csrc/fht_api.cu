@@ -21,11 +21,13 @@
 #include "../../include/fht.h"
 #include "fht_kernels.cuh"
 #include "fht_tile.cuh"
+#include "fht_internal.cuh"
 #include "fht_peaks.cuh"
 
 namespace {
 
 using namespace fht;
+using namespace fht::detail;
 
 // Pass-1 scratch bytes per batch chunk. Measured (profiles/r01_v2/ab_scratch_budget*.log): fewer, fuller
 // launches beat keeping a chunk's scratch L2-resident -- C5 1528 us at 48 MiB (1 image per chunk),
@@ -213,6 +215,46 @@ ScratchPlan scratch_plan(const Frame& f, int nq, int64_t batch, const RangeDev* 
   return sp;
 }
 
+// ---------------------------------------------------------------- pipelined passes (fht_pipe.cuh)
+// One persistent kernel for both passes over units of (nbu images, one slot), NBUF ring buffers of
+// scratch (L2-resident), pass 1 of unit u + D beside pass 2 of unit u. Used for non-range v2 frames
+// with Hp in [256, 4096] and at least two units; FHT_PIPE=1 opts in (measured slower than the two-launch path: DESIGN.md §5).
+bool pipe_split_ok(int m, int L) {
+  return (m == 4 && L == 4) || (m == 4 && L == 5) || (m == 5 && L == 5) || (m == 6 && L == 5) || (m == 6 && L == 6);
+}
+struct PipePlan {
+  int on;
+  int nbu, D, NBUF, nunits;
+  int64_t pitch;
+  size_t scratch_bytes;  // ring (256-byte rounded); the counters follow
+  size_t bytes;          // ring + counters
+};
+PipePlan pipe_plan(const Frame& f, int nq, int64_t batch, const RangeDev* rg, int es) {
+  PipePlan pp{};
+  if (rg || !use_v2(f, rg) || !pipe_split_ok(f.m, f.L) || env_int("FHT_PIPE", 0) == 0) return pp;  // opt-in (measured slower)
+  pp.pitch = v2_scratch_pitch(f, rg, es);
+  const size_t per = (size_t)f.Hp * (size_t)pp.pitch * es;  // one image, one slot
+  const size_t target = (size_t)env_int("FHT_PIPE_UNIT_MB", 16) << 20;
+  int64_t nbu = (int64_t)(target / per);
+  if (nbu < 1) nbu = 1;
+  if (nbu > batch) nbu = batch;
+  while (batch % nbu) --nbu;  // units of equal size
+  const int64_t nunits = (batch / nbu) * nq;
+  if (nunits < 2 || nunits > (1 << 20)) return pp;
+  pp.nbu = (int)nbu;
+  pp.nunits = (int)nunits;
+  pp.D = env_int("FHT_PIPE_D", 2);
+  if (pp.D < 1) pp.D = 1;
+  if (pp.D > pp.nunits) pp.D = pp.nunits;
+  pp.NBUF = env_int("FHT_PIPE_NBUF", pp.D + 2);
+  if (pp.NBUF < pp.D + 1) pp.NBUF = pp.D + 1;
+  if (pp.NBUF > pp.nunits) pp.NBUF = pp.nunits;
+  pp.scratch_bytes = ((size_t)pp.NBUF * nbu * per + 255) & ~size_t(255);
+  pp.bytes = pp.scratch_bytes + (size_t)(1 + 2 * nunits) * sizeof(int);
+  pp.on = 1;
+  return pp;
+}
+
 // ---------------------------------------------------------------- TMA tensor maps
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = []() -> PFN_cuTensorMapEncodeTiled_v12000 {
@@ -240,22 +282,6 @@ bool make_row_map(CUtensorMap* m, const void* base, bool f32, uint64_t cols, uin
   return fn(m, dt, 2, const_cast<void*>(base), dims,
             strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
             CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
-// ---------------------------------------------------------------- dynamic shared memory opt-in
-// cudaFuncAttributeMaxDynamicSharedMemorySize is a per-device (per-context) attribute: `done` (one
-// per kernel instantiation) records, one bit per device ordinal, where it has been set, so a
-// process that drives several GPUs opts in on each of them (a pure cache of device state).
-template <typename K>
-cudaError_t smem_optin(K kern, size_t bytes, std::atomic<unsigned long long>& done) {
-  int dev = 0;
-  cudaError_t e = cudaGetDevice(&dev);
-  if (e != cudaSuccess) return e;
-  const unsigned long long bit = 1ull << (dev & 63);
-  if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
-  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-  if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
-  return e;
 }
 
 // ---------------------------------------------------------------- v1 launch helpers
@@ -311,23 +337,6 @@ cudaError_t launch_pass2(int logr, dim3 grid, const Pass2Args& a, cudaStream_t s
 }
 
 // ---------------------------------------------------------------- v2 launch helpers
-// Launch with programmatic stream serialization (PDL): the kernel may be scheduled while its
-// predecessor in the stream drains; it calls griddepcontrol.wait before touching memory.
-template <typename... KArgs, typename... Args>
-cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
-                       Args&&... args) {
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = grid;
-  cfg.blockDim = block;
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = FHT_PDL;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
-}
 struct P1Maps {
   CUtensorMap img0, img1, scr;
 };
@@ -428,7 +437,9 @@ int run_orientation(const fht_image* img, const Frame& f, const Slot* slots, int
                     size_t ws_bytes, cudaStream_t st, const RangeDev* rg, LaunchLog& log) {
   const int ses = scratch_es(img->dtype);
   const ScratchPlan sp = scratch_plan(f, nq, img->batch, rg, ses);
-  if (!ws || ws_bytes < sp.bytes) return FHT_ERR_WORKSPACE;
+  const PipePlan pq = pipe_plan(f, nq, img->batch, rg, ses);
+  const bool pipe = pq.on && ws && ws_bytes >= pq.bytes;
+  if (!ws || (ws_bytes < sp.bytes && !pipe)) return FHT_ERR_WORKSPACE;
   int launches = 0;
   const fht_hough* any = outs.d[0] ? outs.d[0] : outs.d[1];
 
@@ -554,7 +565,7 @@ int run_orientation(const fht_image* img, const Frame& f, const Slot* slots, int
     if (p2.ndest == 1) m2.out1 = m2.out0;
     if (!outs.d[0]) m2.out0_box = m2.out0;
     const bool f32 = img->dtype == FHT_F32;
-    const uint64_t scr_rows = (uint64_t)sp.nbuf * sp.chunk * p1.scratch_img_rows;
+    const uint64_t scr_rows = pipe ? (uint64_t)pq.NBUF * pq.nbu * f.Hp : (uint64_t)sp.nbuf * sp.chunk * p1.scratch_img_rows;
     P1Maps m1;
     {  // pass-1 stores: scratch as [z*2^m + j][strip][column], one box {TX, 1, 2^m} per tile
       auto fn = encode_fn();
@@ -581,6 +592,39 @@ int run_orientation(const fht_image* img, const Frame& f, const Slot* slots, int
         !make_row_map(&m2.scr1, ws, f32, (uint64_t)span1, scr_rows, (uint64_t)sp.pitch, ses == 2 ? 40 : 36, 1,
                       ses == 2))
       return FHT_ERR_CUDA;
+
+    if (pipe) {  // both passes in one persistent launch (fht_pipe.cuh)
+      p1.ntiles = ntile1;
+      p2.ntiles = ntile2;
+      p2.m = f.m;
+      p2.ngroups = ngroups;
+      v2::PipeParams pp{};
+      pp.nunits = pq.nunits;
+      pp.nq = nq;
+      pp.nbu = pq.nbu;
+      pp.D = pq.D;
+      pp.NBUF = pq.NBUF;
+      pp.nstrips = nstrips;
+      pp.ntiles1 = ntile1;
+      pp.ngroups = ngroups;
+      pp.ntiles2 = ntile2;
+      pp.L = f.L;
+      pp.buf_rows = (int64_t)pq.nbu * f.Hp;
+      pp.counters = reinterpret_cast<int*>(static_cast<char*>(ws) + pq.scratch_bytes);
+      if (const char* tp = std::getenv("FHT_PIPE_TRACE_PTR")) {  // debug hook: tools/pipe_trace.py
+        pp.trace = reinterpret_cast<unsigned long long*>(std::strtoull(tp, nullptr, 0));
+        pp.trace_n = env_int("FHT_PIPE_TRACE_N", 0);
+      }
+      PipeMaps pm{m1.img0, m1.img1, m1.scr, m2.scr0, m2.scr1, m2.out0, m2.out1, m2.out0_box};
+      log.before(st);
+      if (cudaMemsetAsync(pp.counters, 0, (size_t)(1 + 2 * pq.nunits) * sizeof(int), st) != cudaSuccess)
+        return FHT_ERR_CUDA;
+      if (launch_pipe(img->dtype == FHT_U8 ? 0 : img->dtype == FHT_I32 ? 1 : 2, f.m, f.L, pm, p1, p2, pp, st) !=
+          cudaSuccess)
+        return FHT_ERR_CUDA;
+      log.after(st);
+      return 1;
+    }
 
     // Chunks of the batch; with an auxiliary stream and two scratch buffers, pass 1 of chunk k+1
     // (aux) overlaps pass 2 of chunk k (main): p2(k) waits for p1(k), p1(k+2) for p2(k).
@@ -1063,15 +1107,20 @@ size_t fht_workspace_bytes(int mode, const fht_image* img, const fht_angle_plan_
     return ((sp.bytes + 255) & ~size_t(255)) + range_tables_bytes(plan);
   }
   size_t need = 0;
+  const int es = scratch_es(img->dtype);
   if (mode == FHT_MODE_FULL && next_pow2(img->h) == next_pow2(img->w)) {
     const Frame f = make_frame(img->h, img->w, 0, 1);
-    if (use_v2(f, nullptr)) return scratch_plan(f, 4, img->batch, nullptr, scratch_es(img->dtype)).bytes;  // one 4-slot pass
+    if (use_v2(f, nullptr)) {  // one 4-slot pass (two-launch schedule or the pipelined kernel)
+      const size_t a = scratch_plan(f, 4, img->batch, nullptr, es).bytes, b = pipe_plan(f, 4, img->batch, nullptr, es).bytes;
+      return a > b ? a : b;
+    }
   }
   for (int tr = 0; tr < 2; ++tr) {
     const Frame f = make_frame(img->h, img->w, tr, mode == FHT_MODE_FULL);
     const int nq = mode == FHT_MODE_FULL ? 2 : 1;
-    const ScratchPlan sp = scratch_plan(f, nq, img->batch, nullptr, scratch_es(img->dtype));
-    need = sp.bytes > need ? sp.bytes : need;
+    const size_t a = scratch_plan(f, nq, img->batch, nullptr, es).bytes, b = pipe_plan(f, nq, img->batch, nullptr, es).bytes;
+    need = a > need ? a : need;
+    need = b > need ? b : need;
   }
   return need;
 }
@@ -1211,8 +1260,9 @@ int fht_full(const fht_image* img, int layout, fht_hough* out, fht_hough* out_sh
                          : nullptr;
   const ScratchPlan sp2 = scratch_plan(f0, 2, img->batch, nullptr, scratch_es(img->dtype));
   const size_t half = (sp2.bytes + 255) & ~size_t(255);
-  if (FHT_SPLIT_ORIENT && aux && Hp == Wp && use_v2(f0, nullptr) && sp2.nbuf == 1 && sp2.chunk >= img->batch &&
-      2 * half <= ws_bytes) {
+  const bool pipe4 = Hp == Wp && pipe_plan(f0, 4, img->batch, nullptr, scratch_es(img->dtype)).on;
+  if (FHT_SPLIT_ORIENT && aux && !pipe4 && Hp == Wp && use_v2(f0, nullptr) && sp2.nbuf == 1 &&
+      sp2.chunk >= img->batch && 2 * half <= ws_bytes) {
     cudaEvent_t ev[2] = {nullptr, nullptr};
     auto destroy = [&]() {
       for (cudaEvent_t e : ev)

@@ -86,6 +86,27 @@ __device__ __forceinline__ void pdl_trigger() {
 #endif
 }
 
+// Thread groups: a tile body runs on a group of threads that synchronise among themselves. GrpAll is
+// the whole CTA (__syncthreads); GrpPart<N> is N threads from `base` (a multiple of 32) with their
+// own named barrier, so one CTA can run two independent tiles side by side (the pipelined kernel).
+struct GrpAll {
+  __device__ __forceinline__ int tid() const { return (int)threadIdx.x; }
+  __device__ __forceinline__ void sync() const { __syncthreads(); }
+  __device__ __forceinline__ bool sync_or(bool v) const { return __syncthreads_or(v) != 0; }
+};
+template <int N>
+struct GrpPart {
+  int base, bar;  // first thread; named barrier id (1..15; 0 is __syncthreads)
+  __device__ __forceinline__ int tid() const { return (int)threadIdx.x - base; }
+  __device__ __forceinline__ void sync() const { asm volatile("bar.sync %0, %1;" ::"r"(bar), "n"(N) : "memory"); }
+  __device__ __forceinline__ bool sync_or(bool v) const {
+    uint32_t r;
+    asm volatile("{ .reg .pred p, q; setp.ne.u32 p, %1, 0; bar.red.or.pred q, %2, %3, p; selp.u32 %0, 1, 0, q; }"
+                 : "=r"(r) : "r"((uint32_t)v), "r"(bar), "n"(N) : "memory");
+    return r != 0;
+  }
+};
+
 constexpr int VA = 9;            // local columns per lane, sub-pass A (odd => conflict-free)
 constexpr int VB = 7;            // local columns per lane, sub-pass B (odd => conflict-free)
 constexpr int WA = 32 * VA;      // 288 local input columns per tile
@@ -189,6 +210,14 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar) {
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
+// wait for the completion of the phase with parity `par` (a barrier reused across tiles alternates)
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t par) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(done) : "r"(smem_u32(bar)), "r"(par) : "memory");
+  }
+}
 __device__ __forceinline__ void mbar_wait0(uint64_t* bar) {
   uint32_t done = 0;
   while (!done) {
@@ -245,13 +274,13 @@ __device__ __forceinline__ void warp_fht(A (&v)[1 << NB][V]) {
 // ------------------------------------------------------------------------------------------
 // The loader fills v[r][q] = input (row blk*2^a + r, x-order index e) for the lane's columns,
 // e = lane*VA + q (SIG = +1) or (WA - 1) - lane*VA - q (SIG = -1).
-template <int R, int SIG, typename A, typename LoadA>
-__device__ __forceinline__ void tile_fht_ld(const LoadA& load, A* fa, int fa_pitch,
+template <int R, int SIG, typename A, typename LoadA, typename G>
+__device__ __forceinline__ void tile_fht_ld(const G& grp, const LoadA& load, A* fa, int fa_pitch,
                                             A (&w)[kTPW<R>][1 << Split<R>::b][VB]) {
   using S = Split<R>;
   constexpr int a = S::a, b = S::b, NW = S::nw;
   constexpr int NA = 1 << a, NBk = 1 << b;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = grp.tid() >> 5, lane = threadIdx.x & 31;
 
   // sub-pass A: block blk = rows blk*2^a .. +2^a-1 -> fa row blk*2^a + j' = F_a[blk][j']
 #pragma unroll 1
@@ -265,7 +294,7 @@ __device__ __forceinline__ void tile_fht_ld(const LoadA& load, A* fa, int fa_pit
 #pragma unroll
       for (int q = 0; q < VA; ++q) d[r * fa_pitch + q] = v[r][q];
   }
-  __syncthreads();
+  grp.sync();
 
   // sub-pass B: group jp: G[i'](c) = F_a[i'][jp](c + jp*i')  (pre-shear identity, local frame)
 #pragma unroll
@@ -281,18 +310,19 @@ __device__ __forceinline__ void tile_fht_ld(const LoadA& load, A* fa, int fa_pit
       warp_fht<b, VB>(w[g]);
     }
   }
-  __syncthreads();
+  grp.sync();
 }
 
 // Input rows from shared memory: element (rho, e) at src[rho*src_pitch + rowoff[rho] + e]; with
 // blk_bars, a block's rows are waited for (TMA) by the warp that reads them.
-template <int R, int SIG, typename A, typename Tsrc>
-__device__ __forceinline__ void tile_fht(const Tsrc* src, int src_pitch, const int* rowoff, A* fa, int fa_pitch,
-                                         A (&w)[kTPW<R>][1 << Split<R>::b][VB], uint64_t* blk_bars = nullptr) {
+template <int R, int SIG, typename A, typename Tsrc, typename G>
+__device__ __forceinline__ void tile_fht(const G& grp, const Tsrc* src, int src_pitch, const int* rowoff, A* fa,
+                                         int fa_pitch, A (&w)[kTPW<R>][1 << Split<R>::b][VB],
+                                         uint64_t* blk_bars = nullptr, uint32_t par = 0) {
   constexpr int NA = 1 << Split<R>::a;
   const int lane = threadIdx.x & 31;
   auto load = [&](int blk, A (&v)[NA][VA]) {
-    if (blk_bars) mbar_wait0(blk_bars + blk);  // this block's rows have landed (TMA)
+    if (blk_bars) mbar_wait(blk_bars + blk, (par >> blk) & 1u);  // this block's rows have landed (TMA)
 #pragma unroll
     for (int r = 0; r < NA; ++r) {
       const int rho = blk * NA + r;
@@ -301,7 +331,7 @@ __device__ __forceinline__ void tile_fht(const Tsrc* src, int src_pitch, const i
       for (int q = 0; q < VA; ++q) v[r][q] = static_cast<A>(p[SIG > 0 ? q : -q]);
     }
   };
-  tile_fht_ld<R, SIG, A>(load, fa, fa_pitch, w);
+  tile_fht_ld<R, SIG, A>(grp, load, fa, fa_pitch, w);
 }
 
 // Sg: the staged element type (A, or uint16_t for the u8 pipeline's pass-1 scratch)
@@ -325,12 +355,12 @@ __device__ __forceinline__ void st_pred_row(uint32_t a, int lo, int box, const A
 // Write the register results into a staging plane of row pitch `pitch`: output row tau, window
 // index s stored at s - soff[tau] when 0 <= that < box. Explicitly predicated st.shared (one
 // ISETP + one STS per element, no branches). Then fence for the TMA engine and synchronise.
-template <int R, int SIG, typename A, typename Sg = A>
-__device__ __forceinline__ void stage_rows(A (&w)[kTPW<R>][1 << Split<R>::b][VB], Sg* stg, const int* soff, int box,
-                                           int pitch) {
+template <int R, int SIG, typename A, typename Sg = A, typename G = GrpAll>
+__device__ __forceinline__ void stage_rows(const G& grp, A (&w)[kTPW<R>][1 << Split<R>::b][VB], Sg* stg,
+                                           const int* soff, int box, int pitch) {
   using S = Split<R>;
   constexpr int NA = 1 << S::a, NBk = 1 << S::b, NW = S::nw;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = grp.tid() >> 5, lane = threadIdx.x & 31;
 #pragma unroll
   for (int g = 0; g < kTPW<R>; ++g) {
     const int jp = warp + g * NW;
@@ -354,7 +384,7 @@ __device__ __forceinline__ void stage_rows(A (&w)[kTPW<R>][1 << Split<R>::b][VB]
     }
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  __syncthreads();
+  grp.sync();
 }
 
 // ------------------------------------------------------------------------------------------
@@ -406,17 +436,17 @@ constexpr int kNoRow = -2147483647 - 1;  // range fill: the row has no content i
 // FILL = 1 (§4 range loader, sigma = +1): tsrc holds, per row rho, the image row y0 + rho from
 // column rowoff[rho] on (TMA); the transformed row T(x', y) = I[y][colmap[x' - e_y]] (P:146,
 // P:152) is gathered from it through colmap, e_y = erow[rho].
-template <typename Tin, int R, int SIG, typename Tsrc, int FILL = 0>
-__device__ __noinline__ void p1_tail(const CUtensorMap* tm_scr, const P1Params& p, const P1Slot& sl, int img,
-                                     int strip, int X, const Tsrc* tsrc, int tpitch, int fa_pitch, bool bars) {
+// zscr: the scratch z (= buffer image x slot) the tile's F_m rows go to; smem: the group's shared memory.
+template <typename Tin, int R, int SIG, typename Tsrc, int FILL = 0, typename G>
+__device__ __forceinline__ void p1_tail_impl(const G grp, unsigned char* smem, const CUtensorMap* tm_scr, const P1Params& p,
+                                     const P1Slot& sl, int strip, int X, int zscr, const Tsrc* tsrc, int tpitch,
+                                     int fa_pitch, uint64_t* bars, uint32_t par) {
   using A = typename AccOf<Tin>::type;
   using S = Split<R>;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  A* buf = reinterpret_cast<A*>(smem_raw);
-  unsigned char* tab = smem_raw + main_buf_bytes(R) + (sizeof(Tin) == 1 ? u8_tile_bytes(R) : 0);
+  A* buf = reinterpret_cast<A*>(smem);
+  unsigned char* tab = smem + main_buf_bytes(R) + (sizeof(Tin) == 1 ? u8_tile_bytes(R) : 0);
   const int* rowoff = reinterpret_cast<const int*>(tab);
   const int* soff = rowoff + 64;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(tab + 768);
   A w[kTPW<R>][1 << S::b][VB];
   if constexpr (FILL == 1) {
     constexpr int NA = 1 << S::a;
@@ -425,7 +455,7 @@ __device__ __noinline__ void p1_tail(const CUtensorMap* tm_scr, const P1Params& 
     const int cm_lo = reinterpret_cast<const int*>(tab)[224], cm_n = reinterpret_cast<const int*>(tab)[225];
     const int lane = threadIdx.x & 31;
     auto load = [&](int blk, A (&v)[NA][VA]) {
-      mbar_wait0(bar + blk);
+      mbar_wait(bars + blk, (par >> blk) & 1u);
       if (cm_n <= kColmapStage) {  // every u of the strip is inside the staged slice
 #pragma unroll
         for (int r = 0; r < NA; ++r) {
@@ -456,54 +486,79 @@ __device__ __noinline__ void p1_tail(const CUtensorMap* tm_scr, const P1Params& 
         }
       }
     };
-    tile_fht_ld<R, SIG, A>(load, buf, fa_pitch, w);
+    tile_fht_ld<R, SIG, A>(grp, load, buf, fa_pitch, w);
   } else {
-    tile_fht<R, SIG, A>(tsrc, tpitch, rowoff, buf, fa_pitch, w, bars ? bar : nullptr);
+    tile_fht<R, SIG, A>(grp, tsrc, tpitch, rowoff, buf, fa_pitch, w, bars, par);
   }
   // dense [NR][TX] in the scratch type (u8 input: uint16), the box layout
   using Sc = typename ScrOf<Tin>::type;
-  stage_rows<R, SIG, A, Sc>(w, reinterpret_cast<Sc*>(buf), soff, p.TX, p.TX);
+  stage_rows<R, SIG, A, Sc>(grp, w, reinterpret_cast<Sc*>(buf), soff, p.TX, p.TX);
   // ---- store F_m[strip][j] for all j in ONE box {TX, 1, NR} of the 3-D scratch view
   // [z*2^m + j][strip][column] (z = image-in-chunk * nq + slot); column X - xlo is 16-B aligned
-  if (threadIdx.x == 0) {
-    const int z = p.z0 + (img - p.img0) * p.nq + (int)(sl.srow0 >> (R + p.L));
+  if (grp.tid() == 0) {
 #if FHT_SCR_KEEP
-    tma_store_3d_keep(tm_scr, buf, X - sl.xlo, strip, z << R);
+    tma_store_3d_keep(tm_scr, buf, X - sl.xlo, strip, zscr << R);
 #else
-    tma_store_3d(tm_scr, buf, X - sl.xlo, strip, z << R);
+    tma_store_3d(tm_scr, buf, X - sl.xlo, strip, zscr << R);
 #endif
     tma_commit();
   }
   pdl_trigger();
-  if (threadIdx.x == 0) tma_wait_read();
+  if (grp.tid() == 0) tma_wait_read();
 }
 
-template <typename Tin, int R, typename Tsrc, int FILL = 0>
-__device__ __forceinline__ void p1_tail_sig(int sigma, const CUtensorMap* tm_scr, const P1Params& p, const P1Slot& sl,
-                                            int img, int strip, int X, const Tsrc* tsrc, int tpitch, int fa_pitch,
-                                            bool bars = false) {
-  if constexpr (FILL == 1) {  // the range frame is sigma = +1 only
-    p1_tail<Tin, R, 1, Tsrc, 1>(tm_scr, p, sl, img, strip, X, tsrc, tpitch, fa_pitch, true);
+// The tail behind a call boundary in k_p1 (one instance per sign: the kernel's code stays inside the
+// instruction cache); inlined (INL) where a caller keeps state across it (the pipelined kernel).
+template <typename Tin, int R, int SIG, typename Tsrc, int FILL = 0, typename G>
+__device__ __noinline__ void p1_tail(const G grp, unsigned char* smem, const CUtensorMap* tm_scr, const P1Params& p,
+                                     const P1Slot& sl, int strip, int X, int zscr, const Tsrc* tsrc, int tpitch,
+                                     int fa_pitch, uint64_t* bars, uint32_t par) {
+  p1_tail_impl<Tin, R, SIG, Tsrc, FILL>(grp, smem, tm_scr, p, sl, strip, X, zscr, tsrc, tpitch, fa_pitch, bars, par);
+}
+
+template <typename Tin, int R, typename Tsrc, int FILL = 0, bool INL = false, typename G>
+__device__ __forceinline__ void p1_tail_sig(const G& grp, unsigned char* smem, int sigma, const CUtensorMap* tm_scr,
+                                            const P1Params& p, const P1Slot& sl, int strip, int X, int zscr,
+                                            const Tsrc* tsrc, int tpitch, int fa_pitch, uint64_t* bars = nullptr,
+                                            uint32_t par = 0) {
+  if constexpr (INL) {
+    if constexpr (FILL == 1) {
+      p1_tail_impl<Tin, R, 1, Tsrc, 1>(grp, smem, tm_scr, p, sl, strip, X, zscr, tsrc, tpitch, fa_pitch, bars, par);
+    } else {
+      if (sigma > 0)
+        p1_tail_impl<Tin, R, 1, Tsrc, 0>(grp, smem, tm_scr, p, sl, strip, X, zscr, tsrc, tpitch, fa_pitch, bars, par);
+      else
+        p1_tail_impl<Tin, R, -1, Tsrc, 0>(grp, smem, tm_scr, p, sl, strip, X, zscr, tsrc, tpitch, fa_pitch, bars, par);
+    }
+  } else if constexpr (FILL == 1) {  // the range frame is sigma = +1 only
+    p1_tail<Tin, R, 1, Tsrc, 1>(grp, smem, tm_scr, p, sl, strip, X, zscr, tsrc, tpitch, fa_pitch, bars, par);
   } else {
-    if (sigma > 0) p1_tail<Tin, R, 1>(tm_scr, p, sl, img, strip, X, tsrc, tpitch, fa_pitch, bars);
-    else p1_tail<Tin, R, -1>(tm_scr, p, sl, img, strip, X, tsrc, tpitch, fa_pitch, bars);
+    if (sigma > 0)
+      p1_tail<Tin, R, 1, Tsrc, 0>(grp, smem, tm_scr, p, sl, strip, X, zscr, tsrc, tpitch, fa_pitch, bars, par);
+    else
+      p1_tail<Tin, R, -1, Tsrc, 0>(grp, smem, tm_scr, p, sl, strip, X, zscr, tsrc, tpitch, fa_pitch, bars, par);
   }
 }
 
-template <typename Tin, int R>
-__device__ __forceinline__ void p1_body(const CUtensorMap* tm_img0, const CUtensorMap* tm_img1,
-                                        const CUtensorMap* tm_scr, const P1Params& p, const P1Slot& sl, int img,
-                                        int strip, int X) {
+// Returns whether the tile used its per-block mbarriers (one phase each): the TMA fills. INL: the tail
+// inlined (see p1_tail).
+template <typename Tin, int R, bool INL = false, typename G>
+__device__ __forceinline__ bool p1_body(const G& grp, unsigned char* smem_raw, const CUtensorMap* tm_img0,
+                                        const CUtensorMap* tm_img1, const CUtensorMap* tm_scr, const P1Params& p,
+                                        const P1Slot& sl, int img, int strip, int X, int zscr,
+                                        uint64_t* ext_bars = nullptr, uint32_t par = 0) {
   using A = typename AccOf<Tin>::type;
   using S = Split<R>;
   constexpr int NT = S::nw * 32;
   constexpr int NR = 1 << R;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int tid = grp.tid();
   A* buf = reinterpret_cast<A*>(smem_raw);
   unsigned char* tab = smem_raw + main_buf_bytes(R) + (sizeof(Tin) == 1 ? u8_tile_bytes(R) : 0);
   int* rowoff = reinterpret_cast<int*>(tab);          // [NR]
   int* soff = rowoff + 64;                            // [NR]
-  uint64_t* bar = reinterpret_cast<uint64_t*>(tab + 768);
+  // per-block mbarriers: the tile's own (initialised here, phase 0), or the caller's persistent ones
+  // (initialised once, phase parity `par` bit per block: the pipelined kernel)
+  uint64_t* bar = ext_bars ? ext_bars : reinterpret_cast<uint64_t*>(tab + 768);
   const Tin* src = static_cast<const Tin*>(p.img) + (int64_t)img * p.img_bstride;
   const int y0 = strip * NR;
   const int Xa = sl.sigma > 0 ? X : X - (WA - WC);  // x of input index e = 0
@@ -519,7 +574,7 @@ __device__ __forceinline__ void p1_body(const CUtensorMap* tm_img0, const CUtens
     constexpr int NA = 1 << S::a, NBk = 1 << S::b, NW = S::nw;
     Tin* tile = reinterpret_cast<Tin*>(sizeof(Tin) == 1 ? smem_raw + main_buf_bytes(R) : smem_raw);
     int* erow = soff + 64;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int warp = tid >> 5, lane = threadIdx.x & 31;
     bool any_row = false;  // some row of the tile has transformed content (the warp's blocks)
     for (int b = warp; b < NBk; b += NW) {
       const int rho = b * NA + lane, y = y0 + rho;
@@ -541,7 +596,7 @@ __device__ __forceinline__ void p1_body(const CUtensorMap* tm_img0, const CUtens
       const unsigned m = __ballot_sync(0xffffffffu, ne);
       any_row |= m != 0u;
       if (lane == 0) {
-        mbar_init(bar + b);
+        if (!ext_bars) mbar_init(bar + b);
         mbar_expect_tx(bar + b, (uint32_t)__popc(m) * row_bytes);
       }
       __syncwarp();
@@ -563,30 +618,29 @@ __device__ __forceinline__ void p1_body(const CUtensorMap* tm_img0, const CUtens
         n = max(0, min(p.w_content, Xa + WA - min(ea, eb)) - ulo);
       }
       if (n <= kColmapStage)
-        for (int i = threadIdx.x; i < n; i += NT) cm_s[i] = __ldg(p.colmap + ulo + i);
-      if (threadIdx.x == 0) {
+        for (int i = tid; i < n; i += NT) cm_s[i] = __ldg(p.colmap + ulo + i);
+      if (tid == 0) {
         rowoff[224] = ulo;
         rowoff[225] = n;
       }
-      if (!__syncthreads_or(any_row)) {
+      if (!grp.sync_or(any_row)) {
         // no row of the tile has content (no load was issued): F_m is 0 over the whole tile
         A* z = reinterpret_cast<A*>(smem_raw);
-        for (int idx = threadIdx.x; idx < NR * p.TX; idx += NT) z[idx] = A(0);
+        for (int idx = tid; idx < NR * p.TX; idx += NT) z[idx] = A(0);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncthreads();
-        if (threadIdx.x == 0) {
-          const int zz = p.z0 + (img - p.img0) * p.nq + (int)(sl.srow0 >> (R + p.L));
-          tma_store_3d_keep(tm_scr, z, X - sl.xlo, strip, zz << R);
+        grp.sync();
+        if (tid == 0) {
+          tma_store_3d_keep(tm_scr, z, X - sl.xlo, strip, zscr << R);
           tma_commit();
         }
         pdl_trigger();
-        if (threadIdx.x == 0) tma_wait_read();
-        return;
+        if (tid == 0) tma_wait_read();
+        return true;
       }
     }
-    p1_tail_sig<Tin, R, Tin, 1>(1, tm_scr, p, sl, img, strip, X, static_cast<const Tin*>(tile), TP,
-                                sizeof(Tin) == 1 ? FA_PITCH : TMA_PITCH);
-    return;
+    p1_tail_sig<Tin, R, Tin, 1, INL>(grp, smem_raw, 1, tm_scr, p, sl, strip, X, zscr, static_cast<const Tin*>(tile), TP,
+                                sizeof(Tin) == 1 ? FA_PITCH : TMA_PITCH, bar, par);
+    return true;
   }
   if (!sl.transposed && p.fill_tma) {
     // ---- TMA: NR image rows, columns [Xa, Xa + 288) from the 16-byte aligned column below
@@ -598,10 +652,10 @@ __device__ __forceinline__ void p1_body(const CUtensorMap* tm_img0, const CUtens
 #if FHT_P1_WARPLOAD
     // each warp issues (lane 0) and waits for (in tile_fht) the rows of its own sub-pass-A blocks
     constexpr int NA = 1 << S::a, NBk = 1 << S::b, NW = S::nw;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int warp = tid >> 5, lane = threadIdx.x & 31;
     for (int b = warp; b < NBk; b += NW) {
       if (lane == 0) {
-        mbar_init(bar + b);
+        if (!ext_bars) mbar_init(bar + b);
         mbar_expect_tx(bar + b, NA * row_bytes);
         for (int rho = b * NA; rho < (b + 1) * NA; ++rho) {
           Tin* d = tile + rho * TP;
@@ -615,36 +669,37 @@ __device__ __forceinline__ void p1_body(const CUtensorMap* tm_img0, const CUtens
       }
     }
     __syncwarp();
-    constexpr bool bars = true;
+    uint64_t* const bars = bar;
 #else
-    if (threadIdx.x < NR) {
-      rowoff[threadIdx.x] = Xa - a0;
-      soff[threadIdx.x] = 0;
+    if (tid < NR) {
+      rowoff[tid] = Xa - a0;
+      soff[tid] = 0;
     }
-    if (threadIdx.x == 0) mbar_init(bar);
-    __syncthreads();
-    if (threadIdx.x < 32) {
-      if (threadIdx.x == 0) mbar_expect_tx(bar, NR * row_bytes);
+    if (tid == 0) mbar_init(bar);
+    grp.sync();
+    if (tid < 32) {
+      if (tid == 0) mbar_expect_tx(bar, NR * row_bytes);
       __syncwarp();
-      for (int rho = threadIdx.x; rho < NR; rho += 32) {
+      for (int rho = tid; rho < NR; rho += 32) {
         Tin* d = tile + rho * TP;
         tma_load_3d(tm_img0, d, bar, a0, y0 + rho, img);
         tma_load_3d(tm_img1, d + 256, bar, a0 + 256, y0 + rho, img);
       }
     }
     mbar_wait0(bar);
-    constexpr bool bars = false;
+    uint64_t* const bars = nullptr;
 #endif
     if constexpr (sizeof(Tin) == 1)
-      p1_tail_sig<Tin, R>(sl.sigma, tm_scr, p, sl, img, strip, X, static_cast<const Tin*>(tile), TP, FA_PITCH, bars);
+      p1_tail_sig<Tin, R, Tin, 0, INL>(grp, smem_raw, sl.sigma, tm_scr, p, sl, strip, X, zscr,
+                                       static_cast<const Tin*>(tile), TP, FA_PITCH, bars, par);
     else
-      p1_tail_sig<Tin, R>(sl.sigma, tm_scr, p, sl, img, strip, X, reinterpret_cast<const A*>(tile), TP, TMA_PITCH,
-                          bars);
-    return;
+      p1_tail_sig<Tin, R, A, 0, INL>(grp, smem_raw, sl.sigma, tm_scr, p, sl, strip, X, zscr,
+                                     reinterpret_cast<const A*>(tile), TP, TMA_PITCH, bars, par);
+    return bars != nullptr;
   }
-  if (threadIdx.x < NR) {
-    rowoff[threadIdx.x] = 0;
-    soff[threadIdx.x] = 0;
+  if (tid < NR) {
+    rowoff[tid] = 0;
+    soff[tid] = 0;
   }
   if (!sl.transposed || p.range) {
     // ---- scalar fill (angle-range gather T(x, y) = I[y][colmap[x - e_y]], or odd pitches), in
@@ -661,7 +716,7 @@ __device__ __forceinline__ void p1_body(const CUtensorMap* tm_img0, const CUtens
       A v[CH];
 #pragma unroll
       for (int c = 0; c < CH; ++c) {  // stage 1: colmap (range) or the column index itself
-        const int idx = threadIdx.x + (it0 + c) * NT;
+        const int idx = tid + (it0 + c) * NT;
         const int rho = idx / WA, e = idx - rho * WA;
         const int y = y0 + rho, x = Xa + e;
         cm[c] = -1;
@@ -676,7 +731,7 @@ __device__ __forceinline__ void p1_body(const CUtensorMap* tm_img0, const CUtens
       }
 #pragma unroll
       for (int c = 0; c < CH; ++c) {  // stage 2: the pixels
-        const int idx = threadIdx.x + (it0 + c) * NT;
+        const int idx = tid + (it0 + c) * NT;
         const int rho = idx / WA;
         const int64_t off = sl.transposed ? (int64_t)cm[c] * p.img_rstride + (y0 + rho)
                                           : (int64_t)(y0 + rho) * p.img_rstride + cm[c];
@@ -684,7 +739,7 @@ __device__ __forceinline__ void p1_body(const CUtensorMap* tm_img0, const CUtens
       }
 #pragma unroll
       for (int c = 0; c < CH; ++c) {  // stage 3: shared memory
-        const int idx = threadIdx.x + (it0 + c) * NT;
+        const int idx = tid + (it0 + c) * NT;
         if (it0 + c < ITS && idx < NR * WA) {
           const int rho = idx / WA, e = idx - rho * WA;
           buf[rho * FA_PITCH + e] = v[c];
@@ -702,7 +757,7 @@ __device__ __forceinline__ void p1_body(const CUtensorMap* tm_img0, const CUtens
     V4 vals[IT];
 #pragma unroll
     for (int it = 0; it < IT; ++it) {
-      const int idx = threadIdx.x + it * NT;
+      const int idx = tid + it * NT;
       const int e = idx / YQ, yq = idx - e * YQ;
       const int x = Xa + e, y = y0 + 4 * yq;
       vals[it] = V4{};
@@ -722,7 +777,7 @@ __device__ __forceinline__ void p1_body(const CUtensorMap* tm_img0, const CUtens
     }
 #pragma unroll
     for (int it = 0; it < IT; ++it) {
-      const int idx = threadIdx.x + it * NT;
+      const int idx = tid + it * NT;
       if (idx < WA * YQ) {
         const int e = idx / YQ, yq = idx - e * YQ;
         A* d = buf + (4 * yq) * FA_PITCH + e;
@@ -733,7 +788,7 @@ __device__ __forceinline__ void p1_body(const CUtensorMap* tm_img0, const CUtens
       }
     }
   } else {
-    for (int idx = threadIdx.x; idx < NR * WA; idx += NT) {
+    for (int idx = tid; idx < NR * WA; idx += NT) {
       const int e = idx / NR, rho = idx - e * NR;  // consecutive threads: consecutive image columns
       const int y = y0 + rho, x = Xa + e;
       A v = A(0);
@@ -741,8 +796,10 @@ __device__ __forceinline__ void p1_body(const CUtensorMap* tm_img0, const CUtens
       buf[rho * FA_PITCH + e] = v;
     }
   }
-  __syncthreads();
-  p1_tail_sig<Tin, R>(sl.sigma, tm_scr, p, sl, img, strip, X, static_cast<const A*>(buf), FA_PITCH, FA_PITCH);
+  grp.sync();
+  p1_tail_sig<Tin, R, A, 0, INL>(grp, smem_raw, sl.sigma, tm_scr, p, sl, strip, X, zscr, static_cast<const A*>(buf),
+                                 FA_PITCH, FA_PITCH);
+  return false;
 }
 
 // tm_img0: image [batch][h][w], box 1 x 1 x 256 columns; tm_img1: box 36 (u8: 48) columns;
@@ -764,7 +821,9 @@ k_p1(const __grid_constant__ CUtensorMap tm_img0, const __grid_constant__ CUtens
   const P1Slot& sl = p.slot[qi];
   if (n >= sl.ntiles) return;
   const int X = min(sl.xlo + p.TX * n, sl.xhi - p.TX);  // tile = window start (Xw = X)
-  p1_body<Tin, R>(&tm_img0, &tm_img1, &tm_scr, p, sl, img, strip, X);
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  p1_body<Tin, R>(GrpAll{}, smem_raw, &tm_img0, &tm_img1, &tm_scr, p, sl, img, strip, X,
+                  p.z0 + (img - p.img0) * p.nq + qi);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -815,26 +874,31 @@ struct RowInfo {  // per (destination, output row), shared memory, 16 B
 };
 constexpr int kTmaBit = 1 << 30;
 
-template <typename A, int R, int SIG, typename Tscr>
-__device__ __forceinline__ void p2_body(const CUtensorMap* tm_scr0, const CUtensorMap* tm_scr1,
-                                        const CUtensorMap* tm0, const CUtensorMap* tm1, const CUtensorMap* tm0_box,
-                                        const P2Params& p, const P2Slot& sl, int img, int j, int X, int own) {
+// rbase: the scratch row of (group j, strip 0); strip i is row rbase + i. smem: the group's shared memory.
+// Returns whether the tile used its per-block mbarriers (every tile but a black one).
+template <typename A, int R, int SIG, typename Tscr, typename G>
+__device__ __forceinline__ bool p2_body(const G& grp, unsigned char* smem_raw, const CUtensorMap* tm_scr0,
+                                        const CUtensorMap* tm_scr1, const CUtensorMap* tm0, const CUtensorMap* tm1,
+                                        const CUtensorMap* tm0_box, const P2Params& p, const P2Slot& sl, int img,
+                                        int j, int X, int own, int64_t rbase, uint64_t* ext_bars = nullptr,
+                                        uint32_t par = 0) {
   using S = Split<R>;
   constexpr int NW = S::nw;
   constexpr int NT = NW * 32;
   constexpr int NR = 1 << R;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int tid = grp.tid();
   A* buf = reinterpret_cast<A*>(smem_raw);
   unsigned char* tab = smem_raw + main_buf_bytes(R);
   int* rowoff = reinterpret_cast<int*>(tab);                  // [64]
   int* soff = rowoff + 64;                                    // [2][64]
-  uint64_t* bar = reinterpret_cast<uint64_t*>(tab + 768);     // [8] per-block mbarriers
+  // [8] per-block mbarriers: the tile's own, or the caller's persistent ones (parity bits `par`)
+  uint64_t* bar = ext_bars ? ext_bars : reinterpret_cast<uint64_t*>(tab + 768);
   RowInfo* info = reinterpret_cast<RowInfo*>(tab + 1024);     // [2][NR], 16 B each
   const int TX = p.TX, box = TX + WO2;
   const int Xw = X - WO2;                        // window start: window index s <-> x = Xw + s
   const int Xa = SIG > 0 ? Xw : Xw - (WA - WC);  // x of input index e = 0
   const int t0 = j * NR, tmax = t0 + NR - 1;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = tid >> 5, lane = threadIdx.x & 31;
   A w[kTPW<R>][1 << S::b][VB];
 
   bool black = false;  // the whole window is outside every row's pattern support
@@ -849,14 +913,13 @@ __device__ __forceinline__ void p2_body(const CUtensorMap* tm_scr0, const CUtens
   // warp + NW, ...: no CTA-wide barrier between the issue and the butterflies, and the four warps
   // issue in parallel. rowoff of a block's rows is written by the warp that reads them.
   if (!black) {
-    const int64_t rbase = p.row0 + (int64_t)(img - p.img0) * p.scratch_img_rows + sl.srow0 + t0;
     // scratch rows of Tscr: loads start at the 16-byte aligned column below (kAl elements) and
     // take 256 + kBox1 columns (kBox1 * sizeof(Tscr) a multiple of 16); row i lands at byte
     // i * TMA_PITCH * 4 of the buffer, where its fa row will be written in place
     constexpr int kAl = 16 / (int)sizeof(Tscr), kBox1 = sizeof(Tscr) == 2 ? 40 : 36;
     for (int b = warp; b < NBk; b += NW) {
       if (lane == 0) {
-        mbar_init(bar + b);
+        if (!ext_bars) mbar_init(bar + b);
         mbar_expect_tx(bar + b, NA * (256 + kBox1) * (uint32_t)sizeof(Tscr));
         for (int i = b * NA; i < (b + 1) * NA; ++i) {
           const int a0 = (Xa + SIG * j * i - sl.xlo1) & ~(kAl - 1);
@@ -870,9 +933,8 @@ __device__ __forceinline__ void p2_body(const CUtensorMap* tm_scr0, const CUtens
     __syncwarp();
   }
 #else
-  if (!black && threadIdx.x == 0) {
+  if (!black && tid == 0) {
     for (int b = 0; b < NBk; ++b) mbar_init(bar + b);
-    const int64_t rbase = p.row0 + (int64_t)(img - p.img0) * p.scratch_img_rows + sl.srow0 + t0;
     for (int b = 0; b < NBk; ++b) {
       mbar_expect_tx(bar + b, NA * (256 + 36) * 4);
       for (int i = b * NA; i < (b + 1) * NA; ++i) {
@@ -886,7 +948,7 @@ __device__ __forceinline__ void p2_body(const CUtensorMap* tm_scr0, const CUtens
 #endif
 
   // ---- store plan per (destination, row): shift k, 16-byte aligned start, TMA or plain stores
-  for (int it = threadIdx.x; it < p.ndest * NR; it += NT) {
+  for (int it = tid; it < p.ndest * NR; it += NT) {
     const int d = it / NR, tau = it - d * NR, t = t0 + tau;
     const P2Dest& D = p.dest[d];
     int vlo = sl.xbeg, vhi = sl.xend, k = 0;
@@ -924,16 +986,16 @@ __device__ __forceinline__ void p2_body(const CUtensorMap* tm_scr0, const CUtens
     soff[d * 64 + tau] = WO2 - r;
   }
 #if FHT_P2_WARPLOAD
-  // the plan (info, soff) is read after tile_fht's first __syncthreads; a black tile has none
-  if (black) __syncthreads();
+  // the plan (info, soff) is read after tile_fht's first group barrier; a black tile has none
+  if (black) grp.sync();
 #else
-  if (!black && threadIdx.x < NR) rowoff[threadIdx.x] = (Xa + SIG * j * (int)threadIdx.x - sl.xlo1) & 3;
-  __syncthreads();
+  if (!black && tid < NR) rowoff[tid] = (Xa + SIG * j * tid - sl.xlo1) & 3;
+  grp.sync();
 #endif
 
   if (!black)
-    tile_fht<R, SIG, A>(reinterpret_cast<const Tscr*>(buf), TMA_PITCH * 4 / (int)sizeof(Tscr), rowoff, buf, TMA_PITCH,
-                        w, bar);
+    tile_fht<R, SIG, A>(grp, reinterpret_cast<const Tscr*>(buf), TMA_PITCH * 4 / (int)sizeof(Tscr), rowoff, buf,
+                        TMA_PITCH, w, bar, par);
 
   // ---- stores, one destination at a time (the staging plane is reused)
   bool issued = false;
@@ -944,7 +1006,7 @@ __device__ __forceinline__ void p2_body(const CUtensorMap* tm_scr0, const CUtens
     const int* so = soff + d * 64;
     if (dd > 0) {
       if (issued) tma_wait_read();
-      __syncthreads();
+      grp.sync();
     }
     // plain destination of an interior QUADS tile: every row has the same aligned start and no
     // remainder, rows ascend -> ONE 2-D box {box, NR} from a dense [NR][box] staging plane
@@ -953,22 +1015,22 @@ __device__ __forceinline__ void p2_body(const CUtensorMap* tm_scr0, const CUtens
                        (inf[0].d0 & kTmaBit) && inf[0].mlo >= inf[0].mhi;
     const int pitch = dense ? box : ST_PITCH;
     if (!black) {
-      stage_rows<R, SIG, A>(w, buf, so, pitch, pitch);  // every computed column that fits the row
+      stage_rows<R, SIG, A>(grp, w, buf, so, pitch, pitch);  // every computed column that fits the row
     } else {  // every output of a black tile is 0 (no pattern touches a pixel)
-      for (int idx = threadIdx.x; idx < NR * pitch; idx += NT) buf[idx] = A(0);
+      for (int idx = tid; idx < NR * pitch; idx += NT) buf[idx] = A(0);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      __syncthreads();
+      grp.sync();
     }
     if (dense) {
-      if (threadIdx.x == 0) {
+      if (tid == 0) {
         tma_store_row_stream(tm0_box, buf, inf[0].d0 & ~kTmaBit, inf[0].orow);  // box {box, NR}
         tma_commit();
         issued = true;
       }
     } else {
-      if (threadIdx.x < NR && (inf[threadIdx.x].d0 & kTmaBit)) {  // one row store per thread
-        const RowInfo ri = inf[threadIdx.x];
-        tma_store_row_stream(d == 0 ? tm0 : tm1, buf + threadIdx.x * ST_PITCH, ri.d0 & ~kTmaBit, ri.orow);  // clipped at W
+      if (tid < NR && (inf[tid].d0 & kTmaBit)) {  // one row store per thread
+        const RowInfo ri = inf[tid];
+        tma_store_row_stream(d == 0 ? tm0 : tm1, buf + tid * ST_PITCH, ri.d0 & ~kTmaBit, ri.orow);  // clipped at W
         tma_commit();
         issued = true;
       }
@@ -988,6 +1050,7 @@ __device__ __forceinline__ void p2_body(const CUtensorMap* tm_scr0, const CUtens
   }
   pdl_trigger();
   if (issued) tma_wait_read();
+  return !black;
 }
 
 // tm_scr0: scratch, one row x 256 columns; tm_scr1: one row x 36 columns; tm0 / tm1: destinations
@@ -1029,8 +1092,12 @@ k_p2(const __grid_constant__ CUtensorMap tm_scr0, const __grid_constant__ CUtens
   }
   const int X = k + 1 < nk ? lo + p.TX * k : max(lo, hi - (p.TX + WO2));
   const int own = k + 1 < nk ? p.TX : hi - X;
-  if (sl.sigma > 0) p2_body<A, R, 1, Tscr>(&tm_scr0, &tm_scr1, &tm0, &tm1, &tm0_box, p, sl, img, j, X, own);
-  else p2_body<A, R, -1, Tscr>(&tm_scr0, &tm_scr1, &tm0, &tm1, &tm0_box, p, sl, img, j, X, own);
+  const int64_t rbase = p.row0 + (int64_t)(img - p.img0) * p.scratch_img_rows + sl.srow0 + ((int64_t)j << R);
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  if (sl.sigma > 0)
+    p2_body<A, R, 1, Tscr>(GrpAll{}, smem_raw, &tm_scr0, &tm_scr1, &tm0, &tm1, &tm0_box, p, sl, img, j, X, own, rbase);
+  else
+    p2_body<A, R, -1, Tscr>(GrpAll{}, smem_raw, &tm_scr0, &tm_scr1, &tm0, &tm1, &tm0_box, p, sl, img, j, X, own, rbase);
 }
 
 }  // namespace v2

@@ -736,3 +736,43 @@ def test_i32_signed_large_values(fht, O, shape):
         n = quads[q].shape[0]
         check(hq.view[0, q, :n].cpu().numpy(), quads[q], True)
         check(sq.view[0, q, :n].cpu().numpy(), O.fhtshift_quadrant(quads[q], O.QUADRANT_FRAME[q][1]), True)
+
+
+# ------------------------------------------------------------------ the pipelined kernel (fht_pipe.cuh)
+PIPE_VARIANTS = [{}, {"FHT_PIPE_D": "1", "FHT_PIPE_NBUF": "2"}, {"FHT_PIPE_D": "3", "FHT_PIPE_NBUF": "4"},
+                 {"FHT_PIPE_UNIT_MB": "1"}]
+
+
+@pytest.mark.parametrize("shape,dt,batch", [((256, 256), "u8", 3), ((300, 500), "f32", 1), ((512, 512), "u8", 6),
+                                            ((1024, 1024), "f32", 2), ((2048, 2048), "f32", 1), ((4096, 4096), "f32", 1),
+                                            ((700, 900), "i32", 2)], ids=str)
+def test_pipe_matches_two_launch_and_oracle(fht, O, monkeypatch, shape, dt, batch):
+    """One persistent launch for both passes (pass 1 of unit u + D beside pass 2 of unit u, a ring of NBUF
+    scratch buffers): bit-identical to the two-launch schedule for every lookahead / ring / unit size
+    (including the tight ring D = 1, NBUF = 2 whose pass-1 items wait on buffer reuse), one launch per
+    call, and every cell of image 0 against the oracle."""
+    from synth import random_image
+    imgs = np.stack([random_image(shape, dt, seed=shape[0] + b) for b in range(batch)])
+    t = dev(imgs)
+    monkeypatch.setenv("FHT_PIPE", "0")
+    h0, s0 = fht.full(t, pair=True)
+    torch.cuda.synchronize()
+    assert h0.launches >= 2
+    for env in PIPE_VARIANTS:
+        monkeypatch.setenv("FHT_PIPE", "1")
+        for k in ("FHT_PIPE_D", "FHT_PIPE_NBUF", "FHT_PIPE_UNIT_MB"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        h, s = fht.full(t, pair=True)
+        q1 = fht.quadrant(t, fht.QC)
+        torch.cuda.synchronize()
+        assert h.launches == 1, env
+        assert torch.equal(h.storage, h0.storage) and torch.equal(s.storage, s0.storage), env
+    quads = O.full_quadrants(imgs[0])
+    got = h.view[0].cpu().numpy()
+    for q in range(4):
+        n = quads[q].shape[0]
+        check(got[q, :n], quads[q], dt != "f32")
+    if batch > 1:   # one quadrant of a batch: units = images
+        check(q1.view[batch - 1, 0].cpu().numpy(), O.hough_recursive(imgs[batch - 1], O.QC), dt != "f32")
