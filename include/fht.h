@@ -104,6 +104,7 @@ typedef struct {
   int64_t batch_stride, quad_stride, row_stride;
   int64_t h, w, Hp, Wp;                   /* source image dims; Hp/Wp = padded powers of two */
   fht_angle_plan_t plan;                    /* valid iff mode == RANGE */
+  int64_t row0;     /* a row band of a sharded transform (fht_shard_describe): row r holds shift row0 + r */
 } fht_hough;
 
 /* Optional per-call execution options (may be NULL).
@@ -228,6 +229,51 @@ int fht_angle_range_plan(const fht_image* img, const fht_angle_plan_t* plan, fht
  * mode each block first reduces its rows' support (start_s, len_s) from an e_y table in shared
  * memory. Allocates nothing. Returns 1 (kernels enqueued). */
 int fhtshift(const fht_hough* in, fht_hough* out, fht_stream_t stream);
+
+/* ---- Single-image sharding over ranks ------------------------------------------
+ * The full transform (FULL/QUADS; square frames, Hp == Wp) split over `world` GPUs, one process per
+ * GPU. With the pass split K = m + L of the frame, rank g runs pass 1 (levels 1..m) on
+ * its strips i in [g S, (g+1) S), S = 2^L / world -- image rows [g Hp/world, (g+1) Hp/world) of QA/QB
+ * and image columns of QC/QD -- and sends the shifts j of rank h's groups J_h = [h J, (h+1) J),
+ * J = 2^m / world, to rank h; rank h runs pass 2 (levels m+1..K) on J_h, which yields output rows
+ * t in [h Hp/world, (h+1) Hp/world) of every quadrant (t = j 2^L + u), a row band. Pass 2 of group j
+ * needs F_m[i][j] of EVERY strip i (the pre-shear identity), so the exchange between the passes is ONE
+ * all-to-all of the pass-1 scratch (Fig. 6 iteration; the multi-pass identity). The paper
+ * has no multi-GPU content; this is the north_star's data-parallel path at a size beyond one GPU.
+ *
+ * Buffers (device, caller-owned, all ranks the same sizes): rank g's chunk for rank h is
+ * [z = image * 4 + quadrant][j_local < J][strip_local < S][pitch] elements of the scratch type (u16 for
+ * u8 input, else the accumulator), chunk_bytes each; a receive buffer is world chunks, chunk g from
+ * rank g. Requires world a power of two <= 8 that divides 2^m and 2^L (FHT_ERR_UNSUPPORTED otherwise). */
+typedef struct {
+  int32_t world, rank;
+  int32_t m, L;              /* the frame's pass split (K = m + L) */
+  int64_t S, J;              /* strips and groups per rank */
+  int64_t rows_per_rank;     /* Hp / world: rows of this rank's output band */
+  int64_t pitch;             /* scratch row pitch, elements */
+  int32_t scratch_es, _pad0; /* scratch element bytes */
+  int64_t chunk_rows;        /* batch * 4 * J * S */
+  int64_t chunk_bytes;       /* one chunk (16-byte multiple) */
+  int64_t send_bytes, recv_bytes;  /* world * chunk_bytes */
+  fht_hough band;            /* this rank's output band: FULL/QUADS, rows = Hp/world, row0 = rank Hp/world */
+} fht_shard;
+
+/* Host-only: the geometry above for `img` (data may be NULL). */
+int fht_shard_describe(const fht_image* img, int world, int rank, fht_shard* out);
+
+/* Pass 1 of rank sh->rank. dst[h] (h < world, device pointers): where rank h's chunk goes -- either
+ * this rank's send buffer + h * chunk_bytes (the caller then runs one all-to-all, e.g. NCCL), or rank
+ * h's RECEIVE buffer + rank * chunk_bytes mapped into this process (peer memory over NVLink /
+ * NVSwitch): the exchange then happens in pass 1's own TMA stores and no collective is needed. One
+ * kernel; returns 1. */
+int fht_shard_pass1(const fht_image* img, const fht_shard* sh, void* const* dst, fht_stream_t stream);
+
+/* Pass 2 of rank sh->rank from its receive buffer (all world chunks present; the caller orders it
+ * after every rank's pass 1 / the all-to-all). band / band_shifted: descriptors equal to sh->band with
+ * `data` set (either may be NULL, not both); band_shifted receives the fhtshift-ed rows (§5, R11: the
+ * shift of global row row0 + r). One kernel; returns 1. */
+int fht_shard_pass2(const fht_image* img, const fht_shard* sh, const void* recv, fht_hough* band,
+                    fht_hough* band_shifted, fht_stream_t stream);
 
 /* Human-readable name of a status code (static string). */
 const char* fht_status_string(int status);

@@ -215,28 +215,31 @@ def hough_cells_direct(fr: Frame, cells) -> np.ndarray:
 # ----------------------------------------------------------------------------------------
 # Tier 2: Fig. 6 block-doubling recursion
 # ----------------------------------------------------------------------------------------
-def hough_of_frame_recursive(fr: Frame, dtype=None) -> np.ndarray:
-    """Level k merges blocks 2b, 2b+1 of level k-1:
+def recursion_levels(F: np.ndarray, sigma: int, levels: int) -> np.ndarray:
+    """`levels` iterations of the Fig. 6 block doubling on F[b][t][x] (blocks of
+    size n = F.shape[1] rows, cyclic width W = F.shape[2]); level k merges blocks 2b, 2b+1:
 
         F_k[b][t](x) = F_{k-1}[2b][t>>1](x) + F_{k-1}[2b+1][t>>1]((x + sigma*ceil(t/2)) mod W)
-
-    starting from F_0[r][0](x) = rows[r][x]. `dtype=np.float32` gives the float32 debugging run.
     """
-    rows = fr.rows if dtype is None else fr.rows.astype(dtype)
-    Hp, W = fr.Hp, fr.W
-    F = rows.reshape(Hp, 1, W).copy()          # F[b][t][x], blocks of size 1
-    size = 1
-    while size < Hp:
-        nb = F.shape[0] // 2
+    for _ in range(levels):
+        nb, size, W = F.shape[0] // 2, F.shape[1], F.shape[2]
         G = np.empty((nb, 2 * size, W), dtype=F.dtype)
         for b in range(nb):
             A, B = F[2 * b], F[2 * b + 1]
             for t in range(2 * size):
                 c = (t + 1) // 2
-                G[b, t] = A[t >> 1] + np.roll(B[t >> 1], -fr.sigma * c)
+                G[b, t] = A[t >> 1] + np.roll(B[t >> 1], -sigma * c)
         F = G
-        size *= 2
-    return F[0]
+    return F
+
+
+def hough_of_frame_recursive(fr: Frame, dtype=None) -> np.ndarray:
+    """All log2(Hp) levels of `recursion_levels` starting from F_0[r][0](x) = rows[r][x].
+    `dtype=np.float32` gives the float32 debugging run."""
+    rows = fr.rows if dtype is None else fr.rows.astype(dtype)
+    Hp, W = fr.Hp, fr.W
+    F = rows.reshape(Hp, 1, W).copy()          # F[b][t][x], blocks of size 1
+    return recursion_levels(F, fr.sigma, Hp.bit_length() - 1)[0]
 
 
 def hough_recursive(img: np.ndarray, quadrant: int, pad: int | None = None, dtype=None) -> np.ndarray:

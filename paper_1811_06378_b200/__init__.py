@@ -27,7 +27,8 @@ from ._lib import (FHT_F32, FHT_I32, FHT_LAYOUT_CONCAT, FHT_LAYOUT_QUADS, FHT_MO
                    FHT_MODE_RANGE, FHT_QA, FHT_QB, FHT_QC, FHT_QD, FHT_U8, FhtAnglePlan, FhtError, FhtHough,
                    FhtImage)
 
-__all__ = ["full", "quadrant", "angle_plan", "angle_range", "angle_of_row", "fhtshift", "HoughImage", "FhtError",
+__all__ = ["full", "quadrant", "angle_plan", "angle_range", "angle_of_row", "fhtshift", "full_sharded", "HoughImage",
+           "FhtError",
            "QA", "QB", "QC", "QD", "workspace_bytes", "LIB_PATH"]
 
 QA, QB, QC, QD = FHT_QA, FHT_QB, FHT_QC, FHT_QD
@@ -296,3 +297,6 @@ class Graph:
     def replay(self):
         self.graph.replay()
         return self.result
+
+
+from .sharding import full_sharded, shard_describe  # noqa: E402  (one image over several GPUs)

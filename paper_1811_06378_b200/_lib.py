@@ -30,6 +30,7 @@ EXPORTED = (
     "fht_angle_plan_make_pruned", "fht_angle_plan_make_ex", "fht_angle_range", "fht_angle_range_workspace_bytes",
     "fht_angle_range_plan", "fhtshift", "fht_status_string", "fht_peaks_workspace_bytes",
     "fht_peaks", "fht_cell_segment", "fht_hough_describe_pad", "fht_quadrant_workspace_bytes",
+    "fht_shard_describe", "fht_shard_pass1", "fht_shard_pass2",
 )
 
 
@@ -66,7 +67,17 @@ class FhtHough(ctypes.Structure):
         ("batch", ctypes.c_int64), ("nquad", ctypes.c_int64), ("rows", ctypes.c_int64), ("cols", ctypes.c_int64),
         ("batch_stride", ctypes.c_int64), ("quad_stride", ctypes.c_int64), ("row_stride", ctypes.c_int64),
         ("h", ctypes.c_int64), ("w", ctypes.c_int64), ("Hp", ctypes.c_int64), ("Wp", ctypes.c_int64),
-        ("plan", FhtAnglePlan),
+        ("plan", FhtAnglePlan), ("row0", ctypes.c_int64),
+    ]
+
+
+class FhtShard(ctypes.Structure):
+    _fields_ = [
+        ("world", ctypes.c_int32), ("rank", ctypes.c_int32), ("m", ctypes.c_int32), ("L", ctypes.c_int32),
+        ("S", ctypes.c_int64), ("J", ctypes.c_int64), ("rows_per_rank", ctypes.c_int64), ("pitch", ctypes.c_int64),
+        ("scratch_es", ctypes.c_int32), ("_pad0", ctypes.c_int32), ("chunk_rows", ctypes.c_int64),
+        ("chunk_bytes", ctypes.c_int64), ("send_bytes", ctypes.c_int64), ("recv_bytes", ctypes.c_int64),
+        ("band", FhtHough),
     ]
 
 
@@ -109,11 +120,15 @@ def _load():
     lib.fht_hough_describe_pad.argtypes = [i32, P(FhtImage), i64, P(FhtHough)]
     lib.fht_quadrant_workspace_bytes.argtypes = [P(FhtImage), i32, i64]
     lib.fht_quadrant_workspace_bytes.restype = sz
+    lib.fht_shard_describe.argtypes = [P(FhtImage), i32, i32, P(FhtShard)]
+    lib.fht_shard_pass1.argtypes = [P(FhtImage), P(FhtShard), P(vp), vp]
+    lib.fht_shard_pass2.argtypes = [P(FhtImage), P(FhtShard), vp, P(FhtHough), P(FhtHough), vp]
     lib.fht_status_string.argtypes = [i32]
     lib.fht_status_string.restype = ctypes.c_char_p
     for name in ("fht_hough_describe", "fht_quadrant", "fht_full", "fht_angle_plan", "fht_angle_of_row",
                  "fht_angle_plan_make_pruned", "fht_angle_plan_make_ex", "fht_angle_range", "fht_angle_range_plan",
-                 "fhtshift", "fht_peaks", "fht_cell_segment", "fht_hough_describe_pad"):
+                 "fhtshift", "fht_peaks", "fht_cell_segment", "fht_hough_describe_pad", "fht_shard_describe",
+                 "fht_shard_pass1", "fht_shard_pass2"):
         getattr(lib, name).restype = i32
     return lib
 

@@ -338,8 +338,26 @@ cudaError_t launch_pass2(int logr, dim3 grid, const Pass2Args& a, cudaStream_t s
 
 // ---------------------------------------------------------------- v2 launch helpers
 struct P1Maps {
-  CUtensorMap img0, img1, scr;
+  CUtensorMap img0, img1;
+  v2::P1Dst dst;
 };
+
+// Pass-1 destination view [z][j][strip][column] of a scratch buffer (dims column, strip, j, z; S strips,
+// J shifts, Z images x slots), box {TX, 1, jper, 1}: one tile's shifts j of one destination.
+bool make_dst_map(CUtensorMap* m, void* base, int ses, bool f32, int64_t pitch, int64_t S, int64_t J, int64_t Z, int TX,
+                  int jper) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  const cuuint64_t rb = (cuuint64_t)(pitch * ses);
+  cuuint64_t dims[4] = {(cuuint64_t)pitch, (cuuint64_t)S, (cuuint64_t)J, (cuuint64_t)Z};
+  cuuint64_t strides[3] = {rb, rb * (cuuint64_t)S, rb * (cuuint64_t)(S * J)};
+  cuuint32_t box[4] = {(cuuint32_t)TX, 1, (cuuint32_t)jper, 1};
+  cuuint32_t e[4] = {1, 1, 1, 1};
+  const CUtensorMapDataType sdt = ses == 2 ? CU_TENSOR_MAP_DATA_TYPE_UINT16
+                                           : f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_INT32;
+  return fn(m, sdt, 4, base, dims, strides, box, e, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 template <typename Tin, int R>
 cudaError_t launch_p1_t(dim3 grid, const P1Maps& m, const v2::P1Params& a, cudaStream_t st) {
   // range launches with the TMA loader also stage the strip's colmap slice (kColmapStageBytes)
@@ -348,7 +366,7 @@ cudaError_t launch_p1_t(dim3 grid, const P1Maps& m, const v2::P1Params& a, cudaS
   const cudaError_t attr =
       smem_optin(v2::k_p1<Tin, R>, v2::p1_smem_bytes(R, sizeof(Tin) == 1) + v2::kColmapStageBytes, done);
   if (attr != cudaSuccess) return attr;
-  return launch_pdl(v2::k_p1<Tin, R>, grid, dim3(v2::Split<R>::nw * 32), smem, st, m.img0, m.img1, m.scr, a);
+  return launch_pdl(v2::k_p1<Tin, R>, grid, dim3(v2::Split<R>::nw * 32), smem, st, m.img0, m.img1, m.dst, a);
 }
 template <typename Tin>
 cudaError_t launch_p1(int r, dim3 grid, const P1Maps& m, const v2::P1Params& a, cudaStream_t st) {
@@ -432,14 +450,27 @@ struct LaunchLog {
   }
 };
 
-// Run the two passes for one orientation over all images, chunked. Returns launches or error.
+// One phase of a sharded transform (fht_shard_*): phase 1 runs pass 1 on this rank's
+// strips into the world destinations dst[h]; phase 2 runs pass 2 on this rank's groups from `recv`.
+struct ShardCfg {
+  int world, rank, phase;
+  int64_t S, J;          // strips and groups per rank (2^L / world, 2^m / world)
+  void* const* dst;      // phase 1: dst[h] = where rank h's chunk goes
+  const void* recv;      // phase 2: [world][z][j_local][strip_local][pitch]
+  int64_t chunk_rows;    // z * J * S
+};
+
+// Run the two passes for one orientation over all images, chunked (or one phase of a shard). Returns
+// launches or error.
 int run_orientation(const fht_image* img, const Frame& f, const Slot* slots, int nq, const Outs& outs, void* ws,
-                    size_t ws_bytes, cudaStream_t st, const RangeDev* rg, LaunchLog& log) {
+                    size_t ws_bytes, cudaStream_t st, const RangeDev* rg, LaunchLog& log,
+                    const ShardCfg* sh = nullptr) {
   const int ses = scratch_es(img->dtype);
   const ScratchPlan sp = scratch_plan(f, nq, img->batch, rg, ses);
-  const PipePlan pq = pipe_plan(f, nq, img->batch, rg, ses);
+  const PipePlan pq = sh ? PipePlan{} : pipe_plan(f, nq, img->batch, rg, ses);
   const bool pipe = pq.on && ws && ws_bytes >= pq.bytes;
-  if (!ws || (ws_bytes < sp.bytes && !pipe)) return FHT_ERR_WORKSPACE;
+  if (!sh && (!ws || (ws_bytes < sp.bytes && !pipe))) return FHT_ERR_WORKSPACE;
+  if (sh && !sp.v2) return FHT_ERR_UNSUPPORTED;
   int launches = 0;
   const fht_hough* any = outs.d[0] ? outs.d[0] : outs.d[1];
 
@@ -477,6 +508,11 @@ int run_orientation(const fht_image* img, const Frame& f, const Slot* slots, int
       span1 = (s.xhi - s.xlo) < span1 ? (s.xhi - s.xlo) : span1;
     }
     p1.TX = span1 < v2::TX1 ? span1 : v2::TX1;
+    if (sh) {  // each destination's box starts jper * TX elements into the staging plane: 128-byte aligned
+      const int64_t jb = sh->J * ses;
+      if ((jb * p1.TX) % 128 != 0) p1.TX = p1.TX >= 192 ? 192 : (p1.TX & ~31);
+      if (p1.TX < 32 || (jb * p1.TX) % 128 != 0) return FHT_ERR_UNSUPPORTED;
+    }
     int ntile1 = 0;
     for (int q = 0; q < nq; ++q) {
       v2::P1Slot& s = p1.slot[q];
@@ -498,7 +534,7 @@ int run_orientation(const fht_image* img, const Frame& f, const Slot* slots, int
       p2.no_tma = (e && e[0] == '1') ? 1 : 0;
     }
     p2.nq = nq;
-    p2.W = (int)any->cols;
+    p2.W = any ? (int)any->cols : f.W;
     p2.Hp = f.Hp;
     p2.wc = f.wc;
     const int span2 = rg ? rg->out_hi - rg->out_lo : p2.W;
@@ -565,27 +601,85 @@ int run_orientation(const fht_image* img, const Frame& f, const Slot* slots, int
     if (p2.ndest == 1) m2.out1 = m2.out0;
     if (!outs.d[0]) m2.out0_box = m2.out0;
     const bool f32 = img->dtype == FHT_F32;
+    if (sh) {
+      const int64_t Z = img->batch * nq;
+      const int logS = ilog2(sh->S);
+      P1Maps m1s;
+      P2Maps m2s = m2;
+      if (sh->phase == 1) {  // pass 1 of strips [rank S, (rank + 1) S): every rank's groups to dst[h]
+        p1.ndst = sh->world;
+        p1.jper = (int)sh->J;
+        p1.strip0 = (int)(sh->rank * sh->S);
+        p1.L = logS;  // the grid's strips per image
+        p1.z0 = 0;
+        p1.img0 = 0;
+        p1.ntiles = ntile1;
+        for (int h = 0; h < sh->world; ++h)
+          if (!make_dst_map(&m1s.dst.m[h], sh->dst[h], ses, f32, sp.pitch, sh->S, sh->J, Z, p1.TX, (int)sh->J))
+            return FHT_ERR_CUDA;
+        if (p1.fill_tma) {
+          if (!make_image_map(&m1s.img0, img, 256) || !make_image_map(&m1s.img1, img, es == 1 ? 48 : 36))
+            return FHT_ERR_CUDA;
+        } else {
+          m1s.img0 = m1s.dst.m[0];
+          m1s.img1 = m1s.dst.m[0];
+        }
+        const dim3 g1((unsigned)(ntile1 * sh->S * img->batch * nq));
+        log.before(st);
+        cudaError_t e;
+        switch (img->dtype) {
+          case FHT_U8: e = launch_p1<uint8_t>(f.m, g1, m1s, p1, st); break;
+          case FHT_I32: e = launch_p1<int32_t>(f.m, g1, m1s, p1, st); break;
+          default: e = launch_p1<float>(f.m, g1, m1s, p1, st); break;
+        }
+        if (e != cudaSuccess) return FHT_ERR_CUDA;
+        log.after(st);
+        return 1;
+      }
+      // pass 2 of groups [rank J, (rank + 1) J) from the received chunks [g][z][j_local][strip_local]
+      const uint64_t rows = (uint64_t)sh->world * sh->chunk_rows;
+      void* recv = const_cast<void*>(sh->recv);
+      if (!make_row_map(&m2s.scr0, recv, f32, (uint64_t)span1, rows, (uint64_t)sp.pitch, 256, 1, ses == 2) ||
+          !make_row_map(&m2s.scr1, recv, f32, (uint64_t)span1, rows, (uint64_t)sp.pitch, ses == 2 ? 40 : 36, 1,
+                        ses == 2))
+        return FHT_ERR_CUDA;
+      p2.scratch_img_rows = nq * sh->J * sh->S;
+      for (int q = 0; q < nq; ++q) p2.slot[q].srow0 = q * sh->J * sh->S;
+      p2.row0 = 0;
+      p2.img0 = 0;
+      p2.j0 = (int)(sh->rank * sh->J);
+      p2.logS = logS;
+      p2.strideG = sh->chunk_rows;
+      p2.ntiles = ntile2;
+      p2.m = f.m;
+      p2.ngroups = (int)sh->J;
+      const dim3 g2((unsigned)(ntile2 * sh->J * img->batch * nq));
+      log.before(st);
+      const cudaError_t e = f32 ? launch_p2<float>(f.L, g2, m2s, p2, st)
+                                : ses == 2 ? launch_p2<int, uint16_t>(f.L, g2, m2s, p2, st)
+                                           : launch_p2<int>(f.L, g2, m2s, p2, st);
+      if (e != cudaSuccess) return FHT_ERR_CUDA;
+      log.after(st);
+      return 1;
+    }
     const uint64_t scr_rows = pipe ? (uint64_t)pq.NBUF * pq.nbu * f.Hp : (uint64_t)sp.nbuf * sp.chunk * p1.scratch_img_rows;
     P1Maps m1;
-    {  // pass-1 stores: scratch as [z*2^m + j][strip][column], one box {TX, 1, 2^m} per tile
-      auto fn = encode_fn();
-      cuuint64_t dims[3] = {(cuuint64_t)sp.pitch, (cuuint64_t)nstrips, (cuuint64_t)(scr_rows / nstrips)};
-      cuuint64_t strides[2] = {(cuuint64_t)(sp.pitch * ses), (cuuint64_t)(sp.pitch * ses * nstrips)};
-      cuuint32_t box[3] = {(cuuint32_t)p1.TX, 1, (cuuint32_t)ngroups};  // shifts j < ngroups only
-      cuuint32_t e[3] = {1, 1, 1};
-      const CUtensorMapDataType sdt = ses == 2 ? CU_TENSOR_MAP_DATA_TYPE_UINT16
-                                               : f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_INT32;
-      if (!fn || fn(&m1.scr, sdt, 3, ws, dims, strides,
-                    box, e, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
-                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-        return FHT_ERR_CUDA;
-    }
+    // pass-1 stores: scratch [z][j][strip][column], one box {TX, 1, ngroups, 1} per tile (shifts j < ngroups)
+    p1.ndst = 1;
+    p1.jper = ngroups;
+    p1.strip0 = 0;
+    p2.j0 = 0;
+    p2.logS = f.L;
+    p2.strideG = 0;
+    if (!make_dst_map(&m1.dst.m[0], ws, ses, f32, sp.pitch, nstrips, 1 << f.m, (int64_t)(scr_rows / f.Hp), p1.TX,
+                      ngroups))
+      return FHT_ERR_CUDA;
     if (p1.fill_tma) {
       if (!make_image_map(&m1.img0, img, 256) || !make_image_map(&m1.img1, img, es == 1 ? 48 : 36))
         return FHT_ERR_CUDA;
     } else {
-      m1.img0 = m1.scr;
-      m1.img1 = m1.scr;
+      m1.img0 = m1.dst.m[0];
+      m1.img1 = m1.dst.m[0];
     }
     // scratch as pass 2 reads it: columns [0, span1) = what pass 1 wrote; TMA zero-fills the rest
     if (!make_row_map(&m2.scr0, ws, f32, (uint64_t)span1, scr_rows, (uint64_t)sp.pitch, 256, 1, ses == 2) ||
@@ -615,7 +709,7 @@ int run_orientation(const fht_image* img, const Frame& f, const Slot* slots, int
         pp.trace = reinterpret_cast<unsigned long long*>(std::strtoull(tp, nullptr, 0));
         pp.trace_n = env_int("FHT_PIPE_TRACE_N", 0);
       }
-      PipeMaps pm{m1.img0, m1.img1, m1.scr, m2.scr0, m2.scr1, m2.out0, m2.out1, m2.out0_box};
+      PipeMaps pm{m1.img0, m1.img1, m1.dst, m2.scr0, m2.scr1, m2.out0, m2.out1, m2.out0_box};
       log.before(st);
       if (cudaMemsetAsync(pp.counters, 0, (size_t)(1 + 2 * pq.nunits) * sizeof(int), st) != cudaSuccess)
         return FHT_ERR_CUDA;
@@ -1213,6 +1307,110 @@ int fht_quadrant(const fht_image* img, int quadrant, int64_t pad_cols, fht_hough
   return quadrant_run(img, quadrant, pad_cols, out, out_shifted, ws, ws_bytes, stream, log);
 }
 
+}  // extern "C"
+
+namespace {
+// sharded transform: validate (img, sh) against a fresh description
+int shard_check(const fht_image* img, const fht_shard* sh) {
+  if (!sh) return FHT_ERR_ARG;
+  fht_shard want;
+  const int s = fht_shard_describe(img, sh->world, sh->rank, &want);
+  if (s) return s;
+  if (want.chunk_bytes != sh->chunk_bytes || want.pitch != sh->pitch || want.S != sh->S || want.J != sh->J)
+    return FHT_ERR_ARG;
+  return FHT_OK;
+}
+void quads_slots(Slot* sl, int64_t rows_per_quad, int64_t row_base) {
+  const int qid[4] = {FHT_QA, FHT_QB, FHT_QC, FHT_QD};
+  for (int k = 0; k < 4; ++k) {
+    sl[k].sigma = (qid[k] == FHT_QA || qid[k] == FHT_QD) ? 1 : -1;
+    sl[k].transposed = qid[k] >= FHT_QC;
+    sl[k].qrow = (int64_t)qid[k] * rows_per_quad;
+    sl[k].row_base = (int)row_base;
+    sl[k].row_sign = 1;
+    sl[k].skip_t = -1;
+  }
+}
+}  // namespace
+
+extern "C" {
+
+int fht_shard_describe(const fht_image* img, int world, int rank, fht_shard* out) {
+  if (!img || !out) return FHT_ERR_ARG;
+  if (img->dtype != FHT_U8 && img->dtype != FHT_I32 && img->dtype != FHT_F32) return FHT_ERR_DTYPE;
+  if (img->batch < 1 || img->h < 1 || img->w < 1) return FHT_ERR_ARG;
+  if (world < 1 || (world & (world - 1)) || rank < 0 || rank >= world) return FHT_ERR_ARG;
+  if (world > v2::kMaxDst) return FHT_ERR_UNSUPPORTED;
+  if (next_pow2(img->h) != next_pow2(img->w)) return FHT_ERR_UNSUPPORTED;  // one frame for all four slots
+  const Frame f = make_frame(img->h, img->w, 0, 1);
+  if (check_frame_supported(f) || !use_v2(f, nullptr)) return FHT_ERR_UNSUPPORTED;
+  if ((1 << f.m) % world || (1 << f.L) % world) return FHT_ERR_UNSUPPORTED;
+  fht_shard d{};
+  d.world = world;
+  d.rank = rank;
+  d.m = f.m;
+  d.L = f.L;
+  d.S = (1 << f.L) / world;
+  d.J = (1 << f.m) / world;
+  d.rows_per_rank = f.Hp / world;
+  d.scratch_es = scratch_es(img->dtype);
+  d.pitch = v2_scratch_pitch(f, nullptr, d.scratch_es);
+  d.chunk_rows = img->batch * 4 * d.J * d.S;
+  d.chunk_bytes = d.chunk_rows * d.pitch * d.scratch_es;
+  d.send_bytes = d.recv_bytes = world * d.chunk_bytes;
+  int s = fht_hough_describe(FHT_MODE_FULL, FHT_LAYOUT_QUADS, 0, img, nullptr, &d.band);
+  if (s) return s;
+  d.band.rows = d.rows_per_rank;
+  d.band.row0 = rank * d.rows_per_rank;
+  d.band.quad_stride = d.band.rows * d.band.row_stride;
+  d.band.batch_stride = d.band.nquad * d.band.quad_stride;
+  *out = d;
+  return FHT_OK;
+}
+
+int fht_shard_pass1(const fht_image* img, const fht_shard* sh, void* const* dst, fht_stream_t stream) {
+  int s = check_image(img);
+  if (s) return s;
+  if ((s = shard_check(img, sh))) return s;
+  if (!dst) return FHT_ERR_ARG;
+  for (int h = 0; h < sh->world; ++h)
+    if (!dst[h] || !aligned16(dst[h])) return dst[h] ? FHT_ERR_ALIGN : FHT_ERR_ARG;
+  const Frame f = make_frame(img->h, img->w, 0, 1);
+  Slot sl[4];
+  quads_slots(sl, sh->rows_per_rank, -sh->band.row0);
+  ShardCfg cfg{sh->world, sh->rank, 1, sh->S, sh->J, dst, nullptr, sh->chunk_rows};
+  Outs o{{nullptr, nullptr}};
+  LaunchLog log{nullptr, 0};
+  return run_orientation(img, f, sl, 4, o, nullptr, 0, (cudaStream_t)stream, nullptr, log, &cfg);
+}
+
+int fht_shard_pass2(const fht_image* img, const fht_shard* sh, const void* recv, fht_hough* band,
+                    fht_hough* band_shifted, fht_stream_t stream) {
+  int s = check_image(img);
+  if (s) return s;
+  if ((s = shard_check(img, sh))) return s;
+  if (!recv || (!band && !band_shifted)) return FHT_ERR_ARG;
+  if (!aligned16(recv)) return FHT_ERR_ALIGN;
+  for (fht_hough* o : {band, band_shifted}) {
+    if (!o) continue;
+    if ((s = validate_out(o, sh->band))) return s;
+    if (o->row0 != sh->band.row0) return FHT_ERR_SHAPE;
+    if (overlaps(recv, (size_t)sh->recv_bytes, o->data, hough_extent_bytes(o))) return FHT_ERR_ARG;
+  }
+  if (band && band_shifted && overlaps(band->data, hough_extent_bytes(band), band_shifted->data,
+                                       hough_extent_bytes(band_shifted)))
+    return FHT_ERR_ARG;
+  const Frame f = make_frame(img->h, img->w, 0, 1);
+  Slot sl[4];
+  quads_slots(sl, sh->rows_per_rank, -sh->band.row0);
+  ShardCfg cfg{sh->world, sh->rank, 2, sh->S, sh->J, nullptr, recv, sh->chunk_rows};
+  Outs o{{band, band_shifted}};
+  LaunchLog log{nullptr, 0};
+  const int r = run_orientation(img, f, sl, 4, o, nullptr, 0, (cudaStream_t)stream, nullptr, log, &cfg);
+  if (r > 0) mark_outs(band, band_shifted);
+  return r;
+}
+
 int fht_full(const fht_image* img, int layout, fht_hough* out, fht_hough* out_shifted, void* ws, size_t ws_bytes,
              fht_stream_t stream, const fht_exec_opts* opts) {
   int s = check_image(img);
@@ -1397,6 +1595,8 @@ int fhtshift(const fht_hough* in, fht_hough* out, fht_stream_t stream) {
   a.out_q_stride = out->quad_stride;
   a.out_row_stride = out->row_stride;
   a.rows = (int)in->rows;
+  a.row0 = (int)in->row0;  // a shard's band: row r is shift row0 + r
+  if (in->row0 != out->row0 || (in->row0 && in->mode != FHT_MODE_FULL)) return FHT_ERR_SHAPE;
   a.W = (int)in->cols;
   a.nquad = (int)in->nquad;
   a.rows_total = in->batch * in->nquad * in->rows;
@@ -1496,7 +1696,7 @@ int fht_cell_segment(const fht_hough* h, int64_t slot, int64_t row, int64_t col,
   } else if (h->mode == FHT_MODE_FULL) {
     if (h->layout == FHT_LAYOUT_QUADS) {
       q = (int)slot;
-      s = row;
+      s = row + h->row0;  // a shard's band starts at shift row0
     } else {  // CONCAT: P:111-113 thresholds, a shared row belongs to the earlier quadrant (R8)
       const int64_t Hp = h->Hp, Wp = h->Wp;
       if (row < Hp) { q = FHT_QA; s = Hp - 1 - row; }

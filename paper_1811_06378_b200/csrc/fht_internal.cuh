@@ -52,7 +52,9 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
 }
 
 struct PipeMaps {
-  CUtensorMap img0, img1, scr, scr0, scr1, out0, out1, out0_box;
+  CUtensorMap img0, img1;
+  v2::P1Dst dst;
+  CUtensorMap scr0, scr1, out0, out1, out0_box;
 };
 
 // k_pipe<Tin, m, L> (fht_pipe.cu): dtype 0 = u8, 1 = i32, 2 = f32. Sets the per-unit item counts and the

@@ -345,6 +345,7 @@ struct ShiftArgs {
   int quadrant;         // QUADRANT mode
   int Hp, Wp;           // quadrant row counts (QA/QB: Hp, QC/QD: Wp)
   int pad;              // QUADRANT mode: the frame's extension W - w_frame (FULL: pad = the row count)
+  int row0;             // FULL/QUADS band of a sharded transform: row r is shift row0 + r
   int vec;              // 16-byte path: W, every stride a multiple of 4 elements, bases 16-B aligned
   double g;             // RANGE: shear e_y = floor(g*y + 0.5), y < h; K = log2 Hp; w' (R17 support)
   int h, K, w_content;
@@ -364,7 +365,7 @@ __device__ __forceinline__ int shift_amount(const ShiftArgs& a, int r, int qs) {
     else { q = 3; s = r - (2 * Hp + Wp - 3); }
   } else {
     q = a.mode == 0 ? a.quadrant : qs;
-    s = r;
+    s = r + a.row0;
   }
   const int n = (q < 2) ? a.Hp : a.Wp;
   if (s >= n) return 0;

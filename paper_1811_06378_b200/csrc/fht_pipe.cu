@@ -32,7 +32,7 @@ cudaError_t launch_pipe_t(const PipeMaps& m, const v2::P1Params& a, const v2::P2
     std::fprintf(stderr, "k_pipe<%d,%d>: occ %d/SM x %d SMs, grid %lld, NT %d, smem %zu, units %d (nbu %d, D %d, NBUF %d), "
                  "items %lld (n1 %d, n2 %d)\n", R1, R2, occ, nsm, (long long)grid, PS::NT, smem, pp.nunits, pp.nbu, pp.D,
                  pp.NBUF, (long long)pp.n_items, pp.n1, pp.n2);
-  return launch_pdl(v2::k_pipe<Tin, R1, R2>, dim3((unsigned)grid), dim3(PS::NT), smem, st, m.img0, m.img1, m.scr,
+  return launch_pdl(v2::k_pipe<Tin, R1, R2>, dim3((unsigned)grid), dim3(PS::NT), smem, st, m.img0, m.img1, m.dst,
                     m.scr0, m.scr1, m.out0, m.out1, m.out0_box, a, b, pp);
 }
 template <typename Tin>

@@ -136,10 +136,10 @@ __host__ __device__ constexpr size_t pipe_smem_bytes() {
 // they have in k_p1 / k_p2 (a call boundary instead costs every tile a callee-saved register spill).
 template <typename Tin, int R, typename G>
 __device__ __forceinline__ bool p1_item(const G grp, unsigned char* smem, const CUtensorMap* tm_img0,
-                                     const CUtensorMap* tm_img1, const CUtensorMap* tm_scr, const P1Params& p,
+                                     const CUtensorMap* tm_img1, const P1Dst* dst, const P1Params& p,
                                      const P1Slot& sl, int img, int strip, int X, int zscr, uint64_t* bars,
                                      uint32_t par) {
-  return p1_body<Tin, R>(grp, smem, tm_img0, tm_img1, tm_scr, p, sl, img, strip, X, zscr, bars, par);
+  return p1_body<Tin, R>(grp, smem, tm_img0, tm_img1, dst, p, sl, img, strip, X, zscr, bars, par);
 }
 template <typename A, int R, typename Tscr, typename G>
 __device__ __forceinline__ bool p2_item(const G grp, unsigned char* smem, const CUtensorMap* tm_scr0,
@@ -153,12 +153,12 @@ __device__ __forceinline__ bool p2_item(const G grp, unsigned char* smem, const 
                                  par);
 }
 
-// Maps: as k_p1 (tm_img0/1, tm_scr over the ring: [z*2^m + j][strip][column], z = buffer*nbu + image)
+// Maps: as k_p1 (tm_img0/1, dst over the ring: [z][j][strip][column], z = buffer*nbu + image)
 // and k_p2 (tm_scr0/1 rows of the ring, tm0/tm1/tm0_box destinations).
 template <typename Tin, int R1, int R2>
 __global__ void __launch_bounds__(PipeShape<R1, R2>::NT, PipeShape<R1, R2>::kMinBlocks)
 k_pipe(const __grid_constant__ CUtensorMap tm_img0, const __grid_constant__ CUtensorMap tm_img1,
-       const __grid_constant__ CUtensorMap tm_scr, const __grid_constant__ CUtensorMap tm_scr0,
+       const __grid_constant__ P1Dst dst, const __grid_constant__ CUtensorMap tm_scr0,
        const __grid_constant__ CUtensorMap tm_scr1, const __grid_constant__ CUtensorMap tm0,
        const __grid_constant__ CUtensorMap tm1, const __grid_constant__ CUtensorMap tm0_box,
        const __grid_constant__ P1Params p1, const __grid_constant__ P2Params p2,
@@ -213,9 +213,9 @@ k_pipe(const __grid_constant__ CUtensorMap tm_img0, const __grid_constant__ CUte
         bool used;
         const uint32_t par1 = par_s[threadIdx.x] & 0xffffu;
         if constexpr (PS::TPI1 == 1)
-          used = p1_item<Tin, R1>(GrpAll{}, sm, &tm_img0, &tm_img1, &tm_scr, p1, sl, img, strip, X, z, bars1, par1);
+          used = p1_item<Tin, R1>(GrpAll{}, sm, &tm_img0, &tm_img1, &dst, p1, sl, img, strip, X, z, bars1, par1);
         else
-          used = p1_item<Tin, R1>(GrpPart<PS::G1>{g * PS::G1, 1 + g}, sm, &tm_img0, &tm_img1, &tm_scr, p1, sl, img,
+          used = p1_item<Tin, R1>(GrpPart<PS::G1>{g * PS::G1, 1 + g}, sm, &tm_img0, &tm_img1, &dst, p1, sl, img,
                                   strip, X, z, bars1 + 8 * g, par1);
         if (used) par_s[threadIdx.x] ^= (1u << NB1) - 1u;
         // the tile's scratch box has been WRITTEN (not only read out of shared memory) before it counts

@@ -190,6 +190,20 @@ __device__ __forceinline__ void tma_store_3d_keep(const CUtensorMap* map, const 
                :: "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(smem)), "r"(c0), "r"(c1), "r"(c2), "l"(pol)
                : "memory");
 }
+// 4-D pass-1 scratch box, L2 evict-last (kept for pass 2)
+__device__ __forceinline__ void tma_store_4d_keep(const CUtensorMap* map, const void* smem, int c0, int c1, int c2, int c3) {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%2, %3, %4, %5}], [%1], %6;"
+               :: "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(smem)), "r"(c0), "r"(c1), "r"(c2), "r"(c3),
+                  "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, const void* smem, int c0, int c1, int c2, int c3) {
+  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];"
+               :: "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(smem)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+               : "memory");
+}
 __device__ __forceinline__ void tma_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void tma_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, void* smem, uint64_t* bar, int c0, int c1) {
@@ -422,7 +436,19 @@ struct P1Params {
   int TX;                            // tile width = TMA box (multiple of 4, <= TX1)
   int64_t scratch_img_rows;          // scratch rows per image
   int z0;                            // first z (= image-in-chunk * nq + slot) of this scratch buffer
+  int strip0;                        // first strip of the launch (image rows from strip0 * 2^m): a shard's strips
+  int ndst;                          // scratch destinations (P1Dst): 1, or one per rank of a sharded transform
+  int jper;                          // shifts j per destination (ngroups / ndst)
   P1Slot slot[4];
+};
+
+// Where pass 1 stores F_m: ndst 4-D tensor maps [z][j][strip][column] (dims column, strip, j, z), each
+// taking `jper` consecutive shifts j of the tile's box -- destination d gets j in [d*jper, (d+1)*jper).
+// One destination: the local scratch. A sharded transform: one per rank, each rank's
+// groups J_d, into the send buffer (then one all-to-all) or straight into the peers' receive buffers.
+constexpr int kMaxDst = 8;
+struct P1Dst {
+  CUtensorMap m[kMaxDst];
 };
 
 // scratch layout: row (img, slot, j, i) = img*scratch_img_rows + srow0 + j*2^L + i,
@@ -438,7 +464,7 @@ constexpr int kNoRow = -2147483647 - 1;  // range fill: the row has no content i
 // P:152) is gathered from it through colmap, e_y = erow[rho].
 // zscr: the scratch z (= buffer image x slot) the tile's F_m rows go to; smem: the group's shared memory.
 template <typename Tin, int R, int SIG, typename Tsrc, int FILL = 0, typename G>
-__device__ __forceinline__ void p1_tail_impl(const G grp, unsigned char* smem, const CUtensorMap* tm_scr, const P1Params& p,
+__device__ __forceinline__ void p1_tail_impl(const G grp, unsigned char* smem, const P1Dst* dst, const P1Params& p,
                                      const P1Slot& sl, int strip, int X, int zscr, const Tsrc* tsrc, int tpitch,
                                      int fa_pitch, uint64_t* bars, uint32_t par) {
   using A = typename AccOf<Tin>::type;
@@ -493,14 +519,17 @@ __device__ __forceinline__ void p1_tail_impl(const G grp, unsigned char* smem, c
   // dense [NR][TX] in the scratch type (u8 input: uint16), the box layout
   using Sc = typename ScrOf<Tin>::type;
   stage_rows<R, SIG, A, Sc>(grp, w, reinterpret_cast<Sc*>(buf), soff, p.TX, p.TX);
-  // ---- store F_m[strip][j] for all j in ONE box {TX, 1, NR} of the 3-D scratch view
-  // [z*2^m + j][strip][column] (z = image-in-chunk * nq + slot); column X - xlo is 16-B aligned
+  // ---- store F_m[strip][j] for all j: per destination d ONE box {TX, 1, jper, 1} of its 4-D view
+  // [z][j][strip][column] (z = image-in-chunk * nq + slot); column X - xlo is 16-B aligned
   if (grp.tid() == 0) {
+    for (int d = 0; d < p.ndst; ++d) {
+      const void* src = reinterpret_cast<const Sc*>(buf) + (size_t)d * p.jper * p.TX;
 #if FHT_SCR_KEEP
-    tma_store_3d_keep(tm_scr, buf, X - sl.xlo, strip, zscr << R);
+      tma_store_4d_keep(&dst->m[d], src, X - sl.xlo, strip, 0, zscr);
 #else
-    tma_store_3d(tm_scr, buf, X - sl.xlo, strip, zscr << R);
+      tma_store_4d(&dst->m[d], src, X - sl.xlo, strip, 0, zscr);
 #endif
+    }
     tma_commit();
   }
   pdl_trigger();
@@ -510,33 +539,33 @@ __device__ __forceinline__ void p1_tail_impl(const G grp, unsigned char* smem, c
 // The tail behind a call boundary in k_p1 (one instance per sign: the kernel's code stays inside the
 // instruction cache); inlined (INL) where a caller keeps state across it (the pipelined kernel).
 template <typename Tin, int R, int SIG, typename Tsrc, int FILL = 0, typename G>
-__device__ __noinline__ void p1_tail(const G grp, unsigned char* smem, const CUtensorMap* tm_scr, const P1Params& p,
+__device__ __noinline__ void p1_tail(const G grp, unsigned char* smem, const P1Dst* dst, const P1Params& p,
                                      const P1Slot& sl, int strip, int X, int zscr, const Tsrc* tsrc, int tpitch,
                                      int fa_pitch, uint64_t* bars, uint32_t par) {
-  p1_tail_impl<Tin, R, SIG, Tsrc, FILL>(grp, smem, tm_scr, p, sl, strip, X, zscr, tsrc, tpitch, fa_pitch, bars, par);
+  p1_tail_impl<Tin, R, SIG, Tsrc, FILL>(grp, smem, dst, p, sl, strip, X, zscr, tsrc, tpitch, fa_pitch, bars, par);
 }
 
 template <typename Tin, int R, typename Tsrc, int FILL = 0, bool INL = false, typename G>
-__device__ __forceinline__ void p1_tail_sig(const G& grp, unsigned char* smem, int sigma, const CUtensorMap* tm_scr,
+__device__ __forceinline__ void p1_tail_sig(const G& grp, unsigned char* smem, int sigma, const P1Dst* dst,
                                             const P1Params& p, const P1Slot& sl, int strip, int X, int zscr,
                                             const Tsrc* tsrc, int tpitch, int fa_pitch, uint64_t* bars = nullptr,
                                             uint32_t par = 0) {
   if constexpr (INL) {
     if constexpr (FILL == 1) {
-      p1_tail_impl<Tin, R, 1, Tsrc, 1>(grp, smem, tm_scr, p, sl, strip, X, zscr, tsrc, tpitch, fa_pitch, bars, par);
+      p1_tail_impl<Tin, R, 1, Tsrc, 1>(grp, smem, dst, p, sl, strip, X, zscr, tsrc, tpitch, fa_pitch, bars, par);
     } else {
       if (sigma > 0)
-        p1_tail_impl<Tin, R, 1, Tsrc, 0>(grp, smem, tm_scr, p, sl, strip, X, zscr, tsrc, tpitch, fa_pitch, bars, par);
+        p1_tail_impl<Tin, R, 1, Tsrc, 0>(grp, smem, dst, p, sl, strip, X, zscr, tsrc, tpitch, fa_pitch, bars, par);
       else
-        p1_tail_impl<Tin, R, -1, Tsrc, 0>(grp, smem, tm_scr, p, sl, strip, X, zscr, tsrc, tpitch, fa_pitch, bars, par);
+        p1_tail_impl<Tin, R, -1, Tsrc, 0>(grp, smem, dst, p, sl, strip, X, zscr, tsrc, tpitch, fa_pitch, bars, par);
     }
   } else if constexpr (FILL == 1) {  // the range frame is sigma = +1 only
-    p1_tail<Tin, R, 1, Tsrc, 1>(grp, smem, tm_scr, p, sl, strip, X, zscr, tsrc, tpitch, fa_pitch, bars, par);
+    p1_tail<Tin, R, 1, Tsrc, 1>(grp, smem, dst, p, sl, strip, X, zscr, tsrc, tpitch, fa_pitch, bars, par);
   } else {
     if (sigma > 0)
-      p1_tail<Tin, R, 1, Tsrc, 0>(grp, smem, tm_scr, p, sl, strip, X, zscr, tsrc, tpitch, fa_pitch, bars, par);
+      p1_tail<Tin, R, 1, Tsrc, 0>(grp, smem, dst, p, sl, strip, X, zscr, tsrc, tpitch, fa_pitch, bars, par);
     else
-      p1_tail<Tin, R, -1, Tsrc, 0>(grp, smem, tm_scr, p, sl, strip, X, zscr, tsrc, tpitch, fa_pitch, bars, par);
+      p1_tail<Tin, R, -1, Tsrc, 0>(grp, smem, dst, p, sl, strip, X, zscr, tsrc, tpitch, fa_pitch, bars, par);
   }
 }
 
@@ -544,7 +573,7 @@ __device__ __forceinline__ void p1_tail_sig(const G& grp, unsigned char* smem, i
 // inlined (see p1_tail).
 template <typename Tin, int R, bool INL = false, typename G>
 __device__ __forceinline__ bool p1_body(const G& grp, unsigned char* smem_raw, const CUtensorMap* tm_img0,
-                                        const CUtensorMap* tm_img1, const CUtensorMap* tm_scr, const P1Params& p,
+                                        const CUtensorMap* tm_img1, const P1Dst* dst, const P1Params& p,
                                         const P1Slot& sl, int img, int strip, int X, int zscr,
                                         uint64_t* ext_bars = nullptr, uint32_t par = 0) {
   using A = typename AccOf<Tin>::type;
@@ -560,7 +589,7 @@ __device__ __forceinline__ bool p1_body(const G& grp, unsigned char* smem_raw, c
   // (initialised once, phase parity `par` bit per block: the pipelined kernel)
   uint64_t* bar = ext_bars ? ext_bars : reinterpret_cast<uint64_t*>(tab + 768);
   const Tin* src = static_cast<const Tin*>(p.img) + (int64_t)img * p.img_bstride;
-  const int y0 = strip * NR;
+  const int y0 = (p.strip0 + strip) * NR;  // strip: the launch's (a shard's) local strip index
   const int Xa = sl.sigma > 0 ? X : X - (WA - WC);  // x of input index e = 0
 
   if (p.range && p.fill_tma) {
@@ -630,7 +659,8 @@ __device__ __forceinline__ bool p1_body(const G& grp, unsigned char* smem_raw, c
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         grp.sync();
         if (tid == 0) {
-          tma_store_3d_keep(tm_scr, z, X - sl.xlo, strip, zscr << R);
+          for (int d = 0; d < p.ndst; ++d)
+            tma_store_4d_keep(&dst->m[d], z + (size_t)d * p.jper * p.TX, X - sl.xlo, strip, 0, zscr);
           tma_commit();
         }
         pdl_trigger();
@@ -638,7 +668,7 @@ __device__ __forceinline__ bool p1_body(const G& grp, unsigned char* smem_raw, c
         return true;
       }
     }
-    p1_tail_sig<Tin, R, Tin, 1, INL>(grp, smem_raw, 1, tm_scr, p, sl, strip, X, zscr, static_cast<const Tin*>(tile), TP,
+    p1_tail_sig<Tin, R, Tin, 1, INL>(grp, smem_raw, 1, dst, p, sl, strip, X, zscr, static_cast<const Tin*>(tile), TP,
                                 sizeof(Tin) == 1 ? FA_PITCH : TMA_PITCH, bar, par);
     return true;
   }
@@ -690,10 +720,10 @@ __device__ __forceinline__ bool p1_body(const G& grp, unsigned char* smem_raw, c
     uint64_t* const bars = nullptr;
 #endif
     if constexpr (sizeof(Tin) == 1)
-      p1_tail_sig<Tin, R, Tin, 0, INL>(grp, smem_raw, sl.sigma, tm_scr, p, sl, strip, X, zscr,
+      p1_tail_sig<Tin, R, Tin, 0, INL>(grp, smem_raw, sl.sigma, dst, p, sl, strip, X, zscr,
                                        static_cast<const Tin*>(tile), TP, FA_PITCH, bars, par);
     else
-      p1_tail_sig<Tin, R, A, 0, INL>(grp, smem_raw, sl.sigma, tm_scr, p, sl, strip, X, zscr,
+      p1_tail_sig<Tin, R, A, 0, INL>(grp, smem_raw, sl.sigma, dst, p, sl, strip, X, zscr,
                                      reinterpret_cast<const A*>(tile), TP, TMA_PITCH, bars, par);
     return bars != nullptr;
   }
@@ -797,17 +827,17 @@ __device__ __forceinline__ bool p1_body(const G& grp, unsigned char* smem_raw, c
     }
   }
   grp.sync();
-  p1_tail_sig<Tin, R, A, 0, INL>(grp, smem_raw, sl.sigma, tm_scr, p, sl, strip, X, zscr, static_cast<const A*>(buf),
+  p1_tail_sig<Tin, R, A, 0, INL>(grp, smem_raw, sl.sigma, dst, p, sl, strip, X, zscr, static_cast<const A*>(buf),
                                  FA_PITCH, FA_PITCH);
   return false;
 }
 
 // tm_img0: image [batch][h][w], box 1 x 1 x 256 columns; tm_img1: box 36 (u8: 48) columns;
-// tm_scr: scratch as [z*2^m + j][strip][column], box {TX, 1, 2^m}.
+// dst: where F_m goes (P1Dst; box {TX, 1, jper, 1} each).
 template <typename Tin, int R>
 __global__ void __launch_bounds__(Split<R>::nw * 32, kMinBlocks<R>)
 k_p1(const __grid_constant__ CUtensorMap tm_img0, const __grid_constant__ CUtensorMap tm_img1,
-     const __grid_constant__ CUtensorMap tm_scr, const __grid_constant__ P1Params p) {
+     const __grid_constant__ P1Dst dst, const __grid_constant__ P1Params p) {
   pdl_wait();  // the image may come from the previous kernel; the scratch may still be read by it
   // flat grid, quadrant slot fastest: with 148 SMs (a multiple of 4) the round-robin CTA
   // placement gives every SM CTAs of one slot, i.e. one sign and one fill path (I-cache locality)
@@ -822,7 +852,7 @@ k_p1(const __grid_constant__ CUtensorMap tm_img0, const __grid_constant__ CUtens
   if (n >= sl.ntiles) return;
   const int X = min(sl.xlo + p.TX * n, sl.xhi - p.TX);  // tile = window start (Xw = X)
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  p1_body<Tin, R>(GrpAll{}, smem_raw, &tm_img0, &tm_img1, &tm_scr, p, sl, img, strip, X,
+  p1_body<Tin, R>(GrpAll{}, smem_raw, &tm_img0, &tm_img1, &dst, p, sl, img, strip, X,
                   p.z0 + (img - p.img0) * p.nq + qi);
 }
 
@@ -863,6 +893,11 @@ struct P2Params {
   const int* len_tab;      // range: per-row support length
   int ndest;               // 1 or 2 destinations
   int no_tma;              // debug: write every row with st.global
+  // sharded transform: groups j0 .. j0 + ngroups - 1; strip i of group j is scratch row
+  // rbase(j) + (i >> logS) * strideG + (i & (2^logS - 1)) -- the chunk from rank i >> logS of a receive
+  // buffer [rank][z][j_local][strip_local]. Unsharded: j0 = 0, logS = L (one chunk).
+  int j0, logS;
+  int64_t strideG;
   P2Slot slot[4];
   P2Dest dest[2];
 };
@@ -924,8 +959,9 @@ __device__ __forceinline__ bool p2_body(const G& grp, unsigned char* smem_raw, c
         for (int i = b * NA; i < (b + 1) * NA; ++i) {
           const int a0 = (Xa + SIG * j * i - sl.xlo1) & ~(kAl - 1);
           Tscr* d = reinterpret_cast<Tscr*>(buf + i * TMA_PITCH);
-          tma_load_2d(tm_scr0, d, bar + b, a0, (int)(rbase + i));
-          tma_load_2d(tm_scr1, d + 256, bar + b, a0 + 256, (int)(rbase + i));
+          const int row = (int)(rbase + (int64_t)(i >> p.logS) * p.strideG + (i & ((1 << p.logS) - 1)));
+          tma_load_2d(tm_scr0, d, bar + b, a0, row);
+          tma_load_2d(tm_scr1, d + 256, bar + b, a0 + 256, row);
         }
       }
       if (lane < NA) rowoff[b * NA + lane] = (Xa + SIG * j * (b * NA + lane) - sl.xlo1) & (kAl - 1);
@@ -1066,7 +1102,8 @@ k_p2(const __grid_constant__ CUtensorMap tm_scr0, const __grid_constant__ CUtens
   int id = blockIdx.x;
   const int n = id % p.ntiles;
   id /= p.ntiles;
-  const int j = id % p.ngroups;
+  const int jl = id % p.ngroups;  // the launch's group index; j = j0 + jl is the transform's
+  const int j = p.j0 + jl;
   id /= p.ngroups;
   const int qi = id % p.nq;
   const int img = p.img0 + id / p.nq;
@@ -1092,7 +1129,8 @@ k_p2(const __grid_constant__ CUtensorMap tm_scr0, const __grid_constant__ CUtens
   }
   const int X = k + 1 < nk ? lo + p.TX * k : max(lo, hi - (p.TX + WO2));
   const int own = k + 1 < nk ? p.TX : hi - X;
-  const int64_t rbase = p.row0 + (int64_t)(img - p.img0) * p.scratch_img_rows + sl.srow0 + ((int64_t)j << R);
+  // scratch row of (group j, strip 0): [z][j_local][strip] with p.logS strip bits per chunk
+  const int64_t rbase = p.row0 + (int64_t)(img - p.img0) * p.scratch_img_rows + sl.srow0 + ((int64_t)jl << p.logS);
   extern __shared__ __align__(128) unsigned char smem_raw[];
   if (sl.sigma > 0)
     p2_body<A, R, 1, Tscr>(GrpAll{}, smem_raw, &tm_scr0, &tm_scr1, &tm0, &tm1, &tm0_box, p, sl, img, j, X, own, rbase);

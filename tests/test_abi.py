@@ -343,3 +343,48 @@ def test_workspace_may_not_alias_image():
     d.data = 1 << 42
     n = L.lib.fht_workspace_bytes(L.FHT_MODE_FULL, ctypes.byref(img), None)
     assert L.lib.fht_full(ctypes.byref(img), 0, ctypes.byref(d), None, (1 << 40) + 64, n, None, None) == -1
+
+
+@pytest.mark.parametrize("h,w,b,dt", [(1024, 1024, 1, 2), (2048, 2048, 16, 2), (512, 512, 64, 0), (300, 500, 2, 1)])
+def test_shard_describe_geometry(h, w, b, dt):
+    """fht_shard_describe: S = 2^L / world strips and J = 2^m / world groups per rank,
+    chunks of batch * 4 * J * S scratch rows, a band of Hp / world rows starting at rank * Hp / world."""
+    L = _lib()
+    img = _img(L, h, w, b=b, dt=dt)
+    P = 1 << (max(h, w) - 1).bit_length()
+    K = P.bit_length() - 1
+    Lp = max(K - 6, min(5, (K + 1) // 2))
+    mp_ = K - Lp
+    for world in (1, 2, 4, 8):
+        for rank in range(world):
+            sh = L.FhtShard()
+            r = L.lib.fht_shard_describe(ctypes.byref(img), world, rank, ctypes.byref(sh))
+            if (1 << mp_) % world or (1 << Lp) % world:
+                assert r == -5
+                continue
+            assert r == 0
+            assert (sh.m, sh.L, sh.S, sh.J) == (mp_, Lp, (1 << Lp) // world, (1 << mp_) // world)
+            assert sh.chunk_rows == b * 4 * sh.J * sh.S
+            es = 2 if dt == 0 else 4
+            assert sh.scratch_es == es and sh.chunk_bytes == sh.chunk_rows * sh.pitch * es and sh.chunk_bytes % 16 == 0
+            assert sh.send_bytes == sh.recv_bytes == world * sh.chunk_bytes
+            assert sh.pitch * es % 16 == 0 and sh.pitch >= max(h, w) + (1 << mp_) - 1
+            assert (sh.band.nquad, sh.band.rows, sh.band.cols, sh.band.row0) == (4, P // world, 2 * P, rank * P // world)
+            assert sh.band.batch == b and sh.band.batch_stride == 4 * sh.band.rows * sh.band.row_stride
+
+
+def test_shard_describe_errors():
+    L = _lib()
+    sh = L.FhtShard()
+    img = _img(L, 1024, 1024)
+    assert L.lib.fht_shard_describe(ctypes.byref(img), 3, 0, ctypes.byref(sh)) == -1       # not a power of two
+    assert L.lib.fht_shard_describe(ctypes.byref(img), 2, 2, ctypes.byref(sh)) == -1       # rank out of range
+    assert L.lib.fht_shard_describe(ctypes.byref(img), 16, 0, ctypes.byref(sh)) == -5      # > 8 destinations
+    assert L.lib.fht_shard_describe(ctypes.byref(_img(L, 512, 1024)), 2, 0, ctypes.byref(sh)) == -5  # not square
+    assert L.lib.fht_shard_describe(ctypes.byref(img), 2, 0, None) == -1
+    assert L.lib.fht_shard_describe(ctypes.byref(img), 2, 0, ctypes.byref(sh)) == 0
+    # pass calls check synchronously: a NULL destination list, a mismatched geometry
+    assert L.lib.fht_shard_pass1(ctypes.byref(img), ctypes.byref(sh), None, None) == -1
+    other = L.FhtShard()
+    assert L.lib.fht_shard_describe(ctypes.byref(_img(L, 2048, 2048)), 2, 0, ctypes.byref(other)) == 0
+    assert L.lib.fht_shard_pass2(ctypes.byref(img), ctypes.byref(other), 1 << 40, None, None, None) == -1

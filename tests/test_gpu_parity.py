@@ -776,3 +776,95 @@ def test_pipe_matches_two_launch_and_oracle(fht, O, monkeypatch, shape, dt, batc
         check(got[q, :n], quads[q], dt != "f32")
     if batch > 1:   # one quadrant of a batch: units = images
         check(q1.view[batch - 1, 0].cpu().numpy(), O.hough_recursive(imgs[batch - 1], O.QC), dt != "f32")
+
+
+# ------------------------------------------------------------------ one image over several ranks
+def _emulated_shards(fht, t, world, p2p):
+    """All `world` ranks of a sharded transform run in this process on one GPU (their kernels do not
+    wait on each other, so this is not a multi-rank emulation of waiting kernels): pass 1 of every rank,
+    the all-to-all done as chunk copies (or, p2p, pass 1 storing straight into the receive buffers as
+    the peer-memory path does), pass 2 of every rank. Returns the ranks' (band, band_shifted)."""
+    from paper_1811_06378_b200 import sharding as SH
+    shs = [SH.shard_describe(t, world, r) for r in range(world)]
+    ch = shs[0].chunk_bytes
+    recv = [torch.empty(shs[0].recv_bytes, dtype=torch.uint8, device=t.device) for _ in range(world)]
+    if p2p:
+        for g in range(world):
+            SH.shard_pass1(t, shs[g], [recv[h].data_ptr() + g * ch for h in range(world)])
+    else:
+        send = [torch.empty(shs[0].send_bytes, dtype=torch.uint8, device=t.device) for _ in range(world)]
+        for g in range(world):
+            SH.shard_pass1(t, shs[g], [send[g].data_ptr() + h * ch for h in range(world)])
+        for g in range(world):
+            for h in range(world):
+                recv[h][g * ch:(g + 1) * ch].copy_(send[g][h * ch:(h + 1) * ch])
+    return [SH.shard_pass2(t, shs[h], recv[h], pair=True) for h in range(world)]
+
+
+@pytest.mark.parametrize("shape,dt,batch,world", [((1024, 1024), "f32", 1, 2), ((1024, 1024), "f32", 1, 8),
+                                                  ((512, 512), "u8", 3, 4), ((2048, 2048), "f32", 1, 4),
+                                                  ((300, 500), "i32", 2, 2), ((256, 256), "u8", 1, 8)], ids=str)
+@pytest.mark.parametrize("p2p", [False, True], ids=["nccl-layout", "p2p-stores"])
+def test_shard_bands_equal_full(fht, O, shape, dt, batch, world, p2p):
+    """Concatenated bands of the sharded transform are bit-identical to the one-GPU full transform (same
+    single IEEE add per output, any split of the levels), plain and fhtshift-ed; image 0 against the oracle;
+    the standalone fhtshift of a band (row0) equals the fused one."""
+    from synth import random_image
+    imgs = np.stack([random_image(shape, dt, seed=shape[0] * 3 + b) for b in range(batch)])
+    t = dev(imgs)
+    h, s = fht.full(t, pair=True)
+    bands = _emulated_shards(fht, t, world, p2p)
+    torch.cuda.synchronize()
+    rows = bands[0][0].desc.rows
+    for r, (hb, sb) in enumerate(bands):
+        assert hb.desc.row0 == r * rows and hb.launches == 1
+        assert torch.equal(hb.view, h.view[:, :, r * rows:(r + 1) * rows])
+        assert torch.equal(sb.view, s.view[:, :, r * rows:(r + 1) * rows])
+    s1 = fht.fhtshift(bands[-1][0])
+    torch.cuda.synchronize()
+    assert torch.equal(s1.view, bands[-1][1].view)
+    quads = O.full_quadrants(imgs[0])
+    got = torch.cat([hb.view for hb, _ in bands], dim=2)[0].cpu().numpy()
+    for q in range(4):
+        n = quads[q].shape[0]
+        check(got[q, :n], quads[q], dt != "f32")
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2, reason="needs 2 GPUs")
+def test_shard_two_devices_nccl():
+    """Two ranks on two GPUs over NCCL (torchrun-free: spawned processes): each rank's band equals the
+    corresponding rows of the one-GPU transform. Skipped on one-GPU boxes."""
+    import socket
+    import torch.multiprocessing as mp
+    s_ = socket.socket()
+    s_.bind(("127.0.0.1", 0))
+    port = s_.getsockname()[1]
+    s_.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_nccl_shard_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+    assert res == {0: True, 1: True}
+
+
+def _nccl_shard_worker(rank, world, port, q):
+    import os
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world)
+    import paper_1811_06378_b200 as F
+    from synth import random_image
+    t = torch.from_numpy(random_image((1024, 1024), "f32", seed=5)).cuda()
+    hb, sb = F.full_sharded(t, pair=True)
+    h, s = F.full(t, pair=True)
+    torch.cuda.synchronize()
+    rows = hb.desc.rows
+    ok = torch.equal(hb.view, h.view[:, :, rank * rows:(rank + 1) * rows]) and \
+        torch.equal(sb.view, s.view[:, :, rank * rows:(rank + 1) * rows])
+    q.put((rank, bool(ok)))
+    dist.destroy_process_group()
