@@ -441,12 +441,14 @@ struct Outs {
 struct LaunchLog {
   const fht_exec_opts* opts;
   int n;
+  cudaEvent_t mark_first = nullptr;  // recorded after the first launch (the staggered orientation split)
   void before(cudaStream_t st) {
     if (opts && opts->events && n < opts->n_events) cudaEventRecord((cudaEvent_t)opts->events[n], st);
   }
   void after(cudaStream_t st) {
     ++n;
     if (opts && opts->events && n < opts->n_events) cudaEventRecord((cudaEvent_t)opts->events[n], st);
+    if (mark_first && n == 1) cudaEventRecord(mark_first, st);
   }
 };
 
@@ -1459,21 +1461,31 @@ int fht_full(const fht_image* img, int layout, fht_hough* out, fht_hough* out_sh
   const ScratchPlan sp2 = scratch_plan(f0, 2, img->batch, nullptr, scratch_es(img->dtype));
   const size_t half = (sp2.bytes + 255) & ~size_t(255);
   const bool pipe4 = Hp == Wp && pipe_plan(f0, 4, img->batch, nullptr, scratch_es(img->dtype)).on;
-  if (FHT_SPLIT_ORIENT && aux && !pipe4 && Hp == Wp && use_v2(f0, nullptr) && sp2.nbuf == 1 &&
+  // one image only: for a batch the merged 4-slot launches measured faster (C5 1.386 vs 1.414 ms,
+  // profiles/r02/split_ab.log)
+  if (FHT_SPLIT_ORIENT && aux && !pipe4 && img->batch == 1 && Hp == Wp && use_v2(f0, nullptr) && sp2.nbuf == 1 &&
       sp2.chunk >= img->batch && 2 * half <= ws_bytes) {
-    cudaEvent_t ev[2] = {nullptr, nullptr};
+    cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
     auto destroy = [&]() {
       for (cudaEvent_t e : ev)
         if (e) cudaEventDestroy(e);
     };
+    // FHT_SPLIT_STAGGER=1: the auxiliary orientation starts when the main one's pass 1 has completed, so
+    // its pass 1 runs beside the main pass 2 instead of beside the main pass 1
+    const bool stagger = env_int("FHT_SPLIT_STAGGER", 0) != 0;
     if (cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventRecord(ev[0], (cudaStream_t)stream) != cudaSuccess || cudaStreamWaitEvent(aux, ev[0], 0) != cudaSuccess) {
+        cudaEventCreateWithFlags(&ev[2], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventRecord(ev[0], (cudaStream_t)stream) != cudaSuccess) {
       destroy();
       return FHT_ERR_CUDA;
     }
-    LaunchLog quiet{nullptr, 0};
-    r = run_orientation(img, f0, sl, 2, o, ws, half, (cudaStream_t)stream, nullptr, quiet);
+    LaunchLog quiet{nullptr, 0}, first{nullptr, 0, stagger ? ev[2] : nullptr};
+    r = run_orientation(img, f0, sl, 2, o, ws, half, (cudaStream_t)stream, nullptr, first);
+    if (cudaStreamWaitEvent(aux, stagger ? ev[2] : ev[0], 0) != cudaSuccess) {
+      destroy();
+      return FHT_ERR_CUDA;
+    }
     const int r2 = r < 0 ? r : run_orientation(img, f0, sl + 2, 2, o, static_cast<char*>(ws) + half, half, aux, nullptr,
                                                quiet);
     const bool ok = cudaEventRecord(ev[1], aux) == cudaSuccess &&

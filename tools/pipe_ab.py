@@ -16,10 +16,17 @@ import torch
 import paper_1811_06378_b200 as fht
 import synth
 
-VARIANTS = [("two-launch", {"FHT_PIPE": "0"}), ("pipe D2 N4", {}), ("pipe D1 N3", {"FHT_PIPE_D": "1", "FHT_PIPE_NBUF": "3"}),
-            ("pipe D2 N3", {"FHT_PIPE_D": "2", "FHT_PIPE_NBUF": "3"}), ("pipe D3 N5", {"FHT_PIPE_D": "3", "FHT_PIPE_NBUF": "5"}),
-            ("pipe unit 8MB", {"FHT_PIPE_UNIT_MB": "8"}), ("pipe unit 32MB", {"FHT_PIPE_UNIT_MB": "32"})]
-KEYS = ("FHT_PIPE", "FHT_PIPE_D", "FHT_PIPE_NBUF", "FHT_PIPE_UNIT_MB")
+# (name, environment, auxiliary stream: None = no aux stream, else its priority (0 default, -1 high, 1 low... torch
+# uses lower numbers for higher priority))
+VARIANTS = {
+    "pipe": [("two-launch", {"FHT_PIPE": "0"}, 0), ("pipe D2 N4", {"FHT_PIPE": "1"}, 0),
+             ("pipe D1 N3", {"FHT_PIPE": "1", "FHT_PIPE_D": "1", "FHT_PIPE_NBUF": "3"}, 0),
+             ("pipe D3 N5", {"FHT_PIPE": "1", "FHT_PIPE_D": "3", "FHT_PIPE_NBUF": "5"}, 0)],
+    "split": [("merged (no aux)", {}, None), ("split", {}, 0), ("split stagger", {"FHT_SPLIT_STAGGER": "1"}, 0),
+              ("split stagger, aux high prio", {"FHT_SPLIT_STAGGER": "1"}, -1),
+              ("split, aux high prio", {}, -1)],
+}
+KEYS = ("FHT_PIPE", "FHT_PIPE_D", "FHT_PIPE_NBUF", "FHT_PIPE_UNIT_MB", "FHT_SPLIT_STAGGER")
 
 
 def main():
@@ -27,6 +34,7 @@ def main():
     ap.add_argument("--configs", default="5,2,3")
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--single", action="store_true", help="C2/C5 write only the fhtshift-ed image")
+    ap.add_argument("--set", default="pipe", choices=sorted(VARIANTS))
     args = ap.parse_args()
     dev = torch.device("cuda:0")
     flush = torch.empty(512 << 18, dtype=torch.float32, device=dev)
@@ -34,10 +42,10 @@ def main():
     for cid in [int(c) for c in args.configs.split(",")]:
         cc = synth.CONFIGS[cid]
         t = torch.from_numpy(synth.batch(cid)).to(dev)
-        aux = torch.cuda.Stream()
         small = t.numel() * t.element_size() * 9 < 2 * torch.cuda.get_device_properties(dev).L2_cache_size
         res = {}
-        for name, env in VARIANTS:
+        for name, env, prio in VARIANTS[args.set]:
+            aux = None if prio is None else torch.cuda.Stream(priority=prio)
             for k in KEYS:
                 os.environ.pop(k, None)
             os.environ.update(env)
