@@ -591,6 +591,7 @@ int run_orientation(const fht_image* img, const Frame& f, const Slot* slots, int
       D.ptr = o->data;
       D.pitch = o->row_stride;
       D.rows_per_img = o->batch_stride / o->row_stride;
+      D.nrows = o->batch * D.rows_per_img;
       if (!make_row_map(tm_out[p2.ndest], o->data, o->dtype == FHT_F32, (uint64_t)o->cols,
                         (uint64_t)(o->batch * D.rows_per_img), (uint64_t)o->row_stride, (uint32_t)box2))
         return FHT_ERR_CUDA;
@@ -640,6 +641,7 @@ int run_orientation(const fht_image* img, const Frame& f, const Slot* slots, int
       }
       // pass 2 of groups [rank J, (rank + 1) J) from the received chunks [g][z][j_local][strip_local]
       const uint64_t rows = (uint64_t)sh->world * sh->chunk_rows;
+      p2.scr_rows = (int64_t)rows;
       void* recv = const_cast<void*>(sh->recv);
       if (!make_row_map(&m2s.scr0, recv, f32, (uint64_t)span1, rows, (uint64_t)sp.pitch, 256, 1, ses == 2) ||
           !make_row_map(&m2s.scr1, recv, f32, (uint64_t)span1, rows, (uint64_t)sp.pitch, ses == 2 ? 40 : 36, 1,
@@ -673,6 +675,7 @@ int run_orientation(const fht_image* img, const Frame& f, const Slot* slots, int
     p2.j0 = 0;
     p2.logS = f.L;
     p2.strideG = 0;
+    p2.scr_rows = (int64_t)scr_rows;
     if (!make_dst_map(&m1.dst.m[0], ws, ses, f32, sp.pitch, nstrips, 1 << f.m, (int64_t)(scr_rows / f.Hp), p1.TX,
                       ngroups))
       return FHT_ERR_CUDA;

@@ -15,7 +15,37 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+// Bounds-checked debug build (-DFHT_CHECKS=1; tools/checks_build.sh): every shared-memory access of the
+// tile bodies, every plain global store and every TMA store coordinate is checked, a violation prints
+// and traps. compute-sanitizer is closed on this pool; this build run over the GPU suite stands in.
+#ifndef FHT_CHECKS
+#define FHT_CHECKS 0
+#endif
+#if FHT_CHECKS
+#include <cstdio>
+#define FHT_CHECK(c)                                                                              \
+  do {                                                                                            \
+    if (!(c)) {                                                                                   \
+      printf("FHT_CHECK failed %s:%d (block %d thread %d): %s\n", __FILE__, __LINE__, (int)blockIdx.x, \
+             (int)threadIdx.x, #c);                                                               \
+      __trap();                                                                                   \
+    }                                                                                             \
+  } while (0)
+#else
+#define FHT_CHECK(c) \
+  do {               \
+  } while (0)
+#endif
+
 namespace fht {
+
+// shared-memory access of `bytes` at generic pointer p lies inside the CTA's shared memory
+__device__ __forceinline__ bool smem_in_bounds(const void* p, int bytes) {
+  unsigned total;
+  asm volatile("mov.u32 %0, %%total_smem_size;" : "=r"(total));
+  const unsigned a = (unsigned)__cvta_generic_to_shared(p);
+  return a + (unsigned)bytes <= total;
+}
 
 constexpr int kMaxLog = 6;  // one pass handles <= 6 levels (64-row tiles); Hp <= 4096 in 2 passes
 

@@ -463,6 +463,7 @@ __global__ void __launch_bounds__(kThreads) k_fhtshift(const ShiftArgs a) {
   for (int x = lane; x < a.W; x += 32) {
     int sx = x - k;
     if (sx < 0) sx += a.W;
+    FHT_CHECK(sx >= 0 && sx < a.W);
     __stcs(dst + x, __ldg(src + sx));
   }
 }
@@ -507,6 +508,7 @@ __global__ void __launch_bounds__(kThreads) k_fold(const FoldArgs a) {
       k += k < 0 ? a.W : 0;
       int xs = x0 + k;
       xs -= xs >= a.W ? a.W : 0;
+      FHT_CHECK(xs >= 0 && xs < a.W && k >= 0);
       static_cast<T*>(a.outs)[b * a.outs_batch + (int64_t)s * a.outs_pitch + xs] = acc;
     }
   }

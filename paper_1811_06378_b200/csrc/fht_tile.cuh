@@ -303,6 +303,7 @@ __device__ __forceinline__ void tile_fht_ld(const G& grp, const LoadA& load, A* 
     load(blk, v);
     warp_fht<a, VA>(v);
     A* d = fa + (blk * NA) * fa_pitch + lane * VA;
+    FHT_CHECK(smem_in_bounds(d + (NA - 1) * fa_pitch + VA - 1, sizeof(A)));
 #pragma unroll
     for (int r = 0; r < NA; ++r)
 #pragma unroll
@@ -318,6 +319,7 @@ __device__ __forceinline__ void tile_fht_ld(const G& grp, const LoadA& load, A* 
 #pragma unroll
       for (int i = 0; i < NBk; ++i) {
         const A* s = fa + (i * NA + jp) * fa_pitch + lane * VB + jp * i;
+        FHT_CHECK(smem_in_bounds(s + VB - 1, sizeof(A)) && lane * VB + jp * i + VB <= fa_pitch);
 #pragma unroll
         for (int q = 0; q < VB; ++q) w[g][i][q] = s[q];
       }
@@ -341,6 +343,8 @@ __device__ __forceinline__ void tile_fht(const G& grp, const Tsrc* src, int src_
     for (int r = 0; r < NA; ++r) {
       const int rho = blk * NA + r;
       const Tsrc* p = src + rho * src_pitch + rowoff[rho] + (SIG > 0 ? lane * VA : (WA - 1) - lane * VA);
+      FHT_CHECK(smem_in_bounds(SIG > 0 ? p + VA - 1 : p, sizeof(Tsrc)) &&
+                smem_in_bounds(SIG > 0 ? p : p - (VA - 1), sizeof(Tsrc)));
 #pragma unroll
       for (int q = 0; q < VA; ++q) v[r][q] = static_cast<A>(p[SIG > 0 ? q : -q]);
     }
@@ -384,6 +388,7 @@ __device__ __forceinline__ void stage_rows(const G& grp, A (&w)[kTPW<R>][1 << Sp
         const int tau = jp * NBk + u;
         // lowest window index of the lane's 7 columns, and its staging index
         const int lo = (SIG > 0 ? lane * VB : (WC - VB) - lane * VB) - soff[tau];
+        FHT_CHECK(box <= pitch && smem_in_bounds(stg + tau * pitch + box - 1, sizeof(Sg)));
 #if FHT_STAGE_ASM
         const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(stg + tau * pitch + lo));
         // element q of the lane sits at staging index lo + q
@@ -522,6 +527,7 @@ __device__ __forceinline__ void p1_tail_impl(const G grp, unsigned char* smem, c
   // ---- store F_m[strip][j] for all j: per destination d ONE box {TX, 1, jper, 1} of its 4-D view
   // [z][j][strip][column] (z = image-in-chunk * nq + slot); column X - xlo is 16-B aligned
   if (grp.tid() == 0) {
+    FHT_CHECK(X - sl.xlo >= 0 && X - sl.xlo + p.TX <= sl.xhi - sl.xlo && p.ndst * p.jper <= (1 << R));
     for (int d = 0; d < p.ndst; ++d) {
       const void* src = reinterpret_cast<const Sc*>(buf) + (size_t)d * p.jper * p.TX;
 #if FHT_SCR_KEEP
@@ -875,6 +881,7 @@ struct P2Dest {
   void* ptr;
   int64_t pitch;           // elements
   int64_t rows_per_img;
+  int64_t nrows;           // rows of the destination's [rows_total][W] view (bounds checks)
   int shifted;             // 1 = fused fhtshift (§5) destination
 };
 
@@ -898,6 +905,7 @@ struct P2Params {
   // buffer [rank][z][j_local][strip_local]. Unsharded: j0 = 0, logS = L (one chunk).
   int j0, logS;
   int64_t strideG;
+  int64_t scr_rows;        // rows of the scratch tensor pass 2 reads (bounds checks)
   P2Slot slot[4];
   P2Dest dest[2];
 };
@@ -960,6 +968,7 @@ __device__ __forceinline__ bool p2_body(const G& grp, unsigned char* smem_raw, c
           const int a0 = (Xa + SIG * j * i - sl.xlo1) & ~(kAl - 1);
           Tscr* d = reinterpret_cast<Tscr*>(buf + i * TMA_PITCH);
           const int row = (int)(rbase + (int64_t)(i >> p.logS) * p.strideG + (i & ((1 << p.logS) - 1)));
+          FHT_CHECK(row >= 0 && row < p.scr_rows);
           tma_load_2d(tm_scr0, d, bar + b, a0, row);
           tma_load_2d(tm_scr1, d + 256, bar + b, a0 + 256, row);
         }
@@ -1059,6 +1068,7 @@ __device__ __forceinline__ bool p2_body(const G& grp, unsigned char* smem_raw, c
     }
     if (dense) {
       if (tid == 0) {
+        FHT_CHECK(inf[0].orow >= 0 && inf[0].orow + NR <= D.nrows);
         tma_store_row_stream(tm0_box, buf, inf[0].d0 & ~kTmaBit, inf[0].orow);  // box {box, NR}
         tma_commit();
         issued = true;
@@ -1066,6 +1076,7 @@ __device__ __forceinline__ bool p2_body(const G& grp, unsigned char* smem_raw, c
     } else {
       if (tid < NR && (inf[tid].d0 & kTmaBit)) {  // one row store per thread
         const RowInfo ri = inf[tid];
+        FHT_CHECK((ri.d0 & ~kTmaBit) >= 0 && (ri.d0 & ~kTmaBit) < p.W && ri.orow >= 0 && ri.orow < D.nrows);
         tma_store_row_stream(d == 0 ? tm0 : tm1, buf + tid * ST_PITCH, ri.d0 & ~kTmaBit, ri.orow);  // clipped at W
         tma_commit();
         issued = true;
@@ -1079,6 +1090,7 @@ __device__ __forceinline__ bool p2_body(const G& grp, unsigned char* smem_raw, c
         for (int x = ri.mlo + lane; x < ri.mhi; x += 32) {
           int col = d0 + (x - xs0);
           if (col >= p.W) col -= p.W;
+          FHT_CHECK(col >= 0 && col < p.W && ri.orow >= 0 && ri.orow < D.nrows && x - xs0 >= 0 && x - xs0 < ST_PITCH);
           __stcs(drow + col, srow[x - xs0]);
         }
       }
