@@ -22,11 +22,16 @@ VARIANTS = {
     "pipe": [("two-launch", {"FHT_PIPE": "0"}, 0), ("pipe D2 N4", {"FHT_PIPE": "1"}, 0),
              ("pipe D1 N3", {"FHT_PIPE": "1", "FHT_PIPE_D": "1", "FHT_PIPE_NBUF": "3"}, 0),
              ("pipe D3 N5", {"FHT_PIPE": "1", "FHT_PIPE_D": "3", "FHT_PIPE_NBUF": "5"}, 0)],
+    "chunks": [("one chunk", {}, None), ("70 MB chunks (1 image)", {"FHT_SCRATCH_BUDGET_MB": "70"}, None),
+               ("140 MB chunks (2 images)", {"FHT_SCRATCH_BUDGET_MB": "140"}, None),
+               ("280 MB chunks (4 images)", {"FHT_SCRATCH_BUDGET_MB": "280"}, None),
+               ("70 MB chunks + aux", {"FHT_SCRATCH_BUDGET_MB": "70"}, 0),
+               ("140 MB chunks + aux", {"FHT_SCRATCH_BUDGET_MB": "140"}, 0)],
     "split": [("merged (no aux)", {}, None), ("split", {}, 0), ("split stagger", {"FHT_SPLIT_STAGGER": "1"}, 0),
               ("split stagger, aux high prio", {"FHT_SPLIT_STAGGER": "1"}, -1),
               ("split, aux high prio", {}, -1)],
 }
-KEYS = ("FHT_PIPE", "FHT_PIPE_D", "FHT_PIPE_NBUF", "FHT_PIPE_UNIT_MB", "FHT_SPLIT_STAGGER")
+KEYS = ("FHT_PIPE", "FHT_PIPE_D", "FHT_PIPE_NBUF", "FHT_PIPE_UNIT_MB", "FHT_SPLIT_STAGGER", "FHT_SCRATCH_BUDGET_MB")
 
 
 def main():

@@ -25,8 +25,9 @@ def main():
         h, s = fht.full(t, pair=True)                 # 4-slot merged pass pair, fused fhtshift
         fht.fhtshift(h)
         fht.full(t, layout="concat", shifted=True)
-        fht.quadrant(t, fht.QC, pad=3, pair=True)    # fold path
-        fht.quadrant(t, fht.QB, pad=shape[0] + 5)    # direct pad path
+        if min(shape) >= 8:                          # (pads other than Hp need the v2 tiling)
+            fht.quadrant(t, fht.QC, pad=3, pair=True)    # fold path
+            fht.quadrant(t, fht.QB, pad=shape[0] + 5)    # direct pad path
         fht.peaks(h, 8)
         n += 7
     t = torch.from_numpy(random_image((256, 256), "f32", seed=2)).to(dev)
