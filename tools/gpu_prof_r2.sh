@@ -15,3 +15,13 @@ ncu --set full --clock-control none -k regex:"k_p1|k_p2" -s 2 -c 2 -o gpurun_out
 python tools/prof_call.py --config 4 > gpurun_out/plain4.log 2>&1 && \
 ncu --set full --clock-control none -k regex:"k_p1|k_p2|k_range" -s 3 -c 3 -o gpurun_out/prof_c4 python tools/prof_call.py --config 4 > gpurun_out/ncu_c4.log 2>&1
 ls -la gpurun_out/*.ncu-rep
+# summarise on the box and keep only the C5 / C2 reports (gpurun brings back <= 64 MiB)
+for r in c5_p2 c5s_p2 c2 c3 c4; do
+  python tools/ncu_report.py gpurun_out/prof_$r.ncu-rep "$r" > gpurun_out/ncu_$r.txt 2>&1
+done
+python tools/ncu_summary.py gpurun_out/prof_c5_p2.ncu-rep c5_full_f32_16x2048 > gpurun_out/sum_c5.txt 2>&1
+python tools/ncu_summary.py gpurun_out/prof_c2.ncu-rep c2_full_f32_1024 > gpurun_out/sum_c2.txt 2>&1
+python tools/ncu_summary.py gpurun_out/prof_c3.ncu-rep c3_full_u8_64x512 > gpurun_out/sum_c3.txt 2>&1
+python tools/ncu_summary.py gpurun_out/prof_c4.ncu-rep c4_range_f32_4096 > gpurun_out/sum_c4.txt 2>&1
+rm -f gpurun_out/prof_c5s_p2.ncu-rep gpurun_out/prof_c3.ncu-rep gpurun_out/prof_c4.ncu-rep
+du -sh gpurun_out
