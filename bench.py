@@ -424,14 +424,16 @@ def main():
         comp = torch.cuda.Stream(device=dev)
         down = torch.cuda.Stream(device=dev)
         slots = []
-        for _ in range(2):
+        # two slots pipeline consecutive steps; under torchrun one slot per rank (the pinned host buffers of
+        # C5's 4.3 GB of outputs per slot would be multiplied by every rank on the node)
+        for _ in range(2 if world == 1 else 1):
             t_dev = torch.empty(pinned_in.shape, dtype=pinned_in.dtype, device=dev)
             outs = {}
             slots.append({"t": t_dev, "outs": outs, "step": make_step(fht, cfg_id, cc, t_dev, outs, plan),
                           "host": {}, "done": torch.cuda.Event(), "free": torch.cuda.Event()})
 
         def run(i):
-            sl = slots[i % 2]
+            sl = slots[i % len(slots)]
             with torch.cuda.stream(comp):
                 comp.wait_event(sl["free"])            # this slot's previous download has finished
                 sl["t"].copy_(pinned_in, non_blocking=True)
@@ -466,7 +468,8 @@ def main():
         ms = max_over_ranks(t0.elapsed_time(t1) / steps)
         return {"value": px * world / (ms * 1e-3) / 1e9, "unit": "Gpixel/s", "h2d_bytes_per_step": hb,
                 "d2h_bytes_per_step": db, "ms_per_step": ms,
-                "pipeline": "two slots: upload + transform of step i+1 overlap the download of step i"}
+                "pipeline": ("two slots: upload + transform of step i+1 overlap the download of step i" if len(slots) == 2
+                             else "one slot per rank (torchrun): upload, transform, download in sequence")}
 
     def shift_standalone(cfg_id, steps=20):
         """SURVEY a7 standalone fhtshift (one warp per row, 16-byte rotation) on the config's Hough
