@@ -288,9 +288,11 @@ __device__ __forceinline__ void warp_fht(A (&v)[1 << NB][V]) {
 // ------------------------------------------------------------------------------------------
 // The loader fills v[r][q] = input (row blk*2^a + r, x-order index e) for the lane's columns,
 // e = lane*VA + q (SIG = +1) or (WA - 1) - lane*VA - q (SIG = -1).
+// jp_lim: sub-pass-B groups computed (rows tau < jp_lim * 2^b; the others are not needed: a pruned plan's pass 1
+// stores only its first shifts)
 template <int R, int SIG, typename A, typename LoadA, typename G>
 __device__ __forceinline__ void tile_fht_ld(const G& grp, const LoadA& load, A* fa, int fa_pitch,
-                                            A (&w)[kTPW<R>][1 << Split<R>::b][VB]) {
+                                            A (&w)[kTPW<R>][1 << Split<R>::b][VB], int jp_lim = 1 << Split<R>::a) {
   using S = Split<R>;
   constexpr int a = S::a, b = S::b, NW = S::nw;
   constexpr int NA = 1 << a, NBk = 1 << b;
@@ -315,7 +317,7 @@ __device__ __forceinline__ void tile_fht_ld(const G& grp, const LoadA& load, A* 
 #pragma unroll
   for (int g = 0; g < kTPW<R>; ++g) {
     const int jp = warp + g * NW;
-    if (jp < NA) {
+    if (jp < NA && jp < jp_lim) {
 #pragma unroll
       for (int i = 0; i < NBk; ++i) {
         const A* s = fa + (i * NA + jp) * fa_pitch + lane * VB + jp * i;
@@ -334,7 +336,8 @@ __device__ __forceinline__ void tile_fht_ld(const G& grp, const LoadA& load, A* 
 template <int R, int SIG, typename A, typename Tsrc, typename G>
 __device__ __forceinline__ void tile_fht(const G& grp, const Tsrc* src, int src_pitch, const int* rowoff, A* fa,
                                          int fa_pitch, A (&w)[kTPW<R>][1 << Split<R>::b][VB],
-                                         uint64_t* blk_bars = nullptr, uint32_t par = 0) {
+                                         uint64_t* blk_bars = nullptr, uint32_t par = 0,
+                                         int jp_lim = 1 << Split<R>::a) {
   constexpr int NA = 1 << Split<R>::a;
   const int lane = threadIdx.x & 31;
   auto load = [&](int blk, A (&v)[NA][VA]) {
@@ -349,7 +352,7 @@ __device__ __forceinline__ void tile_fht(const G& grp, const Tsrc* src, int src_
       for (int q = 0; q < VA; ++q) v[r][q] = static_cast<A>(p[SIG > 0 ? q : -q]);
     }
   };
-  tile_fht_ld<R, SIG, A>(grp, load, fa, fa_pitch, w);
+  tile_fht_ld<R, SIG, A>(grp, load, fa, fa_pitch, w, jp_lim);
 }
 
 // Sg: the staged element type (A, or uint16_t for the u8 pipeline's pass-1 scratch)
@@ -375,14 +378,14 @@ __device__ __forceinline__ void st_pred_row(uint32_t a, int lo, int box, const A
 // ISETP + one STS per element, no branches). Then fence for the TMA engine and synchronise.
 template <int R, int SIG, typename A, typename Sg = A, typename G = GrpAll>
 __device__ __forceinline__ void stage_rows(const G& grp, A (&w)[kTPW<R>][1 << Split<R>::b][VB], Sg* stg,
-                                           const int* soff, int box, int pitch) {
+                                           const int* soff, int box, int pitch, int jp_lim = 1 << Split<R>::a) {
   using S = Split<R>;
   constexpr int NA = 1 << S::a, NBk = 1 << S::b, NW = S::nw;
   const int warp = grp.tid() >> 5, lane = threadIdx.x & 31;
 #pragma unroll
   for (int g = 0; g < kTPW<R>; ++g) {
     const int jp = warp + g * NW;
-    if (jp < NA && lane < 31) {
+    if (jp < NA && jp < jp_lim && lane < 31) {
 #pragma unroll
       for (int u = 0; u < NBk; ++u) {
         const int tau = jp * NBk + u;
@@ -476,6 +479,8 @@ __device__ __forceinline__ void p1_tail_impl(const G grp, unsigned char* smem, c
   using S = Split<R>;
   A* buf = reinterpret_cast<A*>(smem);
   unsigned char* tab = smem + main_buf_bytes(R) + (sizeof(Tin) == 1 ? u8_tile_bytes(R) : 0);
+  // only the shifts j < ndst * jper are stored (a pruned plan's groups): sub-pass-B groups past them are skipped
+  const int jp_lim = (p.ndst * p.jper + (1 << S::b) - 1) >> S::b;
   const int* rowoff = reinterpret_cast<const int*>(tab);
   const int* soff = rowoff + 64;
   A w[kTPW<R>][1 << S::b][VB];
@@ -517,13 +522,13 @@ __device__ __forceinline__ void p1_tail_impl(const G grp, unsigned char* smem, c
         }
       }
     };
-    tile_fht_ld<R, SIG, A>(grp, load, buf, fa_pitch, w);
+    tile_fht_ld<R, SIG, A>(grp, load, buf, fa_pitch, w, jp_lim);
   } else {
-    tile_fht<R, SIG, A>(grp, tsrc, tpitch, rowoff, buf, fa_pitch, w, bars, par);
+    tile_fht<R, SIG, A>(grp, tsrc, tpitch, rowoff, buf, fa_pitch, w, bars, par, jp_lim);
   }
   // dense [NR][TX] in the scratch type (u8 input: uint16), the box layout
   using Sc = typename ScrOf<Tin>::type;
-  stage_rows<R, SIG, A, Sc>(grp, w, reinterpret_cast<Sc*>(buf), soff, p.TX, p.TX);
+  stage_rows<R, SIG, A, Sc>(grp, w, reinterpret_cast<Sc*>(buf), soff, p.TX, p.TX, jp_lim);
   // ---- store F_m[strip][j] for all j: per destination d ONE box {TX, 1, jper, 1} of its 4-D view
   // [z][j][strip][column] (z = image-in-chunk * nq + slot); column X - xlo is 16-B aligned
   if (grp.tid() == 0) {
