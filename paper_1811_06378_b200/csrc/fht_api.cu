@@ -1466,7 +1466,7 @@ int fht_full(const fht_image* img, int layout, fht_hough* out, fht_hough* out_sh
   const bool pipe4 = Hp == Wp && pipe_plan(f0, 4, img->batch, nullptr, scratch_es(img->dtype)).on;
   // one image only: for a batch the merged 4-slot launches measured faster (C5 1.386 vs 1.414 ms,
   // profiles/r02/split_ab.log)
-  if (FHT_SPLIT_ORIENT && aux && !pipe4 && img->batch == 1 && Hp == Wp && use_v2(f0, nullptr) && sp2.nbuf == 1 &&
+  if (FHT_SPLIT_ORIENT && aux && !pipe4 && (img->batch == 1 || env_int("FHT_SPLIT_BATCH", 0)) && Hp == Wp && use_v2(f0, nullptr) && sp2.nbuf == 1 &&
       sp2.chunk >= img->batch && 2 * half <= ws_bytes) {
     cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
     auto destroy = [&]() {

@@ -27,11 +27,11 @@ VARIANTS = {
                ("280 MB chunks (4 images)", {"FHT_SCRATCH_BUDGET_MB": "280"}, None),
                ("70 MB chunks + aux", {"FHT_SCRATCH_BUDGET_MB": "70"}, 0),
                ("140 MB chunks + aux", {"FHT_SCRATCH_BUDGET_MB": "140"}, 0)],
-    "split": [("merged (no aux)", {}, None), ("split", {}, 0), ("split stagger", {"FHT_SPLIT_STAGGER": "1"}, 0),
-              ("split stagger, aux high prio", {"FHT_SPLIT_STAGGER": "1"}, -1),
-              ("split, aux high prio", {}, -1)],
+    "split": [("merged (no aux)", {}, None), ("split", {"FHT_SPLIT_BATCH": "1"}, 0), ("split stagger", {"FHT_SPLIT_STAGGER": "1", "FHT_SPLIT_BATCH": "1"}, 0),
+              ("split stagger, aux high prio", {"FHT_SPLIT_STAGGER": "1", "FHT_SPLIT_BATCH": "1"}, -1),
+              ("split, aux high prio", {"FHT_SPLIT_BATCH": "1"}, -1)],
 }
-KEYS = ("FHT_PIPE", "FHT_PIPE_D", "FHT_PIPE_NBUF", "FHT_PIPE_UNIT_MB", "FHT_SPLIT_STAGGER", "FHT_SCRATCH_BUDGET_MB")
+KEYS = ("FHT_PIPE", "FHT_PIPE_D", "FHT_PIPE_NBUF", "FHT_PIPE_UNIT_MB", "FHT_SPLIT_STAGGER", "FHT_SCRATCH_BUDGET_MB", "FHT_SPLIT_BATCH")
 
 
 def main():
