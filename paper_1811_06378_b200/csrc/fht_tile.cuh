@@ -68,6 +68,12 @@
 #ifndef FHT_PDL
 #define FHT_PDL 1         // programmatic dependent launch between the passes (griddepcontrol)
 #endif
+#ifndef FHT_P2_UNPRED
+#define FHT_P2_UNPRED 1   // pass 2: row staging planes with slack, stored without bounds predicates
+#endif
+#ifndef FHT_P1_STAGE2
+#define FHT_P1_STAGE2 1   // pass 1: full-width tiles predicate only the last staged column
+#endif
 
 namespace fht {
 namespace v2 {
@@ -115,6 +121,7 @@ constexpr int FA_PITCH = WA + 1; // 289: odd pitch (A results; conflict-free tra
 constexpr int TMA_PITCH = 320;   // TMA-loaded 4-byte rows: 292 used, 1280-B (128-B multiple) pitch
 constexpr int TMA_PITCH_U8 = 384;// TMA-loaded 1-byte rows: 304 used, 384-B pitch
 constexpr int ST_PITCH = 224;    // staging pitch (elements): 896 B rows, 128-B aligned for TMA
+constexpr int kStgOff = 32;      // row planes start 128 B into the buffer (a margin for row 0's out-of-box columns)
 constexpr int TX1 = 216;         // pass-1 tile width (= its TMA box), multiple of 4
 constexpr int BOX2 = 212;        // pass-2 store box width (multiple of 4)
 constexpr int WO2 = 4;           // pass-2 window starts 4 columns left of the tile's own columns
@@ -376,7 +383,11 @@ __device__ __forceinline__ void st_pred_row(uint32_t a, int lo, int box, const A
 // Write the register results into a staging plane of row pitch `pitch`: output row tau, window
 // index s stored at s - soff[tau] when 0 <= that < box. Explicitly predicated st.shared (one
 // ISETP + one STS per element, no branches). Then fence for the TMA engine and synchronise.
-template <int R, int SIG, typename A, typename Sg = A, typename G = GrpAll>
+// PRED = 0: no bounds predicates -- the plane has slack around every row (staging indices [-4, WC) land inside
+// the pitch, row 0's negatives in a margin before the plane), so the out-of-box columns are written and never read.
+// PRED = 2: soff == 0 and box >= WC - 1 (pass 1's full-width tiles): only a lane's last column can fall outside
+// (window index WC - 1 = 216 of a 216-wide box), so only that store is predicated.
+template <int R, int SIG, typename A, typename Sg = A, typename G = GrpAll, int PRED = 1>
 __device__ __forceinline__ void stage_rows(const G& grp, A (&w)[kTPW<R>][1 << Split<R>::b][VB], Sg* stg,
                                            const int* soff, int box, int pitch, int jp_lim = 1 << Split<R>::a) {
   using S = Split<R>;
@@ -392,6 +403,20 @@ __device__ __forceinline__ void stage_rows(const G& grp, A (&w)[kTPW<R>][1 << Sp
         // lowest window index of the lane's 7 columns, and its staging index
         const int lo = (SIG > 0 ? lane * VB : (WC - VB) - lane * VB) - soff[tau];
         FHT_CHECK(box <= pitch && smem_in_bounds(stg + tau * pitch + box - 1, sizeof(Sg)));
+        if constexpr (PRED == 2) {
+          Sg* dst = stg + tau * pitch + lo;
+#pragma unroll
+          for (int q = 0; q < VB - 1; ++q) dst[q] = static_cast<Sg>(w[g][u][SIG > 0 ? q : VB - 1 - q]);
+          if (lo + VB - 1 < box) dst[VB - 1] = static_cast<Sg>(w[g][u][SIG > 0 ? VB - 1 : 0]);
+          continue;
+        }
+        if constexpr (PRED == 0) {
+          Sg* dst = stg + tau * pitch + lo;
+          FHT_CHECK(lo >= -4 && lo + VB <= pitch - 4 && smem_in_bounds(dst, sizeof(Sg)));
+#pragma unroll
+          for (int q = 0; q < VB; ++q) dst[q] = static_cast<Sg>(w[g][u][SIG > 0 ? q : VB - 1 - q]);
+          continue;
+        }
 #if FHT_STAGE_ASM
         const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(stg + tau * pitch + lo));
         // element q of the lane sits at staging index lo + q
@@ -528,7 +553,10 @@ __device__ __forceinline__ void p1_tail_impl(const G grp, unsigned char* smem, c
   }
   // dense [NR][TX] in the scratch type (u8 input: uint16), the box layout
   using Sc = typename ScrOf<Tin>::type;
-  stage_rows<R, SIG, A, Sc>(grp, w, reinterpret_cast<Sc*>(buf), soff, p.TX, p.TX, jp_lim);
+  if (FHT_P1_STAGE2 && p.TX >= WC - 1)  // full-width tile (soff = 0): only the window's last column can fall outside
+    stage_rows<R, SIG, A, Sc, G, 2>(grp, w, reinterpret_cast<Sc*>(buf), soff, p.TX, p.TX, jp_lim);
+  else
+    stage_rows<R, SIG, A, Sc>(grp, w, reinterpret_cast<Sc*>(buf), soff, p.TX, p.TX, jp_lim);
   // ---- store F_m[strip][j] for all j: per destination d ONE box {TX, 1, jper, 1} of its 4-D view
   // [z][j][strip][column] (z = image-in-chunk * nq + slot); column X - xlo is 16-B aligned
   if (grp.tid() == 0) {
@@ -1064,10 +1092,16 @@ __device__ __forceinline__ bool p2_body(const G& grp, unsigned char* smem_raw, c
                        tmax < p.rows_out &&
                        (inf[0].d0 & kTmaBit) && inf[0].mlo >= inf[0].mhi;
     const int pitch = dense ? box : ST_PITCH;
+    // the dense plane is the 2-D box itself (predicated staging); row planes start kStgOff elements in, with slack
+    // around every row, and stage without predicates
+    A* const stg = (dense || !FHT_P2_UNPRED) ? buf : buf + kStgOff;
     if (!black) {
-      stage_rows<R, SIG, A>(grp, w, buf, so, pitch, pitch);  // every computed column that fits the row
+      if (dense || !FHT_P2_UNPRED)
+        stage_rows<R, SIG, A>(grp, w, stg, so, pitch, pitch);  // every computed column that fits the row
+      else
+        stage_rows<R, SIG, A, A, G, 0>(grp, w, stg, so, pitch, pitch);
     } else {  // every output of a black tile is 0 (no pattern touches a pixel)
-      for (int idx = tid; idx < NR * pitch; idx += NT) buf[idx] = A(0);
+      for (int idx = tid; idx < NR * pitch; idx += NT) stg[idx] = A(0);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       grp.sync();
     }
@@ -1082,7 +1116,7 @@ __device__ __forceinline__ bool p2_body(const G& grp, unsigned char* smem_raw, c
       if (tid < NR && (inf[tid].d0 & kTmaBit)) {  // one row store per thread
         const RowInfo ri = inf[tid];
         FHT_CHECK((ri.d0 & ~kTmaBit) >= 0 && (ri.d0 & ~kTmaBit) < p.W && ri.orow >= 0 && ri.orow < D.nrows);
-        tma_store_row_stream(d == 0 ? tm0 : tm1, buf + tid * ST_PITCH, ri.d0 & ~kTmaBit, ri.orow);  // clipped at W
+        tma_store_row_stream(d == 0 ? tm0 : tm1, stg + tid * ST_PITCH, ri.d0 & ~kTmaBit, ri.orow);  // clipped at W
         tma_commit();
         issued = true;
       }
@@ -1090,7 +1124,7 @@ __device__ __forceinline__ bool p2_body(const G& grp, unsigned char* smem_raw, c
         const RowInfo ri = inf[tau];
         if (ri.mlo >= ri.mhi) continue;
         A* drow = static_cast<A*>(D.ptr) + (int64_t)ri.orow * D.pitch;
-        const A* srow = buf + tau * ST_PITCH;
+        const A* srow = stg + tau * ST_PITCH;
         const int xs0 = X - (WO2 - so[tau]), d0 = ri.d0 & ~kTmaBit;
         for (int x = ri.mlo + lane; x < ri.mhi; x += 32) {
           int col = d0 + (x - xs0);

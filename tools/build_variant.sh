@@ -3,5 +3,8 @@
 set -e
 cd "$(dirname "$0")/.."
 mkdir -p build/ab
-nvcc -gencode arch=compute_100a,code=sm_100a -lineinfo -O3 -std=c++17 -Xcompiler -fPIC,-O2,-ffp-contract=off -shared \
-  -I include $2 -o build/ab/$1.so paper_1811_06378_b200/csrc/fht_api.cu
+python -c "
+import sys; sys.path.insert(0, '.')
+import __graft_entry__ as g
+import os; g.build(out=os.path.abspath('build/ab/$1.so'), extra_flags='$2'.split(), load=False)
+"
