@@ -488,6 +488,7 @@ int run_orientation(const fht_image* img, const Frame& f, const Slot* slots, int
     p1.img_h = (int)img->h;
     p1.img_w = (int)img->w;
     p1.nq = nq;
+    p1.nq_log = nq == 4 ? 2 : nq == 2 ? 1 : 0;
     p1.L = f.L;
     p1.scratch_img_rows = (int64_t)nq * f.Hp;
     const bool pitch16 = aligned16(img->data) && (img->row_stride * es) % 16 == 0 &&
@@ -536,6 +537,7 @@ int run_orientation(const fht_image* img, const Frame& f, const Slot* slots, int
       p2.no_tma = (e && e[0] == '1') ? 1 : 0;
     }
     p2.nq = nq;
+    p2.nq_log = p1.nq_log;
     p2.W = any ? (int)any->cols : f.W;
     p2.Hp = f.Hp;
     p2.wc = f.wc;
@@ -627,7 +629,7 @@ int run_orientation(const fht_image* img, const Frame& f, const Slot* slots, int
           m1s.img0 = m1s.dst.m[0];
           m1s.img1 = m1s.dst.m[0];
         }
-        const dim3 g1((unsigned)(ntile1 * sh->S * img->batch * nq));
+        const dim3 g1((unsigned)(ntile1 * nq), (unsigned)sh->S, (unsigned)img->batch);
         log.before(st);
         cudaError_t e;
         switch (img->dtype) {
@@ -657,7 +659,7 @@ int run_orientation(const fht_image* img, const Frame& f, const Slot* slots, int
       p2.ntiles = ntile2;
       p2.m = f.m;
       p2.ngroups = (int)sh->J;
-      const dim3 g2((unsigned)(ntile2 * sh->J * img->batch * nq));
+      const dim3 g2((unsigned)ntile2, (unsigned)sh->J, (unsigned)(img->batch * nq));
       log.before(st);
       const cudaError_t e = f32 ? launch_p2<float>(f.L, g2, m2s, p2, st)
                                 : ses == 2 ? launch_p2<int, uint16_t>(f.L, g2, m2s, p2, st)
@@ -759,7 +761,7 @@ int run_orientation(const fht_image* img, const Frame& f, const Slot* slots, int
       p1.z0 = buf * sp.chunk * nq;
       p2.row0 = buf * chunk_rows;
       p1.ntiles = ntile1;
-      dim3 g1((unsigned)(ntile1 * nstrips * nb * nq));
+      dim3 g1((unsigned)(ntile1 * nq), (unsigned)nstrips, (unsigned)nb);
       cudaStream_t s1 = aux ? aux : st;
       if (aux && k >= 2 && cudaStreamWaitEvent(aux, ev_p2[buf], 0) != cudaSuccess) {
         destroy_events();
@@ -785,7 +787,7 @@ int run_orientation(const fht_image* img, const Frame& f, const Slot* slots, int
       p2.ntiles = ntile2;
       p2.m = f.m;
       p2.ngroups = ngroups;
-      dim3 g2((unsigned)(ntile2 * ngroups * nb * nq));
+      dim3 g2((unsigned)ntile2, (unsigned)ngroups, (unsigned)(nb * nq));
       e = f32 ? launch_p2<float>(f.L, g2, m2, p2, st)
               : ses == 2 ? launch_p2<int, uint16_t>(f.L, g2, m2, p2, st) : launch_p2<int>(f.L, g2, m2, p2, st);
       if (e != cudaSuccess) {

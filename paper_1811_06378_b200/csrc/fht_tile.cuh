@@ -470,6 +470,7 @@ struct P1Params {
   int64_t scratch_img_rows;          // scratch rows per image
   int z0;                            // first z (= image-in-chunk * nq + slot) of this scratch buffer
   int strip0;                        // first strip of the launch (image rows from strip0 * 2^m): a shard's strips
+  int nq_log;                        // log2 nq (1, 2 or 4 slots)
   int ndst;                          // scratch destinations (P1Dst): 1, or one per rank of a sharded transform
   int jper;                          // shifts j per destination (ngroups / ndst)
   P1Slot slot[4];
@@ -821,18 +822,28 @@ __device__ __forceinline__ bool p1_body(const G& grp, unsigned char* smem_raw, c
     // thread's loads are issued before its first store (memory-level parallelism).
     constexpr int YQ = NR >= 4 ? NR / 4 : 1;  // threads per image row
     constexpr int IT = (WA * YQ + NT - 1) / NT;
+    constexpr int ES = NT / YQ;                // image rows per iteration (NT is a multiple of YQ)
+    static_assert(NT % YQ == 0, "whole image rows per iteration");
     using V4 = typename std::conditional<sizeof(Tin) == 1, uchar4,
                typename std::conditional<std::is_same<Tin, float>::value, float4, int4>::type>::type;
+    // a thread's 4 image columns (yq) are fixed; its image row advances by ES per iteration: one base pointer
+    // and a constant stride instead of a 64-bit multiply and the divisions per element (the fill was ~19% of
+    // the 64-row pass 1's instructions)
+    const int yq = tid & (YQ - 1), e0 = tid / YQ;
+    const int y = y0 + 4 * yq;
+    const bool yfull = y + 3 < p.img_w;
+    const Tin* base = src + (int64_t)(Xa + e0) * p.img_rstride + y;
+    const int64_t step = (int64_t)ES * p.img_rstride;
+    // every image row of the tile inside the image: no per-iteration row check
+    const bool rows_in = Xa >= 0 && Xa + WA <= p.img_h;
     V4 vals[IT];
 #pragma unroll
     for (int it = 0; it < IT; ++it) {
-      const int idx = tid + it * NT;
-      const int e = idx / YQ, yq = idx - e * YQ;
-      const int x = Xa + e, y = y0 + 4 * yq;
+      const int e = e0 + it * ES, x = Xa + e;
       vals[it] = V4{};
-      if (idx < WA * YQ && x >= 0 && x < p.img_h) {
-        const Tin* ps = src + (int64_t)x * p.img_rstride + y;
-        if (y + 3 < p.img_w) {
+      const Tin* ps = base + it * step;
+      if (e < WA && (rows_in || (x >= 0 && x < p.img_h))) {
+        if (yfull) {
           vals[it] = __ldg(reinterpret_cast<const V4*>(ps));
         } else {
           Tin t[4] = {Tin(0), Tin(0), Tin(0), Tin(0)};
@@ -844,12 +855,11 @@ __device__ __forceinline__ bool p1_body(const G& grp, unsigned char* smem_raw, c
         }
       }
     }
+    A* const dbase = buf + (4 * yq) * FA_PITCH + e0;
 #pragma unroll
     for (int it = 0; it < IT; ++it) {
-      const int idx = tid + it * NT;
-      if (idx < WA * YQ) {
-        const int e = idx / YQ, yq = idx - e * YQ;
-        A* d = buf + (4 * yq) * FA_PITCH + e;
+      if (e0 + it * ES < WA) {
+        A* d = dbase + it * ES;
         d[0] = static_cast<A>(vals[it].x);
         d[FA_PITCH] = static_cast<A>(vals[it].y);
         d[2 * FA_PITCH] = static_cast<A>(vals[it].z);
@@ -880,13 +890,11 @@ k_p1(const __grid_constant__ CUtensorMap tm_img0, const __grid_constant__ CUtens
   pdl_wait();  // the image may come from the previous kernel; the scratch may still be read by it
   // flat grid, quadrant slot fastest: with 148 SMs (a multiple of 4) the round-robin CTA
   // placement gives every SM CTAs of one slot, i.e. one sign and one fill path (I-cache locality)
-  int id = blockIdx.x;
-  const int qi = id % p.nq;
-  id /= p.nq;
-  const int n = id % p.ntiles;
-  id /= p.ntiles;
-  const int strip = id & ((1 << p.L) - 1);
-  const int img = p.img0 + (id >> p.L);
+  // grid (ntiles * nq, strips, images): no integer division (it was 4% of the kernel's instructions)
+  const int qi = blockIdx.x & ((1 << p.nq_log) - 1);
+  const int n = blockIdx.x >> p.nq_log;
+  const int strip = blockIdx.y;
+  const int img = p.img0 + blockIdx.z;
   const P1Slot& sl = p.slot[qi];
   if (n >= sl.ntiles) return;
   const int X = min(sl.xlo + p.TX * n, sl.xhi - p.TX);  // tile = window start (Xw = X)
@@ -922,6 +930,7 @@ struct P2Params {
   int64_t scratch_img_rows;
   int64_t row0;            // first scratch row of this chunk's buffer
   int nq, img0;
+  int nq_log;              // log2 nq
   int ntiles;              // tiles per group (max over slots)
   int m;                   // log2(#groups of the transform)
   int ngroups;             // groups launched (2^m, or ceil(rows_out / 2^L) for a pruned range plan)
@@ -1150,14 +1159,12 @@ k_p2(const __grid_constant__ CUtensorMap tm_scr0, const __grid_constant__ CUtens
   pdl_wait();  // pass 1 (the predecessor) has written the scratch
   // flat grid, tile fastest: CTAs running together read overlapping scratch rows (L2 reuse of
   // the 72-column halo and of the sheared rows of one group)
-  int id = blockIdx.x;
-  const int n = id % p.ntiles;
-  id /= p.ntiles;
-  const int jl = id % p.ngroups;  // the launch's group index; j = j0 + jl is the transform's
+  // grid (ntiles, groups, images * nq): no integer division
+  const int n = blockIdx.x;
+  const int jl = blockIdx.y;  // the launch's group index; j = j0 + jl is the transform's
   const int j = p.j0 + jl;
-  id /= p.ngroups;
-  const int qi = id % p.nq;
-  const int img = p.img0 + id / p.nq;
+  const int qi = blockIdx.z & ((1 << p.nq_log) - 1);
+  const int img = p.img0 + (blockIdx.z >> p.nq_log);
   const P2Slot& sl = p.slot[qi];
   if (n >= sl.ntiles) return;
   // tile n of part [lo, hi): X = lo + TX*k, owning TX columns; the last tile of a part sits at
