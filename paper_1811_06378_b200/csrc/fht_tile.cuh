@@ -1110,7 +1110,9 @@ __device__ __forceinline__ bool p2_body(const G& grp, unsigned char* smem_raw, c
       else
         stage_rows<R, SIG, A, A, G, 0>(grp, w, stg, so, pitch, pitch);
     } else {  // every output of a black tile is 0 (no pattern touches a pixel)
-      for (int idx = tid; idx < NR * pitch; idx += NT) stg[idx] = A(0);
+      // 16-byte stores (both planes start 16-byte aligned; NR * pitch is a multiple of 4: pitch is)
+      float4* z4 = reinterpret_cast<float4*>(stg);
+      for (int idx = tid; idx < (NR * pitch) >> 2; idx += NT) z4[idx] = make_float4(0.f, 0.f, 0.f, 0.f);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       grp.sync();
     }
