@@ -71,6 +71,9 @@
 #ifndef FHT_P2_UNPRED
 #define FHT_P2_UNPRED 1   // pass 2: row staging planes with slack, stored without bounds predicates
 #endif
+#ifndef FHT_P2_DENSE_MASK
+#define FHT_P2_DENSE_MASK 1  // pass 2 dense box: the lane's in-box flags computed once for all rows
+#endif
 #ifndef FHT_P1_STAGE2
 #define FHT_P1_STAGE2 1   // pass 1: full-width tiles predicate only the last staged column
 #endif
@@ -387,12 +390,20 @@ __device__ __forceinline__ void st_pred_row(uint32_t a, int lo, int box, const A
 // the pitch, row 0's negatives in a margin before the plane), so the out-of-box columns are written and never read.
 // PRED = 2: soff == 0 and box >= WC - 1 (pass 1's full-width tiles): only a lane's last column can fall outside
 // (window index WC - 1 = 216 of a 216-wide box), so only that store is predicated.
+// PRED = 3: every row has the same soff (pass 2's dense box): the lane's 7 in-box flags are computed once and
+// shared by all its rows.
 template <int R, int SIG, typename A, typename Sg = A, typename G = GrpAll, int PRED = 1>
 __device__ __forceinline__ void stage_rows(const G& grp, A (&w)[kTPW<R>][1 << Split<R>::b][VB], Sg* stg,
                                            const int* soff, int box, int pitch, int jp_lim = 1 << Split<R>::a) {
   using S = Split<R>;
   constexpr int NA = 1 << S::a, NBk = 1 << S::b, NW = S::nw;
   const int warp = grp.tid() >> 5, lane = threadIdx.x & 31;
+  uint32_t inbox = 0;  // PRED == 3: bit q = column q of the lane is inside the box (the same for every row)
+  if constexpr (PRED == 3) {
+    const int lo = (SIG > 0 ? lane * VB : (WC - VB) - lane * VB) - soff[0];
+#pragma unroll
+    for (int q = 0; q < VB; ++q) inbox |= ((unsigned)(lo + q) < (unsigned)box ? 1u : 0u) << q;
+  }
 #pragma unroll
   for (int g = 0; g < kTPW<R>; ++g) {
     const int jp = warp + g * NW;
@@ -403,6 +414,13 @@ __device__ __forceinline__ void stage_rows(const G& grp, A (&w)[kTPW<R>][1 << Sp
         // lowest window index of the lane's 7 columns, and its staging index
         const int lo = (SIG > 0 ? lane * VB : (WC - VB) - lane * VB) - soff[tau];
         FHT_CHECK(box <= pitch && smem_in_bounds(stg + tau * pitch + box - 1, sizeof(Sg)));
+        if constexpr (PRED == 3) {
+          Sg* dst = stg + tau * pitch + lo;
+#pragma unroll
+          for (int q = 0; q < VB; ++q)
+            if (inbox & (1u << q)) dst[q] = static_cast<Sg>(w[g][u][SIG > 0 ? q : VB - 1 - q]);
+          continue;
+        }
         if constexpr (PRED == 2) {
           Sg* dst = stg + tau * pitch + lo;
 #pragma unroll
@@ -1105,7 +1123,9 @@ __device__ __forceinline__ bool p2_body(const G& grp, unsigned char* smem_raw, c
     // around every row, and stage without predicates
     A* const stg = (dense || !FHT_P2_UNPRED) ? buf : buf + kStgOff;
     if (!black) {
-      if (dense || !FHT_P2_UNPRED)
+      if (dense && FHT_P2_DENSE_MASK)  // one aligned start for all rows: the in-box flags once per lane
+        stage_rows<R, SIG, A, A, G, 3>(grp, w, stg, so, pitch, pitch);
+      else if (dense || !FHT_P2_UNPRED)
         stage_rows<R, SIG, A>(grp, w, stg, so, pitch, pitch);  // every computed column that fits the row
       else
         stage_rows<R, SIG, A, A, G, 0>(grp, w, stg, so, pitch, pitch);
