@@ -1638,8 +1638,7 @@ int fhtshift(const fht_hough* in, fht_hough* out, fht_stream_t stream) {
     a.w_content = (int)in->plan.w_content;
     smem = (size_t)a.h * sizeof(int);  // e_y table of the block (h <= 4096)
   }
-  const int64_t rpb = in->mode == FHT_MODE_RANGE ? kRangeShiftRows : kThreads / 32;  // rows per block
-  const int64_t nblk = (a.rows_total + rpb - 1) / rpb;
+  const int64_t nblk = (a.rows_total + kThreads / 32 - 1) / (kThreads / 32);
   if (in->dtype == FHT_F32) k_fhtshift<float><<<(unsigned)nblk, kThreads, smem, (cudaStream_t)stream>>>(a);
   else k_fhtshift<int><<<(unsigned)nblk, kThreads, smem, (cudaStream_t)stream>>>(a);
   if (cudaGetLastError() != cudaSuccess) return FHT_ERR_CUDA;

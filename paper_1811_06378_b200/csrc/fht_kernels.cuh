@@ -422,15 +422,29 @@ __device__ __forceinline__ void shift_row_vec(const T* src, T* dst, int W4, int 
 
 // Standalone fhtshift (R11): out[r][x] = in[r][(x - k_r) mod W]. One warp
 // per row (8 rows per block); 16-byte loads and streaming stores when everything is aligned.
-// RANGE mode: every block first builds the e_y table (h entries) in shared memory, so it serves
-// kRangeShiftRows rows (each warp several) to amortise that; the other modes take one row per warp.
-constexpr int kRangeShiftRows = 32;
-
 template <typename T>
-__device__ __forceinline__ void shift_one_row(const ShiftArgs& a, int64_t row, int k, int lane) {
+__global__ void __launch_bounds__(kThreads) k_fhtshift(const ShiftArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+  int k_range = 0;
+  if (a.mode == 2) {
+    // RANGE (R11 generic rule, R17 support): k = ceil((W' - len)/2) - start, start/len of the row by
+    // the §4 table method -- e_y once per block in shared memory, then one warp per row
+    extern __shared__ int e_s[];  // [h]
+    __shared__ int dh_s[kThreads / 32][128];
+    for (int y = threadIdx.x; y < a.h; y += blockDim.x) e_s[y] = shear_e(a.g, y);
+    __syncthreads();
+    if (row >= a.rows_total) return;
+    int mn, mx;
+    row_support_warp(a.K, a.h, (int)(row % a.rows), e_s, dh_s[threadIdx.x >> 5], lane, mn, mx);
+    k_range = (ceil_half(a.W - (mx - mn + a.w_content)) - mn) % a.W;
+    if (k_range < 0) k_range += a.W;
+  }
+  if (row >= a.rows_total) return;
   const int r = (int)(row % a.rows);
   const int64_t zq = row / a.rows;  // image * nquad + quadrant slot
   const int img = (int)(zq / a.nquad), qs = (int)(zq % a.nquad);
+  const int k = a.mode == 2 ? k_range : shift_amount(a, r, qs);
   const T* src = static_cast<const T*>(a.in) + (int64_t)img * a.in_img_stride + (int64_t)qs * a.in_q_stride +
                  (int64_t)r * a.in_row_stride;
   T* dst = static_cast<T*>(a.out) + (int64_t)img * a.out_img_stride + (int64_t)qs * a.out_q_stride +
@@ -452,36 +466,6 @@ __device__ __forceinline__ void shift_one_row(const ShiftArgs& a, int64_t row, i
     FHT_CHECK(sx >= 0 && sx < a.W);
     __stcs(dst + x, __ldg(src + sx));
   }
-}
-
-// Standalone fhtshift (R11): out[r][x] = in[r][(x - k_r) mod W]. One warp
-// per row; 16-byte loads and streaming stores when everything is aligned.
-template <typename T>
-__global__ void __launch_bounds__(kThreads) k_fhtshift(const ShiftArgs a) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (a.mode == 2) {
-    // RANGE (R11 generic rule, R17 support): k = ceil((W' - len)/2) - start, start/len of the row by
-    // the §4 table method -- e_y once per block in shared memory, then one warp per row
-    extern __shared__ int e_s[];  // [h]
-    __shared__ int dh_s[kThreads / 32][128];
-    for (int y = threadIdx.x; y < a.h; y += blockDim.x) e_s[y] = shear_e(a.g, y);
-    __syncthreads();
-    for (int i = warp; i < kRangeShiftRows; i += kThreads / 32) {
-      const int64_t row = (int64_t)blockIdx.x * kRangeShiftRows + i;
-      if (row >= a.rows_total) return;
-      int mn, mx;
-      row_support_warp(a.K, a.h, (int)(row % a.rows), e_s, dh_s[warp], lane, mn, mx);
-      int k = (ceil_half(a.W - (mx - mn + a.w_content)) - mn) % a.W;
-      if (k < 0) k += a.W;
-      shift_one_row<T>(a, row, k, lane);
-    }
-    return;
-  }
-  const int64_t row = (int64_t)blockIdx.x * (kThreads / 32) + warp;
-  if (row >= a.rows_total) return;
-  const int r = (int)(row % a.rows);
-  const int qs = (int)((row / a.rows) % a.nquad);
-  shift_one_row<T>(a, row, shift_amount(a, r, qs), lane);
 }
 
 // ------------------------------------------------------------------------------------------
