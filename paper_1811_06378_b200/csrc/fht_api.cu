@@ -231,7 +231,10 @@ struct PipePlan {
 };
 PipePlan pipe_plan(const Frame& f, int nq, int64_t batch, const RangeDev* rg, int es) {
   PipePlan pp{};
-  if (rg || !use_v2(f, rg) || !pipe_split_ok(f.m, f.L) || env_int("FHT_PIPE", 0) == 0) return pp;  // opt-in (measured slower)
+  // (the pipelined kernel's persistent mbarriers need the per-warp loads: FHT_P1/P2_WARPLOAD)
+  if (!(FHT_P1_WARPLOAD && FHT_P2_WARPLOAD) || rg || !use_v2(f, rg) || !pipe_split_ok(f.m, f.L) ||
+      env_int("FHT_PIPE", 0) == 0)
+    return pp;  // opt-in (measured slower)
   pp.pitch = v2_scratch_pitch(f, rg, es);
   const size_t per = (size_t)f.Hp * (size_t)pp.pitch * es;  // one image, one slot
   const size_t target = (size_t)env_int("FHT_PIPE_UNIT_MB", 16) << 20;

@@ -166,7 +166,6 @@ k_pipe(const __grid_constant__ CUtensorMap tm_img0, const __grid_constant__ CUte
   using A = typename AccOf<Tin>::type;
   using Tscr = typename ScrOf<Tin>::type;
   using PS = PipeShape<R1, R2>;
-  static_assert(FHT_P1_WARPLOAD && FHT_P2_WARPLOAD, "the pipelined kernel needs the per-warp mbarrier loads");
   constexpr int NB1 = 1 << Split<R1>::b, NB2 = 1 << Split<R2>::b;  // mbarriers (sub-pass-A blocks) per tile
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ int item_s;
