@@ -158,7 +158,9 @@ int scratch_es(int dtype) { return dtype == FHT_U8 ? 2 : 4; }
 // spans rounded to 16 bytes of scratch elements (tile starts and row pitch stay TMA-aligned)
 void v2_pass1_range(const Frame& f, int sigma, const RangeDev* rg, int& lo, int& hi, int es) {
   pass1_range(f, sigma, rg, lo, hi);
-  const int al = 16 / es;
+  // the span is a multiple of 32 columns (FHT_ROW32: pass 2 reads the scratch as [row][col/32][32]); the
+  // columns added past the support are computed by pass 1 as exact zeros
+  const int al = FHT_ROW32 ? 32 : 16 / es;
   hi = lo + ((hi - lo + al - 1) & ~(al - 1));
 }
 int64_t v2_scratch_pitch(const Frame& f, const RangeDev* rg, int es) {
@@ -285,6 +287,31 @@ bool make_row_map(CUtensorMap* m, const void* base, bool f32, uint64_t cols, uin
   return fn(m, dt, 2, const_cast<void*>(base), dims,
             strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
             CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// Pass-2 scratch reads: FHT_ROW32 -- the view [rows][cols/32][32] (cols = the pass-1 span, a multiple of 32), box
+// {32, 10, 1} = one 320-column row per copy (scr1 unused); else 2-D rows, boxes of 256 and 36 (u16: 40) columns.
+bool make_scr_maps(CUtensorMap* m0, CUtensorMap* m1, const void* base, bool f32, bool u16, uint64_t cols,
+                   uint64_t rows, uint64_t pitch_elems) {
+#if FHT_ROW32
+  auto fn = encode_fn();
+  if (!fn || cols % 32 != 0) return false;
+  const uint64_t es = u16 ? 2 : 4;
+  cuuint64_t dims[3] = {32, cols / 32, rows};
+  cuuint64_t strides[2] = {32 * es, pitch_elems * es};
+  cuuint32_t box[3] = {32, 10, 1};
+  cuuint32_t e[3] = {1, 1, 1};
+  const CUtensorMapDataType dt = u16 ? CU_TENSOR_MAP_DATA_TYPE_UINT16
+                                     : f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_INT32;
+  if (fn(m0, dt, 3, const_cast<void*>(base), dims, strides, box, e, CU_TENSOR_MAP_INTERLEAVE_NONE,
+         CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return false;
+  *m1 = *m0;
+  return true;
+#else
+  return make_row_map(m0, base, f32, cols, rows, pitch_elems, 256, 1, u16) &&
+         make_row_map(m1, base, f32, cols, rows, pitch_elems, u16 ? 40 : 36, 1, u16);
+#endif
 }
 
 // ---------------------------------------------------------------- v1 launch helpers
@@ -426,6 +453,30 @@ bool make_image_map(CUtensorMap* m, const fht_image* img, uint32_t box_cols) {
          CUDA_SUCCESS;
 }
 
+// Pass-1 fill32 (FHT_ROW32, 4-byte images with w % 32 == 0): the view [img][row][col/32][32], box {32, 10, 1, 1}
+// = one 320-column row per copy from a 128-byte aligned column.
+bool make_image_map32(CUtensorMap* m, const fht_image* img) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[4] = {32, (cuuint64_t)(img->w / 32), (cuuint64_t)img->h, (cuuint64_t)img->batch};
+  cuuint64_t strides[3] = {128, (cuuint64_t)(img->row_stride * 4), (cuuint64_t)(img->batch_stride * 4)};
+  if (img->batch == 1) strides[2] = (cuuint64_t)(img->h * img->row_stride * 4);
+  cuuint32_t box[4] = {32, 10, 1, 1};
+  cuuint32_t e[4] = {1, 1, 1, 1};
+  const CUtensorMapDataType dt = img->dtype == FHT_I32 ? CU_TENSOR_MAP_DATA_TYPE_INT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+  return fn(m, dt, 4, const_cast<void*>(img->data), dims, strides, box, e, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
+}
+bool make_p1_image_maps(CUtensorMap* m0, CUtensorMap* m1, const fht_image* img, const v2::P1Params& p1, size_t es) {
+  if (p1.fill32) {
+    if (!make_image_map32(m0, img)) return false;
+    *m1 = *m0;
+    return true;
+  }
+  return make_image_map(m0, img, 256) && make_image_map(m1, img, es == 1 ? 48 : 36);
+}
+
 // One quadrant slot: sign, source orientation and output row placement.
 struct Slot {
   int sigma;
@@ -504,6 +555,8 @@ int run_orientation(const fht_image* img, const Frame& f, const Slot* slots, int
     p1.fill_vec = f.m >= 2 && (es == 1 ? ((reinterpret_cast<uintptr_t>(img->data) & 3) == 0 &&
                                           img->row_stride % 4 == 0 && (img->batch == 1 || img->batch_stride % 4 == 0))
                                        : pitch16);
+    // one TMA per image row (view [row][col/32][32]) for 4-byte images whose width is a multiple of 32
+    p1.fill32 = FHT_ROW32 && p1.fill_tma && !rg && es == 4 && img->w % 32 == 0;
     int span1 = 1 << 30;
     for (int q = 0; q < nq; ++q) {
       v2::P1Slot& s = p1.slot[q];
@@ -626,8 +679,7 @@ int run_orientation(const fht_image* img, const Frame& f, const Slot* slots, int
           if (!make_dst_map(&m1s.dst.m[h], sh->dst[h], ses, f32, sp.pitch, sh->S, sh->J, Z, p1.TX, (int)sh->J))
             return FHT_ERR_CUDA;
         if (p1.fill_tma) {
-          if (!make_image_map(&m1s.img0, img, 256) || !make_image_map(&m1s.img1, img, es == 1 ? 48 : 36))
-            return FHT_ERR_CUDA;
+          if (!make_p1_image_maps(&m1s.img0, &m1s.img1, img, p1, es)) return FHT_ERR_CUDA;
         } else {
           m1s.img0 = m1s.dst.m[0];
           m1s.img1 = m1s.dst.m[0];
@@ -648,9 +700,7 @@ int run_orientation(const fht_image* img, const Frame& f, const Slot* slots, int
       const uint64_t rows = (uint64_t)sh->world * sh->chunk_rows;
       p2.scr_rows = (int64_t)rows;
       void* recv = const_cast<void*>(sh->recv);
-      if (!make_row_map(&m2s.scr0, recv, f32, (uint64_t)span1, rows, (uint64_t)sp.pitch, 256, 1, ses == 2) ||
-          !make_row_map(&m2s.scr1, recv, f32, (uint64_t)span1, rows, (uint64_t)sp.pitch, ses == 2 ? 40 : 36, 1,
-                        ses == 2))
+      if (!make_scr_maps(&m2s.scr0, &m2s.scr1, recv, f32, ses == 2, (uint64_t)span1, rows, (uint64_t)sp.pitch))
         return FHT_ERR_CUDA;
       p2.scratch_img_rows = nq * sh->J * sh->S;
       for (int q = 0; q < nq; ++q) p2.slot[q].srow0 = q * sh->J * sh->S;
@@ -685,16 +735,13 @@ int run_orientation(const fht_image* img, const Frame& f, const Slot* slots, int
                       ngroups))
       return FHT_ERR_CUDA;
     if (p1.fill_tma) {
-      if (!make_image_map(&m1.img0, img, 256) || !make_image_map(&m1.img1, img, es == 1 ? 48 : 36))
-        return FHT_ERR_CUDA;
+      if (!make_p1_image_maps(&m1.img0, &m1.img1, img, p1, es)) return FHT_ERR_CUDA;
     } else {
       m1.img0 = m1.dst.m[0];
       m1.img1 = m1.dst.m[0];
     }
     // scratch as pass 2 reads it: columns [0, span1) = what pass 1 wrote; TMA zero-fills the rest
-    if (!make_row_map(&m2.scr0, ws, f32, (uint64_t)span1, scr_rows, (uint64_t)sp.pitch, 256, 1, ses == 2) ||
-        !make_row_map(&m2.scr1, ws, f32, (uint64_t)span1, scr_rows, (uint64_t)sp.pitch, ses == 2 ? 40 : 36, 1,
-                      ses == 2))
+    if (!make_scr_maps(&m2.scr0, &m2.scr1, ws, f32, ses == 2, (uint64_t)span1, scr_rows, (uint64_t)sp.pitch))
       return FHT_ERR_CUDA;
 
     if (pipe) {  // both passes in one persistent launch (fht_pipe.cuh)
@@ -729,6 +776,66 @@ int run_orientation(const fht_image* img, const Frame& f, const Slot* slots, int
       log.after(st);
       return 1;
     }
+
+    // Staggered pass pairs (fht_dual.cuh): chunks of dc images in two scratch buffers; launch k runs pass 1 of
+    // chunk k beside pass 2 of chunk k - 1 in one grid. FHT_DUAL_IMGS = images per chunk (0: off).
+    const int dual_imgs = env_int("FHT_DUAL_IMGS", 0);
+    if (dual_imgs > 0 && !rg && dual_split_ok(f.m, f.L)) {
+      const int64_t cap = sp.nbuf == 2 ? sp.chunk : sp.chunk / 2;  // images per buffer with two buffers
+      const int64_t dc = dual_imgs < cap ? dual_imgs : cap;
+      if (dc >= 1 && img->batch > dc) {
+        const int nch = (int)((img->batch + dc - 1) / dc);
+        const int dt = img->dtype == FHT_U8 ? 0 : img->dtype == FHT_I32 ? 1 : 2;
+        const PipeMaps pm{m1.img0, m1.img1, m1.dst, m2.scr0, m2.scr1, m2.out0, m2.out1, m2.out0_box};
+        p1.ntiles = ntile1;
+        p2.ntiles = ntile2;
+        p2.m = f.m;
+        p2.ngroups = ngroups;
+        auto set1 = [&](int k) {  // pass 1 of chunk k -> buffer k & 1
+          p1.img0 = (int)(k * dc);
+          p1.z0 = (int)((k & 1) * dc * nq);
+          return (int)((img->batch - k * dc) < dc ? (img->batch - k * dc) : dc);
+        };
+        auto set2 = [&](int k) {
+          p2.img0 = (int)(k * dc);
+          p2.row0 = (k & 1) * dc * p1.scratch_img_rows;
+          return (int)((img->batch - k * dc) < dc ? (img->batch - k * dc) : dc);
+        };
+        for (int k = 0; k <= nch; ++k) {
+          cudaError_t e;
+          log.before(st);
+          if (k == 0) {
+            const int nb = set1(0);
+            const dim3 g1((unsigned)(ntile1 * nq), (unsigned)nstrips, (unsigned)nb);
+            switch (img->dtype) {
+              case FHT_U8: e = launch_p1<uint8_t>(f.m, g1, m1, p1, st); break;
+              case FHT_I32: e = launch_p1<int32_t>(f.m, g1, m1, p1, st); break;
+              default: e = launch_p1<float>(f.m, g1, m1, p1, st); break;
+            }
+          } else if (k == nch) {
+            const int nb = set2(nch - 1);
+            const dim3 g2((unsigned)ntile2, (unsigned)ngroups, (unsigned)(nb * nq));
+            e = f32 ? launch_p2<float>(f.L, g2, m2, p2, st)
+                    : ses == 2 ? launch_p2<int, uint16_t>(f.L, g2, m2, p2, st) : launch_p2<int>(f.L, g2, m2, p2, st);
+          } else {
+            const int nb1 = set1(k), nb2 = set2(k - 1);
+            v2::DualParams dp{};
+            dp.ntiles1 = ntile1;
+            dp.nstrips = nstrips;
+            dp.ntiles2 = ntile2;
+            dp.ngroups = ngroups;
+            dp.t1 = (int64_t)nb1 * nstrips * ntile1 * nq;
+            dp.t2 = (int64_t)nb2 * nq * ngroups * ntile2;
+            e = launch_dual(dt, f.m, f.L, pm, p1, p2, dp, st);
+          }
+          if (e != cudaSuccess) return FHT_ERR_CUDA;
+          log.after(st);
+          ++launches;
+        }
+        return launches;
+      }
+    }
+
 
     // Chunks of the batch; with an auxiliary stream and two scratch buffers, pass 1 of chunk k+1
     // (aux) overlaps pass 2 of chunk k (main): p2(k) waits for p1(k), p1(k+2) for p2(k).

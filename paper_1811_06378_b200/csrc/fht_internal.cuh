@@ -6,6 +6,7 @@
 #include <cstdlib>
 #include <utility>
 
+#include "fht_dual.cuh"
 #include "fht_pipe.cuh"
 
 namespace fht {
@@ -61,6 +62,12 @@ struct PipeMaps {
 // persistent grid; the counters must be zero (the caller's memset).
 cudaError_t launch_pipe(int dtype, int m, int L, const PipeMaps& maps, const v2::P1Params& p1,
                         const v2::P2Params& p2, v2::PipeParams pp, cudaStream_t st);
+
+// k_dual<Tin, m, L> (fht_dual.cu): pass 1 of one chunk beside pass 2 of the previous one in one grid; sets the
+// item counts from dp.t1 / dp.t2. dual_split_ok: the instantiated (m, L) pairs.
+bool dual_split_ok(int m, int L);
+cudaError_t launch_dual(int dtype, int m, int L, const PipeMaps& maps, const v2::P1Params& p1, const v2::P2Params& p2,
+                        const v2::DualParams& dp, cudaStream_t st);
 
 }  // namespace detail
 }  // namespace fht

@@ -74,6 +74,12 @@
 #ifndef FHT_P2_DENSE_MASK
 #define FHT_P2_DENSE_MASK 1  // pass 2 dense box: the lane's in-box flags computed once for all rows
 #endif
+#ifndef FHT_ROW32
+#define FHT_ROW32 1       // one TMA per 4-byte row: a [rows][cols/32][32] view, box {32, 10} = 320 columns (was 256 + 36)
+#endif
+#if FHT_ROW32 && !FHT_P2_WARPLOAD
+#error "FHT_ROW32 needs the per-warp pass-2 loads (FHT_P2_WARPLOAD)"
+#endif
 #ifndef FHT_P1_STAGE2
 #define FHT_P1_STAGE2 1   // pass 1: full-width tiles predicate only the last staged column
 #endif
@@ -225,6 +231,13 @@ __device__ __forceinline__ void tma_load_3d(const CUtensorMap* map, void* smem, 
   asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];"
                :: "r"(smem_u32(smem)), "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1),
                   "r"(c2)
+               : "memory");
+}
+__device__ __forceinline__ void tma_load_4d(const CUtensorMap* map, void* smem, uint64_t* bar, int c0, int c1, int c2,
+                                            int c3) {
+  asm volatile("cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], [%2];"
+               :: "r"(smem_u32(smem)), "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1),
+                  "r"(c2), "r"(c3)
                : "memory");
 }
 __device__ __forceinline__ void mbar_init(uint64_t* bar) {
@@ -481,6 +494,7 @@ struct P1Params {
   int w_content;
   int fill_tma;                      // non-transposed rows by TMA (image base/pitch 16-B aligned)
   int fill_vec;                      // transposed fill with 16-byte (u8: 4-byte) loads
+  int fill32;                        // 4-byte rows by ONE TMA each: tm_img0 is the view [img][row][col/32][32] (w % 32 == 0)
   int nq, img0;
   int ntiles;                        // tiles per strip (max over slots)
   int L;                             // log2(#strips)
@@ -741,18 +755,26 @@ __device__ __forceinline__ bool p1_body(const G& grp, unsigned char* smem_raw, c
     // each warp issues (lane 0) and waits for (in tile_fht) the rows of its own sub-pass-A blocks
     constexpr int NA = 1 << S::a, NBk = 1 << S::b, NW = S::nw;
     const int warp = tid >> 5, lane = threadIdx.x & 31;
+    // fill32 (4-byte rows): ONE box {32, 10} of the [img][row][col/32][32] view per row, from the 128-byte
+    // aligned column a32 <= Xa: 320 columns cover the 288 the tile needs for any offset Xa - a32 < 32
+    const int a32 = Xa & ~31;
+    const bool f32r = sizeof(Tin) == 4 && FHT_ROW32 && p.fill32;
     for (int b = warp; b < NBk; b += NW) {
       if (lane == 0) {
         if (!ext_bars) mbar_init(bar + b);
-        mbar_expect_tx(bar + b, NA * row_bytes);
+        mbar_expect_tx(bar + b, f32r ? NA * (uint32_t)TMA_PITCH * 4 : NA * row_bytes);
         for (int rho = b * NA; rho < (b + 1) * NA; ++rho) {
           Tin* d = tile + rho * TP;
-          tma_load_3d(tm_img0, d, bar + b, a0, y0 + rho, img);
-          tma_load_3d(tm_img1, d + 256, bar + b, a0 + 256, y0 + rho, img);
+          if (f32r) {
+            tma_load_4d(tm_img0, d, bar + b, 0, a32 >> 5, y0 + rho, img);
+          } else {
+            tma_load_3d(tm_img0, d, bar + b, a0, y0 + rho, img);
+            tma_load_3d(tm_img1, d + 256, bar + b, a0 + 256, y0 + rho, img);
+          }
         }
       }
       if (lane < NA) {
-        rowoff[b * NA + lane] = Xa - a0;
+        rowoff[b * NA + lane] = Xa - (f32r ? a32 : a0);
         soff[b * NA + lane] = 0;
       }
     }
@@ -1019,18 +1041,30 @@ __device__ __forceinline__ bool p2_body(const G& grp, unsigned char* smem_raw, c
     // scratch rows of Tscr: loads start at the 16-byte aligned column below (kAl elements) and
     // take 256 + kBox1 columns (kBox1 * sizeof(Tscr) a multiple of 16); row i lands at byte
     // i * TMA_PITCH * 4 of the buffer, where its fa row will be written in place
+#if FHT_ROW32
+    // ONE box {32, 10} per row of the scratch view [row][col/32][32] (the pass-1 span is a multiple of 32
+    // columns, host side): 320 columns from the aligned-down column cover the 288 needed
+    constexpr int kAl = 32;
+    constexpr uint32_t kRowBytes = 320 * (uint32_t)sizeof(Tscr);
+#else
     constexpr int kAl = 16 / (int)sizeof(Tscr), kBox1 = sizeof(Tscr) == 2 ? 40 : 36;
+    constexpr uint32_t kRowBytes = (256 + kBox1) * (uint32_t)sizeof(Tscr);
+#endif
     for (int b = warp; b < NBk; b += NW) {
       if (lane == 0) {
         if (!ext_bars) mbar_init(bar + b);
-        mbar_expect_tx(bar + b, NA * (256 + kBox1) * (uint32_t)sizeof(Tscr));
+        mbar_expect_tx(bar + b, NA * kRowBytes);
         for (int i = b * NA; i < (b + 1) * NA; ++i) {
           const int a0 = (Xa + SIG * j * i - sl.xlo1) & ~(kAl - 1);
           Tscr* d = reinterpret_cast<Tscr*>(buf + i * TMA_PITCH);
           const int row = (int)(rbase + (int64_t)(i >> p.logS) * p.strideG + (i & ((1 << p.logS) - 1)));
           FHT_CHECK(row >= 0 && row < p.scr_rows);
+#if FHT_ROW32
+          tma_load_3d(tm_scr0, d, bar + b, 0, a0 >> 5, row);
+#else
           tma_load_2d(tm_scr0, d, bar + b, a0, row);
           tma_load_2d(tm_scr1, d + 256, bar + b, a0 + 256, row);
+#endif
         }
       }
       if (lane < NA) rowoff[b * NA + lane] = (Xa + SIG * j * (b * NA + lane) - sl.xlo1) & (kAl - 1);

@@ -778,6 +778,34 @@ def test_pipe_matches_two_launch_and_oracle(fht, O, monkeypatch, shape, dt, batc
         check(q1.view[batch - 1, 0].cpu().numpy(), O.hough_recursive(imgs[batch - 1], O.QC), dt != "f32")
 
 
+# ------------------------------------------------------------------ staggered pass pairs (fht_dual.cuh)
+@pytest.mark.parametrize("shape,dt,batch,imgs", [((512, 512), "u8", 5, "1"), ((512, 512), "u8", 7, "2"),
+                                                 ((1024, 1024), "f32", 3, "1"), ((2048, 2048), "f32", 3, "1"),
+                                                 ((2048, 2048), "f32", 5, "2"), ((4096, 4096), "f32", 2, "1"),
+                                                 ((700, 900), "i32", 3, "1"), ((1000, 1024), "f32", 4, "3")], ids=str)
+def test_dual_matches_two_launch_and_oracle(fht, O, monkeypatch, shape, dt, batch, imgs):
+    """Pass 1 of chunk k beside pass 2 of chunk k - 1 in one grid (FHT_DUAL_IMGS images per chunk, two
+    scratch buffers, a ragged last chunk when the batch does not divide): bit-identical to the two-launch
+    schedule, nchunks + 1 launches, both outputs, every cell of the last image against the oracle."""
+    from synth import random_image
+    ims = np.stack([random_image(shape, dt, seed=shape[1] + 7 * b) for b in range(batch)])
+    t = dev(ims)
+    monkeypatch.delenv("FHT_DUAL_IMGS", raising=False)
+    h0, s0 = fht.full(t, pair=True)
+    torch.cuda.synchronize()
+    monkeypatch.setenv("FHT_DUAL_IMGS", imgs)
+    h, s = fht.full(t, pair=True)
+    torch.cuda.synchronize()
+    nch = -(-batch // int(imgs))
+    assert h.launches == nch + 1
+    assert torch.equal(h.storage, h0.storage) and torch.equal(s.storage, s0.storage)
+    quads = O.full_quadrants(ims[batch - 1])
+    got = h.view[batch - 1].cpu().numpy()
+    for q in range(4):
+        n = quads[q].shape[0]
+        check(got[q, :n], quads[q], dt != "f32")
+
+
 # ------------------------------------------------------------------ one image over several ranks (SURVEY §8(e))
 def _emulated_shards(fht, t, world, p2p):
     """All `world` ranks of a sharded transform run in this process on one GPU (their kernels do not

@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """A/B timing of alternative libfht builds on the same GPU in one process each, interleaved.
 
-    python tools/abbench.py LIB1.so LIB2.so ... [--configs 2,5] [--rounds 3]
+    python tools/abbench.py LIB1.so LIB2.so@FHT_X=0 ... [--configs 2,5] [--rounds 3]
 
 Every round runs each library's step for each config in a fresh subprocess (FHT_LIB=...), so
 the builds see the same box, clocks and thermal state; prints per-kernel means.
@@ -96,7 +96,10 @@ def main():
     for r in range(rounds):
         for lib in libs:
             for cid in cfgs:
-                env = dict(os.environ, FHT_LIB=os.path.abspath(lib), ROOT=ROOT)
+                # LIB@K=V,K2=V2: the same library under extra environment variables (runtime switches)
+                path, _, kv = lib.partition("@")
+                extra = dict(x.split("=", 1) for x in kv.split(",") if x)
+                env = dict(os.environ, FHT_LIB=os.path.abspath(path), ROOT=ROOT, **extra)
                 try:
                     out = subprocess.run([sys.executable, "-c", CHILD, str(cid)], env=env, capture_output=True,
                                          text=True, timeout=180)
@@ -112,7 +115,7 @@ def main():
     for (lib, cid), ds in sorted(res.items()):
         m = {k: sum(d[k] for d in ds) / len(ds) for k in ds[0]}
         mn = {k: min(d[k] for d in ds) for k in ds[0]}
-        print(f"C{cid} {os.path.basename(lib):28s} step {m['step_us']:9.1f} us (min {mn['step_us']:9.1f})  "
+        print(f"C{cid} {os.path.basename(lib):40s} step {m['step_us']:9.1f} us (min {mn['step_us']:9.1f})  "
               f"p1 {m['p1_us']:9.1f}  p2 {m['p2_us']:9.1f}  | no inter-kernel events: {m['whole_us']:9.1f} us")
 
 
