@@ -655,7 +655,7 @@ int run_orientation(const fht_image* img, const Frame& f, const Slot* slots, int
         return FHT_ERR_CUDA;
       if (p2.ndest == 0 && !make_row_map(&m2.out0_box, o->data, o->dtype == FHT_F32, (uint64_t)o->cols,
                                          (uint64_t)(o->batch * D.rows_per_img), (uint64_t)o->row_stride,
-                                         (uint32_t)box2, (uint32_t)(1 << f.L)))
+                                         (uint32_t)box2, (uint32_t)v2::p2_box_rows(f.L)))
         return FHT_ERR_CUDA;
       ++p2.ndest;
     }

@@ -74,6 +74,9 @@
 #ifndef FHT_P2_DENSE_MASK
 #define FHT_P2_DENSE_MASK 1  // pass 2 dense box: the lane's in-box flags computed once for all rows
 #endif
+#ifndef FHT_P2_WARPSTORE
+#define FHT_P2_WARPSTORE 1  // pass 2: each warp stages and stores its own 8 output rows (no CTA barrier after sub-pass B)
+#endif
 #ifndef FHT_ROW32
 #define FHT_ROW32 1       // one TMA per 4-byte row: a [rows][cols/32][32] view, box {32, 10} = 320 columns (was 256 + 36)
 #endif
@@ -150,6 +153,17 @@ template <typename Tin> struct ScrOf { using type = typename AccOf<Tin>::type; }
 template <> struct ScrOf<uint8_t> { using type = uint16_t; };
 template <int R> constexpr int kMinBlocks = Split<R>::nw == 4 ? 5 : 2;  // occupancy target (regs <= 102 / 128)
 template <int R> constexpr int kTPW = ((1 << Split<R>::a) + Split<R>::nw - 1) / Split<R>::nw;  // B tasks/warp
+// pass 2 stores per warp (FHT_P2_WARPSTORE): every warp owns one sub-pass-B group of 8 rows
+template <int R> constexpr bool kWarpStore = FHT_P2_WARPSTORE && (1 << Split<R>::b) == 8 && kTPW<R> == 1 &&
+                                             (1 << Split<R>::a) == Split<R>::nw && Split<R>::nw * 32 >= 2 * (1 << R);
+// rows of the dense-box store (tensor map box height): a warp's 8 rows, or the whole tile
+inline int p2_box_rows(int R) {
+  switch (R) {
+    case 5: return kWarpStore<5> ? 8 : 32;
+    case 6: return kWarpStore<6> ? 8 : 64;
+  }
+  return 1 << R;
+}
 
 // Shared memory layout (bytes): [main buffer][u8 input tile (pass 1 u8 TMA only)][tables]
 __host__ __device__ constexpr size_t main_buf_bytes(int R) { return (size_t)(1 << R) * TMA_PITCH * 4; }
@@ -1086,7 +1100,10 @@ __device__ __forceinline__ bool p2_body(const G& grp, unsigned char* smem_raw, c
   }
 #endif
 
-  // ---- store plan per (destination, row): shift k, 16-byte aligned start, TMA or plain stores
+  // ---- store plan per (destination, row): shift k, 16-byte aligned start, TMA or plain stores.
+  // remw[c]: some row of plan items [32c, 32c + 32) has columns left to plain stores (one ballot per warp: the
+  // items of a warp are one 32-item chunk while NT >= ndest * NR, which holds for every R)
+  int* const remw = reinterpret_cast<int*>(tab + 896);
   for (int it = tid; it < p.ndest * NR; it += NT) {
     const int d = it / NR, tau = it - d * NR, t = t0 + tau;
     const P2Dest& D = p.dest[d];
@@ -1123,6 +1140,10 @@ __device__ __forceinline__ bool p2_body(const G& grp, unsigned char* smem_raw, c
     }
     info[d * NR + tau] = ri;
     soff[d * 64 + tau] = WO2 - r;
+    if (NT >= 2 * NR) {
+      const unsigned rem = __ballot_sync(__activemask(), ri.mlo < ri.mhi);
+      if ((threadIdx.x & 31) == 0) remw[it >> 5] = rem != 0u;
+    }
   }
 #if FHT_P2_WARPLOAD
   // the plan (info, soff) is read after tile_fht's first group barrier; a black tile has none
@@ -1136,6 +1157,101 @@ __device__ __forceinline__ bool p2_body(const G& grp, unsigned char* smem_raw, c
     tile_fht<R, SIG, A>(grp, reinterpret_cast<const Tscr*>(buf), TMA_PITCH * 4 / (int)sizeof(Tscr), rowoff, buf,
                         TMA_PITCH, w, bar, par);
 
+#if FHT_P2_WARPSTORE
+  if constexpr (kWarpStore<R>) {
+    // ---- warp-owned stores: warp w holds output rows [8w, 8w + 8) (sub-pass-B group jp = w) and stages them in
+    // its own region of the buffer, [8][box] (dense plane of destination 0) or 8 rows of ST_PITCH after a 32-element
+    // margin (row planes), then issues their bulk stores itself: after the sub-pass-B barrier no CTA barrier is
+    // needed, only the warp's own fence / __syncwarp and its lane 0's wait for the bulk reads before it restages.
+    constexpr int RW = 8, WREG = 32 + RW * ST_PITCH;  // rows per warp; region per warp (128-byte multiple)
+    const int r0 = warp * RW;
+    A* const stw = buf + warp * WREG;
+    bool issued = false;
+    for (int dd = 0; dd < p.ndest; ++dd) {
+      const int d = FHT_P2_REVERSE_DEST ? p.ndest - 1 - dd : dd;
+      const P2Dest& D = p.dest[d];
+      const RowInfo* inf = info + d * NR;
+      const int* so = soff + d * 64;
+      if (dd > 0) {
+        if (lane == 0 && issued) tma_wait_read();
+        __syncwarp();
+      }
+      const bool dense = FHT_P2_DENSE && !p.range && !D.shifted && sl.rsign == 1 && (sl.skip < t0 || sl.skip > tmax) &&
+                         tmax < p.rows_out && (inf[0].d0 & kTmaBit) && inf[0].mlo >= inf[0].mhi;
+      A* const stg = dense ? stw : stw + 32;
+      const int pitch = dense ? box : ST_PITCH;
+      if (!black) {
+        const int lo0 = SIG > 0 ? lane * VB : (WC - VB) - lane * VB;  // lowest window index of the lane's columns
+        if (lane < 31) {
+          if (dense) {  // one aligned start for all rows: the lane's in-box flags once
+            const int lo = lo0 - so[0];
+            uint32_t inbox = 0;
+#pragma unroll
+            for (int q = 0; q < VB; ++q) inbox |= ((unsigned)(lo + q) < (unsigned)box ? 1u : 0u) << q;
+#pragma unroll
+            for (int u = 0; u < RW; ++u) {
+              A* dst = stg + u * box + lo;
+              FHT_CHECK(smem_in_bounds(stg + RW * box - 1, sizeof(A)));
+#pragma unroll
+              for (int q = 0; q < VB; ++q)
+                if (inbox & (1u << q)) dst[q] = w[0][u][SIG > 0 ? q : VB - 1 - q];
+            }
+          } else {  // rows with slack: staging indices [-4, WC) stay inside the row's pitch / the margin
+#pragma unroll
+            for (int u = 0; u < RW; ++u) {
+              A* dst = stg + u * ST_PITCH + lo0 - so[r0 + u];
+              FHT_CHECK(smem_in_bounds(dst, sizeof(A)) && smem_in_bounds(dst + VB - 1, sizeof(A)));
+#pragma unroll
+              for (int q = 0; q < VB; ++q) dst[q] = w[0][u][SIG > 0 ? q : VB - 1 - q];
+            }
+          }
+        }
+      } else {  // a black tile's outputs are all 0
+        float4* z4 = reinterpret_cast<float4*>(stg);
+        for (int idx = lane; idx < (RW * pitch) >> 2; idx += 32) z4[idx] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) {
+        if (dense) {
+          FHT_CHECK(inf[r0].orow >= 0 && inf[r0].orow + RW <= D.nrows);
+          tma_store_row_stream(tm0_box, stg, inf[0].d0 & ~kTmaBit, inf[r0].orow);  // box {box, 8}
+        } else {
+#pragma unroll 1
+          for (int u = 0; u < RW; ++u) {
+            const RowInfo ri = inf[r0 + u];
+            if (ri.d0 & kTmaBit) {
+              FHT_CHECK((ri.d0 & ~kTmaBit) >= 0 && (ri.d0 & ~kTmaBit) < p.W && ri.orow >= 0 && ri.orow < D.nrows);
+              tma_store_row_stream(d == 0 ? tm0 : tm1, stg + u * ST_PITCH, ri.d0 & ~kTmaBit, ri.orow);  // clipped at W
+            }
+          }
+        }
+        tma_commit();
+        issued = true;
+      }
+      // columns the boxes do not cover (the cyclic wrap, a tile's end, range row-support edges): coalesced stores
+      if (remw[(d * NR + r0) >> 5]) {
+#pragma unroll 1
+        for (int u = 0; u < RW; ++u) {
+          const RowInfo ri = inf[r0 + u];
+          if (ri.mlo >= ri.mhi) continue;
+          A* drow = static_cast<A*>(D.ptr) + (int64_t)ri.orow * D.pitch;
+          const A* srow = stg + u * pitch;
+          const int xs0 = X - (WO2 - so[dense ? 0 : r0 + u]), d0 = ri.d0 & ~kTmaBit;
+          for (int x = ri.mlo + lane; x < ri.mhi; x += 32) {
+            int col = d0 + (x - xs0);
+            if (col >= p.W) col -= p.W;
+            FHT_CHECK(col >= 0 && col < p.W && ri.orow >= 0 && ri.orow < D.nrows && x - xs0 >= 0 && x - xs0 < pitch);
+            __stcs(drow + col, srow[x - xs0]);
+          }
+        }
+      }
+    }
+    pdl_trigger();
+    if (lane == 0 && issued) tma_wait_read();
+    return !black;
+  }
+#endif
   // ---- stores, one destination at a time (the staging plane is reused)
   bool issued = false;
   for (int dd = 0; dd < p.ndest; ++dd) {
