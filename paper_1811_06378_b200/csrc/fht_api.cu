@@ -75,6 +75,9 @@ void split_levels(Frame& f) {
   const int half_up = (f.K + 1) / 2;
   f.L = f.K - 6 > (half_up < 5 ? half_up : 5) ? f.K - 6 : (half_up < 5 ? half_up : 5);
   if (f.L > f.K) f.L = f.K;
+  if (const int l = env_int("FHT_SPLIT_L", 0)) {  // A/B: pass-2 levels (both passes must stay <= 6)
+    if (l <= 6 && f.K - l <= 6 && l < f.K) f.L = l;
+  }
   f.m = f.K - f.L;
   if (f.m < 1 && f.K >= 2) {  // keep pass 1 non-empty
     f.m = 1;
