@@ -17,14 +17,24 @@
 // assumption). The tile bodies are k_p1's and k_p2's (fht_tile.cuh), so the results are bit-identical.
 //
 // CTA shape: NT = max(pass-1 group, pass-2 group) threads; an item is NT / G1 pass-1 tiles or NT / G2
-// pass-2 tiles, each on its own thread group with its own shared memory (as fht_pipe.cuh). The bodies sit
-// behind call boundaries (one function per kind and sign) and the kernel keeps no state across them, so
-// each gets the register budget it has in its own kernel.
+// pass-2 tiles, each on its own thread group with its own shared memory (as fht_pipe.cuh). The bodies are
+// inlined (behind call boundaries every parameter read became a generic load; FHT_DUAL_NOINLINE=1 restores
+// that variant) and both kinds of items run slot-slowest, so an SM holds one sign's code at a time.
+// Measured slower than the two-launch schedule; opt-in.
 #pragma once
 #include "fht_pipe.cuh"
 
 namespace fht {
 namespace v2 {
+
+#ifndef FHT_DUAL_NOINLINE
+#define FHT_DUAL_NOINLINE 0
+#endif
+#if FHT_DUAL_NOINLINE
+#define DUAL_INLINE __noinline__
+#else
+#define DUAL_INLINE __forceinline__  // parameters stay in the constant bank (a call takes their address: generic loads)
+#endif
 
 struct DualParams {
   int64_t n1, n2;       // pass-1 / pass-2 items of the launch
@@ -44,13 +54,19 @@ struct DualShape {
 };
 
 template <typename Tin, int R, typename G>
-__device__ __noinline__ void dual_p1_tile(const G grp, unsigned char* smem, const CUtensorMap* tm_img0,
-                                          const CUtensorMap* tm_img1, const P1Dst* dst, const P1Params* p, int64_t t) {
-  const int64_t per_img = (int64_t)(p->ntiles << p->nq_log) * (1 << p->L);
-  const int il = (int)(t / per_img);
-  const int64_t r = t - (int64_t)il * per_img;
-  const int x = (int)(r % (p->ntiles << p->nq_log)), strip = (int)(r / (p->ntiles << p->nq_log));
-  const int qi = x & ((1 << p->nq_log) - 1), n = x >> p->nq_log;
+__device__ DUAL_INLINE void dual_p1_tile(const G grp, unsigned char* smem, const CUtensorMap* tm_img0,
+                                          const CUtensorMap* tm_img1, const P1Dst* dst, const P1Params* p, int64_t t,
+                                          int64_t t1_per_slot) {
+  // slot slowest (then image, strip, tile): the launch runs the slots one after another, and pass-2 items are
+  // ordered the same way, so an SM holds one sign's pass-1 tail, one fill path and one sign's pass-2 body at a
+  // time (the instruction cache: mixing them stalled C3's dual launch on instruction fetch, 43% of samples)
+  const int64_t per_slot = t1_per_slot;
+  const int qi = (int)(t / per_slot);
+  const int64_t r0 = t - (int64_t)qi * per_slot;
+  const int64_t per_img = (int64_t)p->ntiles << p->L;
+  const int il = (int)(r0 / per_img);
+  const int64_t r = r0 - (int64_t)il * per_img;
+  const int strip = (int)(r / p->ntiles), n = (int)(r % p->ntiles);
   const P1Slot& sl = p->slot[qi];
   if (n >= sl.ntiles) return;
   const int X = min(sl.xlo + p->TX * n, sl.xhi - p->TX);
@@ -58,7 +74,7 @@ __device__ __noinline__ void dual_p1_tile(const G grp, unsigned char* smem, cons
 }
 
 template <typename A, int R, int SIG, typename Tscr, typename G>
-__device__ __noinline__ void dual_p2_tile(const G grp, unsigned char* smem, const CUtensorMap* tm_scr0,
+__device__ DUAL_INLINE void dual_p2_tile(const G grp, unsigned char* smem, const CUtensorMap* tm_scr0,
                                           const CUtensorMap* tm_scr1, const CUtensorMap* tm0, const CUtensorMap* tm1,
                                           const CUtensorMap* tm0_box, const P2Params* p, int qi, int il, int jl, int n) {
   const P2Slot& sl = p->slot[qi];
@@ -94,20 +110,21 @@ k_dual(const __grid_constant__ CUtensorMap tm_img0, const __grid_constant__ CUte
     if (t >= dp.t1) return;
     unsigned char* sm = smem_raw + (size_t)g * DS::S1;
     if constexpr (DS::TPI1 == 1)
-      dual_p1_tile<Tin, R1>(GrpAll{}, sm, &tm_img0, &tm_img1, &dst, &p1, t);
+      dual_p1_tile<Tin, R1>(GrpAll{}, sm, &tm_img0, &tm_img1, &dst, &p1, t, dp.t1 >> p1.nq_log);
     else
-      dual_p1_tile<Tin, R1>(GrpPart<DS::G1>{g * DS::G1, 1 + g}, sm, &tm_img0, &tm_img1, &dst, &p1, t);
+      dual_p1_tile<Tin, R1>(GrpPart<DS::G1>{g * DS::G1, 1 + g}, sm, &tm_img0, &tm_img1, &dst, &p1, t, dp.t1 >> p1.nq_log);
     return;
   }
   const int g = threadIdx.x / DS::G2;
   const int64_t t = (b - c) * DS::TPI2 + g;
   if (t >= dp.t2) return;
-  // k_p2's order: tile n fastest, then group jl, then z = image-in-chunk * nq + slot
+  // tile n fastest, then group jl, then the image, the slot slowest (as the pass-1 items)
   const int n = (int)(t % dp.ntiles2);
   const int64_t s = t / dp.ntiles2;
   const int jl = (int)(s % dp.ngroups);
-  const int z = (int)(s / dp.ngroups);
-  const int qi = z & ((1 << p2.nq_log) - 1), il = z >> p2.nq_log;
+  const int64_t z = s / dp.ngroups;
+  const int64_t nimg2 = (dp.t2 >> p2.nq_log) / ((int64_t)dp.ngroups * dp.ntiles2);
+  const int qi = (int)(z / nimg2), il = (int)(z % nimg2);
   if (n >= p2.slot[qi].ntiles) return;
   unsigned char* sm = smem_raw + (size_t)g * DS::S2;
   if constexpr (DS::TPI2 == 1) {
