@@ -373,6 +373,7 @@ cudaError_t launch_pass2(int logr, dim3 grid, const Pass2Args& a, cudaStream_t s
 struct P1Maps {
   CUtensorMap img0, img1;
   v2::P1Dst dst;
+  CUtensorMap imgT;  // u8 transposed tiles (v2::P1Params::tfill_tma), else a copy of img0 (unused)
 };
 
 // Pass-1 destination view [z][j][strip][column] of a scratch buffer (dims column, strip, j, z; S strips,
@@ -399,7 +400,7 @@ cudaError_t launch_p1_t(dim3 grid, const P1Maps& m, const v2::P1Params& a, cudaS
   const cudaError_t attr =
       smem_optin(v2::k_p1<Tin, R>, v2::p1_smem_bytes(R, sizeof(Tin) == 1) + v2::kColmapStageBytes, done);
   if (attr != cudaSuccess) return attr;
-  return launch_pdl(v2::k_p1<Tin, R>, grid, dim3(v2::Split<R>::nw * 32), smem, st, m.img0, m.img1, m.dst, a);
+  return launch_pdl(v2::k_p1<Tin, R>, grid, dim3(v2::Split<R>::nw * 32), smem, st, m.img0, m.img1, m.dst, a, m.imgT);
 }
 template <typename Tin>
 cudaError_t launch_p1(int r, dim3 grid, const P1Maps& m, const v2::P1Params& a, cudaStream_t st) {
@@ -496,6 +497,27 @@ bool make_image_map32(CUtensorMap* m, const fht_image* img) {
   return fn(m, dt, 4, const_cast<void*>(img->data), dims, strides, box, e, CU_TENSOR_MAP_INTERLEAVE_NONE,
             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
          CUDA_SUCCESS;
+}
+// u8 transposed pass-1 tiles (v2::P1Params::tfill_tma): the image [img][row][col] bytes, box {2^R columns, 144 rows}
+bool make_imgT_map(P1Maps& m, v2::P1Params& p1, const fht_image* img, int R) {
+  p1.tfill_tma = 0;
+  m.imgT = m.img0;
+  if (img->dtype != FHT_U8 || R < 4 || p1.range || !aligned16(img->data) || img->row_stride % 16 != 0 ||
+      (img->batch > 1 && img->batch_stride % 16 != 0) || env_int("FHT_TFILL_TMA", 1) == 0)
+    return true;
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)img->w, (cuuint64_t)img->h, (cuuint64_t)img->batch};
+  cuuint64_t strides[2] = {(cuuint64_t)img->row_stride,
+                           (cuuint64_t)(img->batch == 1 ? img->h * img->row_stride : img->batch_stride)};
+  cuuint32_t box[3] = {(cuuint32_t)(1 << R), 144, 1};
+  cuuint32_t e[3] = {1, 1, 1};
+  if (fn(&m.imgT, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(img->data), dims, strides, box, e,
+         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return false;
+  p1.tfill_tma = 1;
+  return true;
 }
 bool make_p1_image_maps(CUtensorMap* m0, CUtensorMap* m1, const fht_image* img, const v2::P1Params& p1, size_t es) {
   if (p1.fill32) {
@@ -713,6 +735,7 @@ int run_orientation(const fht_image* img, const Frame& f, const Slot* slots, int
           m1s.img0 = m1s.dst.m[0];
           m1s.img1 = m1s.dst.m[0];
         }
+        if (!make_imgT_map(m1s, p1, img, f.m)) return FHT_ERR_CUDA;
         const dim3 g1((unsigned)(ntile1 * nq), (unsigned)sh->S, (unsigned)img->batch);
         log.before(st);
         cudaError_t e;
@@ -769,6 +792,7 @@ int run_orientation(const fht_image* img, const Frame& f, const Slot* slots, int
       m1.img0 = m1.dst.m[0];
       m1.img1 = m1.dst.m[0];
     }
+    if (!make_imgT_map(m1, p1, img, f.m)) return FHT_ERR_CUDA;
     // scratch as pass 2 reads it: columns [0, span1) = what pass 1 wrote; TMA zero-fills the rest
     if (!make_scr_maps(&m2.scr0, &m2.scr1, ws, f32, ses == 2, (uint64_t)span1, scr_rows, (uint64_t)sp.pitch))
       return FHT_ERR_CUDA;

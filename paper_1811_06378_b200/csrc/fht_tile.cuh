@@ -548,6 +548,7 @@ struct P1Params {
   int fill_tma;                      // non-transposed rows by TMA (image base/pitch 16-B aligned)
   int fill_vec;                      // transposed fill with 16-byte (u8: 4-byte) loads
   int fill32;                        // 4-byte rows by ONE TMA each: tm_img0 is the view [img][row][col/32][32] (w % 32 == 0)
+  int tfill_tma;                     // u8 transposed tiles by TMA (k_p1's tm_imgT: image, box {2^R columns, 144 rows})
   int nq, img0;
   int ntiles;                        // tiles per strip (max over slots)
   int L;                             // log2(#strips)
@@ -700,7 +701,8 @@ template <typename Tin, int R, bool INL = false, typename G>
 __device__ __forceinline__ bool p1_body(const G& grp, unsigned char* smem_raw, const CUtensorMap* tm_img0,
                                         const CUtensorMap* tm_img1, const P1Dst* dst, const P1Params& p,
                                         const P1Slot& sl, int img, int strip, int X, int zscr,
-                                        uint64_t* ext_bars = nullptr, uint32_t par = 0) {
+                                        uint64_t* ext_bars = nullptr, uint32_t par = 0,
+                                        const CUtensorMap* tm_imgT = nullptr) {
   using A = typename AccOf<Tin>::type;
   using S = Split<R>;
   constexpr int NT = S::nw * 32;
@@ -909,6 +911,33 @@ __device__ __forceinline__ bool p1_body(const G& grp, unsigned char* smem_raw, c
         }
       }
     }
+  } else if (sizeof(Tin) == 1 && NR >= 16 && tm_imgT && p.tfill_tma && !ext_bars) {
+    // ---- transposed u8 tile by TMA: the image block [Xa, Xa + 288) rows x [y0, y0 + NR) columns lands dense
+    // ([288][NR] bytes, zero outside the image) in the u8 tile area (two boxes of 144 rows), then each warp
+    // transposes 32 consecutive image rows x 4 columns per step: one 4-byte shared load, four conflict-free
+    // int column stores (FHT row y0 + c = image column, FHT column e = image row). Replaces NR/4 scattered 4-byte
+    // global loads per image row (C3's transposed pass 1 took 1.8x its non-transposed one).
+    uint8_t* tt = reinterpret_cast<uint8_t*>(smem_raw + main_buf_bytes(R));
+    uint64_t* b0 = bar;
+    if (tid == 0) {
+      mbar_init(b0);
+      mbar_expect_tx(b0, (uint32_t)(WA * NR));
+      tma_load_3d(tm_imgT, tt, b0, y0, Xa, img);
+      tma_load_3d(tm_imgT, tt + 144 * NR, b0, y0, Xa + 144, img);
+    }
+    grp.sync();
+    mbar_wait0(b0);
+    constexpr int NQ = NR >= 16 ? NR / 4 : 1;  // 4-byte words per image row
+    const int lane = threadIdx.x & 31, warp = tid >> 5;
+    for (int it = warp; it < (WA / 32) * NQ; it += NT / 32) {
+      const int q = it % NQ, e = (it / NQ) * 32 + lane;  // image row Xa + e, columns y0 + 4q .. + 3
+      const uint32_t wv = reinterpret_cast<const uint32_t*>(tt)[e * NQ + q];
+      A* d = buf + (4 * q) * FA_PITCH + e;
+      d[0] = static_cast<A>(wv & 0xffu);
+      d[FA_PITCH] = static_cast<A>((wv >> 8) & 0xffu);
+      d[2 * FA_PITCH] = static_cast<A>((wv >> 16) & 0xffu);
+      d[3 * FA_PITCH] = static_cast<A>(wv >> 24);
+    }
   } else if (p.fill_vec && NR >= 4) {
     // ---- transposed: FHT row y = image column, FHT column x = image row. Thread = (x, 4 y's):
     // one 16-byte (u8: 4-byte) load from image row x, 4 conflict-free column stores. All of a
@@ -979,7 +1008,8 @@ __device__ __forceinline__ bool p1_body(const G& grp, unsigned char* smem_raw, c
 template <typename Tin, int R>
 __global__ void __launch_bounds__(Split<R>::nw * 32, kMinBlocks<R>)
 k_p1(const __grid_constant__ CUtensorMap tm_img0, const __grid_constant__ CUtensorMap tm_img1,
-     const __grid_constant__ P1Dst dst, const __grid_constant__ P1Params p) {
+     const __grid_constant__ P1Dst dst, const __grid_constant__ P1Params p,
+     const __grid_constant__ CUtensorMap tm_imgT) {
   pdl_wait();  // the image may come from the previous kernel; the scratch may still be read by it
   // flat grid, quadrant slot fastest: with 148 SMs (a multiple of 4) the round-robin CTA
   // placement gives every SM CTAs of one slot, i.e. one sign and one fill path (I-cache locality)
@@ -993,7 +1023,7 @@ k_p1(const __grid_constant__ CUtensorMap tm_img0, const __grid_constant__ CUtens
   const int X = min(sl.xlo + p.TX * n, sl.xhi - p.TX);  // tile = window start (Xw = X)
   extern __shared__ __align__(128) unsigned char smem_raw[];
   p1_body<Tin, R>(GrpAll{}, smem_raw, &tm_img0, &tm_img1, &dst, p, sl, img, strip, X,
-                  p.z0 + (img - p.img0) * p.nq + qi);
+                  p.z0 + (img - p.img0) * p.nq + qi, nullptr, 0, &tm_imgT);
 }
 
 // ------------------------------------------------------------------------------------------
