@@ -409,6 +409,40 @@ __device__ __forceinline__ void tile_fht_ld(const G& grp, const LoadA& load, A* 
 
 // Input rows from shared memory: element (rho, e) at src[rho*src_pitch + rowoff[rho] + e]; with
 // blk_bars, a block's rows are waited for (TMA) by the warp that reads them.
+// The lane's VA = 9 consecutive narrow elements (u8 pass-1 rows, u16 pass-2 scratch rows) by 32-bit shared loads:
+// the aligned words covering them (3 for 9 bytes, 5 for 9 u16), funnel-shifted by the misalignment and split with
+// byte permutes -- a third (u8) / a half (u16) of the shared-memory wavefronts of one narrow load per element (these
+// passes are bound by the L1 / shared-memory pipe). e[k] = element lo + k.
+#ifndef FHT_NARROW_VEC
+#define FHT_NARROW_VEC 1
+#endif
+template <typename Tsrc>
+__device__ __forceinline__ void load9_narrow(const Tsrc* lo, uint32_t (&e)[VA]) {
+  const uintptr_t la = reinterpret_cast<uintptr_t>(lo);
+  const uint32_t* wp = reinterpret_cast<const uint32_t*>(la & ~uintptr_t(3));
+  const uint32_t sh = (uint32_t)(la & 3u) * 8u;
+  if constexpr (sizeof(Tsrc) == 1) {
+    const uint32_t w0 = wp[0], w1 = wp[1], w2 = wp[2];
+    const uint32_t x0 = __funnelshift_r(w0, w1, sh), x1 = __funnelshift_r(w1, w2, sh);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      e[k] = __byte_perm(x0, 0u, 0x4440u | k);
+      e[4 + k] = __byte_perm(x1, 0u, 0x4440u | k);
+    }
+    e[8] = (w2 >> sh) & 0xffu;
+  } else {
+    const uint32_t w0 = wp[0], w1 = wp[1], w2 = wp[2], w3 = wp[3], w4 = wp[4];
+    const uint32_t x[4] = {__funnelshift_r(w0, w1, sh), __funnelshift_r(w1, w2, sh), __funnelshift_r(w2, w3, sh),
+                           __funnelshift_r(w3, w4, sh)};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      e[2 * j] = x[j] & 0xffffu;
+      e[2 * j + 1] = x[j] >> 16;
+    }
+    e[8] = (w4 >> sh) & 0xffffu;
+  }
+}
+
 template <int R, int SIG, typename A, typename Tsrc, typename G, int CL = 1>
 __device__ __forceinline__ void tile_fht(const G& grp, const Tsrc* src, int src_pitch, const int* rowoff, A* fa,
                                          int fa_pitch, A (&w)[kTPW<R>][1 << Split<R>::b][VB],
@@ -424,8 +458,15 @@ __device__ __forceinline__ void tile_fht(const G& grp, const Tsrc* src, int src_
       const Tsrc* p = src + rho * src_pitch + rowoff[rho] + (SIG > 0 ? lane * VA : (WA - 1) - lane * VA);
       FHT_CHECK(smem_in_bounds(SIG > 0 ? p + VA - 1 : p, sizeof(Tsrc)) &&
                 smem_in_bounds(SIG > 0 ? p : p - (VA - 1), sizeof(Tsrc)));
+      if constexpr (FHT_NARROW_VEC && sizeof(Tsrc) < 4) {
+        uint32_t e[VA];
+        load9_narrow<Tsrc>(SIG > 0 ? p : p - (VA - 1), e);
 #pragma unroll
-      for (int q = 0; q < VA; ++q) v[r][q] = static_cast<A>(p[SIG > 0 ? q : -q]);
+        for (int q = 0; q < VA; ++q) v[r][q] = static_cast<A>(e[SIG > 0 ? q : VA - 1 - q]);
+      } else {
+#pragma unroll
+        for (int q = 0; q < VA; ++q) v[r][q] = static_cast<A>(p[SIG > 0 ? q : -q]);
+      }
     }
   };
   tile_fht_ld<R, SIG, A, decltype(load), G, CL>(grp, load, fa, fa_pitch, w, jp_lim);
