@@ -416,13 +416,18 @@ __device__ __forceinline__ void tile_fht_ld(const G& grp, const LoadA& load, A* 
 #ifndef FHT_NARROW_VEC
 #define FHT_NARROW_VEC 1
 #endif
+__device__ __forceinline__ uint32_t lds_b32(uint32_t a) {  // shared-space load (a generic load would be LD, not LDS)
+  uint32_t v;
+  asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");  // ordered before the in-place fa stores
+  return v;
+}
 template <typename Tsrc>
 __device__ __forceinline__ void load9_narrow(const Tsrc* lo, uint32_t (&e)[VA]) {
-  const uintptr_t la = reinterpret_cast<uintptr_t>(lo);
-  const uint32_t* wp = reinterpret_cast<const uint32_t*>(la & ~uintptr_t(3));
-  const uint32_t sh = (uint32_t)(la & 3u) * 8u;
+  const uint32_t la = smem_u32(lo);
+  const uint32_t wa = la & ~3u;
+  const uint32_t sh = (la & 3u) * 8u;
   if constexpr (sizeof(Tsrc) == 1) {
-    const uint32_t w0 = wp[0], w1 = wp[1], w2 = wp[2];
+    const uint32_t w0 = lds_b32(wa), w1 = lds_b32(wa + 4), w2 = lds_b32(wa + 8);
     const uint32_t x0 = __funnelshift_r(w0, w1, sh), x1 = __funnelshift_r(w1, w2, sh);
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -431,7 +436,8 @@ __device__ __forceinline__ void load9_narrow(const Tsrc* lo, uint32_t (&e)[VA]) 
     }
     e[8] = (w2 >> sh) & 0xffu;
   } else {
-    const uint32_t w0 = wp[0], w1 = wp[1], w2 = wp[2], w3 = wp[3], w4 = wp[4];
+    const uint32_t w0 = lds_b32(wa), w1 = lds_b32(wa + 4), w2 = lds_b32(wa + 8), w3 = lds_b32(wa + 12),
+                   w4 = lds_b32(wa + 16);
     const uint32_t x[4] = {__funnelshift_r(w0, w1, sh), __funnelshift_r(w1, w2, sh), __funnelshift_r(w2, w3, sh),
                            __funnelshift_r(w3, w4, sh)};
 #pragma unroll
