@@ -426,34 +426,8 @@ cudaError_t launch_p2_t(dim3 grid, const P2Maps& m, const v2::P2Params& a, cudaS
   return launch_pdl(v2::k_p2<A, R, Tscr>, grid, dim3(v2::Split<R>::nw * 32), smem, st, m.scr0, m.scr1, m.out0, m.out1,
                     m.out0_box, a);
 }
-// the 64-row pass-2 tile on a CTA pair (v2::k_p2c): cluster dims {2, 1, 1}, grid.x doubled. Opt-in
-// (FHT_P2_CLUSTER=1): measured 2x slower than k_p2<6> (DSMEM loads saturate the MIO queue).
-template <typename A, typename Tscr>
-cudaError_t launch_p2c(dim3 grid, const P2Maps& m, const v2::P2Params& a, cudaStream_t st) {
-  constexpr size_t smem = v2::p2c_smem_bytes<6>();
-  static std::atomic<unsigned long long> done{0};
-  const cudaError_t attr = smem_optin(v2::k_p2c<A, 6, Tscr>, smem, done);
-  if (attr != cudaSuccess) return attr;
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(grid.x * 2, grid.y, grid.z);
-  cfg.blockDim = dim3(v2::Split<6>::nw * 16);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute at[2];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = FHT_PDL;
-  at[1].id = cudaLaunchAttributeClusterDimension;
-  at[1].val.clusterDim.x = 2;
-  at[1].val.clusterDim.y = 1;
-  at[1].val.clusterDim.z = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 2;
-  return cudaLaunchKernelEx(&cfg, v2::k_p2c<A, 6, Tscr>, m.scr0, m.scr1, m.out0, m.out1, m.out0_box, a);
-}
-bool p2_cluster_on() { return env_int("FHT_P2_CLUSTER", 0) != 0; }  // opt-in: measured 2x slower
 template <typename A, typename Tscr = A>
 cudaError_t launch_p2(int r, dim3 grid, const P2Maps& m, const v2::P2Params& a, cudaStream_t st) {
-  if (r == 6 && p2_cluster_on()) return launch_p2c<A, Tscr>(grid, m, a, st);
   switch (r) {
     case 1: return launch_p2_t<A, 1, Tscr>(grid, m, a, st);
     case 2: return launch_p2_t<A, 2, Tscr>(grid, m, a, st);

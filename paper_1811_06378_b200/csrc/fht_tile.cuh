@@ -277,29 +277,6 @@ __device__ __forceinline__ void mbar_wait0(uint64_t* bar) {
   }
 }
 
-// Thread-block clusters (a 64-row tile on a CTA pair, CL = 2): rank, the cluster-wide barrier (release /
-// acquire: the partner's shared-memory writes before it are visible after it) and loads from the partner's
-// shared memory (mapa + ld.shared::cluster; DSMEM).
-__device__ __forceinline__ uint32_t cluster_rank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-__device__ __forceinline__ uint32_t mapa_u32(uint32_t addr, uint32_t rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
-  return r;
-}
-template <typename A>
-__device__ __forceinline__ A ld_dsmem(uint32_t addr) {
-  uint32_t v;
-  asm volatile("ld.shared::cluster.b32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
-  return *reinterpret_cast<const A*>(&v);
-}
-
 template <int NB, int V, int K, typename A>
 struct Level {
   static __device__ __forceinline__ void run(A (&v)[1 << NB][V]) {
@@ -350,24 +327,17 @@ __device__ __forceinline__ void warp_fht(A (&v)[1 << NB][V]) {
 // e = lane*VA + q (SIG = +1) or (WA - 1) - lane*VA - q (SIG = -1).
 // jp_lim: sub-pass-B groups computed (rows tau < jp_lim * 2^b; the others are not needed: a pruned plan's pass 1
 // stores only its first shifts)
-//
-// CL = 2 (a 64-row tile on a CTA pair of a cluster): each CTA holds half of the sub-pass-A blocks (its local
-// blocks 0 .. NBk/2 - 1 are the pair's blocks rank*NBk/2 + ...) and computes half of the sub-pass-B groups
-// (jp = rank*NA/2 + warp); a group reads row jp of every block, half of them from the partner's shared memory
-// after a cluster barrier, and a second cluster barrier keeps both CTAs' fa alive until both have read it.
-template <int R, int SIG, typename A, typename LoadA, typename G, int CL = 1>
+template <int R, int SIG, typename A, typename LoadA, typename G>
 __device__ __forceinline__ void tile_fht_ld(const G& grp, const LoadA& load, A* fa, int fa_pitch,
                                             A (&w)[kTPW<R>][1 << Split<R>::b][VB], int jp_lim = 1 << Split<R>::a) {
   using S = Split<R>;
-  constexpr int a = S::a, b = S::b, NW = S::nw / CL;
-  constexpr int NA = 1 << a, NBk = 1 << b, NBl = NBk / CL, NAl = NA / CL;
-  static_assert(CL == 1 || (NBl % NW == 0 && NAl <= NW * kTPW<R>), "cluster tile split");
+  constexpr int a = S::a, b = S::b, NW = S::nw;
+  constexpr int NA = 1 << a, NBk = 1 << b;
   const int warp = grp.tid() >> 5, lane = threadIdx.x & 31;
-  const int crank = CL > 1 ? (int)cluster_rank() : 0;
 
-  // sub-pass A: block blk = rows blk*2^a .. +2^a-1 -> fa row blk*2^a + j' = F_a[blk][j'] (CL: the CTA's local blocks)
+  // sub-pass A: block blk = rows blk*2^a .. +2^a-1 -> fa row blk*2^a + j' = F_a[blk][j']
 #pragma unroll 1
-  for (int blk = warp; blk < NBl; blk += NW) {
+  for (int blk = warp; blk < NBk; blk += NW) {
     A v[NA][VA];
     load(blk, v);
     warp_fht<a, VA>(v);
@@ -378,33 +348,24 @@ __device__ __forceinline__ void tile_fht_ld(const G& grp, const LoadA& load, A* 
 #pragma unroll
       for (int q = 0; q < VA; ++q) d[r * fa_pitch + q] = v[r][q];
   }
-  if constexpr (CL > 1) cluster_sync_all();
-  else grp.sync();
+  grp.sync();
 
   // sub-pass B: group jp: G[i'](c) = F_a[i'][jp](c + jp*i')  (pre-shear identity, local frame)
 #pragma unroll
   for (int g = 0; g < kTPW<R>; ++g) {
-    const int jl = warp + g * NW, jp = crank * NAl + jl;
-    if (jl < NAl && jp < jp_lim) {
+    const int jp = warp + g * NW;
+    if (jp < NA && jp < jp_lim) {
 #pragma unroll
       for (int i = 0; i < NBk; ++i) {
-        const int owner = i / NBl;  // the CTA holding block i (0 when CL == 1)
-        const A* s = fa + ((i - owner * NBl) * NA + jp) * fa_pitch + lane * VB + jp * i;
+        const A* s = fa + (i * NA + jp) * fa_pitch + lane * VB + jp * i;
         FHT_CHECK(smem_in_bounds(s + VB - 1, sizeof(A)) && lane * VB + jp * i + VB <= fa_pitch);
-        if (CL == 1 || owner == crank) {
 #pragma unroll
-          for (int q = 0; q < VB; ++q) w[g][i][q] = s[q];
-        } else {
-          const uint32_t ra = mapa_u32(smem_u32(s), (uint32_t)owner);
-#pragma unroll
-          for (int q = 0; q < VB; ++q) w[g][i][q] = ld_dsmem<A>(ra + 4 * q);
-        }
+        for (int q = 0; q < VB; ++q) w[g][i][q] = s[q];
       }
       warp_fht<b, VB>(w[g]);
     }
   }
-  if constexpr (CL > 1) cluster_sync_all();
-  else grp.sync();
+  grp.sync();
 }
 
 // Input rows from shared memory: element (rho, e) at src[rho*src_pitch + rowoff[rho] + e]; with
@@ -449,7 +410,7 @@ __device__ __forceinline__ void load9_narrow(const Tsrc* lo, uint32_t (&e)[VA]) 
   }
 }
 
-template <int R, int SIG, typename A, typename Tsrc, typename G, int CL = 1>
+template <int R, int SIG, typename A, typename Tsrc, typename G>
 __device__ __forceinline__ void tile_fht(const G& grp, const Tsrc* src, int src_pitch, const int* rowoff, A* fa,
                                          int fa_pitch, A (&w)[kTPW<R>][1 << Split<R>::b][VB],
                                          uint64_t* blk_bars = nullptr, uint32_t par = 0,
@@ -475,7 +436,7 @@ __device__ __forceinline__ void tile_fht(const G& grp, const Tsrc* src, int src_
       }
     }
   };
-  tile_fht_ld<R, SIG, A, decltype(load), G, CL>(grp, load, fa, fa_pitch, w, jp_lim);
+  tile_fht_ld<R, SIG, A>(grp, load, fa, fa_pitch, w, jp_lim);
 }
 
 // Sg: the staged element type (A, or uint16_t for the u8 pipeline's pass-1 scratch)
@@ -1131,32 +1092,28 @@ constexpr int kTmaBit = 1 << 30;
 
 // rbase: the scratch row of (group j, strip 0); strip i is row rbase + i. smem: the group's shared memory.
 // Returns whether the tile used its per-block mbarriers (every tile but a black one).
-// CL = 2: the 2^R-row tile on a CTA pair of a cluster (tile_fht_ld): this CTA loads strips [rank*NR/2, +NR/2)
-// and plans and stores output rows [rank*NR/2, +NR/2) of the group.
-template <typename A, int R, int SIG, typename Tscr, typename G, int CL = 1>
+template <typename A, int R, int SIG, typename Tscr, typename G>
 __device__ __forceinline__ bool p2_body(const G& grp, unsigned char* smem_raw, const CUtensorMap* tm_scr0,
                                         const CUtensorMap* tm_scr1, const CUtensorMap* tm0, const CUtensorMap* tm1,
                                         const CUtensorMap* tm0_box, const P2Params& p, const P2Slot& sl, int img,
                                         int j, int X, int own, int64_t rbase, uint64_t* ext_bars = nullptr,
                                         uint32_t par = 0) {
   using S = Split<R>;
-  constexpr int NW = S::nw / CL;
+  constexpr int NW = S::nw;
   constexpr int NT = NW * 32;
   constexpr int NR = 1 << R;
-  constexpr int NRo = NR / CL;                   // strips loaded / output rows stored by this CTA
   const int tid = grp.tid();
   A* buf = reinterpret_cast<A*>(smem_raw);
-  unsigned char* tab = smem_raw + main_buf_bytes(R) / CL;
+  unsigned char* tab = smem_raw + main_buf_bytes(R);
   int* rowoff = reinterpret_cast<int*>(tab);                  // [64]
   int* soff = rowoff + 64;                                    // [2][64]
   // [8] per-block mbarriers: the tile's own, or the caller's persistent ones (parity bits `par`)
   uint64_t* bar = ext_bars ? ext_bars : reinterpret_cast<uint64_t*>(tab + 768);
-  RowInfo* info = reinterpret_cast<RowInfo*>(tab + 1024);     // [2][NRo], 16 B each
+  RowInfo* info = reinterpret_cast<RowInfo*>(tab + 1024);     // [2][NR], 16 B each
   const int TX = p.TX, box = TX + WO2;
   const int Xw = X - WO2;                        // window start: window index s <-> x = Xw + s
   const int Xa = SIG > 0 ? Xw : Xw - (WA - WC);  // x of input index e = 0
   const int t0 = j * NR, tmax = t0 + NR - 1;
-  const int tau0 = CL > 1 ? (int)cluster_rank() * NRo : 0;  // this CTA's first strip / output row of the tile
   const int warp = tid >> 5, lane = threadIdx.x & 31;
   A w[kTPW<R>][1 << S::b][VB];
 
@@ -1184,14 +1141,13 @@ __device__ __forceinline__ bool p2_body(const G& grp, unsigned char* smem_raw, c
     constexpr int kAl = 16 / (int)sizeof(Tscr), kBox1 = sizeof(Tscr) == 2 ? 40 : 36;
     constexpr uint32_t kRowBytes = (256 + kBox1) * (uint32_t)sizeof(Tscr);
 #endif
-    for (int b = warp; b < NBk / CL; b += NW) {
+    for (int b = warp; b < NBk; b += NW) {
       if (lane == 0) {
         if (!ext_bars) mbar_init(bar + b);
         mbar_expect_tx(bar + b, NA * kRowBytes);
-        for (int il = b * NA; il < (b + 1) * NA; ++il) {
-          const int i = tau0 + il;  // strip of the tile (local row il)
+        for (int i = b * NA; i < (b + 1) * NA; ++i) {
           const int a0 = (Xa + SIG * j * i - sl.xlo1) & ~(kAl - 1);
-          Tscr* d = reinterpret_cast<Tscr*>(buf + il * TMA_PITCH);
+          Tscr* d = reinterpret_cast<Tscr*>(buf + i * TMA_PITCH);
           const int row = (int)(rbase + (int64_t)(i >> p.logS) * p.strideG + (i & ((1 << p.logS) - 1)));
           FHT_CHECK(row >= 0 && row < p.scr_rows);
 #if FHT_ROW32
@@ -1202,7 +1158,7 @@ __device__ __forceinline__ bool p2_body(const G& grp, unsigned char* smem_raw, c
 #endif
         }
       }
-      if (lane < NA) rowoff[b * NA + lane] = (Xa + SIG * j * (tau0 + b * NA + lane) - sl.xlo1) & (kAl - 1);
+      if (lane < NA) rowoff[b * NA + lane] = (Xa + SIG * j * (b * NA + lane) - sl.xlo1) & (kAl - 1);
     }
     __syncwarp();
   }
@@ -1225,8 +1181,8 @@ __device__ __forceinline__ bool p2_body(const G& grp, unsigned char* smem_raw, c
   // remw[c]: some row of plan items [32c, 32c + 32) has columns left to plain stores (one ballot per warp: the
   // items of a warp are one 32-item chunk while NT >= ndest * NR, which holds for every R)
   int* const remw = reinterpret_cast<int*>(tab + 896);
-  for (int it = tid; it < p.ndest * NRo; it += NT) {
-    const int d = it / NRo, tau = it - d * NRo, t = t0 + tau0 + tau;
+  for (int it = tid; it < p.ndest * NR; it += NT) {
+    const int d = it / NR, tau = it - d * NR, t = t0 + tau;
     const P2Dest& D = p.dest[d];
     int vlo = sl.xbeg, vhi = sl.xend, k = 0;
     if (p.range) {
@@ -1259,9 +1215,9 @@ __device__ __forceinline__ bool p2_body(const G& grp, unsigned char* smem_raw, c
       ri.d0 |= kTmaBit;
       ri.mlo = max(ri.mlo, xs0 + min(box, p.W - d0));  // what the box does not cover (wrap, tile end)
     }
-    info[d * NRo + tau] = ri;
+    info[d * NR + tau] = ri;
     soff[d * 64 + tau] = WO2 - r;
-    if (NT >= 2 * NRo) {
+    if (NT >= 2 * NR) {
       const unsigned rem = __ballot_sync(__activemask(), ri.mlo < ri.mhi);
       if ((threadIdx.x & 31) == 0) remw[it >> 5] = rem != 0u;
     }
@@ -1275,10 +1231,9 @@ __device__ __forceinline__ bool p2_body(const G& grp, unsigned char* smem_raw, c
 #endif
 
   if (!black)
-    tile_fht<R, SIG, A, Tscr, G, CL>(grp, reinterpret_cast<const Tscr*>(buf), TMA_PITCH * 4 / (int)sizeof(Tscr), rowoff,
+    tile_fht<R, SIG, A, Tscr, G>(grp, reinterpret_cast<const Tscr*>(buf), TMA_PITCH * 4 / (int)sizeof(Tscr), rowoff,
                                      buf, TMA_PITCH, w, bar, par);
 
-  static_assert(CL == 1 || kWarpStore<R>, "a cluster tile stores per warp");
 #if FHT_P2_WARPSTORE
   if constexpr (kWarpStore<R>) {
     // ---- warp-owned stores: warp w holds output rows [8w, 8w + 8) (sub-pass-B group jp = w) and stages them in
@@ -1292,7 +1247,7 @@ __device__ __forceinline__ bool p2_body(const G& grp, unsigned char* smem_raw, c
     for (int dd = 0; dd < p.ndest; ++dd) {
       const int d = FHT_P2_REVERSE_DEST ? p.ndest - 1 - dd : dd;
       const P2Dest& D = p.dest[d];
-      const RowInfo* inf = info + d * NRo;
+      const RowInfo* inf = info + d * NR;
       const int* so = soff + d * 64;
       if (dd > 0) {
         if (lane == 0 && issued) tma_wait_read();
@@ -1352,7 +1307,7 @@ __device__ __forceinline__ bool p2_body(const G& grp, unsigned char* smem_raw, c
         issued = true;
       }
       // columns the boxes do not cover (the cyclic wrap, a tile's end, range row-support edges): coalesced stores
-      if (remw[(d * NRo + r0) >> 5]) {
+      if (remw[(d * NR + r0) >> 5]) {
 #pragma unroll 1
         for (int u = 0; u < RW; ++u) {
           const RowInfo ri = inf[r0 + u];

@@ -778,53 +778,6 @@ def test_pipe_matches_two_launch_and_oracle(fht, O, monkeypatch, shape, dt, batc
         check(q1.view[batch - 1, 0].cpu().numpy(), O.hough_recursive(imgs[batch - 1], O.QC), dt != "f32")
 
 
-# ------------------------------------------------------------------ 64-row pass-2 tiles on a CTA pair (k_p2c)
-@pytest.mark.parametrize("shape,dt,batch,split", [((4096, 4096), "f32", 1, ""), ((2048, 2048), "f32", 2, "6"),
-                                                  ((4096, 1000), "u8", 1, ""), ((3000, 3000), "i32", 1, ""),
-                                                  ((2048, 1500), "u8", 2, "6")], ids=str)
-def test_p2_cluster_matches_single_cta_and_oracle(fht, O, monkeypatch, shape, dt, batch, split):
-    """A 64-row pass-2 tile split over the two CTAs of a cluster (half the strips each, sub-pass-B rows of the
-    partner's blocks read from its shared memory) is bit-identical to the one-CTA k_p2<6> for f32 / u8 (u16
-    scratch) / i32, both outputs, K = 12 (6 + 6) and K = 11 forced to 5 + 6; the last image's quadrants match the
-    oracle on sampled rows."""
-    from synth import random_image
-    ims = np.stack([random_image(shape, dt, seed=shape[0] + 11 * b) for b in range(batch)])
-    t = dev(ims)
-    if split:
-        monkeypatch.setenv("FHT_SPLIT_L", split)
-    monkeypatch.delenv("FHT_P2_CLUSTER", raising=False)
-    h0, s0 = fht.full(t, pair=True)
-    torch.cuda.synchronize()
-    monkeypatch.setenv("FHT_P2_CLUSTER", "1")
-    h, s = fht.full(t, pair=True)
-    torch.cuda.synchronize()
-    Hps = O.full_padding(*shape)
-    for q in range(4):  # the rows every quadrant has (a non-square frame's short quadrants leave the rest unwritten)
-        n = Hps[0] if q in (O.QA, O.QB) else Hps[1]
-        assert torch.equal(h.view[:, q, :n], h0.view[:, q, :n]) and torch.equal(s.view[:, q, :n], s0.view[:, q, :n]), q
-    img = ims[batch - 1]
-    got = h.view[batch - 1].cpu().numpy()
-    rng = np.random.default_rng(5)
-    for q in range(4):
-        fr = O.quadrant_frame(img, q, square_to=O.full_padding(*shape))
-        cells = _sample_cells(fr.Hp, fr.W, 48, rng)
-        check(np.array([got[q, a, c] for a, c in cells], dtype=got.dtype), O.hough_cells_direct(fr, cells), dt != "f32")
-
-
-def test_p2_cluster_angle_range(fht, O, monkeypatch):
-    """C4's call (the §4 plan built in the call, 6 + 6 levels, both outputs) with cluster and one-CTA pass 2."""
-    from synth import random_image
-    img = random_image((4096, 4096), "f32", seed=44)
-    t = dev(img)
-    monkeypatch.delenv("FHT_P2_CLUSTER", raising=False)
-    r0, rs0 = fht.angle_range(t, -15.0, 15.0, pair=True)
-    torch.cuda.synchronize()
-    monkeypatch.setenv("FHT_P2_CLUSTER", "1")
-    r1, rs1 = fht.angle_range(t, -15.0, 15.0, pair=True)
-    torch.cuda.synchronize()
-    assert torch.equal(r0.storage, r1.storage) and torch.equal(rs0.storage, rs1.storage)
-
-
 # ------------------------------------------------------------------ staggered pass pairs (fht_dual.cuh)
 @pytest.mark.parametrize("shape,dt,batch,imgs", [((512, 512), "u8", 5, "1"), ((512, 512), "u8", 7, "2"),
                                                  ((1024, 1024), "f32", 3, "1"), ((2048, 2048), "f32", 3, "1"),
