@@ -21,6 +21,7 @@
 #include "../../include/fht.h"
 #include "fht_kernels.cuh"
 #include "fht_tile.cuh"
+#include "fht_p1p.cuh"
 #include "fht_internal.cuh"
 #include "fht_peaks.cuh"
 
@@ -374,6 +375,9 @@ struct P1Maps {
   CUtensorMap img0, img1;
   v2::P1Dst dst;
   CUtensorMap imgT;  // u8 transposed tiles (v2::P1Params::tfill_tma), else a copy of img0 (unused)
+  CUtensorMap img8, imgS, dst4;  // persistent pass 1 (k_p1p): image box {32, 10, 8, 1}, swizzled image box
+                                 // {32, 144, 1} (transposed slots), scratch box {TX, 1, 4, 1}
+  int persist = 0;         // launch k_p1p instead of k_p1 (make_p1p_maps)
 };
 
 // Pass-1 destination view [z][j][strip][column] of a scratch buffer (dims column, strip, j, z; S strips,
@@ -402,8 +406,31 @@ cudaError_t launch_p1_t(dim3 grid, const P1Maps& m, const v2::P1Params& a, cudaS
   if (attr != cudaSuccess) return attr;
   return launch_pdl(v2::k_p1<Tin, R>, grid, dim3(v2::Split<R>::nw * 32), smem, st, m.img0, m.img1, m.dst, a, m.imgT);
 }
+// Persistent pass 1 (fht_p1p.cuh): 64-row strips of 4-byte images, all 64 shifts to one scratch; two CTAs per SM
+// walk the tiles of `grid` (the k_p1 grid of the same launch), gridDim.x a multiple of the slot count.
+template <typename Tin>
+cudaError_t launch_p1p_t(dim3 grid, const P1Maps& m, const v2::P1Params& a, cudaStream_t st) {
+  const size_t smem = v2::p1p_smem_bytes();
+  static std::atomic<unsigned long long> done{0};
+  cudaError_t e = smem_optin(v2::k_p1p<Tin>, smem, done);
+  if (e != cudaSuccess) return e;
+  int dev = 0, nsm = 0;
+  if ((e = cudaGetDevice(&dev)) != cudaSuccess ||
+      (e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess)
+    return e;
+  const long long total = (long long)grid.x * grid.y * grid.z;
+  if (total <= 0 || total >= (1ll << 31) - 4096) return cudaErrorInvalidValue;
+  long long G = 2ll * nsm;
+  G -= G % a.nq;
+  if (G < a.nq) G = a.nq;
+  if (G > total) G = total;
+  return launch_pdl(v2::k_p1p<Tin>, dim3((unsigned)G), dim3(256), smem, st, m.img8, m.imgS, m.dst4, a, (int)total);
+}
 template <typename Tin>
 cudaError_t launch_p1(int r, dim3 grid, const P1Maps& m, const v2::P1Params& a, cudaStream_t st) {
+  if constexpr (sizeof(Tin) == 4) {
+    if (m.persist && r == 6) return launch_p1p_t<Tin>(grid, m, a, st);
+  }
   switch (r) {
     case 1: return launch_p1_t<Tin, 1>(grid, m, a, st);
     case 2: return launch_p1_t<Tin, 2>(grid, m, a, st);
@@ -459,17 +486,33 @@ bool make_image_map(CUtensorMap* m, const fht_image* img, uint32_t box_cols) {
 
 // Pass-1 fill32 (FHT_ROW32, 4-byte images with w % 32 == 0): the view [img][row][col/32][32], box {32, 10, 1, 1}
 // = one 320-column row per copy from a 128-byte aligned column.
-bool make_image_map32(CUtensorMap* m, const fht_image* img) {
+bool make_image_map32(CUtensorMap* m, const fht_image* img, uint32_t box_rows = 1) {
   auto fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[4] = {32, (cuuint64_t)(img->w / 32), (cuuint64_t)img->h, (cuuint64_t)img->batch};
   cuuint64_t strides[3] = {128, (cuuint64_t)(img->row_stride * 4), (cuuint64_t)(img->batch_stride * 4)};
   if (img->batch == 1) strides[2] = (cuuint64_t)(img->h * img->row_stride * 4);
-  cuuint32_t box[4] = {32, 10, 1, 1};
+  cuuint32_t box[4] = {32, 10, box_rows, 1};
   cuuint32_t e[4] = {1, 1, 1, 1};
   const CUtensorMapDataType dt = img->dtype == FHT_I32 ? CU_TENSOR_MAP_DATA_TYPE_INT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
   return fn(m, dt, 4, const_cast<void*>(img->data), dims, strides, box, e, CU_TENSOR_MAP_INTERLEAVE_NONE,
             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
+}
+// Persistent pass 1, transposed slots (k_p1p): the 4-byte image [img][row][col], box {32 columns, 144 rows, 1} with
+// the 128-byte swizzle (16-byte chunk ^ (row & 7)): the block lands untransposed and is read column-wise without
+// bank conflicts.
+bool make_image_map_swz(CUtensorMap* m, const fht_image* img) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)img->w, (cuuint64_t)img->h, (cuuint64_t)img->batch};
+  cuuint64_t strides[2] = {(cuuint64_t)(img->row_stride * 4), (cuuint64_t)(img->batch_stride * 4)};
+  if (img->batch == 1) strides[1] = (cuuint64_t)(img->h * img->row_stride * 4);
+  cuuint32_t box[3] = {32, (cuuint32_t)v2::kP1pBoxRows, 1};
+  cuuint32_t e[3] = {1, 1, 1};
+  const CUtensorMapDataType dt = img->dtype == FHT_I32 ? CU_TENSOR_MAP_DATA_TYPE_INT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+  return fn(m, dt, 3, const_cast<void*>(img->data), dims, strides, box, e, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
          CUDA_SUCCESS;
 }
 // u8 transposed pass-1 tiles (v2::P1Params::tfill_tma): the image [img][row][col] bytes, box {2^R columns, 144 rows}
@@ -767,6 +810,15 @@ int run_orientation(const fht_image* img, const Frame& f, const Slot* slots, int
       m1.img1 = m1.dst.m[0];
     }
     if (!make_imgT_map(m1, p1, img, f.m)) return FHT_ERR_CUDA;
+    // persistent pass 1 (k_p1p): 64-row strips of 4-byte images with one-TMA rows, full-width tiles, all 64 shifts
+    if (f.m == 6 && es == 4 && !rg && p1.fill_tma && p1.fill32 && p1.TX == v2::TX1 && ngroups == 64 && !pipe &&
+        (int64_t)ntile1 * nq * nstrips * sp.chunk < (1ll << 30) && env_int("FHT_P1_PERSIST", 1) != 0) {
+      if (!make_image_map32(&m1.img8, img, 8) || !make_image_map_swz(&m1.imgS, img) ||
+          !make_dst_map(&m1.dst4, ws, ses, f32, sp.pitch, nstrips, 1 << f.m, (int64_t)(scr_rows / f.Hp), p1.TX,
+                        v2::kP1pHalf))
+        return FHT_ERR_CUDA;
+      m1.persist = 1;
+    }
     // scratch as pass 2 reads it: columns [0, span1) = what pass 1 wrote; TMA zero-fills the rest
     if (!make_scr_maps(&m2.scr0, &m2.scr1, ws, f32, ses == 2, (uint64_t)span1, scr_rows, (uint64_t)sp.pitch))
       return FHT_ERR_CUDA;

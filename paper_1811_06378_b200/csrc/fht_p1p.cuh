@@ -1,0 +1,231 @@
+// fht_p1p.cuh -- persistent pass 1 for 64-row strips of 4-byte images (k_p1p; DESIGN.md §4 "Persistent pass 1").
+//
+// k_p1 runs one tile per CTA: launch, TMA issue, DRAM latency, sub-passes A and B, staging, the scratch store and
+// its drain are one dependent chain, and with two 8-warp CTAs per SM (the 80 KB plane of a 64-row tile) an SM often
+// holds a single computing CTA. Here a CTA walks tiles T = blockIdx.x, + gridDim.x, ... (two CTAs per SM; gridDim.x
+// is a multiple of the slot count, so a CTA stays on one quadrant slot: one sign, one fill path) and
+//   * issues the NEXT tile's loads as soon as sub-pass B has read the plane (the barrier that ends tile_fht_ld):
+//     non-transposed slots one TMA box {32, 10, 8 rows} per warp (its own sub-pass-A block, its own mbarrier, phase
+//     parity alternating per tile); transposed slots (FHT row = image column) four TMA boxes {32 image columns, 144
+//     image rows} with the 128-byte swizzle: the block lands UNtransposed, and sub-pass A reads a lane's column e of
+//     its 8 FHT rows (8 consecutive image columns = two 16-byte chunks of image row e) with two 16-byte loads -- the
+//     swizzle (chunk ^ (row & 7)) makes the eight lanes of a quarter-warp, whose rows e = 9 lane + q differ mod 8,
+//     hit eight different chunks: conflict-free, 18 loads per lane instead of 72. The transposition is index
+//     arithmetic; a CTA barrier separates those reads from the in-place sub-pass-A stores. (4-byte
+//     cp.async copies that transpose on the way in measured 1.45x slower than k_p1's vector fill.)
+//   * stages the results outside the plane: every warp owns the 8 rows of its sub-pass-B group and writes them in
+//     two halves through its own [4][TX] slot (3456 B), one bulk store {TX, 1, 4, 1} per half, waiting only for its
+//     own previous bulk read. No CTA barrier after sub-pass B's, no drain before the next tile.
+// The arithmetic is tile_fht_ld's (the same butterflies in the same order as k_p1): results are bit-identical.
+#pragma once
+#include "fht_tile.cuh"
+
+namespace fht {
+namespace v2 {
+
+constexpr int kP1pHalf = 4;                                                  // rows per staged half
+constexpr size_t kP1pStageBytes = (size_t)8 * kP1pHalf * TX1 * 4;            // 8 warps x [4][216] x 4 B = 27648
+__host__ __device__ constexpr size_t p1p_smem_bytes() { return main_buf_bytes(6) + kP1pStageBytes + 128; }
+
+constexpr int kP1pBoxRows = 144;                                 // transposed slots: image rows per TMA box
+constexpr uint32_t kP1pBoxBytes = kP1pBoxRows * 128;             // {32 columns, 144 rows} x 4 B = 18432 (18 x 1024)
+
+struct P1pTile {
+  int X, strip, img_l;
+};
+
+// One CTA's tiles of slot `sl` (sign SIG, transposed TR). tm_img8: the image view [img][row][col/32][32] with box
+// {32, 10, 8, 1}; tm_imgS: the image [img][row][col] with box {32, 144, 1} and the 128-byte swizzle; tm_dst4: the
+// scratch view [z][j][strip][column] with box {TX, 1, 4, 1}.
+template <typename Tin, int SIG, bool TR>
+__device__ __forceinline__ void p1p_run(unsigned char* smem, const CUtensorMap* tm_img8, const CUtensorMap* tm_imgS,
+                                        const CUtensorMap* tm_dst4, const P1Params& p, const P1Slot& sl, int qi,
+                                        int total) {
+  using A = typename AccOf<Tin>::type;
+  static_assert(sizeof(Tin) == 4 && sizeof(A) == 4, "4-byte images");
+  constexpr int R = 6, NA = 1 << Split<R>::a, NR = 1 << R;
+  static_assert(Split<R>::nw == 8 && NA == 8 && (1 << Split<R>::b) == 8, "one sub-pass-A block and one B group per warp");
+  constexpr int PITCH = TMA_PITCH;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  A* plane = reinterpret_cast<A*>(smem);
+  A* stg = reinterpret_cast<A*>(smem + main_buf_bytes(R)) + warp * (kP1pHalf * TX1);
+  // non-transposed: one mbarrier per warp (its block's rows); transposed: one for the tile's four boxes
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + main_buf_bytes(R) + kP1pStageBytes) + (TR ? 8 : warp);
+  const int ntq = p.ntiles << p.nq_log;
+  const int G = (int)gridDim.x;
+
+  auto decode = [&](int T, P1pTile& t) -> bool {
+    const int rest = T / ntq, x = T - rest * ntq;
+    const int n = x >> p.nq_log;
+    if (n >= sl.ntiles) return false;
+    t.X = min(sl.xlo + p.TX * n, sl.xhi - p.TX);
+    t.strip = rest & ((1 << p.L) - 1);
+    t.img_l = rest >> p.L;
+    return true;
+  };
+  auto next = [&](int T, P1pTile& t) {
+    do {
+      T += G;
+    } while (T < total && !decode(T, t));
+    return T;
+  };
+  // loads of a tile into the plane (free: every warp is past sub-pass B's reads)
+  auto issue = [&](const P1pTile& t) {
+    const int Xa = SIG > 0 ? t.X : t.X - (WA - WC);
+    const int y0 = (p.strip0 + t.strip) * NR;
+    const int img = p.img0 + t.img_l;
+    if constexpr (!TR) {
+      if (lane == 0) {
+        mbar_expect_tx(bar, (uint32_t)NA * TMA_PITCH * 4);
+        tma_load_4d(tm_img8, plane + warp * NA * TMA_PITCH, bar, 0, (Xa & ~31) >> 5, y0 + warp * NA, img);
+      }
+    } else {
+      // image rows [Xa, Xa + 288) x image columns [y0, y0 + 64): box (hb, rb) = columns y0 + 32 hb.., rows Xa + 144 rb..
+      if (tid == 0) {
+        mbar_expect_tx(bar, 4u * kP1pBoxBytes);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          tma_load_3d(tm_imgS, smem + k * kP1pBoxBytes, bar, y0 + 32 * (k >> 1), Xa + kP1pBoxRows * (k & 1), img);
+      }
+    }
+  };
+
+  if constexpr (!TR) {
+    if (lane == 0) mbar_init(bar);
+    __syncwarp();
+  } else {
+    if (tid == 0) mbar_init(bar);
+    __syncthreads();
+  }
+  int T = (int)blockIdx.x;
+  P1pTile cur{}, nxt{};
+  if (T < total && !decode(T, cur)) T = next(T, cur);
+  if (T < total) {
+    issue(cur);
+    uint32_t par = 0;
+    while (true) {
+      const int Tn = next(T, nxt);
+      const bool more = Tn < total;
+      const int Xa = SIG > 0 ? cur.X : cur.X - (WA - WC);
+      A w[1][1 << Split<R>::b][VB];
+      if constexpr (!TR) {
+        const int rowoff = Xa & 31;
+        auto load = [&](int blk, A (&v)[NA][VA]) {
+          mbar_wait(bar, par);  // blk == warp: this warp's own rows
+#pragma unroll
+          for (int r = 0; r < NA; ++r) {
+            const A* q0 = plane + (blk * NA + r) * PITCH + rowoff + (SIG > 0 ? lane * VA : (WA - 1) - lane * VA);
+#pragma unroll
+            for (int q = 0; q < VA; ++q) v[r][q] = q0[SIG > 0 ? q : -q];
+          }
+        };
+        tile_fht_ld<R, SIG, A>(GrpAll{}, load, plane, PITCH, w);
+      } else {
+        // sub-pass A from the untransposed, swizzled block: FHT rows warp * 8 + r = image columns = chunks
+        // ch, ch + 1 of box column hb; FHT column e = image row e
+        A v[NA][VA];
+        mbar_wait(bar, par);
+        {
+          const uint32_t base = smem_u32(smem) + (uint32_t)(warp >> 2) * 2u * kP1pBoxBytes;
+          const uint32_t ch = (2u * (uint32_t)warp) & 7u;
+#pragma unroll
+          for (int q = 0; q < VA; ++q) {
+            const int e = SIG > 0 ? lane * VA + q : (WA - 1) - lane * VA - q;
+            const int rb = e >= kP1pBoxRows ? 1 : 0, er = e - rb * kP1pBoxRows;
+            const uint32_t a0 = base + (uint32_t)rb * kP1pBoxBytes + (uint32_t)er * 128u + ((ch ^ ((uint32_t)er & 7u)) << 4);
+            uint32_t x[8];
+            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(x[0]), "=r"(x[1]), "=r"(x[2]), "=r"(x[3]) : "r"(a0) : "memory");
+            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(x[4]), "=r"(x[5]), "=r"(x[6]), "=r"(x[7]) : "r"(a0 ^ 16u) : "memory");
+#pragma unroll
+            for (int r = 0; r < NA; ++r) {
+              if constexpr (std::is_same<A, float>::value)
+                v[r][q] = __uint_as_float(x[r]);
+              else
+                v[r][q] = static_cast<A>(x[r]);
+            }
+          }
+        }
+        __syncthreads();  // every warp has read the block: sub-pass A's rows overwrite it
+        warp_fht<Split<R>::a, VA>(v);
+        {
+          A* d = plane + (warp * NA) * PITCH + lane * VA;
+#pragma unroll
+          for (int r = 0; r < NA; ++r)
+#pragma unroll
+            for (int q = 0; q < VA; ++q) d[r * PITCH + q] = v[r][q];
+        }
+        __syncthreads();
+        // sub-pass B (as tile_fht_ld): group jp = warp reads row jp of every block at column c + jp * i
+#pragma unroll
+        for (int i = 0; i < NA; ++i) {
+          const A* sp = plane + (i * NA + warp) * PITCH + lane * VB + warp * i;
+#pragma unroll
+          for (int q = 0; q < VB; ++q) w[0][i][q] = sp[q];
+        }
+        warp_fht<Split<R>::b, VB>(w[0]);
+        __syncthreads();
+      }
+      par ^= 1u;
+      if (more) issue(nxt);
+      // ---- the warp's 8 rows tau = warp * 8 + u, in two halves through its slot
+      const int Xs = cur.X - sl.xlo, zscr = p.z0 + cur.img_l * p.nq + qi;
+      FHT_CHECK(Xs >= 0 && Xs + p.TX <= sl.xhi - sl.xlo && p.TX == TX1);
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        if (lane == 0) tma_wait_read();  // the slot's previous bulk store has read it
+        __syncwarp();
+        if (lane < 31) {
+          const int lo = SIG > 0 ? lane * VB : (WC - VB) - lane * VB;
+#pragma unroll
+          for (int u = 0; u < kP1pHalf; ++u) {
+            A* d = stg + u * TX1 + lo;
+#pragma unroll
+            for (int q = 0; q < VB - 1; ++q) d[q] = w[0][half * kP1pHalf + u][SIG > 0 ? q : VB - 1 - q];
+            if (lo + VB - 1 < TX1) d[VB - 1] = w[0][half * kP1pHalf + u][SIG > 0 ? VB - 1 : 0];
+          }
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+#if FHT_SCR_KEEP
+          tma_store_4d_keep(tm_dst4, stg, Xs, cur.strip, warp * 8 + half * kP1pHalf, zscr);
+#else
+          tma_store_4d(tm_dst4, stg, Xs, cur.strip, warp * 8 + half * kP1pHalf, zscr);
+#endif
+          tma_commit();
+        }
+      }
+      if (!more) break;
+      T = Tn;
+      cur = nxt;
+    }
+  }
+  pdl_trigger();
+  if (lane == 0) tma_wait_read();
+}
+
+template <typename Tin>
+__global__ void __launch_bounds__(256, 2)
+k_p1p(const __grid_constant__ CUtensorMap tm_img8, const __grid_constant__ CUtensorMap tm_imgS,
+      const __grid_constant__ CUtensorMap tm_dst4, const __grid_constant__ P1Params p, int total) {
+  pdl_wait();  // the image may come from the previous kernel; the scratch may still be read by it
+  extern __shared__ __align__(1024) unsigned char smem_raw[];  // swizzled boxes: 1024-byte aligned
+  const int qi = blockIdx.x & ((1 << p.nq_log) - 1);  // gridDim.x % nq == 0: every tile of this CTA is slot qi's
+  const P1Slot& sl = p.slot[qi];
+  if (!sl.transposed) {
+    if (sl.sigma > 0)
+      p1p_run<Tin, 1, false>(smem_raw, &tm_img8, &tm_imgS, &tm_dst4, p, sl, qi, total);
+    else
+      p1p_run<Tin, -1, false>(smem_raw, &tm_img8, &tm_imgS, &tm_dst4, p, sl, qi, total);
+  } else {
+    if (sl.sigma > 0)
+      p1p_run<Tin, 1, true>(smem_raw, &tm_img8, &tm_imgS, &tm_dst4, p, sl, qi, total);
+    else
+      p1p_run<Tin, -1, true>(smem_raw, &tm_img8, &tm_imgS, &tm_dst4, p, sl, qi, total);
+  }
+}
+
+}  // namespace v2
+}  // namespace fht

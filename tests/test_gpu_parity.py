@@ -896,3 +896,42 @@ def _nccl_shard_worker(rank, world, port, q):
         torch.equal(sb.view, s.view[:, :, rank * rows:(rank + 1) * rows])
     q.put((rank, bool(ok)))
     dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("shape,dt,batch", [((2048, 2048), "f32", 2), ((2048, 2048), "i32", 1), ((4096, 4096), "f32", 1),
+                                            ((1500, 1504), "f32", 3), ((2048, 1056), "i32", 2), ((1100, 2080), "f32", 1),
+                                            ((3000, 2016), "f32", 1)],
+                         ids=lambda v: str(v))
+def test_persistent_pass1(fht, O, monkeypatch, shape, dt, batch):
+    """The persistent pass 1 (k_p1p: 64-row strips of 4-byte images, prefetched loads, warp-owned half-slot
+    stores) against k_p1 on the same call: both outputs bit-identical, over square / non-square / non-power-of-two
+    frames, batches and the chunked schedule; and sampled cells of image 0 against the direct pattern sums."""
+    from synth import random_image
+    h_, w_ = shape
+    imgs = np.stack([random_image(shape, dt, seed=6100 + 7 * b + h_) for b in range(batch)])
+    if dt == "i32":  # signed, large
+        imgs = (imgs.astype(np.int64) * 4001 - 500000).astype(np.int32)
+    t = dev(imgs)
+    monkeypatch.setenv("FHT_P1_PERSIST", "0")
+    h0, s0 = fht.full(t, pair=True)
+    torch.cuda.synchronize()
+    a0, b0 = h0.view.cpu().numpy(), s0.view.cpu().numpy()
+    del h0, s0
+    monkeypatch.setenv("FHT_P1_PERSIST", "1")
+    h1, s1 = fht.full(t, pair=True)
+    torch.cuda.synchronize()
+    a1, b1 = h1.view.cpu().numpy(), s1.view.cpu().numpy()
+    assert np.array_equal(a0.view(np.int32), a1.view(np.int32))
+    assert np.array_equal(b0.view(np.int32), b1.view(np.int32))
+    if batch > 1:  # several chunks (two scratch buffers)
+        monkeypatch.setenv("FHT_SCRATCH_BUDGET_MB", "80")
+        h2 = fht.full(t)
+        torch.cuda.synchronize()
+        assert np.array_equal(h2.view.cpu().numpy().view(np.int32), a1.view(np.int32))
+    rng = np.random.default_rng(h_ * 3 + w_)
+    for q in range(4):
+        fr = O.quadrant_frame(imgs[0], q, square_to=O.full_padding(h_, w_))
+        cells = _sample_cells(fr.Hp, fr.W, 48, rng)
+        want = O.hough_cells_direct(fr, cells)
+        vals = np.array([a1[0, q, a, c] for a, c in cells], dtype=a1.dtype)
+        check(vals, want, dt != "f32")
