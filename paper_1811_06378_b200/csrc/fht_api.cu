@@ -377,7 +377,9 @@ struct P1Maps {
   CUtensorMap imgT;  // u8 transposed tiles (v2::P1Params::tfill_tma), else a copy of img0 (unused)
   CUtensorMap img8, imgS, dst4;  // persistent pass 1 (k_p1p): image box {32, 10, 8, 1}, swizzled image box
                                  // {32, 144, 1} (transposed slots), scratch box {TX, 1, 4, 1}
-  int persist = 0;         // launch k_p1p instead of k_p1 (make_p1p_maps)
+  int persist = 0;         // launch k_p1p instead of k_p1
+  void* scr = nullptr;     // k_p1p: the scratch buffer [z][j][strip][pitch] and its row pitch (elements)
+  int64_t scr_pitch = 0;
 };
 
 // Pass-1 destination view [z][j][strip][column] of a scratch buffer (dims column, strip, j, z; S strips,
@@ -424,7 +426,8 @@ cudaError_t launch_p1p_t(dim3 grid, const P1Maps& m, const v2::P1Params& a, cuda
   G -= G % a.nq;
   if (G < a.nq) G = a.nq;
   if (G > total) G = total;
-  return launch_pdl(v2::k_p1p<Tin>, dim3((unsigned)G), dim3(256), smem, st, m.img8, m.imgS, m.dst4, a, (int)total);
+  return launch_pdl(v2::k_p1p<Tin>, dim3((unsigned)G), dim3(256), smem, st, m.img8, m.imgS, m.dst4, a, (int)total, m.scr,
+                    m.scr_pitch);
 }
 template <typename Tin>
 cudaError_t launch_p1(int r, dim3 grid, const P1Maps& m, const v2::P1Params& a, cudaStream_t st) {
@@ -818,6 +821,8 @@ int run_orientation(const fht_image* img, const Frame& f, const Slot* slots, int
                         v2::kP1pHalf))
         return FHT_ERR_CUDA;
       m1.persist = 1;
+      m1.scr = ws;
+      m1.scr_pitch = sp.pitch;
     }
     // scratch as pass 2 reads it: columns [0, span1) = what pass 1 wrote; TMA zero-fills the rest
     if (!make_scr_maps(&m2.scr0, &m2.scr1, ws, f32, ses == 2, (uint64_t)span1, scr_rows, (uint64_t)sp.pitch))

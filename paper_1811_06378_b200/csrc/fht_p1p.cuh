@@ -20,6 +20,13 @@
 #pragma once
 #include "fht_tile.cuh"
 
+#ifndef FHT_P1P_HALF0_STG
+#define FHT_P1P_HALF0_STG 1  // first half of a warp's rows: read back from its slot and stored with 16-byte st.global
+#endif                       // (no bulk-read wait before the second half is staged); second half: bulk store
+#ifndef FHT_P1P_LOAD_AFTER_STORE0
+#define FHT_P1P_LOAD_AFTER_STORE0 0  // measured: C5 pass 1 343 us (0) vs 354 us (1)
+#endif
+
 namespace fht {
 namespace v2 {
 
@@ -40,7 +47,7 @@ struct P1pTile {
 template <typename Tin, int SIG, bool TR>
 __device__ __forceinline__ void p1p_run(unsigned char* smem, const CUtensorMap* tm_img8, const CUtensorMap* tm_imgS,
                                         const CUtensorMap* tm_dst4, const P1Params& p, const P1Slot& sl, int qi,
-                                        int total) {
+                                        int total, void* scr, int64_t scr_pitch) {
   using A = typename AccOf<Tin>::type;
   static_assert(sizeof(Tin) == 4 && sizeof(A) == 4, "4-byte images");
   constexpr int R = 6, NA = 1 << Split<R>::a, NR = 1 << R;
@@ -168,14 +175,18 @@ __device__ __forceinline__ void p1p_run(unsigned char* smem, const CUtensorMap* 
         __syncthreads();
       }
       par ^= 1u;
+#if !FHT_P1P_LOAD_AFTER_STORE0
       if (more) issue(nxt);
+#endif
       // ---- the warp's 8 rows tau = warp * 8 + u, in two halves through its slot
       const int Xs = cur.X - sl.xlo, zscr = p.z0 + cur.img_l * p.nq + qi;
       FHT_CHECK(Xs >= 0 && Xs + p.TX <= sl.xhi - sl.xlo && p.TX == TX1);
 #pragma unroll
       for (int half = 0; half < 2; ++half) {
-        if (lane == 0) tma_wait_read();  // the slot's previous bulk store has read it
-        __syncwarp();
+        if (half == 0 || !FHT_P1P_HALF0_STG) {
+          if (lane == 0) tma_wait_read();  // the slot's previous bulk store has read it
+          __syncwarp();
+        }
         if (lane < 31) {
           const int lo = SIG > 0 ? lane * VB : (WC - VB) - lane * VB;
 #pragma unroll
@@ -185,6 +196,31 @@ __device__ __forceinline__ void p1p_run(unsigned char* smem, const CUtensorMap* 
             for (int q = 0; q < VB - 1; ++q) d[q] = w[0][half * kP1pHalf + u][SIG > 0 ? q : VB - 1 - q];
             if (lo + VB - 1 < TX1) d[VB - 1] = w[0][half * kP1pHalf + u][SIG > 0 ? VB - 1 : 0];
           }
+        }
+        if (FHT_P1P_HALF0_STG && half == 0) {
+          // rows j = warp * 8 + u of F_m[strip] at scratch row (z * 64 + j) * strips + strip, columns [Xs, Xs + TX):
+          // 54 aligned 16-byte groups per row, read back from the slot (conflict-free) and stored coalesced
+          __syncwarp();
+          const int64_t srow = ((int64_t)zscr * NR + warp * 8) << p.L;
+#pragma unroll
+          for (int u0 = 0; u0 < kP1pHalf; u0 += 2) {  // two rows in flight (16 registers)
+            uint4 g[2][2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              const uint4* sv = reinterpret_cast<const uint4*>(stg + (u0 + u) * TX1);
+              g[u][0] = sv[lane];
+              if (lane < TX1 / 4 - 32) g[u][1] = sv[lane + 32];
+            }
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              uint4* gv = reinterpret_cast<uint4*>(static_cast<A*>(scr) +
+                                                   (srow + ((int64_t)(u0 + u) << p.L) + cur.strip) * scr_pitch + Xs);
+              gv[lane] = g[u][0];
+              if (lane < TX1 / 4 - 32) gv[lane + 32] = g[u][1];
+            }
+          }
+          __syncwarp();  // every lane has read the slot before the second half is staged
+          continue;
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
@@ -196,6 +232,11 @@ __device__ __forceinline__ void p1p_run(unsigned char* smem, const CUtensorMap* 
 #endif
           tma_commit();
         }
+#if FHT_P1P_LOAD_AFTER_STORE0
+        // A/B: the next tile's loads behind the first half's store (so that store's shared-memory read, which the
+        // second half waits for, is not queued behind 80 KB of loads): slower, the loads' head start matters more
+        if (half == 0 && more) issue(nxt);
+#endif
       }
       if (!more) break;
       T = Tn;
@@ -209,21 +250,22 @@ __device__ __forceinline__ void p1p_run(unsigned char* smem, const CUtensorMap* 
 template <typename Tin>
 __global__ void __launch_bounds__(256, 2)
 k_p1p(const __grid_constant__ CUtensorMap tm_img8, const __grid_constant__ CUtensorMap tm_imgS,
-      const __grid_constant__ CUtensorMap tm_dst4, const __grid_constant__ P1Params p, int total) {
+      const __grid_constant__ CUtensorMap tm_dst4, const __grid_constant__ P1Params p, int total, void* scr,
+      int64_t scr_pitch) {
   pdl_wait();  // the image may come from the previous kernel; the scratch may still be read by it
-  extern __shared__ __align__(1024) unsigned char smem_raw[];  // swizzled boxes: 1024-byte aligned
+  extern __shared__ __align__(1024) unsigned char smem_p1p[];  // swizzled boxes: 1024-byte aligned
   const int qi = blockIdx.x & ((1 << p.nq_log) - 1);  // gridDim.x % nq == 0: every tile of this CTA is slot qi's
   const P1Slot& sl = p.slot[qi];
   if (!sl.transposed) {
     if (sl.sigma > 0)
-      p1p_run<Tin, 1, false>(smem_raw, &tm_img8, &tm_imgS, &tm_dst4, p, sl, qi, total);
+      p1p_run<Tin, 1, false>(smem_p1p, &tm_img8, &tm_imgS, &tm_dst4, p, sl, qi, total, scr, scr_pitch);
     else
-      p1p_run<Tin, -1, false>(smem_raw, &tm_img8, &tm_imgS, &tm_dst4, p, sl, qi, total);
+      p1p_run<Tin, -1, false>(smem_p1p, &tm_img8, &tm_imgS, &tm_dst4, p, sl, qi, total, scr, scr_pitch);
   } else {
     if (sl.sigma > 0)
-      p1p_run<Tin, 1, true>(smem_raw, &tm_img8, &tm_imgS, &tm_dst4, p, sl, qi, total);
+      p1p_run<Tin, 1, true>(smem_p1p, &tm_img8, &tm_imgS, &tm_dst4, p, sl, qi, total, scr, scr_pitch);
     else
-      p1p_run<Tin, -1, true>(smem_raw, &tm_img8, &tm_imgS, &tm_dst4, p, sl, qi, total);
+      p1p_run<Tin, -1, true>(smem_p1p, &tm_img8, &tm_imgS, &tm_dst4, p, sl, qi, total, scr, scr_pitch);
   }
 }
 
