@@ -4,7 +4,8 @@
 // its drain are one dependent chain, and with two 8-warp CTAs per SM (the 80 KB plane of a 64-row tile) an SM often
 // holds a single computing CTA. Here a CTA walks tiles T = blockIdx.x, + gridDim.x, ... (two CTAs per SM; gridDim.x
 // is a multiple of the slot count, so a CTA stays on one quadrant slot: one sign, one fill path) and
-//   * issues the NEXT tile's loads as soon as sub-pass B has read the plane (the barrier that ends tile_fht_ld):
+//   * issues the NEXT tile's loads as soon as every warp holds its sub-pass-B inputs in registers (a CTA barrier
+//     after sub-pass B's shared-memory reads, BEFORE its butterflies):
 //     non-transposed slots one TMA box {32, 10, 8 rows} per warp (its own sub-pass-A block, its own mbarrier, phase
 //     parity alternating per tile); transposed slots (FHT row = image column) four TMA boxes {32 image columns, 144
 //     image rows} with the 128-byte swizzle: the block lands UNtransposed, and sub-pass A reads a lane's column e of
@@ -16,12 +17,12 @@
 //   * stages the results outside the plane: every warp owns the 8 rows of its sub-pass-B group and writes them in
 //     two halves through its own [4][TX] slot (3456 B), one bulk store {TX, 1, 4, 1} per half, waiting only for its
 //     own previous bulk read. No CTA barrier after sub-pass B's, no drain before the next tile.
-// The arithmetic is tile_fht_ld's (the same butterflies in the same order as k_p1): results are bit-identical.
+// The arithmetic is tile_fht_ld's (warp_fht on the same operands in the same order as k_p1): bit-identical results.
 #pragma once
 #include "fht_tile.cuh"
 
 #ifndef FHT_P1P_HALF0_STG
-#define FHT_P1P_HALF0_STG 1  // first half of a warp's rows: read back from its slot and stored with 16-byte st.global
+#define FHT_P1P_HALF0_STG 0  // A/B (measured slower: C5 pass 1 381 vs 341 us): first half of a warp's rows: read back from its slot and stored with 16-byte st.global
 #endif                       // (no bulk-read wait before the second half is staged); second half: bulk store
 #ifndef FHT_P1P_LOAD_AFTER_STORE0
 #define FHT_P1P_LOAD_AFTER_STORE0 0  // measured: C5 pass 1 343 us (0) vs 354 us (1)
@@ -115,24 +116,23 @@ __device__ __forceinline__ void p1p_run(unsigned char* smem, const CUtensorMap* 
       const bool more = Tn < total;
       const int Xa = SIG > 0 ? cur.X : cur.X - (WA - WC);
       A w[1][1 << Split<R>::b][VB];
-      if constexpr (!TR) {
-        const int rowoff = Xa & 31;
-        auto load = [&](int blk, A (&v)[NA][VA]) {
-          mbar_wait(bar, par);  // blk == warp: this warp's own rows
+      {
+        // ---- sub-pass A: block = warp, rows warp * 8 + r; v[r][q] = input (row, x-order index e), e = lane * 9 + q
+        // (SIG = +1) or 287 - lane * 9 - q (SIG = -1): the local frame of tile_fht_ld
+        A v[NA][VA];
+        mbar_wait(bar, par);
+        if constexpr (!TR) {
+          const int rowoff = Xa & 31;
 #pragma unroll
           for (int r = 0; r < NA; ++r) {
-            const A* q0 = plane + (blk * NA + r) * PITCH + rowoff + (SIG > 0 ? lane * VA : (WA - 1) - lane * VA);
+            const A* q0 = plane + (warp * NA + r) * PITCH + rowoff + (SIG > 0 ? lane * VA : (WA - 1) - lane * VA);
 #pragma unroll
             for (int q = 0; q < VA; ++q) v[r][q] = q0[SIG > 0 ? q : -q];
           }
-        };
-        tile_fht_ld<R, SIG, A>(GrpAll{}, load, plane, PITCH, w);
-      } else {
-        // sub-pass A from the untransposed, swizzled block: FHT rows warp * 8 + r = image columns = chunks
-        // ch, ch + 1 of box column hb; FHT column e = image row e
-        A v[NA][VA];
-        mbar_wait(bar, par);
-        {
+          // in place: the warp has read all rows of its block (its own TMA box) before it overwrites them
+        } else {
+          // from the untransposed, swizzled block: FHT rows warp * 8 + r = image columns = chunks ch, ch + 1 of box
+          // column hb; FHT column e = image row e
           const uint32_t base = smem_u32(smem) + (uint32_t)(warp >> 2) * 2u * kP1pBoxBytes;
           const uint32_t ch = (2u * (uint32_t)warp) & 7u;
 #pragma unroll
@@ -153,31 +153,29 @@ __device__ __forceinline__ void p1p_run(unsigned char* smem, const CUtensorMap* 
                 v[r][q] = static_cast<A>(x[r]);
             }
           }
+          __syncthreads();  // every warp has read the block: sub-pass A's rows overwrite it
         }
-        __syncthreads();  // every warp has read the block: sub-pass A's rows overwrite it
         warp_fht<Split<R>::a, VA>(v);
-        {
-          A* d = plane + (warp * NA) * PITCH + lane * VA;
+        A* d = plane + (warp * NA) * PITCH + lane * VA;
 #pragma unroll
-          for (int r = 0; r < NA; ++r)
+        for (int r = 0; r < NA; ++r)
 #pragma unroll
-            for (int q = 0; q < VA; ++q) d[r * PITCH + q] = v[r][q];
-        }
-        __syncthreads();
-        // sub-pass B (as tile_fht_ld): group jp = warp reads row jp of every block at column c + jp * i
-#pragma unroll
-        for (int i = 0; i < NA; ++i) {
-          const A* sp = plane + (i * NA + warp) * PITCH + lane * VB + warp * i;
-#pragma unroll
-          for (int q = 0; q < VB; ++q) w[0][i][q] = sp[q];
-        }
-        warp_fht<Split<R>::b, VB>(w[0]);
-        __syncthreads();
+          for (int q = 0; q < VA; ++q) d[r * PITCH + q] = v[r][q];
       }
+      __syncthreads();
+      // ---- sub-pass B (as tile_fht_ld): group jp = warp reads row jp of every block at column c + jp * i
+#pragma unroll
+      for (int i = 0; i < NA; ++i) {
+        const A* sp = plane + (i * NA + warp) * PITCH + lane * VB + warp * i;
+#pragma unroll
+        for (int q = 0; q < VB; ++q) w[0][i][q] = sp[q];
+      }
+      __syncthreads();  // every warp holds its sub-pass-B inputs in registers: the plane is free
       par ^= 1u;
 #if !FHT_P1P_LOAD_AFTER_STORE0
-      if (more) issue(nxt);
+      if (more) issue(nxt);  // the next tile's loads fly during the sub-pass-B butterflies and the stores
 #endif
+      warp_fht<Split<R>::b, VB>(w[0]);
       // ---- the warp's 8 rows tau = warp * 8 + u, in two halves through its slot
       const int Xs = cur.X - sl.xlo, zscr = p.z0 + cur.img_l * p.nq + qi;
       FHT_CHECK(Xs >= 0 && Xs + p.TX <= sl.xhi - sl.xlo && p.TX == TX1);
