@@ -170,6 +170,10 @@ __device__ __forceinline__ void p1p_run(unsigned char* smem, const CUtensorMap* 
 #pragma unroll
         for (int q = 0; q < VB; ++q) w[0][i][q] = sp[q];
       }
+      // The next tile's TMA loads overwrite the plane through the async proxy: each thread orders its (possibly still
+      // in-flight) shared-memory reads before them with a proxy fence, the barrier makes that cumulative. Without the
+      // fence the equality test failed about once in three runs (a bulk copy overtaking queued ld.shared).
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncthreads();  // every warp holds its sub-pass-B inputs in registers: the plane is free
       par ^= 1u;
 #if !FHT_P1P_LOAD_AFTER_STORE0

@@ -923,11 +923,21 @@ def test_persistent_pass1(fht, O, monkeypatch, shape, dt, batch):
     a1, b1 = h1.view.cpu().numpy(), s1.view.cpu().numpy()
     assert np.array_equal(a0.view(np.int32), a1.view(np.int32))
     assert np.array_equal(b0.view(np.int32), b1.view(np.int32))
+    for _ in range(3):  # repeated: a shared-memory reuse race in the tile loop showed up about once in three runs
+        hr = fht.full(t, out=h1)
+        torch.cuda.synchronize()
+        assert np.array_equal(hr.view.cpu().numpy().view(np.int32), a1.view(np.int32))
     if batch > 1:  # several chunks (two scratch buffers)
         monkeypatch.setenv("FHT_SCRATCH_BUDGET_MB", "80")
         h2 = fht.full(t)
         torch.cuda.synchronize()
         assert np.array_equal(h2.view.cpu().numpy().view(np.int32), a1.view(np.int32))
+        # the chunks pipelined over an auxiliary stream (pass 1 of chunk k + 1 beside pass 2 of chunk k)
+        h3, s3 = fht.full(t, pair=True, aux_stream=torch.cuda.Stream())
+        torch.cuda.synchronize()
+        assert h3.launches >= 4
+        assert np.array_equal(h3.view.cpu().numpy().view(np.int32), a1.view(np.int32))
+        assert np.array_equal(s3.view.cpu().numpy().view(np.int32), b1.view(np.int32))
     rng = np.random.default_rng(h_ * 3 + w_)
     for q in range(4):
         fr = O.quadrant_frame(imgs[0], q, square_to=O.full_padding(h_, w_))

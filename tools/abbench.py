@@ -23,7 +23,7 @@ c = synth.CONFIGS[cid]
 imgs = synth.batch(cid)
 t = torch.from_numpy(imgs).cuda()
 outs = {}
-aux = torch.cuda.Stream() if os.environ.get("AB_AUX") == "1" else None
+aux = (torch.cuda.Stream(priority=int(os.environ.get("AB_AUX_PRIO", "0"))) if os.environ.get("AB_AUX") == "1" else None)
 plan = fht.angle_plan(c["h"], c["w"], c["theta_min"], c["theta_max"]) if c["mode"] == "range" else None
 def step(ev=None):
     if c["mode"] == "full":
