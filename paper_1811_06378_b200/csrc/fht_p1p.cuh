@@ -126,6 +126,8 @@ __device__ __forceinline__ void p1p_run(unsigned char* smem, const CUtensorMap* 
 #pragma unroll
           for (int r = 0; r < NA; ++r) {
             const A* q0 = plane + (warp * NA + r) * PITCH + rowoff + (SIG > 0 ? lane * VA : (WA - 1) - lane * VA);
+            FHT_CHECK((SIG > 0 ? q0 : q0 - (VA - 1)) >= plane + (warp * NA + r) * PITCH &&
+                      (SIG > 0 ? q0 + VA : q0 + 1) <= plane + (warp * NA + r + 1) * PITCH);
 #pragma unroll
             for (int q = 0; q < VA; ++q) v[r][q] = q0[SIG > 0 ? q : -q];
           }
@@ -140,6 +142,8 @@ __device__ __forceinline__ void p1p_run(unsigned char* smem, const CUtensorMap* 
             const int e = SIG > 0 ? lane * VA + q : (WA - 1) - lane * VA - q;
             const int rb = e >= kP1pBoxRows ? 1 : 0, er = e - rb * kP1pBoxRows;
             const uint32_t a0 = base + (uint32_t)rb * kP1pBoxBytes + (uint32_t)er * 128u + ((ch ^ ((uint32_t)er & 7u)) << 4);
+            FHT_CHECK(e >= 0 && e < WA && (a0 & 15u) == 0 && a0 >= smem_u32(smem) &&
+                      (a0 | 16u) + 16u <= smem_u32(smem) + 4u * kP1pBoxBytes);
             uint32_t x[8];
             asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
                          : "=r"(x[0]), "=r"(x[1]), "=r"(x[2]), "=r"(x[3]) : "r"(a0) : "memory");
@@ -157,6 +161,7 @@ __device__ __forceinline__ void p1p_run(unsigned char* smem, const CUtensorMap* 
         }
         warp_fht<Split<R>::a, VA>(v);
         A* d = plane + (warp * NA) * PITCH + lane * VA;
+        FHT_CHECK(d + (NA - 1) * PITCH + VA <= plane + NR * PITCH && lane * VA + VA <= PITCH);
 #pragma unroll
         for (int r = 0; r < NA; ++r)
 #pragma unroll
@@ -167,6 +172,7 @@ __device__ __forceinline__ void p1p_run(unsigned char* smem, const CUtensorMap* 
 #pragma unroll
       for (int i = 0; i < NA; ++i) {
         const A* sp = plane + (i * NA + warp) * PITCH + lane * VB + warp * i;
+        FHT_CHECK(lane * VB + warp * i + VB <= WA && sp + VB <= plane + NR * PITCH);
 #pragma unroll
         for (int q = 0; q < VB; ++q) w[0][i][q] = sp[q];
       }
@@ -182,7 +188,8 @@ __device__ __forceinline__ void p1p_run(unsigned char* smem, const CUtensorMap* 
       warp_fht<Split<R>::b, VB>(w[0]);
       // ---- the warp's 8 rows tau = warp * 8 + u, in two halves through its slot
       const int Xs = cur.X - sl.xlo, zscr = p.z0 + cur.img_l * p.nq + qi;
-      FHT_CHECK(Xs >= 0 && Xs + p.TX <= sl.xhi - sl.xlo && p.TX == TX1);
+      FHT_CHECK(Xs >= 0 && Xs + p.TX <= sl.xhi - sl.xlo && p.TX == TX1 && (Xs & 3) == 0 && zscr >= 0 &&
+                cur.strip >= 0 && cur.strip < (1 << p.L));
 #pragma unroll
       for (int half = 0; half < 2; ++half) {
         if (half == 0 || !FHT_P1P_HALF0_STG) {
@@ -194,6 +201,10 @@ __device__ __forceinline__ void p1p_run(unsigned char* smem, const CUtensorMap* 
 #pragma unroll
           for (int u = 0; u < kP1pHalf; ++u) {
             A* d = stg + u * TX1 + lo;
+            // (pointer ranges, not smem_in_bounds: its %total_smem_size bound does not count the 1 KB the system
+            // reserves below the dynamic window, and the slots reach the window's last kilobyte)
+            FHT_CHECK(lo >= 0 && lo + VB - 1 <= TX1 && d >= stg && d + VB - 1 <= stg + kP1pHalf * TX1 &&
+                      reinterpret_cast<unsigned char*>(stg + kP1pHalf * TX1) <= smem + main_buf_bytes(R) + kP1pStageBytes);
 #pragma unroll
             for (int q = 0; q < VB - 1; ++q) d[q] = w[0][half * kP1pHalf + u][SIG > 0 ? q : VB - 1 - q];
             if (lo + VB - 1 < TX1) d[VB - 1] = w[0][half * kP1pHalf + u][SIG > 0 ? VB - 1 : 0];
