@@ -1771,7 +1771,15 @@ int fht_angle_range_plan(const fht_image* img, const fht_angle_plan_t* plan, fht
                      (int)((std::max<int64_t>(plan->h, plan->w_content) + kThreads - 1) / kThreads);
   LaunchLog log{opts, 0};
   log.before((cudaStream_t)stream);
-  k_range_tables<<<nb_tab, kThreads, (size_t)plan->h * sizeof(int), (cudaStream_t)stream>>>(ta);
+  if (env_int("FHT_RANGE_TABLES_REC", 1) != 0) {  // supports by the (min, max) block recursion in one block
+    const size_t smem = 4 * (size_t)f.Hp * sizeof(int);
+    static std::atomic<unsigned long long> done{0};
+    if (smem_optin(k_range_tables_rec, 4 * (size_t)4096 * sizeof(int), done) != cudaSuccess) return FHT_ERR_CUDA;
+    const int nb = 1 + (int)((std::max<int64_t>(plan->h, plan->w_content) + kRangeRecThreads - 1) / kRangeRecThreads);
+    k_range_tables_rec<<<nb, kRangeRecThreads, smem, (cudaStream_t)stream>>>(ta);
+  } else {
+    k_range_tables<<<nb_tab, kThreads, (size_t)plan->h * sizeof(int), (cudaStream_t)stream>>>(ta);
+  }
   if (cudaGetLastError() != cudaSuccess) return FHT_ERR_CUDA;
   log.after((cudaStream_t)stream);
   Slot sl{};

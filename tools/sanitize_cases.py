@@ -1,5 +1,5 @@
 """Small invocations of every kernel for compute-sanitizer: k_p1 / k_p2 (all four slots,
-u8 / i32 / f32, the R = 6 tiles, the range loaders), k_fhtshift, k_fold, k_range_tables, the peaks
+u8 / i32 / f32, the R = 6 tiles, the persistent pass 1 k_p1p, the range loaders), k_fhtshift, k_fold, k_range_tables, the peaks
 kernels and the v1 kernels of degenerate frames. Exits 0 when every call ran (results are checked by
 the GPU test suite, not here).
 
@@ -37,6 +37,10 @@ def main():
     fht.quadrant(t, fht.QA, pair=True)
     u = torch.from_numpy(random_image((2048, 24), "u8", seed=4)).to(dev)
     fht.quadrant(u, fht.QB)
+    # persistent pass 1 (k_p1p): 64-row strips of a 4-byte image, all four slots (two transposed), two images
+    t = torch.from_numpy(np.stack([random_image((2048, 2048), "f32", seed=6 + b) for b in range(2)])).to(dev)
+    fht.full(t, pair=True)
+    n += 1
     # §4 range: scaled (TMA gather loader, alpha >= 1), alpha < 1 gather, pruned, horizontal
     t = torch.from_numpy(random_image((96, 80), "f32", seed=5)).to(dev)
     fht.angle_range(t, -15.0, 15.0, pair=True)
