@@ -389,9 +389,9 @@ def main():
         if n_launch - first == 1:
             names = ["k_pipe"]
         else:
-            # pass 1 of 64-row strips of 4-byte images (Hp >= 2048, full mode) is the persistent kernel k_p1p
+            # pass 1 of 64-row strips of 4-byte images (Hp >= 2048; full mode, or the §4 range loader) is the persistent kernel k_p1p
             hp = 1 << (max(cc["h"], 1) - 1).bit_length()
-            p1n = ("k_p1p" if cc["mode"] == "full" and cc["dtype"] in ("f32", "i32") and hp >= 2048 and cc["w"] % 32 == 0
+            p1n = ("k_p1p" if cc["mode"] in ("full", "range") and cc["dtype"] in ("f32", "i32") and hp >= 2048 and cc["w"] % 32 == 0
                    and os.environ.get("FHT_P1_PERSIST", "1") != "0" else "k_p1")
             names = (["k_range_tables"] if first else []) + [p1n, "k_p2"] * ((n_launch - first) // 2)
         p2 = [k for k in range(n_launch) if names[k] == "k_p2"]

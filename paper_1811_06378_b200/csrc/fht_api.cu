@@ -412,9 +412,9 @@ cudaError_t launch_p1_t(dim3 grid, const P1Maps& m, const v2::P1Params& a, cudaS
 // walk the tiles of `grid` (the k_p1 grid of the same launch), gridDim.x a multiple of the slot count.
 template <typename Tin>
 cudaError_t launch_p1p_t(dim3 grid, const P1Maps& m, const v2::P1Params& a, cudaStream_t st) {
-  const size_t smem = v2::p1p_smem_bytes();
+  const size_t smem = v2::p1p_smem_bytes(a.range != 0);
   static std::atomic<unsigned long long> done{0};
-  cudaError_t e = smem_optin(v2::k_p1p<Tin>, smem, done);
+  cudaError_t e = smem_optin(v2::k_p1p<Tin>, v2::p1p_smem_bytes(true), done);
   if (e != cudaSuccess) return e;
   int dev = 0, nsm = 0;
   if ((e = cudaGetDevice(&dev)) != cudaSuccess ||
@@ -818,6 +818,17 @@ int run_orientation(const fht_image* img, const Frame& f, const Slot* slots, int
         (int64_t)ntile1 * nq * nstrips * sp.chunk < (1ll << 30) && env_int("FHT_P1_PERSIST", 1) != 0) {
       if (!make_image_map32(&m1.img8, img, 8) || !make_image_map_swz(&m1.imgS, img) ||
           !make_dst_map(&m1.dst4, ws, ses, f32, sp.pitch, nstrips, 1 << f.m, (int64_t)(scr_rows / f.Hp), p1.TX,
+                        v2::kP1pHalf))
+        return FHT_ERR_CUDA;
+      m1.persist = 1;
+      m1.scr = ws;
+      m1.scr_pitch = sp.pitch;
+    } else if (f.m == 6 && es == 4 && rg && nq == 1 && p1.fill_tma && !p1.fill32 && p1.TX == v2::TX1 && !pipe &&
+               env_int("FHT_P1_PERSIST", 1) != 0 && env_int("FHT_P1_PERSIST_RANGE", 1) != 0) {
+      // the §4 range loader in the persistent kernel: the 256- and 36-column row maps stand in for img8 / imgS
+      m1.img8 = m1.img0;
+      m1.imgS = m1.img1;
+      if (!make_dst_map(&m1.dst4, ws, ses, f32, sp.pitch, nstrips, 1 << f.m, (int64_t)(scr_rows / f.Hp), p1.TX,
                         v2::kP1pHalf))
         return FHT_ERR_CUDA;
       m1.persist = 1;

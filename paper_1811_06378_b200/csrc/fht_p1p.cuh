@@ -33,7 +33,11 @@ namespace v2 {
 
 constexpr int kP1pHalf = 4;                                                  // rows per staged half
 constexpr size_t kP1pStageBytes = (size_t)8 * kP1pHalf * TX1 * 4;            // 8 warps x [4][216] x 4 B = 27648
-__host__ __device__ constexpr size_t p1p_smem_bytes() { return main_buf_bytes(6) + kP1pStageBytes + 128; }
+// tail: 128 B (mbarriers), then the §4 range loader's tables: rowoff[64], erow[64], {cm_lo, cm_n}, colmap slice [512]
+constexpr size_t kP1pRangeBytes = 64 * 4 + 64 * 4 + 64 + kColmapStageBytes;
+__host__ __device__ constexpr size_t p1p_smem_bytes(bool range = false) {
+  return main_buf_bytes(6) + kP1pStageBytes + 128 + (range ? kP1pRangeBytes : 0);
+}
 
 constexpr int kP1pBoxRows = 144;                                 // transposed slots: image rows per TMA box
 constexpr uint32_t kP1pBoxBytes = kP1pBoxRows * 128;             // {32 columns, 144 rows} x 4 B = 18432 (18 x 1024)
@@ -45,7 +49,10 @@ struct P1pTile {
 // One CTA's tiles of slot `sl` (sign SIG, transposed TR). tm_img8: the image view [img][row][col/32][32] with box
 // {32, 10, 8, 1}; tm_imgS: the image [img][row][col] with box {32, 144, 1} and the 128-byte swizzle; tm_dst4: the
 // scratch view [z][j][strip][column] with box {TX, 1, 4, 1}.
-template <typename Tin, int SIG, bool TR>
+// RG: the §4 range loader (sigma = +1, not transposed): rows by TMA from the aligned-down column of
+// colmap[max(0, Xa - e_y)] (tm_img8 / tm_imgS are then the 3-D image maps with boxes of 256 and 36 columns), the
+// transform T(x', y) = I[y][colmap[x' - e_y]] gathered from shared memory in sub-pass A, as in p1_body.
+template <typename Tin, int SIG, bool TR, bool RG = false>
 __device__ __forceinline__ void p1p_run(unsigned char* smem, const CUtensorMap* tm_img8, const CUtensorMap* tm_imgS,
                                         const CUtensorMap* tm_dst4, const P1Params& p, const P1Slot& sl, int qi,
                                         int total, void* scr, int64_t scr_pitch) {
@@ -77,16 +84,61 @@ __device__ __forceinline__ void p1p_run(unsigned char* smem, const CUtensorMap* 
     } while (T < total && !decode(T, t));
     return T;
   };
-  // loads of a tile into the plane (free: every warp is past sub-pass B's reads)
-  auto issue = [&](const P1pTile& t) {
+  // §4 range tables (shared memory tail)
+  int* rowoff = reinterpret_cast<int*>(smem + main_buf_bytes(R) + kP1pStageBytes + 128);  // [64] a0 or kNoRow
+  int* erow = rowoff + 64;                                                                 // [64] e_y
+  int* cmhdr = erow + 64;                                                                  // cm_lo, cm_n
+  int* cm_s = cmhdr + 16;                                                                  // colmap[cm_lo + i]
+  // loads of a tile into the plane (free: every warp is past sub-pass B's reads); RG: also the tile's tables, and
+  // the return value says whether any row of the tile has content (CTA-uniform; ends with a CTA barrier)
+  auto issue = [&](const P1pTile& t) -> bool {
     const int Xa = SIG > 0 ? t.X : t.X - (WA - WC);
     const int y0 = (p.strip0 + t.strip) * NR;
     const int img = p.img0 + t.img_l;
-    if constexpr (!TR) {
+    if constexpr (RG) {
+      const int rho = warp * NA + lane, y = y0 + rho;
+      int a0 = kNoRow, e = 0;
+      bool ne = false;
+      if (lane < NA) {
+        if (y < p.img_h) {
+          e = __ldg(p.e_tab + y);
+          const int u0 = Xa - e;
+          if (u0 < p.w_content && u0 + WA > 0) {
+            a0 = __ldg(p.colmap + max(0, u0)) & ~3;
+            ne = true;
+          }
+        }
+        rowoff[rho] = a0;
+        erow[rho] = e;
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, ne);
+      if (lane == 0) mbar_expect_tx(bar, (uint32_t)__popc(m) * (256 + 36) * 4);
+      __syncwarp();
+      if (ne) {
+        A* d = plane + rho * TMA_PITCH;
+        tma_load_3d(tm_img8, d, bar, a0, y, img);
+        tma_load_3d(tm_imgS, d + 256, bar, a0 + 256, y, img);
+      }
+      // the strip's colmap slice (e_y is monotonic in y: the u range comes from the first and last rows)
+      int ulo = 0, n = 0;
+      if (y0 < p.img_h) {
+        const int ea = __ldg(p.e_tab + y0), eb = __ldg(p.e_tab + min(y0 + NR - 1, p.img_h - 1));
+        ulo = max(0, Xa - max(ea, eb));
+        n = max(0, min(p.w_content, Xa + WA - min(ea, eb)) - ulo);
+      }
+      if (n <= kColmapStage)
+        for (int i = tid; i < n; i += 256) cm_s[i] = __ldg(p.colmap + ulo + i);
+      if (tid == 0) {
+        cmhdr[0] = ulo;
+        cmhdr[1] = n;
+      }
+      return __syncthreads_or(m != 0u) != 0;
+    } else if constexpr (!TR) {
       if (lane == 0) {
         mbar_expect_tx(bar, (uint32_t)NA * TMA_PITCH * 4);
         tma_load_4d(tm_img8, plane + warp * NA * TMA_PITCH, bar, 0, (Xa & ~31) >> 5, y0 + warp * NA, img);
       }
+      return true;
     } else {
       // image rows [Xa, Xa + 288) x image columns [y0, y0 + 64): box (hb, rb) = columns y0 + 32 hb.., rows Xa + 144 rb..
       if (tid == 0) {
@@ -95,6 +147,7 @@ __device__ __forceinline__ void p1p_run(unsigned char* smem, const CUtensorMap* 
         for (int k = 0; k < 4; ++k)
           tma_load_3d(tm_imgS, smem + k * kP1pBoxBytes, bar, y0 + 32 * (k >> 1), Xa + kP1pBoxRows * (k & 1), img);
       }
+      return true;
     }
   };
 
@@ -109,19 +162,37 @@ __device__ __forceinline__ void p1p_run(unsigned char* smem, const CUtensorMap* 
   P1pTile cur{}, nxt{};
   if (T < total && !decode(T, cur)) T = next(T, cur);
   if (T < total) {
-    issue(cur);
+    bool cur_any = issue(cur), nxt_any = false;
     uint32_t par = 0;
     while (true) {
       const int Tn = next(T, nxt);
       const bool more = Tn < total;
       const int Xa = SIG > 0 ? cur.X : cur.X - (WA - WC);
       A w[1][1 << Split<R>::b][VB];
-      {
+      mbar_wait(bar, par);  // (a range tile without content: its warps' empty phases complete at once)
+      if (cur_any) {
         // ---- sub-pass A: block = warp, rows warp * 8 + r; v[r][q] = input (row, x-order index e), e = lane * 9 + q
         // (SIG = +1) or 287 - lane * 9 - q (SIG = -1): the local frame of tile_fht_ld
         A v[NA][VA];
-        mbar_wait(bar, par);
-        if constexpr (!TR) {
+        if constexpr (RG) {
+          const int cm_lo = cmhdr[0], cm_n = cmhdr[1];
+#pragma unroll
+          for (int r = 0; r < NA; ++r) {
+            const int rho = warp * NA + r;
+            const int a0 = rowoff[rho], u0 = cur.X + lane * VA - erow[rho];
+#pragma unroll
+            for (int q = 0; q < VA; ++q) {
+              const int u = u0 + q;
+              A val = A(0);
+              if (a0 != kNoRow && (unsigned)u < (unsigned)p.w_content) {
+                const int c = cm_n <= kColmapStage ? cm_s[u - cm_lo] : __ldg(p.colmap + u);
+                FHT_CHECK(c - a0 >= 0 && c - a0 < 256 + 36 && (cm_n > kColmapStage || (u - cm_lo >= 0 && u - cm_lo < cm_n)));
+                val = plane[rho * PITCH + (c - a0)];
+              }
+              v[r][q] = val;
+            }
+          }
+        } else if constexpr (!TR) {
           const int rowoff = Xa & 31;
 #pragma unroll
           for (int r = 0; r < NA; ++r) {
@@ -166,15 +237,20 @@ __device__ __forceinline__ void p1p_run(unsigned char* smem, const CUtensorMap* 
         for (int r = 0; r < NA; ++r)
 #pragma unroll
           for (int q = 0; q < VA; ++q) d[r * PITCH + q] = v[r][q];
-      }
-      __syncthreads();
-      // ---- sub-pass B (as tile_fht_ld): group jp = warp reads row jp of every block at column c + jp * i
+        __syncthreads();
+        // ---- sub-pass B (as tile_fht_ld): group jp = warp reads row jp of every block at column c + jp * i
 #pragma unroll
-      for (int i = 0; i < NA; ++i) {
-        const A* sp = plane + (i * NA + warp) * PITCH + lane * VB + warp * i;
-        FHT_CHECK(lane * VB + warp * i + VB <= WA && sp + VB <= plane + NR * PITCH);
+        for (int i = 0; i < NA; ++i) {
+          const A* sp = plane + (i * NA + warp) * PITCH + lane * VB + warp * i;
+          FHT_CHECK(lane * VB + warp * i + VB <= WA && sp + VB <= plane + NR * PITCH);
 #pragma unroll
-        for (int q = 0; q < VB; ++q) w[0][i][q] = sp[q];
+          for (int q = 0; q < VB; ++q) w[0][i][q] = sp[q];
+        }
+      } else {  // (range) no row of the tile has content: F_m is 0 over the whole tile
+#pragma unroll
+        for (int i = 0; i < NA; ++i)
+#pragma unroll
+          for (int q = 0; q < VB; ++q) w[0][i][q] = A(0);
       }
       // The next tile's TMA loads overwrite the plane through the async proxy: each thread orders its (possibly still
       // in-flight) shared-memory reads before them with a proxy fence, the barrier makes that cumulative. Without the
@@ -183,9 +259,9 @@ __device__ __forceinline__ void p1p_run(unsigned char* smem, const CUtensorMap* 
       __syncthreads();  // every warp holds its sub-pass-B inputs in registers: the plane is free
       par ^= 1u;
 #if !FHT_P1P_LOAD_AFTER_STORE0
-      if (more) issue(nxt);  // the next tile's loads fly during the sub-pass-B butterflies and the stores
+      if (more) nxt_any = issue(nxt);  // the next tile's loads fly during the sub-pass-B butterflies and the stores
 #endif
-      warp_fht<Split<R>::b, VB>(w[0]);
+      if (cur_any) warp_fht<Split<R>::b, VB>(w[0]);
       // ---- the warp's 8 rows tau = warp * 8 + u, in two halves through its slot
       const int Xs = cur.X - sl.xlo, zscr = p.z0 + cur.img_l * p.nq + qi;
       FHT_CHECK(Xs >= 0 && Xs + p.TX <= sl.xhi - sl.xlo && p.TX == TX1 && (Xs & 3) == 0 && zscr >= 0 &&
@@ -248,12 +324,13 @@ __device__ __forceinline__ void p1p_run(unsigned char* smem, const CUtensorMap* 
 #if FHT_P1P_LOAD_AFTER_STORE0
         // A/B: the next tile's loads behind the first half's store (so that store's shared-memory read, which the
         // second half waits for, is not queued behind 80 KB of loads): slower, the loads' head start matters more
-        if (half == 0 && more) issue(nxt);
+        if (half == 0 && more) nxt_any = issue(nxt);
 #endif
       }
       if (!more) break;
       T = Tn;
       cur = nxt;
+      cur_any = nxt_any;
     }
   }
   pdl_trigger();
@@ -269,7 +346,9 @@ k_p1p(const __grid_constant__ CUtensorMap tm_img8, const __grid_constant__ CUten
   extern __shared__ __align__(1024) unsigned char smem_p1p[];  // swizzled boxes: 1024-byte aligned
   const int qi = blockIdx.x & ((1 << p.nq_log) - 1);  // gridDim.x % nq == 0: every tile of this CTA is slot qi's
   const P1Slot& sl = p.slot[qi];
-  if (!sl.transposed) {
+  if (p.range) {  // §4 range frame: sigma = +1, not transposed; tm_img8 / tm_imgS: the 256- and 36-column row maps
+    p1p_run<Tin, 1, false, true>(smem_p1p, &tm_img8, &tm_imgS, &tm_dst4, p, sl, qi, total, scr, scr_pitch);
+  } else if (!sl.transposed) {
     if (sl.sigma > 0)
       p1p_run<Tin, 1, false>(smem_p1p, &tm_img8, &tm_imgS, &tm_dst4, p, sl, qi, total, scr, scr_pitch);
     else

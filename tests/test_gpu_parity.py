@@ -945,3 +945,27 @@ def test_persistent_pass1(fht, O, monkeypatch, shape, dt, batch):
         want = O.hough_cells_direct(fr, cells)
         vals = np.array([a1[0, q, a, c] for a, c in cells], dtype=a1.dtype)
         check(vals, want, dt != "f32")
+
+
+@pytest.mark.parametrize("shape,dt,rng_deg,pruned", [((4096, 4096), "f32", (-15.0, 15.0), False),
+                                                     ((4096, 4096), "f32", (-15.0, 15.0), True),
+                                                     ((2048, 1200), "i32", (5.0, 30.0), False),
+                                                     ((1700, 2304), "f32", (-40.0, -10.0), False)], ids=lambda v: str(v))
+def test_persistent_pass1_range(fht, monkeypatch, shape, dt, rng_deg, pruned):
+    """The §4 range loader inside the persistent pass 1 (k_p1p, 64-row strips) against k_p1 on the same call:
+    the range Hough image and its fhtshift bit-identical (the oracle comparisons of these frames are
+    test_config4_* and test_range_*; this pins the two kernels to each other on more frames), repeated."""
+    from synth import random_image
+    img = random_image(shape, dt, seed=7300 + shape[0] + shape[1])
+    t = dev(img)
+    plan = fht.angle_plan(shape[0], shape[1], rng_deg[0], rng_deg[1], pruned=pruned)
+    monkeypatch.setenv("FHT_P1_PERSIST", "0")
+    h0, s0 = fht.angle_range(t, plan, pair=True)
+    torch.cuda.synchronize()
+    a0, b0 = h0.view.cpu().numpy(), s0.view.cpu().numpy()
+    monkeypatch.setenv("FHT_P1_PERSIST", "1")
+    for _ in range(3):
+        h1, s1 = fht.angle_range(t, plan, pair=True)
+        torch.cuda.synchronize()
+        assert np.array_equal(h1.view.cpu().numpy().view(np.int32), a0.view(np.int32))
+        assert np.array_equal(s1.view.cpu().numpy().view(np.int32), b0.view(np.int32))
