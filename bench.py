@@ -393,10 +393,13 @@ def main():
             hp = 1 << (max(cc["h"], 1) - 1).bit_length()
             p1n = ("k_p1p" if cc["mode"] in ("full", "range") and cc["dtype"] in ("f32", "i32") and hp >= 2048 and cc["w"] % 32 == 0
                    and os.environ.get("FHT_P1_PERSIST", "1") != "0" else "k_p1")
+            if (cc["dtype"] == "u8" and hp in (256, 512) and cc["w"] % 128 == 0 and cc["mode"] in ("full", "quadrant")
+                    and os.environ.get("FHT_P1_PERSIST", "1") != "0"):
+                p1n = "k_p1p8"  # 16-row strips of u8 images: the persistent u8 kernel
             names = (["k_range_tables"] if first else []) + [p1n, "k_p2"] * ((n_launch - first) // 2)
         p2 = [k for k in range(n_launch) if names[k] == "k_p2"]
         p2_ms = sum(kms[k] for k in p2)
-        p1_ms = sum(kms[k] for k in range(n_launch) if names[k] in ("k_p1", "k_p1p", "k_range_tables"))
+        p1_ms = sum(kms[k] for k in range(n_launch) if names[k] in ("k_p1", "k_p1p", "k_p1p8", "k_range_tables"))
         pipe_ms = sum(kms[k] for k in range(n_launch) if names[k] == "k_pipe")
         tot = sum(kms)
         # the dominant kernel: k_pipe (one read of the image + every output written, per launch) or

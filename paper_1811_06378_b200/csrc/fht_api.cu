@@ -22,6 +22,7 @@
 #include "fht_kernels.cuh"
 #include "fht_tile.cuh"
 #include "fht_p1p.cuh"
+#include "fht_p1p8.cuh"
 #include "fht_internal.cuh"
 #include "fht_peaks.cuh"
 
@@ -429,10 +430,31 @@ cudaError_t launch_p1p_t(dim3 grid, const P1Maps& m, const v2::P1Params& a, cuda
   return launch_pdl(v2::k_p1p<Tin>, dim3((unsigned)G), dim3(256), smem, st, m.img8, m.imgS, m.dst4, a, (int)total, m.scr,
                     m.scr_pitch);
 }
+// Persistent pass 1 for 16-row strips of u8 images (fht_p1p8.cuh): six 4-warp CTAs per SM.
+inline cudaError_t launch_p1p8(dim3 grid, const P1Maps& m, const v2::P1Params& a, cudaStream_t st) {
+  const size_t smem = v2::p1p8_smem_bytes();
+  static std::atomic<unsigned long long> done{0};
+  cudaError_t e = smem_optin(v2::k_p1p8, smem, done);
+  if (e != cudaSuccess) return e;
+  int dev = 0, nsm = 0;
+  if ((e = cudaGetDevice(&dev)) != cudaSuccess ||
+      (e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess)
+    return e;
+  const long long total = (long long)grid.x * grid.y * grid.z;
+  if (total <= 0 || total >= (1ll << 31) - 4096) return cudaErrorInvalidValue;
+  long long G = 6ll * nsm;
+  G -= G % a.nq;
+  if (G < a.nq) G = a.nq;
+  if (G > total) G = total;
+  return launch_pdl(v2::k_p1p8, dim3((unsigned)G), dim3(128), smem, st, m.img8, m.imgT, m.dst4, a, (int)total);
+}
 template <typename Tin>
 cudaError_t launch_p1(int r, dim3 grid, const P1Maps& m, const v2::P1Params& a, cudaStream_t st) {
   if constexpr (sizeof(Tin) == 4) {
     if (m.persist && r == 6) return launch_p1p_t<Tin>(grid, m, a, st);
+  }
+  if constexpr (sizeof(Tin) == 1) {
+    if (m.persist && r == 4) return launch_p1p8(grid, m, a, st);
   }
   switch (r) {
     case 1: return launch_p1_t<Tin, 1>(grid, m, a, st);
@@ -501,6 +523,20 @@ bool make_image_map32(CUtensorMap* m, const fht_image* img, uint32_t box_rows = 
   return fn(m, dt, 4, const_cast<void*>(img->data), dims, strides, box, e, CU_TENSOR_MAP_INTERLEAVE_NONE,
             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
          CUDA_SUCCESS;
+}
+// Persistent u8 pass 1 (k_p1p8): the view [img][row][col/128][128] bytes, box {128, 4, 4 rows, 1}: one copy of 4
+// rows x 512 columns from a 128-byte aligned column (w % 128 == 0).
+bool make_image_map128(CUtensorMap* m, const fht_image* img) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[4] = {128, (cuuint64_t)(img->w / 128), (cuuint64_t)img->h, (cuuint64_t)img->batch};
+  cuuint64_t strides[3] = {128, (cuuint64_t)img->row_stride, (cuuint64_t)img->batch_stride};
+  if (img->batch == 1) strides[2] = (cuuint64_t)(img->h * img->row_stride);
+  cuuint32_t box[4] = {128, 4, 4, 1};
+  cuuint32_t e[4] = {1, 1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<void*>(img->data), dims, strides, box, e,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 // Persistent pass 1, transposed slots (k_p1p): the 4-byte image [img][row][col], box {32 columns, 144 rows, 1} with
 // the 128-byte swizzle (16-byte chunk ^ (row & 7)): the block lands untransposed and is read column-wise without
@@ -823,6 +859,14 @@ int run_orientation(const fht_image* img, const Frame& f, const Slot* slots, int
       m1.persist = 1;
       m1.scr = ws;
       m1.scr_pitch = sp.pitch;
+    } else if (f.m == 4 && es == 1 && ses == 2 && !rg && p1.fill_tma && p1.tfill_tma && img->w % 128 == 0 &&
+               p1.TX == v2::TX1 && ngroups == 16 && !pipe && env_int("FHT_P1_PERSIST", 1) != 0 &&
+               env_int("FHT_P1_PERSIST_U8", 1) != 0) {
+      // 16-row strips of u8 images (k_p1p8): img8 = the [row][col/128][128] view, imgT = the transposed-tile map
+      if (!make_image_map128(&m1.img8, img) ||
+          !make_dst_map(&m1.dst4, ws, ses, f32, sp.pitch, nstrips, 1 << f.m, (int64_t)(scr_rows / f.Hp), p1.TX, 4))
+        return FHT_ERR_CUDA;
+      m1.persist = 1;
     } else if (f.m == 6 && es == 4 && rg && nq == 1 && p1.fill_tma && !p1.fill32 && p1.TX == v2::TX1 && !pipe &&
                env_int("FHT_P1_PERSIST", 1) != 0 && env_int("FHT_P1_PERSIST_RANGE", 1) != 0) {
       // the §4 range loader in the persistent kernel: the 256- and 36-column row maps stand in for img8 / imgS

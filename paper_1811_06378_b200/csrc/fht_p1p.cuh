@@ -170,7 +170,8 @@ __device__ __forceinline__ void p1p_run(unsigned char* smem, const CUtensorMap* 
       const int Xa = SIG > 0 ? cur.X : cur.X - (WA - WC);
       A w[1][1 << Split<R>::b][VB];
       mbar_wait(bar, par);  // (a range tile without content: its warps' empty phases complete at once)
-      if (cur_any) {
+      const bool any = !RG || cur_any;  // (compile-time true outside the range loader)
+      if (any) {
         // ---- sub-pass A: block = warp, rows warp * 8 + r; v[r][q] = input (row, x-order index e), e = lane * 9 + q
         // (SIG = +1) or 287 - lane * 9 - q (SIG = -1): the local frame of tile_fht_ld
         A v[NA][VA];
@@ -261,7 +262,7 @@ __device__ __forceinline__ void p1p_run(unsigned char* smem, const CUtensorMap* 
 #if !FHT_P1P_LOAD_AFTER_STORE0
       if (more) nxt_any = issue(nxt);  // the next tile's loads fly during the sub-pass-B butterflies and the stores
 #endif
-      if (cur_any) warp_fht<Split<R>::b, VB>(w[0]);
+      if (any) warp_fht<Split<R>::b, VB>(w[0]);
       // ---- the warp's 8 rows tau = warp * 8 + u, in two halves through its slot
       const int Xs = cur.X - sl.xlo, zscr = p.z0 + cur.img_l * p.nq + qi;
       FHT_CHECK(Xs >= 0 && Xs + p.TX <= sl.xhi - sl.xlo && p.TX == TX1 && (Xs & 3) == 0 && zscr >= 0 &&

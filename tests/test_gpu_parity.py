@@ -898,6 +898,15 @@ def _nccl_shard_worker(rank, world, port, q):
     dist.destroy_process_group()
 
 
+def _same_planes(x, y, shape):
+    """Bitwise equality of two QUADS views [B][4][rows][W] on the rows each quadrant holds (QA/QB: Hp, QC/QD: Wp; for
+    non-square frames the planes' remaining rows are never written)."""
+    from oracle import fht_oracle as _O
+    Hp, Wp = _O.full_padding(*shape)
+    return all(np.array_equal(x[:, q, :n].view(np.int32), y[:, q, :n].view(np.int32))
+               for q, n in ((0, Hp), (1, Hp), (2, Wp), (3, Wp)))
+
+
 @pytest.mark.parametrize("shape,dt,batch", [((2048, 2048), "f32", 2), ((2048, 2048), "i32", 1), ((4096, 4096), "f32", 1),
                                             ((1500, 1504), "f32", 3), ((2048, 1056), "i32", 2), ((1100, 2080), "f32", 1),
                                             ((3000, 2016), "f32", 1)],
@@ -921,23 +930,23 @@ def test_persistent_pass1(fht, O, monkeypatch, shape, dt, batch):
     h1, s1 = fht.full(t, pair=True)
     torch.cuda.synchronize()
     a1, b1 = h1.view.cpu().numpy(), s1.view.cpu().numpy()
-    assert np.array_equal(a0.view(np.int32), a1.view(np.int32))
-    assert np.array_equal(b0.view(np.int32), b1.view(np.int32))
+    assert _same_planes(a0, a1, shape)
+    assert _same_planes(b0, b1, shape)
     for _ in range(3):  # repeated: a shared-memory reuse race in the tile loop showed up about once in three runs
         hr = fht.full(t, out=h1)
         torch.cuda.synchronize()
-        assert np.array_equal(hr.view.cpu().numpy().view(np.int32), a1.view(np.int32))
+        assert _same_planes(hr.view.cpu().numpy(), a1, shape)
     if batch > 1:  # several chunks (two scratch buffers)
         monkeypatch.setenv("FHT_SCRATCH_BUDGET_MB", "80")
         h2 = fht.full(t)
         torch.cuda.synchronize()
-        assert np.array_equal(h2.view.cpu().numpy().view(np.int32), a1.view(np.int32))
+        assert _same_planes(h2.view.cpu().numpy(), a1, shape)
         # the chunks pipelined over an auxiliary stream (pass 1 of chunk k + 1 beside pass 2 of chunk k)
         h3, s3 = fht.full(t, pair=True, aux_stream=torch.cuda.Stream())
         torch.cuda.synchronize()
         assert h3.launches >= 4
-        assert np.array_equal(h3.view.cpu().numpy().view(np.int32), a1.view(np.int32))
-        assert np.array_equal(s3.view.cpu().numpy().view(np.int32), b1.view(np.int32))
+        assert _same_planes(h3.view.cpu().numpy(), a1, shape)
+        assert _same_planes(s3.view.cpu().numpy(), b1, shape)
     rng = np.random.default_rng(h_ * 3 + w_)
     for q in range(4):
         fr = O.quadrant_frame(imgs[0], q, square_to=O.full_padding(h_, w_))
@@ -969,3 +978,32 @@ def test_persistent_pass1_range(fht, monkeypatch, shape, dt, rng_deg, pruned):
         torch.cuda.synchronize()
         assert np.array_equal(h1.view.cpu().numpy().view(np.int32), a0.view(np.int32))
         assert np.array_equal(s1.view.cpu().numpy().view(np.int32), b0.view(np.int32))
+
+
+@pytest.mark.parametrize("shape,batch", [((512, 512), 5), ((256, 256), 1), ((300, 384), 2), ((512, 640), 2),
+                                         ((200, 128), 3)], ids=lambda v: str(v))
+def test_persistent_pass1_u8(fht, O, monkeypatch, shape, batch):
+    """The persistent pass 1 for 16-row strips of u8 images (k_p1p8: per-warp prefetched row boxes, transposed tiles
+    read as words of the untransposed block, uint16 scratch through per-warp slots) against k_p1 on the same call:
+    both outputs bit-identical, repeated; and sampled cells of image 0 against the direct pattern sums."""
+    from synth import random_image
+    h_, w_ = shape
+    imgs = np.stack([random_image(shape, "u8", seed=8100 + 5 * b + w_) for b in range(batch)])
+    t = dev(imgs)
+    monkeypatch.setenv("FHT_P1_PERSIST", "0")
+    h0, s0 = fht.full(t, pair=True)
+    torch.cuda.synchronize()
+    a0, b0 = h0.view.cpu().numpy(), s0.view.cpu().numpy()
+    monkeypatch.setenv("FHT_P1_PERSIST", "1")
+    for _ in range(3):
+        h1, s1 = fht.full(t, pair=True)
+        torch.cuda.synchronize()
+        assert _same_planes(h1.view.cpu().numpy(), a0, shape)
+        assert _same_planes(s1.view.cpu().numpy(), b0, shape)
+    rng = np.random.default_rng(h_ + 7 * w_)
+    for q in range(4):
+        fr = O.quadrant_frame(imgs[0], q, square_to=O.full_padding(h_, w_))
+        cells = _sample_cells(fr.Hp, fr.W, 48, rng)
+        want = O.hough_cells_direct(fr, cells)
+        vals = np.array([a0[0, q, a, c] for a, c in cells], dtype=a0.dtype)
+        check(vals, want, True)
