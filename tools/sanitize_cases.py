@@ -41,6 +41,14 @@ def main():
     t = torch.from_numpy(np.stack([random_image((2048, 2048), "f32", seed=6 + b) for b in range(2)])).to(dev)
     fht.full(t, pair=True)
     n += 1
+    # persistent u8 pass 1 (k_p1p8): 16-row strips, all four slots, three images
+    u = torch.from_numpy(np.stack([random_image((512, 512), "u8", seed=9 + b) for b in range(3)])).to(dev)
+    fht.full(u, pair=True)
+    n += 1
+    # §4 range in the persistent pass 1 (64-row strips)
+    t = torch.from_numpy(random_image((2048, 1200), "f32", seed=10)).to(dev)
+    fht.angle_range(t, 5.0, 30.0, pair=True)
+    n += 1
     # §4 range: scaled (TMA gather loader, alpha >= 1), alpha < 1 gather, pruned, horizontal
     t = torch.from_numpy(random_image((96, 80), "f32", seed=5)).to(dev)
     fht.angle_range(t, -15.0, 15.0, pair=True)
