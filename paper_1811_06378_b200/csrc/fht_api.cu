@@ -442,7 +442,7 @@ inline cudaError_t launch_p1p8(dim3 grid, const P1Maps& m, const v2::P1Params& a
     return e;
   const long long total = (long long)grid.x * grid.y * grid.z;
   if (total <= 0 || total >= (1ll << 31) - 4096) return cudaErrorInvalidValue;
-  long long G = 6ll * nsm;
+  long long G = (long long)env_int("FHT_P1P8_CTAS", 6) * nsm;  // CTAs per SM (A/B; 6 fit: 36 KB each)
   G -= G % a.nq;
   if (G < a.nq) G = a.nq;
   if (G > total) G = total;
