@@ -24,6 +24,9 @@
 #ifndef FHT_P1P_HALF0_STG
 #define FHT_P1P_HALF0_STG 0  // A/B (measured slower: C5 pass 1 381 vs 341 us): first half of a warp's rows: read back from its slot and stored with 16-byte st.global
 #endif                       // (no bulk-read wait before the second half is staged); second half: bulk store
+#ifndef FHT_P1P_TR_SPLIT
+#define FHT_P1P_TR_SPLIT 1  // transposed slots: one mbarrier (and one issuing thread) per column half of the tile
+#endif
 #ifndef FHT_P1P_LOAD_AFTER_STORE0
 #define FHT_P1P_LOAD_AFTER_STORE0 0  // measured: C5 pass 1 343 us (0) vs 354 us (1)
 #endif
@@ -65,7 +68,7 @@ __device__ __forceinline__ void p1p_run(unsigned char* smem, const CUtensorMap* 
   A* plane = reinterpret_cast<A*>(smem);
   A* stg = reinterpret_cast<A*>(smem + main_buf_bytes(R)) + warp * (kP1pHalf * TX1);
   // non-transposed: one mbarrier per warp (its block's rows); transposed: one for the tile's four boxes
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + main_buf_bytes(R) + kP1pStageBytes) + (TR ? 8 : warp);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + main_buf_bytes(R) + kP1pStageBytes) + (TR ? 8 + (FHT_P1P_TR_SPLIT ? (warp >> 2) : 0) : warp);
   const int ntq = p.ntiles << p.nq_log;
   const int G = (int)gridDim.x;
 
@@ -141,12 +144,23 @@ __device__ __forceinline__ void p1p_run(unsigned char* smem, const CUtensorMap* 
       return true;
     } else {
       // image rows [Xa, Xa + 288) x image columns [y0, y0 + 64): box (hb, rb) = columns y0 + 32 hb.., rows Xa + 144 rb..
+#if FHT_P1P_TR_SPLIT
+      // one mbarrier per column half: warps 0-3 read only the boxes of columns y0 .. y0 + 31, warps 4-7 the others
+      if ((tid & 127) == 0) {
+        const int hb = tid >> 7;
+        mbar_expect_tx(bar, 2u * kP1pBoxBytes);
+#pragma unroll
+        for (int rb = 0; rb < 2; ++rb)
+          tma_load_3d(tm_imgS, smem + (2 * hb + rb) * kP1pBoxBytes, bar, y0 + 32 * hb, Xa + kP1pBoxRows * rb, img);
+      }
+#else
       if (tid == 0) {
         mbar_expect_tx(bar, 4u * kP1pBoxBytes);
 #pragma unroll
         for (int k = 0; k < 4; ++k)
           tma_load_3d(tm_imgS, smem + k * kP1pBoxBytes, bar, y0 + 32 * (k >> 1), Xa + kP1pBoxRows * (k & 1), img);
       }
+#endif
       return true;
     }
   };
@@ -155,7 +169,7 @@ __device__ __forceinline__ void p1p_run(unsigned char* smem, const CUtensorMap* 
     if (lane == 0) mbar_init(bar);
     __syncwarp();
   } else {
-    if (tid == 0) mbar_init(bar);
+    if ((tid & (FHT_P1P_TR_SPLIT ? 127 : 255)) == 0) mbar_init(bar);
     __syncthreads();
   }
   int T = (int)blockIdx.x;
